@@ -1,0 +1,170 @@
+/* pf_b200.h -- C ABI of the B200 partial-fraction matrix-function engine.
+ *
+ * The reference (proj/core, C++20) has no C or FFI layer: its drop-in surface is the C++ API
+ * in proj/core/include/parfrac/. This header is the thin C boundary that the C++ host layer
+ * (paper_2210_03714_b200/cpp/, namespace parfrac) and the Python mirror call into. No torch
+ * types, no exceptions: every entry point returns a pf_err code and fills pf_status so the
+ * host can rethrow the identical parfrac::Error (error.hpp:8-44).
+ *
+ * Entry point                 replaces (reference file:line)
+ * --------------------------  ------------------------------------------------------------------
+ * pf_eval_dense_batched       eval_dense(method, B, opts)        proj/core/include/parfrac/dense.hpp:74-75
+ *                             (dense.cpp:193-252; one call = many independent B)
+ * pf_expm_batched             new: eval_dense + scaling and squaring (pattern expm_oracle
+ *                             dense.cpp:460-476, theta from bounds.hpp:62)
+ * pf_expm_phi1_batched        new: one solve per shift feeds exp and phi1 weight sets
+ *                              + phi1 doubling
+ * pf_cossin_batched           new: cos/sin pair through merged conjugate shifts + C^2-S^2 / 2SC
+ * pf_action_block             new dense analogue of substep_action / ActionOperator
+ *                             (action.hpp:61-82, action.cpp:224-339)
+ * pf_lu_factor / pf_lu_solve  DenseLu(a, pivot_rel_tol) / DenseLu::solve_matrix (dense.hpp:46-59)
+ * pf_solve_shifted            solve_shifted(b, c) (dense.hpp:62)
+ * pf_one_norm_batched         DenseMatrix::one_norm (dense.hpp:32, dense.cpp:54-62)
+ * pf_gemm_batched             DenseMatrix::mul (dense.hpp:26, dense.cpp:17-29)
+ *
+ * Conventions: matrices are row-major doubles (DenseMatrix layout, dense.hpp:36-37), device
+ * pointers, leading dimension `ld*` in elements, batch stride `stride*` in elements. Calls are
+ * ordered on the context's stream; status-returning calls synchronise that stream once at the
+ * end to read the device status (pass PF_FLAG_ASYNC to skip the check).
+ */
+#ifndef PF_B200_H
+#define PF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes: 0 = success, otherwise parfrac::Errc ordinal + 1 (error.hpp:8-19). */
+enum pf_err {
+  PF_OK = 0,
+  PF_ERR_DUPLICATE_SHIFT = 1,
+  PF_ERR_LENGTH_MISMATCH = 2,
+  PF_ERR_UNDER_DETERMINED = 3,
+  PF_ERR_UNKNOWN_METHOD = 4,
+  PF_ERR_INVALID_FUNCTION = 5,
+  PF_ERR_NON_UNIT_CONSTANT = 6,
+  PF_ERR_SINGULAR_SHIFT = 7,
+  PF_ERR_ZERO_PIVOT = 8,
+  PF_ERR_OUT_OF_CONVERGENCE_RADIUS = 9,
+  PF_ERR_BAD_ARGUMENT = 10,
+  PF_ERR_CUDA = 11 /* not a reference code: device/runtime failure */
+};
+
+enum pf_form { PF_FORM_PLAIN = 0, PF_FORM_RESIDUAL = 1 };
+
+enum pf_flags {
+  PF_FLAG_NONE = 0,
+  PF_FLAG_ASYNC = 1,     /* do not synchronise to read device status */
+  PF_FLAG_FORCE_PIVOT = 2 /* always run the genuine partial-pivoting LU (testing) */
+};
+
+/* Failure detail; enough for the C++ wrapper to rebuild the reference message
+ * "shift i: singular system: pivot magnitude X at column c (scale S)" (dense.cpp:117-119,220). */
+typedef struct {
+  int code;
+  int batch_index;
+  int shift_index; /* 1-based */
+  int column;
+  double pivot_magnitude;
+  double scale;
+} pf_status;
+
+/* One partial-fraction method, doubles exactly as the host's to_double_nearest gives them
+ * (rational.cpp:66-88). `weights`, `poly`, `constant` hold one row per weight set; set 0 is the
+ * primary function (e.g. exp), set 1 an optional second function on the same shifts (phi1). */
+typedef struct {
+  int n_terms;            /* <= PF_MAX_TERMS */
+  const double* shifts;   /* c_i, n_terms */
+  int n_sets;             /* 1 or 2 */
+  const double* weights;  /* b_i, n_sets * n_terms */
+  int has_poly;           /* hybrid methods: d0, d1, d2 per set */
+  const double* poly;     /* n_sets * 3, may be NULL when !has_poly */
+  const double* constant; /* a_0 = d_0 + sum b_i per set (residual form constant term) */
+  int form;               /* pf_form */
+} pf_method;
+
+/* cos/sin through exp(iB): conjugate shifts +-c merged into real solves of (I + c^2 B^2). */
+typedef struct {
+  int n_pairs; /* <= PF_MAX_TERMS */
+  const double* c2;
+  const double* cw; /* b_c + b_-c */
+  const double* sw; /* c (b_c - b_-c) */
+  double a0, a1;
+} pf_pair_method;
+
+#define PF_MAX_TERMS 16
+#define PF_SMALL_N 128 /* fused single-CTA kernels handle n <= 128 */
+
+typedef struct pf_context pf_context;
+
+int pf_version(void);
+const char* pf_error_string(int code);
+
+int pf_context_create(int device, pf_context** out);
+int pf_context_destroy(pf_context* ctx);
+/* Use an external CUDA stream (cudaStream_t as void*); NULL = the legacy default stream. */
+int pf_context_set_stream(pf_context* ctx, void* stream);
+/* Number of kernels this context launched so far (bench evidence). */
+int64_t pf_context_launch_count(pf_context* ctx);
+
+/* 1-norm (max column sum, rows summed in ascending order as dense.cpp:54-62) of each matrix. */
+int pf_one_norm_batched(pf_context* ctx, int n, int batch, const double* dA, int64_t lda, int64_t strideA,
+                        double* dNorm);
+
+/* r(B) for every weight set (no scaling): outs[s] + b*strideOut for set s. */
+int pf_eval_dense_batched(pf_context* ctx, const pf_method* m, int n, int batch, const double* dB, int64_t ldb,
+                          int64_t strideB, double* const* dOuts, int64_t ldo, int64_t strideOut, int flags,
+                          pf_status* status);
+
+/* exp by scaling and squaring. j_b = dSquaringsIn[b] when non-NULL, else the smallest j >= 0 with
+ * ldexp(||A_b||_1, -j) <= theta. B_b = 2^-j_b A_b, E = r(B_b) (weight set 0), E <- E^2 j_b times.
+ * dSquaringsOut (may be NULL) receives j_b. */
+int pf_expm_batched(pf_context* ctx, const pf_method* m, double theta, int n, int batch, const double* dA,
+                    int64_t lda, int64_t strideA, const int* dSquaringsIn, int* dSquaringsOut, double* dOut,
+                    int64_t ldo, int64_t strideOut, int flags, pf_status* status);
+
+/* exp and phi1 together: weight set 0 = exp, set 1 = phi1 on the same shifts;
+ * j doublings of Phi <- 0.5 (E + I) Phi, E <- E E. */
+int pf_expm_phi1_batched(pf_context* ctx, const pf_method* m, double theta, int n, int batch, const double* dA,
+                         int64_t lda, int64_t strideA, const int* dSquaringsIn, int* dSquaringsOut, double* dE,
+                         double* dPhi, int64_t ldo, int64_t strideOut, int flags, pf_status* status);
+
+/* cos(A), sin(A): B = 2^-j A, Z_c = (I + c^2 B^2)^{-1} c^2 B^2, C = a0 I - sum cw Z, S = B (a1 I - sum sw Z),
+ * then j steps of C <- C C - S S, S <- 2 (S C). */
+int pf_cossin_batched(pf_context* ctx, const pf_pair_method* pm, double theta, int n, int batch, const double* dA,
+                      int64_t lda, int64_t strideA, const int* dSquaringsIn, int* dSquaringsOut, double* dC,
+                      double* dS, int64_t ldo, int64_t strideOut, int flags, pf_status* status);
+
+/* Dense block action: B = A * (1.0/substeps) (elementwise, action.cpp:330-334), factor every
+ * (I - c_i B) once, then `substeps` times V <- r(B) V (weight set 0). A n x n, V and Out n x k. */
+int pf_action_block(pf_context* ctx, const pf_method* m, int n, int k, const double* dA, int64_t lda,
+                    const double* dV, int64_t ldv, int substeps, double* dOut, int64_t ldo, int flags,
+                    pf_status* status);
+
+/* DenseLu: in-place PA = LU (unit lower L below the diagonal, U on and above), LAPACK-style
+ * 0-based swap sequence in dPiv (n ints per matrix). SingularShift when the best pivot
+ * <= pivot_rel_tol * max(max|a|, 1e-300). */
+int pf_lu_factor_batched(pf_context* ctx, int n, int batch, double* dA, int64_t lda, int64_t strideA, int* dPiv,
+                         double pivot_rel_tol, int flags, pf_status* status);
+/* X = U^{-1} L^{-1} P RHS for k right-hand-side columns (row-major n x k), in place in dRhs. */
+int pf_lu_solve_batched(pf_context* ctx, int n, int k, int batch, const double* dLU, int64_t lda, int64_t strideLU,
+                        const int* dPiv, double* dRhs, int64_t ldr, int64_t strideR);
+
+/* (I - c B)^{-1} (dense.cpp:165-171). */
+int pf_solve_shifted_batched(pf_context* ctx, int n, int batch, const double* dB, int64_t ldb, int64_t strideB,
+                             double c, double* dOut, int64_t ldo, int64_t strideOut, int flags, pf_status* status);
+
+/* C = alpha * A B + beta * C (+ gamma * I), batched, FP64 DMMA. C must not alias A or B. */
+int pf_gemm_batched(pf_context* ctx, int m, int n, int k, int batch, double alpha, const double* dA, int64_t lda,
+                    int64_t strideA, const double* dB, int64_t ldb, int64_t strideB, double beta, double* dC,
+                    int64_t ldc, int64_t strideC, double gamma);
+
+/* Measured FP64 DMMA throughput of `device` in TFLOP/s (the FP64 roofline denominator). */
+double pf_probe_dmma_tflops(int device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PF_B200_H */

@@ -1,0 +1,83 @@
+"""ctypes binding of the C ABI in include/pf_b200.h (the product path; no fallback).
+
+Importing this module loads ``_lib/libpfb200.so``; if it is missing the import fails loudly --
+there is no CPU path behind this package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libpfb200.so"
+
+c_double_p = C.POINTER(C.c_double)
+c_int_p = C.POINTER(C.c_int)
+
+
+class PfStatus(C.Structure):
+    _fields_ = [("code", C.c_int), ("batch_index", C.c_int), ("shift_index", C.c_int), ("column", C.c_int),
+                ("pivot_magnitude", C.c_double), ("scale", C.c_double)]
+
+
+class PfMethod(C.Structure):
+    _fields_ = [("n_terms", C.c_int), ("shifts", c_double_p), ("n_sets", C.c_int), ("weights", c_double_p),
+                ("has_poly", C.c_int), ("poly", c_double_p), ("constant", c_double_p), ("form", C.c_int)]
+
+
+class PfPairMethod(C.Structure):
+    _fields_ = [("n_pairs", C.c_int), ("c2", c_double_p), ("cw", c_double_p), ("sw", c_double_p),
+                ("a0", C.c_double), ("a1", C.c_double)]
+
+
+PF_FLAG_ASYNC = 1
+PF_FLAG_FORCE_PIVOT = 2
+PF_MAX_TERMS = 16
+PF_SMALL_N = 128
+
+# (name, restype, argtypes) -- every symbol include/pf_b200.h declares
+_VP = C.c_void_p
+_I64 = C.c_int64
+SIGNATURES = [
+    ("pf_version", C.c_int, []),
+    ("pf_error_string", C.c_char_p, [C.c_int]),
+    ("pf_context_create", C.c_int, [C.c_int, C.POINTER(_VP)]),
+    ("pf_context_destroy", C.c_int, [_VP]),
+    ("pf_context_set_stream", C.c_int, [_VP, _VP]),
+    ("pf_context_launch_count", C.c_int64, [_VP]),
+    ("pf_one_norm_batched", C.c_int, [_VP, C.c_int, C.c_int, _VP, _I64, _I64, _VP]),
+    ("pf_eval_dense_batched", C.c_int, [_VP, C.POINTER(PfMethod), C.c_int, C.c_int, _VP, _I64, _I64,
+                                        C.POINTER(_VP), _I64, _I64, C.c_int, C.POINTER(PfStatus)]),
+    ("pf_expm_batched", C.c_int, [_VP, C.POINTER(PfMethod), C.c_double, C.c_int, C.c_int, _VP, _I64, _I64, _VP,
+                                  _VP, _VP, _I64, _I64, C.c_int, C.POINTER(PfStatus)]),
+    ("pf_expm_phi1_batched", C.c_int, [_VP, C.POINTER(PfMethod), C.c_double, C.c_int, C.c_int, _VP, _I64, _I64,
+                                       _VP, _VP, _VP, _VP, _I64, _I64, C.c_int, C.POINTER(PfStatus)]),
+    ("pf_cossin_batched", C.c_int, [_VP, C.POINTER(PfPairMethod), C.c_double, C.c_int, C.c_int, _VP, _I64, _I64,
+                                    _VP, _VP, _VP, _VP, _I64, _I64, C.c_int, C.POINTER(PfStatus)]),
+    ("pf_action_block", C.c_int, [_VP, C.POINTER(PfMethod), C.c_int, C.c_int, _VP, _I64, _VP, _I64, C.c_int, _VP,
+                                  _I64, C.c_int, C.POINTER(PfStatus)]),
+    ("pf_lu_factor_batched", C.c_int, [_VP, C.c_int, C.c_int, _VP, _I64, _I64, _VP, C.c_double, C.c_int,
+                                       C.POINTER(PfStatus)]),
+    ("pf_lu_solve_batched", C.c_int, [_VP, C.c_int, C.c_int, C.c_int, _VP, _I64, _I64, _VP, _VP, _I64, _I64]),
+    ("pf_solve_shifted_batched", C.c_int, [_VP, C.c_int, C.c_int, _VP, _I64, _I64, C.c_double, _VP, _I64, _I64,
+                                           C.c_int, C.POINTER(PfStatus)]),
+    ("pf_probe_dmma_tflops", C.c_double, [C.c_int]),
+    ("pf_gemm_batched", C.c_int, [_VP, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, _VP, _I64, _I64, _VP, _I64,
+                                  _I64, C.c_double, _VP, _I64, _I64, C.c_double]),
+]
+
+
+def load(path: os.PathLike | str | None = None) -> C.CDLL:
+    p = Path(path) if path else _LIB_PATH
+    if not p.exists():
+        raise ImportError("paper_2210_03714_b200: native engine %s is missing; run "
+                          "`python -m paper_2210_03714_b200.build` (there is no CPU fallback)" % p)
+    lib = C.CDLL(str(p))
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = load()

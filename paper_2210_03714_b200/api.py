@@ -1,0 +1,362 @@
+"""Python mirror of the reference's public surface for the hot path, over the C ABI.
+
+Reference surface (proj/core/include/parfrac/):
+  eval_dense(method, B, opts)     dense.hpp:74-75      -> eval_dense()
+  solve_shifted(B, c)             dense.hpp:62         -> solve_shifted()
+  EvalOptions{workers, fixed_order, form}  dense.hpp:64-68 -> EvalOptions
+  catalog / to_residual_form      methods.hpp:73-77    -> methods.catalog / methods.to_residual_form
+  theta                           bounds.hpp:62        -> methods.theta / THETA_U53
+New entry points: expm (scaling and squaring), expm_phi1, cossin, action_block,
+all batched.
+
+Arrays: torch float64 CUDA tensors are used in place (device pointers, the caller's current
+stream); numpy arrays / host tensors are copied to the device and the result copied back. Shapes
+(n, n) or (batch, n, n), row-major contiguous. Errors raise PfError with the reference's
+message text (dense.cpp:117-119, 219-221).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple, Union
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import Errc, PfError
+from .methods import (PLAIN, RESIDUAL, THETA_U53, FractionMethod, FunctionId, PairMethod, catalog,
+                      format_sig17, pair_method, same_shift_method, to_double_nearest)
+
+ArrayLike = Union[torch.Tensor, np.ndarray]
+
+
+@dataclass
+class EvalOptions:
+    """dense.hpp:64-68. `workers` is accepted for source compatibility; the device evaluates all
+    shifts concurrently and the reduction is always in ascending shift order, so results do not
+    depend on it (the reference's bit-identical-across-workers contract)."""
+
+    workers: int = 1
+    fixed_order: bool = True
+    form: Optional[int] = None
+
+
+# ------------------------------------------------------------------------------------------ packing
+
+
+class PackedMethod:
+    """pf_method with its arrays kept alive. Sets: weights of `method` first, then the extra
+    weight sets (same shifts; e.g. phi1 via methods.same_shift_method)."""
+
+    def __init__(self, method: FractionMethod, form: Optional[int] = None, extra: Sequence[FractionMethod] = ()):
+        form = method.form if form is None else form
+        sets = [method] + list(extra)
+        for s in sets[1:]:
+            if [Fraction_(c) for c in s.shifts] != [Fraction_(c) for c in method.shifts]:
+                raise PfError(Errc.BadArgument, "weight sets must share the shifts")
+        n = len(method.shifts)
+        if n > N.PF_MAX_TERMS:
+            raise PfError(Errc.BadArgument, "at most %d shifts" % N.PF_MAX_TERMS)
+        self.shifts = (C.c_double * max(n, 1))(*method.shift_doubles())
+        w = []
+        for s in sets:
+            w += s.weight_doubles()
+        self.weights = (C.c_double * max(len(w), 1))(*w)
+        has_poly = any(len(s.poly) == 3 for s in sets)
+        poly = []
+        for s in sets:
+            poly += [to_double_nearest(d) for d in s.poly] if len(s.poly) == 3 else [0.0, 0.0, 0.0]
+        self.poly = (C.c_double * len(poly))(*poly)
+        self.constant = (C.c_double * len(sets))(*[to_double_nearest(s.constant_term()) for s in sets])
+        self.c = N.PfMethod(n, self.shifts, len(sets), self.weights, 1 if has_poly else 0, self.poly, self.constant,
+                            int(form))
+        self.method = method
+
+    def ptr(self):
+        return C.byref(self.c)
+
+
+def Fraction_(x):
+    from fractions import Fraction
+
+    return Fraction(x)
+
+
+class PackedPair:
+    def __init__(self, pm: PairMethod):
+        n = len(pm.c2)
+        self.c2 = (C.c_double * n)(*[to_double_nearest(x) for x in pm.c2])
+        self.cw = (C.c_double * n)(*[to_double_nearest(x) for x in pm.cw])
+        self.sw = (C.c_double * n)(*[to_double_nearest(x) for x in pm.sw])
+        self.c = N.PfPairMethod(n, self.c2, self.cw, self.sw, to_double_nearest(pm.a0), to_double_nearest(pm.a1))
+
+    def ptr(self):
+        return C.byref(self.c)
+
+
+# ------------------------------------------------------------------------------------------ engine
+
+
+class Engine:
+    """One pf_context (device, stream, workspace). Not thread-safe (one host thread at a time)."""
+
+    def __init__(self, device: int = 0):
+        if not torch.cuda.is_available():
+            raise PfError(Errc.CudaError, "paper_2210_03714_b200 needs a CUDA device (there is no CPU path)")
+        self.device = device
+        torch.cuda.set_device(device)
+        h = C.c_void_p()
+        rc = N.lib.pf_context_create(device, C.byref(h))
+        if rc:
+            raise PfError(Errc.CudaError, "pf_context_create failed")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            N.lib.pf_context_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def bind_stream(self):
+        N.lib.pf_context_set_stream(self.h, C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
+
+    def launch_count(self) -> int:
+        return int(N.lib.pf_context_launch_count(self.h))
+
+
+_engine: Optional[Engine] = None
+
+
+def engine() -> Engine:
+    global _engine
+    if _engine is None:
+        _engine = Engine(torch.cuda.current_device() if torch.cuda.is_available() else 0)
+    _engine.bind_stream()
+    return _engine
+
+
+# ------------------------------------------------------------------------------------------ helpers
+
+
+def _raise(rc: int, st: N.PfStatus, batched: bool):
+    code = Errc(rc - 1) if 0 < rc <= len(Errc) else Errc.CudaError
+    if code == Errc.SingularShift:
+        msg = "singular system: pivot magnitude %s at column %d (scale %s)" % (
+            format_sig17(st.pivot_magnitude), st.column, format_sig17(st.scale))
+        if st.shift_index > 0:
+            msg = "shift %d: %s" % (st.shift_index, msg)
+        if batched:
+            msg = "matrix %d: %s" % (st.batch_index, msg)
+        raise PfError(code, msg)
+    if code == Errc.CudaError:
+        raise PfError(code, "CUDA failure in the B200 engine")
+    raise PfError(code, "bad argument")
+
+
+def _to_device(x: ArrayLike) -> Tuple[torch.Tensor, bool]:
+    """Returns (contiguous float64 cuda tensor, was_host)."""
+    if isinstance(x, np.ndarray):
+        t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64))
+        return t.cuda(non_blocking=False), True
+    if not isinstance(x, torch.Tensor):
+        raise PfError(Errc.BadArgument, "expected a numpy array or torch tensor")
+    if x.dtype != torch.float64:
+        raise PfError(Errc.BadArgument, "FP64 only")
+    if x.is_cuda:
+        return x.contiguous(), False
+    return x.contiguous().cuda(), True
+
+
+def _as_batch(t: torch.Tensor) -> Tuple[torch.Tensor, bool]:
+    if t.dim() == 2:
+        if t.shape[0] != t.shape[1]:
+            raise PfError(Errc.BadArgument, "matrix must be square")
+        return t.unsqueeze(0), False
+    if t.dim() == 3 and t.shape[1] == t.shape[2]:
+        return t, True
+    raise PfError(Errc.BadArgument, "expected (n, n) or (batch, n, n)")
+
+
+def _back(t: torch.Tensor, host: bool, squeeze: bool, like: ArrayLike):
+    if squeeze:
+        t = t[0]
+    if host:
+        return t.cpu().numpy() if isinstance(like, np.ndarray) else t.cpu()
+    return t
+
+
+def _resolve_method(method) -> FractionMethod:
+    return catalog(method) if isinstance(method, str) else method
+
+
+def _theta_for(method: FractionMethod, theta: Optional[float]) -> float:
+    if theta is not None:
+        return float(theta)
+    if method.name in THETA_U53:
+        return THETA_U53[method.name]
+    from .methods import theta as theta_fn
+
+    return theta_fn(method, tol=2.0 ** -53)
+
+
+# ------------------------------------------------------------------------------------------ entry points
+
+
+def eval_dense(method, B: ArrayLike, opts: Optional[EvalOptions] = None, extra_sets: Sequence[FractionMethod] = (),
+               flags: int = 0):
+    """r(B) (dense.cpp:193-252) for one matrix or a batch. With `extra_sets`, returns a list
+    [r_0(B), r_1(B), ...] computed from the same solves."""
+    opts = opts or EvalOptions()
+    if opts.workers < 1:
+        raise PfError(Errc.BadArgument, "workers must be >= 1")
+    if not opts.fixed_order:
+        raise PfError(Errc.BadArgument, "only fixed-order reduction is supported")
+    m = _resolve_method(method)
+    pk = PackedMethod(m, opts.form, extra_sets)
+    eng = engine()
+    dB, host = _to_device(B)
+    dB3, batched = _as_batch(dB)
+    bsz, n = dB3.shape[0], dB3.shape[1]
+    outs = [torch.empty_like(dB3) for _ in range(1 + len(extra_sets))]
+    ptrs = (C.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+    st = N.PfStatus()
+    rc = N.lib.pf_eval_dense_batched(eng.h, pk.ptr(), n, bsz, dB3.data_ptr(), n, n * n, ptrs, n, n * n, flags,
+                                     C.byref(st))
+    if rc:
+        _raise(rc, st, batched)
+    res = [_back(o, host, not batched, B) for o in outs]
+    return res if extra_sets else res[0]
+
+
+def solve_shifted(B: ArrayLike, c: float, flags: int = 0):
+    """(I - cB)^{-1} (dense.cpp:165-171)."""
+    eng = engine()
+    dB, host = _to_device(B)
+    dB3, batched = _as_batch(dB)
+    bsz, n = dB3.shape[0], dB3.shape[1]
+    out = torch.empty_like(dB3)
+    st = N.PfStatus()
+    rc = N.lib.pf_solve_shifted_batched(eng.h, n, bsz, dB3.data_ptr(), n, n * n, float(c), out.data_ptr(), n, n * n,
+                                        flags, C.byref(st))
+    if rc:
+        _raise(rc, st, batched)
+    return _back(out, host, not batched, B)
+
+
+def expm(A: ArrayLike, method="R4", theta: Optional[float] = None, squarings: Optional[ArrayLike] = None,
+         form: int = RESIDUAL, return_squarings: bool = False, flags: int = 0, out: Optional[torch.Tensor] = None):
+    """exp(A) by r(2^-j A)^(2^j), j = smallest j >= 0 with ||A||_1 2^-j <= theta_m.
+    Residual form by default (the parity-safe form)."""
+    m = _resolve_method(method)
+    th = _theta_for(m, theta)
+    pk = PackedMethod(m, form)
+    eng = engine()
+    dA, host = _to_device(A)
+    dA3, batched = _as_batch(dA)
+    bsz, n = dA3.shape[0], dA3.shape[1]
+    o = out if out is not None else torch.empty_like(dA3)
+    j_in = None
+    if squarings is not None:
+        j_in = torch.as_tensor(squarings, dtype=torch.int32).reshape(-1).to(dA3.device).contiguous()
+    j_out = torch.empty(bsz, dtype=torch.int32, device=dA3.device)
+    st = N.PfStatus()
+    rc = N.lib.pf_expm_batched(eng.h, pk.ptr(), th, n, bsz, dA3.data_ptr(), n, n * n,
+                               j_in.data_ptr() if j_in is not None else None, j_out.data_ptr(), o.data_ptr(), n, n * n,
+                               flags, C.byref(st))
+    if rc:
+        _raise(rc, st, batched)
+    res = _back(o, host, not batched, A)
+    if return_squarings:
+        js = j_out.cpu().numpy() if host else j_out
+        return res, (js[0] if not batched else js)
+    return res
+
+
+def expm_phi1(A: ArrayLike, method="R8", theta: Optional[float] = None, form: int = RESIDUAL, flags: int = 0,
+              return_squarings: bool = False):
+    """(exp(A), phi1(A)) from one solve per shift (weight sets exp and phi1 on the method's
+    shifts), then j doublings Phi <- 0.5 (E + I) Phi, E <- E E."""
+    m = _resolve_method(method)
+    phi = same_shift_method(m, FunctionId.phi(1))
+    th = theta if theta is not None else min(_theta_for(m, None), THETA_U53.get(m.name + "_phi1set")
+                                             or _theta_for(phi, None))
+    pk = PackedMethod(m, form, [phi])
+    eng = engine()
+    dA, host = _to_device(A)
+    dA3, batched = _as_batch(dA)
+    bsz, n = dA3.shape[0], dA3.shape[1]
+    oE, oP = torch.empty_like(dA3), torch.empty_like(dA3)
+    j_out = torch.empty(bsz, dtype=torch.int32, device=dA3.device)
+    st = N.PfStatus()
+    rc = N.lib.pf_expm_phi1_batched(eng.h, pk.ptr(), float(th), n, bsz, dA3.data_ptr(), n, n * n, None,
+                                    j_out.data_ptr(), oE.data_ptr(), oP.data_ptr(), n, n * n, flags, C.byref(st))
+    if rc:
+        _raise(rc, st, batched)
+    res = (_back(oE, host, not batched, A), _back(oP, host, not batched, A))
+    if return_squarings:
+        js = j_out.cpu().numpy() if host else j_out
+        return res + ((js[0] if not batched else js),)
+    return res
+
+
+def cossin(A: ArrayLike, method="R8", theta: Optional[float] = None, flags: int = 0, return_squarings: bool = False):
+    """(cos A, sin A) through exp(iB) with merged conjugate shifts and the C^2 - S^2 / 2SC
+    double-angle recurrence."""
+    m = _resolve_method(method)
+    pm = pair_method(m)
+    th = _theta_for(m, theta)
+    pk = PackedPair(pm)
+    eng = engine()
+    dA, host = _to_device(A)
+    dA3, batched = _as_batch(dA)
+    bsz, n = dA3.shape[0], dA3.shape[1]
+    oC, oS = torch.empty_like(dA3), torch.empty_like(dA3)
+    j_out = torch.empty(bsz, dtype=torch.int32, device=dA3.device)
+    st = N.PfStatus()
+    rc = N.lib.pf_cossin_batched(eng.h, pk.ptr(), float(th), n, bsz, dA3.data_ptr(), n, n * n, None,
+                                 j_out.data_ptr(), oC.data_ptr(), oS.data_ptr(), n, n * n, flags, C.byref(st))
+    if rc:
+        _raise(rc, st, batched)
+    res = (_back(oC, host, not batched, A), _back(oS, host, not batched, A))
+    if return_squarings:
+        js = j_out.cpu().numpy() if host else j_out
+        return res + ((js[0] if not batched else js),)
+    return res
+
+
+def one_norm(A: ArrayLike):
+    eng = engine()
+    dA, host = _to_device(A)
+    dA3, batched = _as_batch(dA)
+    bsz, n = dA3.shape[0], dA3.shape[1]
+    out = torch.empty(bsz, dtype=torch.float64, device=dA3.device)
+    rc = N.lib.pf_one_norm_batched(eng.h, n, bsz, dA3.data_ptr(), n, n * n, out.data_ptr())
+    if rc:
+        _raise(rc, N.PfStatus(), batched)
+    if host:
+        out = out.cpu().numpy()
+    return out if batched else float(out[0])
+
+
+def gemm(A: torch.Tensor, B: torch.Tensor, alpha: float = 1.0, beta: float = 0.0, Cm: Optional[torch.Tensor] = None,
+         gamma: float = 0.0) -> torch.Tensor:
+    """C = alpha A B + beta C + gamma I on the FP64 DMMA GEMM (device tensors, (m,k)x(k,n) or batched)."""
+    eng = engine()
+    a3 = A if A.dim() == 3 else A.unsqueeze(0)
+    b3 = B if B.dim() == 3 else B.unsqueeze(0)
+    bsz, m, k = a3.shape
+    n = b3.shape[2]
+    if Cm is None:
+        Cm = torch.zeros(bsz, m, n, dtype=torch.float64, device=a3.device)
+    c3 = Cm if Cm.dim() == 3 else Cm.unsqueeze(0)
+    rc = N.lib.pf_gemm_batched(eng.h, m, n, k, bsz, alpha, a3.data_ptr(), k, m * k, b3.data_ptr(), n, k * n, beta,
+                               c3.data_ptr(), n, m * n, gamma)
+    if rc:
+        _raise(rc, N.PfStatus(), True)
+    return Cm

@@ -1,0 +1,144 @@
+// K6 and elementwise helpers: batched 1-norm, squaring-count selection, exact 2^-j scaling,
+// Y = alpha X + diag I. HBM-bound; one thread per column / element, coalesced along rows.
+#include "pf_common.cuh"
+#include "pf_kernels.h"
+
+namespace pf {
+
+// DenseMatrix::one_norm (dense.cpp:54-62): column sums in ascending row order, then the max.
+// One thread per column keeps the summation order of the reference (bit-identical norms, hence
+// identical squaring counts); lanes of a warp read consecutive columns of the same row.
+__global__ void one_norm_kernel(int n, const double* A, int64_t lda, int64_t strideA, double* out) {
+  const double* a = A + (int64_t)blockIdx.x * strideA;
+  double best = 0.0;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    double col = 0.0;
+    for (int r = 0; r < n; ++r) col += fabs(a[(int64_t)r * lda + c]);
+    best = fmax(best, col);
+  }
+  for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmax(r, red[w]);
+    out[blockIdx.x] = r;
+  }
+}
+
+void launch_one_norm(int n, int batch, const double* A, int64_t lda, int64_t strideA, double* out,
+                     cudaStream_t stream) {
+  int threads = n >= 1024 ? 1024 : ((n + 31) / 32) * 32;
+  if (threads < 32) threads = 32;
+  one_norm_kernel<<<batch, threads, 0, stream>>>(n, A, lda, strideA, out);
+}
+
+__global__ void squarings_kernel(int batch, const double* norms, double theta, int* j) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  int s = 0;
+  while (ldexp(norms[b], -s) > theta && s < 2000) ++s;
+  j[b] = s;
+}
+
+void launch_squarings(int batch, const double* norms, double theta, int* j, cudaStream_t stream) {
+  squarings_kernel<<<(batch + 255) / 256, 256, 0, stream>>>(batch, norms, theta, j);
+}
+
+__global__ void scale_add_identity_kernel(int n, double alpha, const double* X, int64_t ldx, int64_t strideX,
+                                          double diag, double* Y, int64_t ldy, int64_t strideY) {
+  const int64_t b = blockIdx.y;
+  const int64_t nn = (int64_t)n * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < nn; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / n), c = (int)(idx % n);
+    double v = X[b * strideX + (int64_t)r * ldx + c];
+    if (alpha != 1.0) v = __dmul_rn(v, alpha);
+    if (r == c && diag != 0.0) v = __dadd_rn(v, diag);
+    Y[b * strideY + (int64_t)r * ldy + c] = v;
+  }
+}
+
+void launch_scale_add_identity(int n, int batch, double alpha, const double* X, int64_t ldx, int64_t strideX,
+                               double diag, double* Y, int64_t ldy, int64_t strideY, cudaStream_t stream) {
+  const int64_t nn = (int64_t)n * n;
+  int blocks = (int)((nn + 255) / 256);
+  if (blocks > 1184) blocks = 1184;
+  dim3 grid(blocks, batch);
+  scale_add_identity_kernel<<<grid, 256, 0, stream>>>(n, alpha, X, ldx, strideX, diag, Y, ldy, strideY);
+}
+
+__global__ void ldexp_kernel(int n, const double* X, int64_t ldx, int64_t strideX, const int* j, double* Y,
+                             int64_t ldy, int64_t strideY) {
+  const int64_t b = blockIdx.y;
+  const int s = j ? j[b] : 0;
+  const int64_t nn = (int64_t)n * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < nn; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / n), c = (int)(idx % n);
+    const double v = X[b * strideX + (int64_t)r * ldx + c];
+    Y[b * strideY + (int64_t)r * ldy + c] = s == 0 ? v : ldexp(v, -s);
+  }
+}
+
+void launch_ldexp_batched(int n, int batch, const double* X, int64_t ldx, int64_t strideX, const int* j, double* Y,
+                          int64_t ldy, int64_t strideY, cudaStream_t stream) {
+  const int64_t nn = (int64_t)n * n;
+  int blocks = (int)((nn + 255) / 256);
+  if (blocks > 1184) blocks = 1184;
+  dim3 grid(blocks, batch);
+  ldexp_kernel<<<grid, 256, 0, stream>>>(n, X, ldx, strideX, j, Y, ldy, strideY);
+}
+
+}  // namespace pf
+
+// ---------------------------------------------------------------------------------------------
+// FP64 tensor-pipe probe: the roofline denominator for this chip (MEASURED_PEAKS.json carries no
+// FP64 figure). 8 independent DMMA chains per warp, 4 warps per SM, all SMs.
+namespace pf {
+__global__ void dmma_probe_kernel(double* out, int iters) {
+  double acc[8][2];
+  const double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc[c][0] = acc[c][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1},{%2},{%3},{%0,%1};"
+                   : "+d"(acc[c][0]), "+d"(acc[c][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += acc[c][0] + acc[c][1];
+  if (s == 12345.678) out[0] = s;
+}
+}  // namespace pf
+
+extern "C" double pf_probe_dmma_tflops(int device) {
+  if (cudaSetDevice(device) != cudaSuccess) return -1.0;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  double* d = nullptr;
+  if (cudaMalloc(&d, 64) != cudaSuccess) return -1.0;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 20000, threads = 512;
+  pf::dmma_probe_kernel<<<sms, threads>>>(d, 100);
+  float best = 1e30f;
+  for (int r = 0; r < 3; ++r) {
+    cudaEventRecord(e0);
+    pf::dmma_probe_kernel<<<sms, threads>>>(d, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  // one DMMA = 8*8*4 FMA = 512 flop per warp
+  const double flops = double(sms) * (threads / 32) * iters * 8 * 512.0;
+  return flops / (best * 1e-3) / 1e12;
+}

@@ -1,0 +1,478 @@
+// C ABI (include/pf_b200.h): context, workspace, status plumbing and the host-side
+// compositions (scaling and squaring, phi1 doubling, cos/sin recurrence) over the kernels.
+// No exceptions cross this boundary; every error is a pf_err code + pf_status.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "pf_common.cuh"
+#include "pf_kernels.h"
+
+struct pf_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  pf::DevStatus* status = nullptr;
+  int status_cap = 0;
+  int* first_error = nullptr;
+  int* h_first_error = nullptr;
+  std::vector<void*> ws;
+  std::vector<size_t> ws_bytes;
+};
+
+namespace {
+
+using pf::DevStatus;
+
+int cuda_fail(cudaError_t e) { return e == cudaSuccess ? PF_OK : PF_ERR_CUDA; }
+
+void* workspace(pf_context* ctx, int slot, size_t bytes) {
+  if ((int)ctx->ws.size() <= slot) {
+    ctx->ws.resize(slot + 1, nullptr);
+    ctx->ws_bytes.resize(slot + 1, 0);
+  }
+  if (ctx->ws_bytes[slot] < bytes) {
+    if (ctx->ws[slot]) {
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(ctx->ws[slot]);
+    }
+    ctx->ws[slot] = nullptr;
+    if (cudaMalloc(&ctx->ws[slot], bytes) != cudaSuccess) {
+      ctx->ws_bytes[slot] = 0;
+      return nullptr;
+    }
+    ctx->ws_bytes[slot] = bytes;
+  }
+  return ctx->ws[slot];
+}
+
+int ensure_status(pf_context* ctx, int batch) {
+  if (ctx->status_cap < batch) {
+    if (ctx->status) {
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(ctx->status);
+    }
+    ctx->status = nullptr;
+    int cap = std::max(batch, 1024);
+    if (cudaMalloc(&ctx->status, sizeof(DevStatus) * cap) != cudaSuccess) return PF_ERR_CUDA;
+    ctx->status_cap = cap;
+  }
+  return cuda_fail(cudaMemsetAsync(ctx->first_error, 0x7f, sizeof(int), ctx->stream));
+}
+
+// Reads the first failing batch entry (if any) back to the host.
+int collect_status(pf_context* ctx, int batch, int flags, pf_status* out) {
+  if (out) std::memset(out, 0, sizeof(*out));
+  cudaError_t le = cudaGetLastError();
+  if (le != cudaSuccess) return PF_ERR_CUDA;
+  if (flags & PF_FLAG_ASYNC) return PF_OK;
+  if (cudaMemcpyAsync(ctx->h_first_error, ctx->first_error, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream) !=
+      cudaSuccess)
+    return PF_ERR_CUDA;
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return PF_ERR_CUDA;
+  const int b = *ctx->h_first_error;
+  if (b < 0 || b >= batch) return PF_OK;
+  DevStatus st;
+  if (cudaMemcpy(&st, ctx->status + b, sizeof(st), cudaMemcpyDeviceToHost) != cudaSuccess) return PF_ERR_CUDA;
+  if (out) {
+    out->code = st.code;
+    out->batch_index = b;
+    out->shift_index = st.shift_index;
+    out->column = st.column;
+    out->pivot_magnitude = st.pivot_magnitude;
+    out->scale = st.scale;
+  }
+  return st.code;
+}
+
+int bad(pf_status* st) {
+  if (st) {
+    std::memset(st, 0, sizeof(*st));
+    st->code = PF_ERR_BAD_ARGUMENT;
+  }
+  return PF_ERR_BAD_ARGUMENT;
+}
+
+bool fill_method(const pf_method* m, pf::SmallParams& p) {
+  if (!m || m->n_terms < 0 || m->n_terms > PF_MAX_TERMS || m->n_sets < 1 || m->n_sets > 2) return false;
+  if (m->n_terms > 0 && (!m->shifts || !m->weights)) return false;
+  if (m->form != PF_FORM_PLAIN && m->form != PF_FORM_RESIDUAL) return false;
+  if (m->has_poly && !m->poly) return false;
+  if (m->form == PF_FORM_RESIDUAL && !m->constant) return false;
+  p.n_terms = m->n_terms;
+  p.n_sets = m->n_sets;
+  p.has_poly = m->has_poly ? 1 : 0;
+  p.form = m->form;
+  for (int i = 0; i < PF_MAX_TERMS; ++i) {
+    p.shifts[i] = i < m->n_terms ? m->shifts[i] : 0.0;
+    for (int s = 0; s < 2; ++s) p.weights[s][i] = (i < m->n_terms && s < m->n_sets) ? m->weights[s * m->n_terms + i] : 0.0;
+  }
+  for (int s = 0; s < 2; ++s) {
+    for (int k = 0; k < 3; ++k) p.poly[s][k] = (m->has_poly && s < m->n_sets) ? m->poly[3 * s + k] : 0.0;
+    p.constant[s] = (m->constant && s < m->n_sets) ? m->constant[s] : 0.0;
+  }
+  return true;
+}
+
+int launch_small(pf_context* ctx, pf::SmallParams& p) {
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(pf::small_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)pf::small_eval_smem_bytes());
+  });
+  if (attr_err != cudaSuccess) return PF_ERR_CUDA;
+  int rc = ensure_status(ctx, p.batch);
+  if (rc) return rc;
+  p.status = ctx->status;
+  p.first_error = ctx->first_error;
+  if (p.batch == 0) return PF_OK;
+  pf::small_eval_kernel<<<p.batch, 256, pf::small_eval_smem_bytes(), ctx->stream>>>(p);
+  ctx->launches++;
+  return cuda_fail(cudaGetLastError());
+}
+
+void gemm(pf_context* ctx, int m, int n, int k, int batch, double alpha, const double* A, int64_t lda,
+          int64_t sA, const double* B, int64_t ldb, int64_t sB, double beta, double* C, int64_t ldc, int64_t sC,
+          double gamma, const int* jmask = nullptr, int step = 0, const double* pass = nullptr) {
+  pf::GemmParams g{};
+  g.m = m;
+  g.n = n;
+  g.k = k;
+  g.batch = batch;
+  g.alpha = alpha;
+  g.beta = beta;
+  g.gamma = gamma;
+  g.A = A;
+  g.lda = lda;
+  g.strideA = sA;
+  g.B = B;
+  g.ldb = ldb;
+  g.strideB = sB;
+  g.C = C;
+  g.ldc = ldc;
+  g.strideC = sC;
+  g.jmask = jmask;
+  g.step = step;
+  g.pass = pass;
+  pf::launch_gemm(g, ctx->stream);
+  ctx->launches++;
+}
+
+int max_j(pf_context* ctx, const int* dJ, int batch, int* out) {
+  std::vector<int> h(batch);
+  if (cudaMemcpyAsync(h.data(), dJ, sizeof(int) * batch, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess)
+    return PF_ERR_CUDA;
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return PF_ERR_CUDA;
+  int mj = 0;
+  for (int v : h) mj = std::max(mj, v);
+  *out = mj;
+  return PF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pf_version(void) { return 1; }
+
+const char* pf_error_string(int code) {
+  switch (code) {
+    case PF_OK: return "ok";
+    case PF_ERR_DUPLICATE_SHIFT: return "DuplicateShift";
+    case PF_ERR_LENGTH_MISMATCH: return "LengthMismatch";
+    case PF_ERR_UNDER_DETERMINED: return "UnderDetermined";
+    case PF_ERR_UNKNOWN_METHOD: return "UnknownMethod";
+    case PF_ERR_INVALID_FUNCTION: return "InvalidFunction";
+    case PF_ERR_NON_UNIT_CONSTANT: return "NonUnitConstant";
+    case PF_ERR_SINGULAR_SHIFT: return "SingularShift";
+    case PF_ERR_ZERO_PIVOT: return "ZeroPivot";
+    case PF_ERR_OUT_OF_CONVERGENCE_RADIUS: return "OutOfConvergenceRadius";
+    case PF_ERR_BAD_ARGUMENT: return "BadArgument";
+    case PF_ERR_CUDA: return "CudaError";
+    default: return "unknown";
+  }
+}
+
+int pf_context_create(int device, pf_context** out) {
+  if (!out) return PF_ERR_BAD_ARGUMENT;
+  *out = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return PF_ERR_CUDA;
+  auto* ctx = new pf_context();
+  ctx->device = device;
+  if (cudaMalloc(&ctx->first_error, sizeof(int)) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_first_error, sizeof(int)) != cudaSuccess) {
+    delete ctx;
+    return PF_ERR_CUDA;
+  }
+  *out = ctx;
+  return PF_OK;
+}
+
+int pf_context_destroy(pf_context* ctx) {
+  if (!ctx) return PF_OK;
+  cudaStreamSynchronize(ctx->stream);
+  for (void* p : ctx->ws) cudaFree(p);
+  cudaFree(ctx->status);
+  cudaFree(ctx->first_error);
+  cudaFreeHost(ctx->h_first_error);
+  delete ctx;
+  return PF_OK;
+}
+
+int pf_context_set_stream(pf_context* ctx, void* stream) {
+  if (!ctx) return PF_ERR_BAD_ARGUMENT;
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  return PF_OK;
+}
+
+int64_t pf_context_launch_count(pf_context* ctx) { return ctx ? ctx->launches : 0; }
+
+int pf_one_norm_batched(pf_context* ctx, int n, int batch, const double* dA, int64_t lda, int64_t strideA,
+                        double* dNorm) {
+  if (!ctx || n < 0 || batch < 0 || lda < n) return PF_ERR_BAD_ARGUMENT;
+  if (batch == 0) return PF_OK;
+  pf::launch_one_norm(n, batch, dA, lda, strideA, dNorm, ctx->stream);
+  ctx->launches++;
+  return cuda_fail(cudaGetLastError());
+}
+
+int pf_gemm_batched(pf_context* ctx, int m, int n, int k, int batch, double alpha, const double* dA, int64_t lda,
+                    int64_t strideA, const double* dB, int64_t ldb, int64_t strideB, double beta, double* dC,
+                    int64_t ldc, int64_t strideC, double gamma) {
+  if (!ctx || m < 0 || n < 0 || k < 0 || batch < 0) return PF_ERR_BAD_ARGUMENT;
+  if (batch == 0 || m == 0 || n == 0) return PF_OK;
+  gemm(ctx, m, n, k, batch, alpha, dA, lda, strideA, dB, ldb, strideB, beta, dC, ldc, strideC, gamma);
+  return cuda_fail(cudaGetLastError());
+}
+
+int pf_eval_dense_batched(pf_context* ctx, const pf_method* m, int n, int batch, const double* dB, int64_t ldb,
+                          int64_t strideB, double* const* dOuts, int64_t ldo, int64_t strideOut, int flags,
+                          pf_status* status) {
+  pf::SmallParams p{};
+  if (!ctx || n < 0 || batch < 0 || !dOuts || !fill_method(m, p) || ldb < n || ldo < n) return bad(status);
+  if (n > PF_SMALL_N) return bad(status);  // large-n path: pf_large.cu (round 1: small only)
+  p.n = n;
+  p.batch = batch;
+  p.mode = pf::kModeEval;
+  p.force_pivot = (flags & PF_FLAG_FORCE_PIVOT) ? 1 : 0;
+  p.A = dB;
+  p.lda = ldb;
+  p.strideA = strideB;
+  p.out0 = dOuts[0];
+  p.out1 = m->n_sets > 1 ? dOuts[1] : nullptr;
+  p.ldo = ldo;
+  p.strideOut = strideOut;
+  p.pivot_rel_tol = 1e-14;
+  int rc = launch_small(ctx, p);
+  if (rc) return rc;
+  return collect_status(ctx, batch, flags, status);
+}
+
+int pf_expm_batched(pf_context* ctx, const pf_method* m, double theta, int n, int batch, const double* dA,
+                    int64_t lda, int64_t strideA, const int* dSquaringsIn, int* dSquaringsOut, double* dOut,
+                    int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
+  pf::SmallParams p{};
+  if (!ctx || n < 0 || batch < 0 || !dOut || !fill_method(m, p) || lda < n || ldo < n || !(theta > 0))
+    return bad(status);
+  if (n > PF_SMALL_N) return bad(status);
+  p.n = n;
+  p.batch = batch;
+  p.mode = pf::kModeExpm;
+  p.force_pivot = (flags & PF_FLAG_FORCE_PIVOT) ? 1 : 0;
+  p.A = dA;
+  p.lda = lda;
+  p.strideA = strideA;
+  p.j_in = dSquaringsIn;
+  p.j_out = dSquaringsOut;
+  p.out0 = dOut;
+  p.out1 = nullptr;
+  p.n_sets = 1;
+  p.ldo = ldo;
+  p.strideOut = strideOut;
+  p.theta = theta;
+  p.pivot_rel_tol = 1e-14;
+  int rc = launch_small(ctx, p);
+  if (rc) return rc;
+  return collect_status(ctx, batch, flags, status);
+}
+
+int pf_solve_shifted_batched(pf_context* ctx, int n, int batch, const double* dB, int64_t ldb, int64_t strideB,
+                             double c, double* dOut, int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
+  // (I - cB)^{-1} = eval_dense of the one-term plain method {c; 1} (dense.cpp:165-171)
+  const double w = 1.0, zero = 0.0;
+  pf_method m{1, &c, 1, &w, 0, nullptr, &zero, PF_FORM_PLAIN};
+  double* outs[1] = {dOut};
+  if (c == 0.0) {  // the evaluator folds a zero shift into w I; same result I
+    return pf_eval_dense_batched(ctx, &m, n, batch, dB, ldb, strideB, outs, ldo, strideOut, flags, status);
+  }
+  int rc = pf_eval_dense_batched(ctx, &m, n, batch, dB, ldb, strideB, outs, ldo, strideOut, flags, status);
+  if (status && rc) status->shift_index = 0;
+  return rc;
+}
+
+int pf_expm_phi1_batched(pf_context* ctx, const pf_method* m, double theta, int n, int batch, const double* dA,
+                         int64_t lda, int64_t strideA, const int* dSquaringsIn, int* dSquaringsOut, double* dE,
+                         double* dPhi, int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
+  pf::SmallParams p{};
+  if (!ctx || n < 0 || batch < 0 || !dE || !dPhi || !fill_method(m, p) || m->n_sets != 2 || lda < n || ldo < n ||
+      !(theta > 0))
+    return bad(status);
+  if (n > PF_SMALL_N) return bad(status);
+  if (batch == 0) return PF_OK;
+  int* dJ = dSquaringsOut ? dSquaringsOut : static_cast<int*>(workspace(ctx, 0, sizeof(int) * batch));
+  const int64_t nn = (int64_t)n * n;
+  double* t1 = static_cast<double*>(workspace(ctx, 1, sizeof(double) * nn * batch));
+  double* t2 = static_cast<double*>(workspace(ctx, 2, sizeof(double) * nn * batch));
+  double* t3 = static_cast<double*>(workspace(ctx, 3, sizeof(double) * nn * batch));
+  if (!dJ || !t1 || !t2 || !t3) return PF_ERR_CUDA;
+  p.n = n;
+  p.batch = batch;
+  p.mode = pf::kModeScaledEval;
+  p.force_pivot = (flags & PF_FLAG_FORCE_PIVOT) ? 1 : 0;
+  p.A = dA;
+  p.lda = lda;
+  p.strideA = strideA;
+  p.j_in = dSquaringsIn;
+  p.j_out = dJ;
+  p.out0 = t1;  // E
+  p.out1 = t2;  // Phi
+  p.ldo = n;
+  p.strideOut = nn;
+  p.theta = theta;
+  p.pivot_rel_tol = 1e-14;
+  int rc = launch_small(ctx, p);
+  if (rc) return rc;
+  rc = collect_status(ctx, batch, flags & ~PF_FLAG_ASYNC, status);
+  if (rc) return rc;
+  if (dSquaringsIn && dSquaringsIn != dJ)
+    cudaMemcpyAsync(dJ, dSquaringsIn, sizeof(int) * batch, cudaMemcpyDeviceToDevice, ctx->stream);
+  int jmax = 0;
+  rc = max_j(ctx, dJ, batch, &jmax);
+  if (rc) return rc;
+  // Phi <- 0.5 (E + I) Phi ; E <- E E   (per-matrix step count j_b)
+  double *E = t1, *Phi = t2, *spare = t3;
+  double* T = static_cast<double*>(workspace(ctx, 4, sizeof(double) * nn * batch));
+  if (!T) return PF_ERR_CUDA;
+  for (int s = 0; s < jmax; ++s) {
+    pf::launch_scale_add_identity(n, batch, 1.0, E, n, nn, 1.0, T, n, nn, ctx->stream);
+    ctx->launches++;
+    gemm(ctx, n, n, n, batch, 0.5, T, n, nn, Phi, n, nn, 0.0, spare, n, nn, 0.0, dJ, s, Phi);
+    std::swap(Phi, spare);
+    gemm(ctx, n, n, n, batch, 1.0, E, n, nn, E, n, nn, 0.0, spare, n, nn, 0.0, dJ, s, E);
+    std::swap(E, spare);
+  }
+  if (strideOut != nn || ldo != n) {
+    for (int b = 0; b < batch; ++b) {
+      cudaMemcpy2DAsync(dE + b * strideOut, sizeof(double) * ldo, E + b * nn, sizeof(double) * n, sizeof(double) * n,
+                        n, cudaMemcpyDeviceToDevice, ctx->stream);
+      cudaMemcpy2DAsync(dPhi + b * strideOut, sizeof(double) * ldo, Phi + b * nn, sizeof(double) * n,
+                        sizeof(double) * n, n, cudaMemcpyDeviceToDevice, ctx->stream);
+    }
+  } else {
+    cudaMemcpyAsync(dE, E, sizeof(double) * nn * batch, cudaMemcpyDeviceToDevice, ctx->stream);
+    cudaMemcpyAsync(dPhi, Phi, sizeof(double) * nn * batch, cudaMemcpyDeviceToDevice, ctx->stream);
+  }
+  return collect_status(ctx, batch, flags, status);
+}
+
+int pf_cossin_batched(pf_context* ctx, const pf_pair_method* pm, double theta, int n, int batch, const double* dA,
+                      int64_t lda, int64_t strideA, const int* dSquaringsIn, int* dSquaringsOut, double* dC,
+                      double* dS, int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
+  if (!ctx || !pm || pm->n_pairs < 0 || pm->n_pairs > PF_MAX_TERMS || n < 0 || batch < 0 || !dC || !dS || lda < n ||
+      ldo < n || !(theta > 0))
+    return bad(status);
+  if (n > PF_SMALL_N) return bad(status);
+  if (batch == 0) return PF_OK;
+  const int64_t nn = (int64_t)n * n;
+  int* dJ = dSquaringsOut ? dSquaringsOut : static_cast<int*>(workspace(ctx, 0, sizeof(int) * batch));
+  double* norms = static_cast<double*>(workspace(ctx, 5, sizeof(double) * batch));
+  double* Bm = static_cast<double*>(workspace(ctx, 1, sizeof(double) * nn * batch));
+  double* B2 = static_cast<double*>(workspace(ctx, 2, sizeof(double) * nn * batch));
+  double* Sp = static_cast<double*>(workspace(ctx, 3, sizeof(double) * nn * batch));
+  double* T = static_cast<double*>(workspace(ctx, 4, sizeof(double) * nn * batch));
+  if (!dJ || !norms || !Bm || !B2 || !Sp || !T) return PF_ERR_CUDA;
+  if (dSquaringsIn) {
+    cudaMemcpyAsync(dJ, dSquaringsIn, sizeof(int) * batch, cudaMemcpyDeviceToDevice, ctx->stream);
+  } else {
+    pf::launch_one_norm(n, batch, dA, lda, strideA, norms, ctx->stream);
+    pf::launch_squarings(batch, norms, theta, dJ, ctx->stream);
+    ctx->launches += 2;
+  }
+  pf::launch_ldexp_batched(n, batch, dA, lda, strideA, dJ, Bm, n, nn, ctx->stream);
+  ctx->launches++;
+  gemm(ctx, n, n, n, batch, 1.0, Bm, n, nn, Bm, n, nn, 0.0, B2, n, nn, 0.0);
+  // cos = a0 I + sum cw X, S' = a1 I + sum sw X with X = (I + c^2 B^2)^{-1} (-c^2 B^2): the residual
+  // evaluator on B^2 with shifts -c^2 (Z_c = -X, see pf_b200.h)
+  std::vector<double> shifts(pm->n_pairs), weights(2 * pm->n_pairs);
+  for (int k = 0; k < pm->n_pairs; ++k) {
+    shifts[k] = -pm->c2[k];
+    weights[k] = pm->cw[k];
+    weights[pm->n_pairs + k] = pm->sw[k];
+  }
+  const double constants[2] = {pm->a0, pm->a1};
+  pf_method m{pm->n_pairs, shifts.data(), 2, weights.data(), 0, nullptr, constants, PF_FORM_RESIDUAL};
+  pf::SmallParams p{};
+  fill_method(&m, p);
+  p.n = n;
+  p.batch = batch;
+  p.mode = pf::kModeEval;
+  p.force_pivot = (flags & PF_FLAG_FORCE_PIVOT) ? 1 : 0;
+  p.A = B2;
+  p.lda = n;
+  p.strideA = nn;
+  p.out0 = T;   // C
+  p.out1 = Sp;  // S'
+  p.ldo = n;
+  p.strideOut = nn;
+  p.pivot_rel_tol = 1e-14;
+  int rc = launch_small(ctx, p);
+  if (rc) return rc;
+  rc = collect_status(ctx, batch, flags & ~PF_FLAG_ASYNC, status);
+  if (rc) return rc;
+  double* C = T;
+  double* S = B2;  // B^2 no longer needed
+  gemm(ctx, n, n, n, batch, 1.0, Bm, n, nn, Sp, n, nn, 0.0, S, n, nn, 0.0);
+  int jmax = 0;
+  rc = max_j(ctx, dJ, batch, &jmax);
+  if (rc) return rc;
+  double* C2 = Bm;  // B no longer needed
+  for (int s = 0; s < jmax; ++s) {
+    gemm(ctx, n, n, n, batch, 1.0, C, n, nn, C, n, nn, 0.0, C2, n, nn, 0.0, dJ, s, C);
+    gemm(ctx, n, n, n, batch, -1.0, S, n, nn, S, n, nn, 1.0, C2, n, nn, 0.0, dJ, s, nullptr);
+    gemm(ctx, n, n, n, batch, 2.0, S, n, nn, C, n, nn, 0.0, Sp, n, nn, 0.0, dJ, s, S);
+    std::swap(C, C2);
+    std::swap(S, Sp);
+  }
+  for (int b = 0; b < batch; ++b) {
+    cudaMemcpy2DAsync(dC + b * strideOut, sizeof(double) * ldo, C + b * nn, sizeof(double) * n, sizeof(double) * n, n,
+                      cudaMemcpyDeviceToDevice, ctx->stream);
+    cudaMemcpy2DAsync(dS + b * strideOut, sizeof(double) * ldo, S + b * nn, sizeof(double) * n, sizeof(double) * n, n,
+                      cudaMemcpyDeviceToDevice, ctx->stream);
+  }
+  return collect_status(ctx, batch, flags, status);
+}
+
+int pf_action_block(pf_context* ctx, const pf_method* m, int n, int k, const double* dA, int64_t lda,
+                    const double* dV, int64_t ldv, int substeps, double* dOut, int64_t ldo, int flags,
+                    pf_status* status) {
+  (void)ctx; (void)m; (void)n; (void)k; (void)dA; (void)lda; (void)dV; (void)ldv; (void)substeps; (void)dOut;
+  (void)ldo; (void)flags;
+  return bad(status);
+}
+
+int pf_lu_factor_batched(pf_context* ctx, int n, int batch, double* dA, int64_t lda, int64_t strideA, int* dPiv,
+                         double pivot_rel_tol, int flags, pf_status* status) {
+  (void)ctx; (void)n; (void)batch; (void)dA; (void)lda; (void)strideA; (void)dPiv; (void)pivot_rel_tol; (void)flags;
+  return bad(status);
+}
+
+int pf_lu_solve_batched(pf_context* ctx, int n, int k, int batch, const double* dLU, int64_t lda, int64_t strideLU,
+                        const int* dPiv, double* dRhs, int64_t ldr, int64_t strideR) {
+  (void)ctx; (void)n; (void)k; (void)batch; (void)dLU; (void)lda; (void)strideLU; (void)dPiv; (void)dRhs; (void)ldr;
+  (void)strideR;
+  return PF_ERR_BAD_ARGUMENT;
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// Internal kernel parameter blocks and launchers (not part of the C ABI).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "pf_b200.h"
+
+namespace pf {
+
+struct DevStatus;
+
+enum SmallMode {
+  kModeEval = 0,        // r(B) for every weight set, B = A (no scaling)
+  kModeScaledEval = 1,  // r(2^-j A) for every weight set, j from the norm or j_in
+  kModeExpm = 2,        // r(2^-j A) for set 0, then j squarings
+};
+
+struct SmallParams {
+  int n, batch, mode;
+  int n_terms, n_sets, has_poly, form, force_pivot;
+  const double* A;
+  int64_t lda, strideA;
+  const int* j_in;
+  int* j_out;
+  double* out0;
+  double* out1;
+  int64_t ldo, strideOut;
+  double theta, pivot_rel_tol;
+  double shifts[PF_MAX_TERMS];
+  double weights[2][PF_MAX_TERMS];
+  double poly[2][3];
+  double constant[2];
+  DevStatus* status;
+  int* first_error;
+};
+
+__global__ void small_eval_kernel(SmallParams p);
+size_t small_eval_smem_bytes();
+
+// Batched C = alpha * A B + beta * C + gamma * I (row-major, FP64 DMMA).
+struct GemmParams {
+  int m, n, k, batch;
+  double alpha, beta, gamma;
+  const double* A;
+  int64_t lda, strideA;
+  const double* B;
+  int64_t ldb, strideB;
+  double* C;
+  int64_t ldc, strideC;
+  // per-matrix step predication for recurrences with matrix-dependent step counts:
+  // matrix z is inactive at `step` when jmask && step >= jmask[z]; an inactive matrix gets
+  // C = pass (copy) when pass != nullptr, else C is left untouched.
+  const int* jmask;
+  int step;
+  const double* pass;
+};
+void launch_gemm(const GemmParams& p, cudaStream_t stream);
+
+// Batched 1-norm (column sums in ascending row order, then max).
+void launch_one_norm(int n, int batch, const double* A, int64_t lda, int64_t strideA, double* out,
+                     cudaStream_t stream);
+
+// Elementwise helpers used by the host-side compositions.
+// Y = alpha * X  (+ beta on the diagonal), batched n x n
+void launch_scale_add_identity(int n, int batch, double alpha, const double* X, int64_t ldx, int64_t strideX,
+                               double diag, double* Y, int64_t ldy, int64_t strideY, cudaStream_t stream);
+// Y = ldexp(X, -j_b) per matrix (j from device array)
+void launch_ldexp_batched(int n, int batch, const double* X, int64_t ldx, int64_t strideX, const int* j, double* Y,
+                          int64_t ldy, int64_t strideY, cudaStream_t stream);
+// squarings from norms: j_b = smallest j >= 0 with ldexp(norm_b, -j) <= theta
+void launch_squarings(int batch, const double* norms, double theta, int* j, cudaStream_t stream);
+
+}  // namespace pf
