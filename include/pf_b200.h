@@ -108,6 +108,10 @@ int pf_context_destroy(pf_context* ctx);
 int pf_context_set_stream(pf_context* ctx, void* stream);
 /* Number of kernels this context launched so far (bench evidence). */
 int64_t pf_context_launch_count(pf_context* ctx);
+/* Diagnostics: when non-NULL, the fused small-n kernel adds per-phase SM cycles (thread 0 of each
+ * CTA, clock64) into dev_counters[0..9]: norm, shift-matrix load, LU, diagonal inverses, RHS load,
+ * solve+accumulate, E formation, squaring, output. NULL disables (the default). */
+int pf_context_set_profile(pf_context* ctx, unsigned long long* dev_counters);
 
 /* 1-norm (max column sum, rows summed in ascending order as dense.cpp:54-62) of each matrix. */
 int pf_one_norm_batched(pf_context* ctx, int n, int batch, const double* dA, int64_t lda, int64_t strideA,

@@ -14,7 +14,8 @@ def __getattr__(name):
     # touching the device API loads the engine.
     if name in ("api", "eval_dense", "expm", "expm_phi1", "cossin", "solve_shifted", "one_norm", "gemm",
                 "EvalOptions", "Engine", "engine"):
-        from . import api
+        import importlib
 
+        api = importlib.import_module(__name__ + ".api")
         return api if name == "api" else getattr(api, name)
     raise AttributeError(name)

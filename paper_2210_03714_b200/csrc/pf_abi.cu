@@ -19,6 +19,7 @@ struct pf_context {
   int* h_first_error = nullptr;
   std::vector<void*> ws;
   std::vector<size_t> ws_bytes;
+  unsigned long long* prof = nullptr;
 };
 
 namespace {
@@ -127,8 +128,9 @@ int launch_small(pf_context* ctx, pf::SmallParams& p) {
   if (rc) return rc;
   p.status = ctx->status;
   p.first_error = ctx->first_error;
+  p.prof = ctx->prof;
   if (p.batch == 0) return PF_OK;
-  pf::small_eval_kernel<<<p.batch, 256, pf::small_eval_smem_bytes(), ctx->stream>>>(p);
+  pf::small_eval_kernel<<<p.batch, pf::small_eval_threads(), pf::small_eval_smem_bytes(), ctx->stream>>>(p);
   ctx->launches++;
   return cuda_fail(cudaGetLastError());
 }
@@ -228,6 +230,12 @@ int pf_context_set_stream(pf_context* ctx, void* stream) {
 }
 
 int64_t pf_context_launch_count(pf_context* ctx) { return ctx ? ctx->launches : 0; }
+
+int pf_context_set_profile(pf_context* ctx, unsigned long long* dev_counters) {
+  if (!ctx) return PF_ERR_BAD_ARGUMENT;
+  ctx->prof = dev_counters;
+  return PF_OK;
+}
 
 int pf_one_norm_batched(pf_context* ctx, int n, int batch, const double* dA, int64_t lda, int64_t strideA,
                         double* dNorm) {

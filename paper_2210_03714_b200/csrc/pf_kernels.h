@@ -33,10 +33,12 @@ struct SmallParams {
   double constant[2];
   DevStatus* status;
   int* first_error;
+  unsigned long long* prof;  // optional phase profile (diagnostics), nullptr normally
 };
 
 __global__ void small_eval_kernel(SmallParams p);
 size_t small_eval_smem_bytes();
+int small_eval_threads();
 
 // Batched C = alpha * A B + beta * C + gamma * I (row-major, FP64 DMMA).
 struct GemmParams {
