@@ -282,3 +282,26 @@ def test_native_library_is_loaded(dev):
     assert "paper_2210_03714_b200._native" in sys.modules
     with open("/proc/self/maps") as f:
         assert "libpfb200.so" in f.read()
+
+
+def test_golden_fixtures_on_device(dev, oracle):
+    """Device path against the frozen oracle outputs (tests/golden/)."""
+    import json
+    from pathlib import Path
+
+    from tests.golden.make_golden import inputs
+
+    gold = Path(__file__).resolve().parent / "golden"
+    meta = json.loads((gold / "golden.json").read_text())["cases"]
+    x = inputs()
+    g = lambda k: np.load(gold / meta[k]["file"])  # noqa: E731
+    for name in ("R4", "R8"):
+        assert oracle.rel_diff_1norm(dev.expm(x["cfg1_A"], name), g("cfg1_expm_%s" % name)) <= TOL
+        got = dev.expm(x["cfg2_first4_A"], name)
+        ref = g("cfg2_first4_expm_%s" % name)
+        assert max(oracle.rel_diff_1norm(got[i], ref[i]) for i in range(4)) <= TOL
+    assert oracle.rel_diff_1norm(dev.eval_dense("R8", x["eval24_B"], dev.EvalOptions(form=0)),
+                                 g("eval24_R8_plain")) <= TOL
+    assert oracle.rel_diff_1norm(dev.eval_dense("R8", x["eval24_B"], dev.EvalOptions(form=1)),
+                                 g("eval24_R8_residual")) <= TOL
+    assert oracle.rel_diff_1norm(dev.solve_shifted(x["pivot24_B"], 0.2), g("pivot24_solve_shifted_0.2")) <= 1e-13
