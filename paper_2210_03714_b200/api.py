@@ -330,6 +330,79 @@ def cossin(A: ArrayLike, method="R8", theta: Optional[float] = None, flags: int 
     return res
 
 
+def action(A: ArrayLike, V: ArrayLike, method="R8", substeps: Optional[int] = None, theta: Optional[float] = None,
+           form: int = RESIDUAL, flags: int = 0):
+    """exp(A) V by N-fold substepping V <- r(A/N) V with one LU per shift reused across substeps
+    (dense analogue of substep_action / ActionOperator, action.cpp:300-339). N defaults to
+    ceil(||A||_1 / theta_m) (select_method, action.cpp:398)."""
+    m = _resolve_method(method)
+    pk = PackedMethod(m, form)
+    eng = engine()
+    dA, host = _to_device(A)
+    dV, _ = _to_device(V)
+    if dA.dim() != 2 or dA.shape[0] != dA.shape[1] or dV.dim() not in (1, 2) or dV.shape[0] != dA.shape[0]:
+        raise PfError(Errc.LengthMismatch, "vector length mismatch")
+    vec = dV.dim() == 1
+    dV2 = dV.reshape(dV.shape[0], -1).contiguous()
+    n, k = dV2.shape
+    if substeps is None:
+        from .methods import substeps_for
+
+        substeps = substeps_for(one_norm(dA), _theta_for(m, theta))
+    out = torch.empty_like(dV2)
+    st = N.PfStatus()
+    rc = N.lib.pf_action_block(eng.h, pk.ptr(), n, k, dA.data_ptr(), n, dV2.data_ptr(), k, int(substeps),
+                               out.data_ptr(), k, flags, C.byref(st))
+    if rc:
+        _raise(rc, st, False)
+    res = out.reshape(-1) if vec else out
+    return _back(res.unsqueeze(0), host, True, A)
+
+
+class DenseLu:
+    """DenseLu (dense.hpp:46-59): PA = LU with partial pivoting, reusable across right-hand sides.
+    `piv` is the LAPACK-style 0-based swap sequence (the reference keeps it private, piv_)."""
+
+    def __init__(self, A: ArrayLike, pivot_rel_tol: float = 1e-14, flags: int = 0):
+        eng = engine()
+        dA, self._host = _to_device(A)
+        dA3, self._batched = _as_batch(dA)
+        self.lu = dA3.clone()
+        bsz, n = self.lu.shape[0], self.lu.shape[1]
+        self.piv = torch.empty(bsz, n, dtype=torch.int32, device=self.lu.device)
+        st = N.PfStatus()
+        rc = N.lib.pf_lu_factor_batched(eng.h, n, bsz, self.lu.data_ptr(), n, n * n, self.piv.data_ptr(),
+                                        float(pivot_rel_tol), flags, C.byref(st))
+        if rc:
+            _raise(rc, st, self._batched)
+
+    def solve_matrix(self, rhs: ArrayLike):
+        eng = engine()
+        dR, host = _to_device(rhs)
+        if dR.dim() == 1:
+            dR = dR.reshape(-1, 1)
+        r3 = dR if dR.dim() == 3 else dR.unsqueeze(0)
+        r3 = r3.clone()
+        bsz, n, k = r3.shape
+        rc = N.lib.pf_lu_solve_batched(eng.h, n, k, bsz, self.lu.data_ptr(), n, n * n, self.piv.data_ptr(),
+                                       r3.data_ptr(), k, n * k)
+        if rc:
+            _raise(rc, N.PfStatus(), self._batched)
+        out = r3 if dR.dim() == 3 else r3[0]
+        return out.cpu().numpy() if host and isinstance(rhs, np.ndarray) else (out.cpu() if host else out)
+
+    def solve(self, rhs: ArrayLike):
+        res = self.solve_matrix(rhs)
+        return res.reshape(-1) if hasattr(res, "reshape") else res
+
+    def factors(self):
+        lu = self.lu if self._batched else self.lu[0]
+        piv = self.piv if self._batched else self.piv[0]
+        if self._host:
+            return lu.cpu().numpy(), piv.cpu().numpy()
+        return lu, piv
+
+
 def one_norm(A: ArrayLike):
     eng = engine()
     dA, host = _to_device(A)

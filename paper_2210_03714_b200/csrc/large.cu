@@ -1,0 +1,435 @@
+// K3 / K4 / K6 building blocks for n > 128 (large dense and batched mid-size systems).
+//
+// Every system z of a batch lives in a workspace of order np (n rounded up to a multiple of 64,
+// identity padding), row-major, stride np^2. The host recursion (pf_large.cu) factors
+// M_z = P_z L_z U_z and solves L U X = P R with DMMA GEMMs for all off-diagonal work and the
+// kernels below for the 64 x 64 diagonal blocks:
+//   lu_base64_kernel    no-exchange LU of a 64 x 64 diagonal block (certified systems), plus the
+//                       explicit inverses of its L and U factors (used by every block solve)
+//   diag_inv64_kernel   the same inverses for an already factored block (pivoted fallback)
+//   apply_inv64_kernel  B <- Linv B, B <- Uinv B (left) or B <- B Uinv (right), in place, DMMA
+//   lu_pivot_kernel     genuine partial pivoting, unblocked, in the reference's operation order
+//                       (dense.cpp:105-132) -- the fallback for systems the certificate rejects
+//   form / certificate / accumulate elementwise kernels (HBM-bound)
+#include <climits>
+
+#include "pf_common.cuh"
+#include "pf_kernels.h"
+
+namespace pf {
+namespace {
+
+constexpr int B64 = 64;
+constexpr int L64 = B64 + 4;  // smem row stride
+
+__device__ __forceinline__ double ldexp_j(double x, int j) { return j == 0 ? x : ldexp(x, -j); }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+// LU of the 64 x 64 diagonal block at (off, off) of every system, no row exchanges, in place;
+// inverses of L (unit lower) and U written to inv + z * inv_stride + (off / 64) * 2 * 64 * 64.
+__global__ void __launch_bounds__(256) lu_base64_kernel(double* M, int64_t ld, int64_t strideM, int off,
+                                                        double* inv, int64_t inv_stride, int factor) {
+  __shared__ double s[B64 * L64];
+  __shared__ double prow[B64];
+  const int z = blockIdx.x;
+  double* a = M + (int64_t)z * strideM + (int64_t)off * ld + off;
+  for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
+    const int r = idx >> 6, c = idx & 63;
+    s[r * L64 + c] = a[(int64_t)r * ld + c];
+  }
+  __syncthreads();
+  if (factor) {
+    // right-looking, one column per step: 4 threads per row, 16 columns each
+    const int r = threadIdx.x >> 2, q = threadIdx.x & 3;
+    for (int m = 0; m < B64; ++m) {
+      if (threadIdx.x >= m && threadIdx.x < B64) prow[threadIdx.x] = s[m * L64 + threadIdx.x];
+      __syncthreads();
+      double f = 0.0;
+      if (r > m) {
+        f = s[r * L64 + m] * (1.0 / prow[m]);
+        for (int c = m + 1 + q; c < B64; c += 4) s[r * L64 + c] = fma(-f, prow[c], s[r * L64 + c]);
+      }
+      __syncthreads();
+      if (r > m && q == 0) s[r * L64 + m] = f;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
+      const int rr = idx >> 6, c = idx & 63;
+      a[(int64_t)rr * ld + c] = s[rr * L64 + c];
+    }
+  }
+  // inverses: threads 0-63 column l of L^-1, threads 64-127 column l of U^-1 (right-looking)
+  double* out = inv + (int64_t)z * inv_stride + (int64_t)(off / B64) * 2 * B64 * B64;
+  if (threadIdx.x < 2 * B64) {
+    const bool lower = threadIdx.x < B64;
+    const int l = threadIdx.x & 63;
+    double x[B64];
+#pragma unroll
+    for (int i = 0; i < B64; ++i) x[i] = (i == l) ? 1.0 : 0.0;
+    if (lower) {
+#pragma unroll
+      for (int m = 0; m < B64 - 1; ++m)
+#pragma unroll
+        for (int i = m + 1; i < B64; ++i) x[i] = fma(-s[i * L64 + m], x[m], x[i]);
+#pragma unroll
+      for (int i = 0; i < B64; ++i) out[i * B64 + l] = x[i];
+    } else {
+#pragma unroll
+      for (int m = B64 - 1; m >= 0; --m) {
+        x[m] = x[m] / s[m * L64 + m];
+#pragma unroll
+        for (int i = 0; i < m; ++i) x[i] = fma(-s[i * L64 + m], x[m], x[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < B64; ++i) out[B64 * B64 + i * B64 + l] = x[i];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// In-place block solve with an explicit 64 x 64 inverse T (T = Linv or Uinv of diagonal block blk):
+//   left : B[64 x cols] <- T B     (CTA = 64 columns)
+//   right: B[rows x 64] <- B T     (CTA = 64 rows)
+// 8 warps, each a 16 x 32 output tile (2 x 4 DMMA tiles), K = 64.
+__global__ void __launch_bounds__(256) apply_inv64_kernel(const double* inv, int64_t inv_stride, int blk, int upper,
+                                                          int right, double* Bm, int64_t ld, int64_t strideB,
+                                                          int extent) {
+  extern __shared__ __align__(16) double inv_smem[];
+  double* t = inv_smem;
+  double* bt = inv_smem + B64 * L64;
+  const int z = blockIdx.y;
+  const int tile = blockIdx.x;
+  const double* T = inv + (int64_t)z * inv_stride + (int64_t)blk * 2 * B64 * B64 + (upper ? B64 * B64 : 0);
+  double* b = Bm + (int64_t)z * strideB + (right ? (int64_t)tile * B64 * ld : (int64_t)tile * B64);
+  const int live = min(B64, extent - tile * B64);  // columns (left) or rows (right) in range
+  for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
+    const int r = idx >> 6, c = idx & 63;
+    t[r * L64 + c] = T[r * B64 + c];
+    const bool ok = right ? (r < live) : (c < live);
+    bt[r * L64 + c] = ok ? b[(int64_t)r * ld + c] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int rb = 16 * (warp >> 1), cb = 32 * (warp & 1);
+  const double* As = right ? bt : t;  // left: T * Bt ; right: Bt * T
+  const double* Bs = right ? t : bt;
+  double acc[2][4][2];
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int nj = 0; nj < 4; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < B64; k += 4) {
+    double af[2], bf[4];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) af[mi] = As[(rb + 8 * mi + g) * L64 + k + tq];
+#pragma unroll
+    for (int nj = 0; nj < 4; ++nj) bf[nj] = Bs[(k + tq) * L64 + cb + 8 * nj + g];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int nj = 0; nj < 4; ++nj) dmma(acc[mi][nj], af[mi], bf[nj]);
+  }
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int nj = 0; nj < 4; ++nj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = rb + 8 * mi + g, c = cb + 8 * nj + 2 * tq + e;
+        const bool ok = right ? (r < live) : (c < live);
+        if (ok) b[(int64_t)r * ld + c] = acc[mi][nj][e];
+      }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Genuine partial pivoting (reference operation order, dense.cpp:105-132) on the leading n x n of
+// each np x np system; one CTA of 1024 threads per system, global memory. Fallback only.
+__global__ void __launch_bounds__(1024) lu_pivot_kernel(double* M, int64_t ld, int64_t strideM, int n, int* piv,
+                                                        const double* tol, DevStatus* status, int* first_error) {
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
+  __shared__ int s_p;
+  __shared__ double s_best;
+  const int z = blockIdx.x;
+  double* a = M + (int64_t)z * strideM;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int col = 0; col < n; ++col) {
+    double best = -1.0;
+    int p = INT_MAX;
+    for (int r = col + threadIdx.x; r < n; r += blockDim.x) {
+      const double v = fabs(a[(int64_t)r * ld + col]);
+      if (v > best) {
+        best = v;
+        p = r;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int op = __shfl_xor_sync(0xffffffffu, p, o);
+      if (ob > best || (ob == best && op < p)) {
+        best = ob;
+        p = op;
+      }
+    }
+    if (lane == 0) {
+      red_v[warp] = best;
+      red_i[warp] = p;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double bb = red_v[0];
+      int pp = red_i[0];
+      for (int w = 1; w < nw; ++w)
+        if (red_v[w] > bb || (red_v[w] == bb && red_i[w] < pp)) {
+          bb = red_v[w];
+          pp = red_i[w];
+        }
+      s_best = bb;
+      s_p = pp;
+    }
+    __syncthreads();
+    const int pp = s_p;
+    const double bb = s_best;
+    if (bb <= tol[z]) {
+      if (threadIdx.x == 0) {
+        status[z].code = PF_ERR_SINGULAR_SHIFT;
+        status[z].column = col;
+        status[z].pivot_magnitude = bb;
+        atomicMin(first_error, z);
+      }
+      return;
+    }
+    if (pp != col)
+      for (int c = threadIdx.x; c < n; c += blockDim.x) {
+        const double tmp = a[(int64_t)pp * ld + c];
+        a[(int64_t)pp * ld + c] = a[(int64_t)col * ld + c];
+        a[(int64_t)col * ld + c] = tmp;
+      }
+    if (threadIdx.x == 0) piv[(int64_t)z * n + col] = pp;
+    __syncthreads();
+    const double inv_piv = 1.0 / a[(int64_t)col * ld + col];
+    for (int r = col + 1 + threadIdx.x; r < n; r += blockDim.x)
+      a[(int64_t)r * ld + col] = __dmul_rn(a[(int64_t)r * ld + col], inv_piv);
+    __syncthreads();
+    const int w = n - col - 1;
+    for (int64_t idx = threadIdx.x; idx < (int64_t)w * w; idx += blockDim.x) {
+      const int r = col + 1 + (int)(idx / w), c = col + 1 + (int)(idx % w);
+      const double f = a[(int64_t)r * ld + col];
+      if (f != 0.0) a[(int64_t)r * ld + c] = __dsub_rn(a[(int64_t)r * ld + c], __dmul_rn(f, a[(int64_t)col * ld + c]));
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// System z = i * batch + b (shift i, matrix b). M_z = (-c_i) 2^-j_b A_b + I (padding: identity);
+// also max|M_z| over the true block -> mx[z] (atomicMax on the bit pattern of a non-negative double).
+__global__ void form_shifted_kernel(const double* A, int64_t lda, int64_t strideA, int n, int np, int batch,
+                                    const double* shifts, const int* j, double* M, unsigned long long* mx) {
+  const int z = blockIdx.y;
+  const int b = z % batch, i = z / batch;
+  const double c = shifts[i];
+  const int jb = j ? j[b] : 0;
+  const double* a = A + (int64_t)b * strideA;
+  double* m = M + (int64_t)z * np * np;
+  double loc = 0.0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)np * np;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / np), col = (int)(idx % np);
+    double v;
+    if (r < n && col < n) {
+      v = __dmul_rn(ldexp_j(a[(int64_t)r * lda + col], jb), -c);  // (-c) B + I (dense.cpp:211-213)
+      if (r == col) v = __dadd_rn(v, 1.0);
+      loc = fmax(loc, fabs(v));
+    } else {
+      v = (r == col) ? 1.0 : 0.0;
+    }
+    m[idx] = v;
+  }
+  for (int o = 16; o > 0; o >>= 1) loc = fmax(loc, __shfl_xor_sync(0xffffffffu, loc, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(mx + z, (unsigned long long)__double_as_longlong(loc));
+}
+
+// Strict column diagonal dominance with margin (see small_eval.cu): ok[z] stays 1 only if every
+// column passes. One thread per column, rows summed in order.
+__global__ void certificate_kernel(const double* M, int np, int n, const unsigned long long* mx, double rel_tol,
+                                   int* ok) {
+  const int z = blockIdx.y;
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= n) return;
+  const double* m = M + (int64_t)z * np * np;
+  double off = 0.0;
+  for (int r = 0; r < n; ++r)
+    if (r != col) off += fabs(m[(int64_t)r * np + col]);
+  const double mxz = __longlong_as_double((long long)mx[z]);
+  const double margin = fabs(m[(int64_t)col * np + col]) - off;
+  const bool pass = (margin >= 1e-10 * mxz) && (margin > 2.0 * rel_tol * fmax(mxz, 1e-300)) && (mxz > 1e-250) &&
+                    (mxz < 1e250);
+  if (!pass) atomicAnd(ok + z, 0);
+}
+
+// R_z = c_i 2^-j A_b[perm] (residual) or P I (plain), padded np x cols (cols = np for matrices).
+// For the action, A_b is replaced by the block V (n x k): src_ld / src_stride describe it.
+__global__ void form_rhs_kernel(const double* src, int64_t lds, int64_t strideS, int n, int np, int cols, int ncols_true,
+                                int batch, const double* shifts, const int* j, int residual, const int* perm,
+                                double* R, int64_t strideR) {
+  const int z = blockIdx.y;
+  const int b = z % batch, i = z / batch;
+  const double c = shifts[i];
+  const int jb = j ? j[b] : 0;
+  const double* s = src + (int64_t)b * strideS;
+  double* rz = R + (int64_t)z * strideR;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)np * cols;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / cols), col = (int)(idx % cols);
+    double v = 0.0;
+    if (r < n && col < ncols_true) {
+      const int pr = perm ? perm[(int64_t)z * n + r] : r;
+      if (residual)
+        v = __dmul_rn(ldexp_j(s[(int64_t)pr * lds + col], jb), c);
+      else
+        v = (pr == col) ? 1.0 : 0.0;
+    }
+    rz[idx] = v;
+  }
+}
+
+// out_s[b] = sum_i (w_{s,i} X_{i,b}) in ascending i, then + poly (const I + d1 B + d2 B^2) -- the
+// fixed-order reduction and poly_part of eval_dense (dense.cpp:176-189, 217, 245-250).
+// term_z[t] = system slot of term t (the X of shift t lives at X + (slot * batch + b) * strideX),
+// or -1 for a plain-form zero shift (the w I term).
+__global__ void accumulate_kernel(const double* X, int64_t xld, int64_t strideX, int n, int cols, int batch,
+                                  int n_terms, const int* term_z, const double* w, int add_poly, double constant,
+                                  double d1, double d2, const double* Bsrc, int64_t bld, int64_t strideBs,
+                                  const int* j, const double* B2, int64_t b2ld, int64_t strideB2, double* out,
+                                  int64_t ldo, int64_t strideOut) {
+  const int b = blockIdx.y;
+  const int jb = j ? j[b] : 0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)n * cols;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / cols), col = (int)(idx % cols);
+    double acc = 0.0;
+    for (int t = 0; t < n_terms; ++t) {
+      const int z = term_z[t];
+      double tv;
+      if (z < 0)
+        tv = (r == col) ? __dadd_rn(0.0, w[t]) : 0.0;
+      else
+        tv = __dmul_rn(X[(int64_t)(z * batch + b) * strideX + (int64_t)r * xld + col], w[t]);
+      acc = (t == 0) ? tv : __dadd_rn(acc, tv);
+    }
+    if (add_poly) {
+      double poly = (r == col) ? __dadd_rn(0.0, constant) : 0.0;
+      if (d1 != 0.0 || d2 != 0.0)
+        poly = __dadd_rn(poly, __dmul_rn(d1, ldexp_j(Bsrc[(int64_t)b * strideBs + (int64_t)r * bld + col], jb)));
+      if (d2 != 0.0) poly = __dadd_rn(poly, __dmul_rn(d2, B2[(int64_t)b * strideB2 + (int64_t)r * b2ld + col]));
+      acc = __dadd_rn(acc, poly);
+    }
+    out[(int64_t)b * strideOut + (int64_t)r * ldo + col] = acc;
+  }
+}
+
+// perm_z from the swap sequence piv_z (LAPACK style): perm[r] = row of the original RHS in row r.
+__global__ void perm_from_piv_kernel(const int* piv, int n, int* perm) {
+  const int z = blockIdx.x;
+  if (threadIdx.x != 0) return;
+  int* p = perm + (int64_t)z * n;
+  for (int r = 0; r < n; ++r) p[r] = r;
+  for (int r = 0; r < n; ++r) {
+    const int q = piv[(int64_t)z * n + r];
+    const int t = p[r];
+    p[r] = p[q];
+    p[q] = t;
+  }
+}
+
+// copy (strided 2-D, batched) with optional scale: Y = s X
+__global__ void copy2d_kernel(int rows, int cols, double s, const double* X, int64_t ldx, int64_t strideX, double* Y,
+                              int64_t ldy, int64_t strideY) {
+  const int b = blockIdx.y;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)rows * cols;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / cols), c = (int)(idx % cols);
+    const double v = X[(int64_t)b * strideX + (int64_t)r * ldx + c];
+    Y[(int64_t)b * strideY + (int64_t)r * ldy + c] = s == 1.0 ? v : __dmul_rn(s, v);
+  }
+}
+
+// B = A * inv elementwise (substep_action's A * (1.0 / N), action.cpp:330-334), padded with zeros.
+__global__ void scale_pad_kernel(const double* A, int64_t lda, int n, int np, double s, double* B) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)np * np;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / np), c = (int)(idx % np);
+    B[idx] = (r < n && c < n) ? __dmul_rn(A[(int64_t)r * lda + c], s) : 0.0;
+  }
+}
+
+// M_z = A_z with identity padding; max|a| over the true block -> mx[z]
+__global__ void load_padded_kernel(const double* A, int64_t lda, int64_t strideA, int n, int np, double* M,
+                                   unsigned long long* mx) {
+  const int z = blockIdx.y;
+  const double* a = A + (int64_t)z * strideA;
+  double* m = M + (int64_t)z * np * np;
+  double loc = 0.0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)np * np;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / np), c = (int)(idx % np);
+    double v;
+    if (r < n && c < n) {
+      v = a[(int64_t)r * lda + c];
+      loc = fmax(loc, fabs(v));
+    } else {
+      v = (r == c) ? 1.0 : 0.0;
+    }
+    m[idx] = v;
+  }
+  for (int o = 16; o > 0; o >>= 1) loc = fmax(loc, __shfl_xor_sync(0xffffffffu, loc, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(mx + z, (unsigned long long)__double_as_longlong(loc));
+}
+
+__global__ void iota_kernel(int* p, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[(int64_t)blockIdx.y * n + i] = i;
+}
+
+size_t apply_inv64_smem_bytes() { return sizeof(double) * 2 * B64 * L64; }
+
+__global__ void fill_int_kernel(int* p, int count, int v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) p[i] = v;
+}
+
+}  // namespace pf
+
+namespace pf {
+// action step: out = sum_t w_t T_t (T_t = R_z, or X itself for a plain-form zero shift), then
+// + constant X (+ d1 BX + d2 B(BX)) -- assemble_action's fixed-order reduction (action.cpp:265-282).
+__global__ void action_accumulate_kernel(const double* R, int64_t rld, int64_t strideR, const double* X, int64_t xld,
+                                         int n, int k, int n_terms, const int* term_z, const double* w, int add_poly,
+                                         double constant, int hybrid, double d1, double d2, const double* BX,
+                                         const double* B2X, double* out, int64_t ldo) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)n * k;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / k), c = (int)(idx % k);
+    const double xv = X[(int64_t)r * xld + c];
+    double acc = 0.0;
+    for (int t = 0; t < n_terms; ++t) {
+      const int z = term_z[t];
+      const double tv = __dmul_rn(z < 0 ? xv : R[(int64_t)z * strideR + (int64_t)r * rld + c], w[t]);
+      acc = (t == 0) ? tv : __dadd_rn(acc, tv);
+    }
+    if (add_poly) {
+      acc = __dadd_rn(acc, __dmul_rn(constant, xv));
+      if (hybrid) {
+        const double bx = BX[(int64_t)r * xld + c], b2x = B2X[(int64_t)r * xld + c];
+        acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(d1, bx), __dmul_rn(d2, b2x)));
+      }
+    }
+    out[(int64_t)r * ldo + c] = acc;
+  }
+}
+}  // namespace pf

@@ -6,25 +6,10 @@
 #include <mutex>
 #include <vector>
 
-#include "pf_common.cuh"
-#include "pf_kernels.h"
+#include "pf_host.h"
 
-struct pf_context {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  int64_t launches = 0;
-  pf::DevStatus* status = nullptr;
-  int status_cap = 0;
-  int* first_error = nullptr;
-  int* h_first_error = nullptr;
-  std::vector<void*> ws;
-  std::vector<size_t> ws_bytes;
-  unsigned long long* prof = nullptr;
-};
-
-namespace {
-
-using pf::DevStatus;
+namespace pf {
+namespace host {
 
 int cuda_fail(cudaError_t e) { return e == cudaSuccess ? PF_OK : PF_ERR_CUDA; }
 
@@ -56,7 +41,7 @@ int ensure_status(pf_context* ctx, int batch) {
     }
     ctx->status = nullptr;
     int cap = std::max(batch, 1024);
-    if (cudaMalloc(&ctx->status, sizeof(DevStatus) * cap) != cudaSuccess) return PF_ERR_CUDA;
+    if (cudaMalloc(&ctx->status, sizeof(pf::DevStatus) * cap) != cudaSuccess) return PF_ERR_CUDA;
     ctx->status_cap = cap;
   }
   return cuda_fail(cudaMemsetAsync(ctx->first_error, 0x7f, sizeof(int), ctx->stream));
@@ -74,7 +59,7 @@ int collect_status(pf_context* ctx, int batch, int flags, pf_status* out) {
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return PF_ERR_CUDA;
   const int b = *ctx->h_first_error;
   if (b < 0 || b >= batch) return PF_OK;
-  DevStatus st;
+  pf::DevStatus st;
   if (cudaMemcpy(&st, ctx->status + b, sizeof(st), cudaMemcpyDeviceToHost) != cudaSuccess) return PF_ERR_CUDA;
   if (out) {
     out->code = st.code;
@@ -137,7 +122,7 @@ int launch_small(pf_context* ctx, pf::SmallParams& p) {
 
 void gemm(pf_context* ctx, int m, int n, int k, int batch, double alpha, const double* A, int64_t lda,
           int64_t sA, const double* B, int64_t ldb, int64_t sB, double beta, double* C, int64_t ldc, int64_t sC,
-          double gamma, const int* jmask = nullptr, int step = 0, const double* pass = nullptr) {
+          double gamma, const int* jmask, int step, const double* pass) {
   pf::GemmParams g{};
   g.m = m;
   g.n = n;
@@ -173,7 +158,10 @@ int max_j(pf_context* ctx, const int* dJ, int batch, int* out) {
   return PF_OK;
 }
 
-}  // namespace
+}  // namespace host
+}  // namespace pf
+
+using namespace pf::host;
 
 extern "C" {
 
@@ -260,7 +248,11 @@ int pf_eval_dense_batched(pf_context* ctx, const pf_method* m, int n, int batch,
                           pf_status* status) {
   pf::SmallParams p{};
   if (!ctx || n < 0 || batch < 0 || !dOuts || !fill_method(m, p) || ldb < n || ldo < n) return bad(status);
-  if (n > PF_SMALL_N) return bad(status);  // large-n path: pf_large.cu (round 1: small only)
+  if (n > PF_SMALL_N) {
+    const int rc = large_eval(ctx, m, n, batch, dB, ldb, strideB, nullptr, dOuts, ldo, strideOut, flags, status);
+    if (rc) return rc;
+    return collect_status(ctx, 0, flags, status);
+  }
   p.n = n;
   p.batch = batch;
   p.mode = pf::kModeEval;
@@ -278,13 +270,98 @@ int pf_eval_dense_batched(pf_context* ctx, const pf_method* m, int n, int batch,
   return collect_status(ctx, batch, flags, status);
 }
 
+namespace {
+
+// j_b for every matrix into dJ (device): copied from dJin, or the smallest j >= 0 with
+// ldexp(||A_b||_1, -j) <= theta (one-norm kernel, dense.cpp:54-62, then the exact count).
+void squaring_counts(pf_context* ctx, int n, int batch, const double* dA, int64_t lda, int64_t strideA, double theta,
+                     const int* dJin, int* dJ) {
+  if (dJin) {
+    if (dJin != dJ) cudaMemcpyAsync(dJ, dJin, sizeof(int) * batch, cudaMemcpyDeviceToDevice, ctx->stream);
+    return;
+  }
+  double* norms = static_cast<double*>(workspace(ctx, kWsNorm, sizeof(double) * batch));
+  pf::launch_one_norm(n, batch, dA, lda, strideA, norms, ctx->stream);
+  pf::launch_squarings(batch, norms, theta, dJ, ctx->stream);
+  ctx->launches += 2;
+}
+
+// outs[s] = r_s(2^-j_b A_b) for every weight set; j_b written to dJ (device, required).
+int eval_scaled(pf_context* ctx, const pf_method* m, double theta, int n, int batch, const double* dA, int64_t lda,
+                int64_t strideA, const int* dJin, int* dJ, double* const* outs, int64_t ldo, int64_t strideOut,
+                int flags, pf_status* status) {
+  if (n > PF_SMALL_N) {
+    squaring_counts(ctx, n, batch, dA, lda, strideA, theta, dJin, dJ);
+    const int rc = large_eval(ctx, m, n, batch, dA, lda, strideA, dJ, outs, ldo, strideOut, flags, status);
+    if (rc) return rc;
+    return collect_status(ctx, 0, flags, status);
+  }
+  pf::SmallParams p{};
+  fill_method(m, p);
+  p.n = n;
+  p.batch = batch;
+  p.mode = pf::kModeScaledEval;
+  p.force_pivot = (flags & PF_FLAG_FORCE_PIVOT) ? 1 : 0;
+  p.A = dA;
+  p.lda = lda;
+  p.strideA = strideA;
+  p.j_in = dJin;
+  p.j_out = dJ;
+  p.out0 = outs[0];
+  p.out1 = m->n_sets > 1 ? outs[1] : nullptr;
+  p.ldo = ldo;
+  p.strideOut = strideOut;
+  p.theta = theta;
+  p.pivot_rel_tol = 1e-14;
+  int rc = launch_small(ctx, p);
+  if (rc) return rc;
+  return collect_status(ctx, batch, flags, status);
+}
+
+// copy batch of n x n (contiguous, ld n) into a strided destination
+void copy_out(pf_context* ctx, int n, int batch, const double* src, double* dst, int64_t ldo, int64_t strideOut) {
+  const int64_t nn = (int64_t)n * n;
+  if (ldo == n && strideOut == nn) {
+    if (src != dst) cudaMemcpyAsync(dst, src, sizeof(double) * nn * batch, cudaMemcpyDeviceToDevice, ctx->stream);
+    return;
+  }
+  for (int b = 0; b < batch; ++b)
+    cudaMemcpy2DAsync(dst + b * strideOut, sizeof(double) * ldo, src + b * nn, sizeof(double) * n, sizeof(double) * n,
+                      n, cudaMemcpyDeviceToDevice, ctx->stream);
+}
+
+}  // namespace
+
 int pf_expm_batched(pf_context* ctx, const pf_method* m, double theta, int n, int batch, const double* dA,
                     int64_t lda, int64_t strideA, const int* dSquaringsIn, int* dSquaringsOut, double* dOut,
                     int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
   pf::SmallParams p{};
   if (!ctx || n < 0 || batch < 0 || !dOut || !fill_method(m, p) || lda < n || ldo < n || !(theta > 0))
     return bad(status);
-  if (n > PF_SMALL_N) return bad(status);
+  if (batch == 0 || n == 0) return PF_OK;
+  if (n > PF_SMALL_N) {
+    // eval (set 0) + squaring chain on the DMMA GEMM with per-matrix step counts
+    pf_method m0 = *m;
+    m0.n_sets = 1;
+    const int64_t nn = (int64_t)n * n;
+    int* dJ = dSquaringsOut ? dSquaringsOut : static_cast<int*>(workspace(ctx, kWsJ, sizeof(int) * batch));
+    double* E = static_cast<double*>(workspace(ctx, kWsT1, sizeof(double) * nn * batch));
+    double* T = static_cast<double*>(workspace(ctx, kWsT2, sizeof(double) * nn * batch));
+    if (!dJ || !E || !T) return PF_ERR_CUDA;
+    double* outs[1] = {E};
+    int rc = eval_scaled(ctx, &m0, theta, n, batch, dA, lda, strideA, dSquaringsIn, dJ, outs, n, nn,
+                         flags & ~PF_FLAG_ASYNC, status);
+    if (rc) return rc;
+    int jmax = 0;
+    rc = max_j(ctx, dJ, batch, &jmax);
+    if (rc) return rc;
+    for (int s = 0; s < jmax; ++s) {
+      gemm(ctx, n, n, n, batch, 1.0, E, n, nn, E, n, nn, 0.0, T, n, nn, 0.0, dJ, s, E);
+      std::swap(E, T);
+    }
+    copy_out(ctx, n, batch, E, dOut, ldo, strideOut);
+    return collect_status(ctx, 0, flags, status);
+  }
   p.n = n;
   p.batch = batch;
   p.mode = pf::kModeExpm;
@@ -312,9 +389,6 @@ int pf_solve_shifted_batched(pf_context* ctx, int n, int batch, const double* dB
   const double w = 1.0, zero = 0.0;
   pf_method m{1, &c, 1, &w, 0, nullptr, &zero, PF_FORM_PLAIN};
   double* outs[1] = {dOut};
-  if (c == 0.0) {  // the evaluator folds a zero shift into w I; same result I
-    return pf_eval_dense_batched(ctx, &m, n, batch, dB, ldb, strideB, outs, ldo, strideOut, flags, status);
-  }
   int rc = pf_eval_dense_batched(ctx, &m, n, batch, dB, ldb, strideB, outs, ldo, strideOut, flags, status);
   if (status && rc) status->shift_index = 0;
   return rc;
@@ -327,42 +401,22 @@ int pf_expm_phi1_batched(pf_context* ctx, const pf_method* m, double theta, int 
   if (!ctx || n < 0 || batch < 0 || !dE || !dPhi || !fill_method(m, p) || m->n_sets != 2 || lda < n || ldo < n ||
       !(theta > 0))
     return bad(status);
-  if (n > PF_SMALL_N) return bad(status);
-  if (batch == 0) return PF_OK;
-  int* dJ = dSquaringsOut ? dSquaringsOut : static_cast<int*>(workspace(ctx, 0, sizeof(int) * batch));
+  if (batch == 0 || n == 0) return PF_OK;
+  int* dJ = dSquaringsOut ? dSquaringsOut : static_cast<int*>(workspace(ctx, kWsJ, sizeof(int) * batch));
   const int64_t nn = (int64_t)n * n;
-  double* t1 = static_cast<double*>(workspace(ctx, 1, sizeof(double) * nn * batch));
-  double* t2 = static_cast<double*>(workspace(ctx, 2, sizeof(double) * nn * batch));
-  double* t3 = static_cast<double*>(workspace(ctx, 3, sizeof(double) * nn * batch));
-  if (!dJ || !t1 || !t2 || !t3) return PF_ERR_CUDA;
-  p.n = n;
-  p.batch = batch;
-  p.mode = pf::kModeScaledEval;
-  p.force_pivot = (flags & PF_FLAG_FORCE_PIVOT) ? 1 : 0;
-  p.A = dA;
-  p.lda = lda;
-  p.strideA = strideA;
-  p.j_in = dSquaringsIn;
-  p.j_out = dJ;
-  p.out0 = t1;  // E
-  p.out1 = t2;  // Phi
-  p.ldo = n;
-  p.strideOut = nn;
-  p.theta = theta;
-  p.pivot_rel_tol = 1e-14;
-  int rc = launch_small(ctx, p);
+  double* E = static_cast<double*>(workspace(ctx, kWsT1, sizeof(double) * nn * batch));
+  double* Phi = static_cast<double*>(workspace(ctx, kWsT2, sizeof(double) * nn * batch));
+  double* spare = static_cast<double*>(workspace(ctx, kWsT3, sizeof(double) * nn * batch));
+  double* T = static_cast<double*>(workspace(ctx, kWsT4, sizeof(double) * nn * batch));
+  if (!dJ || !E || !Phi || !spare || !T) return PF_ERR_CUDA;
+  double* outs[2] = {E, Phi};
+  int rc = eval_scaled(ctx, m, theta, n, batch, dA, lda, strideA, dSquaringsIn, dJ, outs, n, nn,
+                       flags & ~PF_FLAG_ASYNC, status);
   if (rc) return rc;
-  rc = collect_status(ctx, batch, flags & ~PF_FLAG_ASYNC, status);
-  if (rc) return rc;
-  if (dSquaringsIn && dSquaringsIn != dJ)
-    cudaMemcpyAsync(dJ, dSquaringsIn, sizeof(int) * batch, cudaMemcpyDeviceToDevice, ctx->stream);
   int jmax = 0;
   rc = max_j(ctx, dJ, batch, &jmax);
   if (rc) return rc;
   // Phi <- 0.5 (E + I) Phi ; E <- E E   (per-matrix step count j_b)
-  double *E = t1, *Phi = t2, *spare = t3;
-  double* T = static_cast<double*>(workspace(ctx, 4, sizeof(double) * nn * batch));
-  if (!T) return PF_ERR_CUDA;
   for (int s = 0; s < jmax; ++s) {
     pf::launch_scale_add_identity(n, batch, 1.0, E, n, nn, 1.0, T, n, nn, ctx->stream);
     ctx->launches++;
@@ -371,18 +425,9 @@ int pf_expm_phi1_batched(pf_context* ctx, const pf_method* m, double theta, int 
     gemm(ctx, n, n, n, batch, 1.0, E, n, nn, E, n, nn, 0.0, spare, n, nn, 0.0, dJ, s, E);
     std::swap(E, spare);
   }
-  if (strideOut != nn || ldo != n) {
-    for (int b = 0; b < batch; ++b) {
-      cudaMemcpy2DAsync(dE + b * strideOut, sizeof(double) * ldo, E + b * nn, sizeof(double) * n, sizeof(double) * n,
-                        n, cudaMemcpyDeviceToDevice, ctx->stream);
-      cudaMemcpy2DAsync(dPhi + b * strideOut, sizeof(double) * ldo, Phi + b * nn, sizeof(double) * n,
-                        sizeof(double) * n, n, cudaMemcpyDeviceToDevice, ctx->stream);
-    }
-  } else {
-    cudaMemcpyAsync(dE, E, sizeof(double) * nn * batch, cudaMemcpyDeviceToDevice, ctx->stream);
-    cudaMemcpyAsync(dPhi, Phi, sizeof(double) * nn * batch, cudaMemcpyDeviceToDevice, ctx->stream);
-  }
-  return collect_status(ctx, batch, flags, status);
+  copy_out(ctx, n, batch, E, dE, ldo, strideOut);
+  copy_out(ctx, n, batch, Phi, dPhi, ldo, strideOut);
+  return collect_status(ctx, 0, flags, status);
 }
 
 int pf_cossin_batched(pf_context* ctx, const pf_pair_method* pm, double theta, int n, int batch, const double* dA,
@@ -391,23 +436,15 @@ int pf_cossin_batched(pf_context* ctx, const pf_pair_method* pm, double theta, i
   if (!ctx || !pm || pm->n_pairs < 0 || pm->n_pairs > PF_MAX_TERMS || n < 0 || batch < 0 || !dC || !dS || lda < n ||
       ldo < n || !(theta > 0))
     return bad(status);
-  if (n > PF_SMALL_N) return bad(status);
-  if (batch == 0) return PF_OK;
+  if (batch == 0 || n == 0) return PF_OK;
   const int64_t nn = (int64_t)n * n;
-  int* dJ = dSquaringsOut ? dSquaringsOut : static_cast<int*>(workspace(ctx, 0, sizeof(int) * batch));
-  double* norms = static_cast<double*>(workspace(ctx, 5, sizeof(double) * batch));
-  double* Bm = static_cast<double*>(workspace(ctx, 1, sizeof(double) * nn * batch));
-  double* B2 = static_cast<double*>(workspace(ctx, 2, sizeof(double) * nn * batch));
-  double* Sp = static_cast<double*>(workspace(ctx, 3, sizeof(double) * nn * batch));
-  double* T = static_cast<double*>(workspace(ctx, 4, sizeof(double) * nn * batch));
-  if (!dJ || !norms || !Bm || !B2 || !Sp || !T) return PF_ERR_CUDA;
-  if (dSquaringsIn) {
-    cudaMemcpyAsync(dJ, dSquaringsIn, sizeof(int) * batch, cudaMemcpyDeviceToDevice, ctx->stream);
-  } else {
-    pf::launch_one_norm(n, batch, dA, lda, strideA, norms, ctx->stream);
-    pf::launch_squarings(batch, norms, theta, dJ, ctx->stream);
-    ctx->launches += 2;
-  }
+  int* dJ = dSquaringsOut ? dSquaringsOut : static_cast<int*>(workspace(ctx, kWsJ, sizeof(int) * batch));
+  double* Bm = static_cast<double*>(workspace(ctx, kWsT1, sizeof(double) * nn * batch));
+  double* B2 = static_cast<double*>(workspace(ctx, kWsT2, sizeof(double) * nn * batch));
+  double* Sp = static_cast<double*>(workspace(ctx, kWsT3, sizeof(double) * nn * batch));
+  double* T = static_cast<double*>(workspace(ctx, kWsT4, sizeof(double) * nn * batch));
+  if (!dJ || !Bm || !B2 || !Sp || !T) return PF_ERR_CUDA;
+  squaring_counts(ctx, n, batch, dA, lda, strideA, theta, dSquaringsIn, dJ);
   pf::launch_ldexp_batched(n, batch, dA, lda, strideA, dJ, Bm, n, nn, ctx->stream);
   ctx->launches++;
   gemm(ctx, n, n, n, batch, 1.0, Bm, n, nn, Bm, n, nn, 0.0, B2, n, nn, 0.0);
@@ -421,23 +458,8 @@ int pf_cossin_batched(pf_context* ctx, const pf_pair_method* pm, double theta, i
   }
   const double constants[2] = {pm->a0, pm->a1};
   pf_method m{pm->n_pairs, shifts.data(), 2, weights.data(), 0, nullptr, constants, PF_FORM_RESIDUAL};
-  pf::SmallParams p{};
-  fill_method(&m, p);
-  p.n = n;
-  p.batch = batch;
-  p.mode = pf::kModeEval;
-  p.force_pivot = (flags & PF_FLAG_FORCE_PIVOT) ? 1 : 0;
-  p.A = B2;
-  p.lda = n;
-  p.strideA = nn;
-  p.out0 = T;   // C
-  p.out1 = Sp;  // S'
-  p.ldo = n;
-  p.strideOut = nn;
-  p.pivot_rel_tol = 1e-14;
-  int rc = launch_small(ctx, p);
-  if (rc) return rc;
-  rc = collect_status(ctx, batch, flags & ~PF_FLAG_ASYNC, status);
+  double* outs[2] = {T, Sp};  // C, S'
+  int rc = pf_eval_dense_batched(ctx, &m, n, batch, B2, n, nn, outs, n, nn, flags & ~PF_FLAG_ASYNC, status);
   if (rc) return rc;
   double* C = T;
   double* S = B2;  // B^2 no longer needed
@@ -453,34 +475,38 @@ int pf_cossin_batched(pf_context* ctx, const pf_pair_method* pm, double theta, i
     std::swap(C, C2);
     std::swap(S, Sp);
   }
-  for (int b = 0; b < batch; ++b) {
-    cudaMemcpy2DAsync(dC + b * strideOut, sizeof(double) * ldo, C + b * nn, sizeof(double) * n, sizeof(double) * n, n,
-                      cudaMemcpyDeviceToDevice, ctx->stream);
-    cudaMemcpy2DAsync(dS + b * strideOut, sizeof(double) * ldo, S + b * nn, sizeof(double) * n, sizeof(double) * n, n,
-                      cudaMemcpyDeviceToDevice, ctx->stream);
-  }
-  return collect_status(ctx, batch, flags, status);
+  copy_out(ctx, n, batch, C, dC, ldo, strideOut);
+  copy_out(ctx, n, batch, S, dS, ldo, strideOut);
+  return collect_status(ctx, 0, flags, status);
 }
 
 int pf_action_block(pf_context* ctx, const pf_method* m, int n, int k, const double* dA, int64_t lda,
                     const double* dV, int64_t ldv, int substeps, double* dOut, int64_t ldo, int flags,
                     pf_status* status) {
-  (void)ctx; (void)m; (void)n; (void)k; (void)dA; (void)lda; (void)dV; (void)ldv; (void)substeps; (void)dOut;
-  (void)ldo; (void)flags;
-  return bad(status);
+  pf::SmallParams p{};
+  if (!ctx || !fill_method(m, p) || n < 0 || k < 0 || substeps < 1 || lda < n || ldv < k || ldo < k || !dA || !dV ||
+      !dOut)
+    return bad(status);
+  if (n == 0 || k == 0) return PF_OK;
+  const int rc = large_action(ctx, m, n, k, dA, lda, dV, ldv, substeps, dOut, ldo, flags, status);
+  if (rc) return rc;
+  return collect_status(ctx, 0, flags, status);
 }
 
 int pf_lu_factor_batched(pf_context* ctx, int n, int batch, double* dA, int64_t lda, int64_t strideA, int* dPiv,
                          double pivot_rel_tol, int flags, pf_status* status) {
-  (void)ctx; (void)n; (void)batch; (void)dA; (void)lda; (void)strideA; (void)dPiv; (void)pivot_rel_tol; (void)flags;
-  return bad(status);
+  if (!ctx || n < 0 || batch < 0 || lda < n || !(pivot_rel_tol >= 0)) return bad(status);
+  const int rc = large_lu_factor(ctx, n, batch, dA, lda, strideA, dPiv, pivot_rel_tol, flags, status);
+  if (rc) return rc;
+  return collect_status(ctx, 0, flags, status);
 }
 
 int pf_lu_solve_batched(pf_context* ctx, int n, int k, int batch, const double* dLU, int64_t lda, int64_t strideLU,
                         const int* dPiv, double* dRhs, int64_t ldr, int64_t strideR) {
-  (void)ctx; (void)n; (void)k; (void)batch; (void)dLU; (void)lda; (void)strideLU; (void)dPiv; (void)dRhs; (void)ldr;
-  (void)strideR;
-  return PF_ERR_BAD_ARGUMENT;
+  if (!ctx || n < 0 || k < 0 || batch < 0 || lda < n || ldr < k || !dPiv) return PF_ERR_BAD_ARGUMENT;
+  const int rc = large_lu_solve(ctx, n, k, batch, dLU, lda, strideLU, dPiv, dRhs, ldr, strideR);
+  if (rc) return rc;
+  return collect_status(ctx, 0, 0, nullptr);
 }
 
 }  // extern "C"

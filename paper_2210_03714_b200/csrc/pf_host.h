@@ -1,0 +1,70 @@
+// Internal host-side declarations shared by the C-ABI translation units (not part of the ABI).
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "pf_common.cuh"
+#include "pf_kernels.h"
+
+struct pf_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  pf::DevStatus* status = nullptr;
+  int status_cap = 0;
+  int* first_error = nullptr;
+  int* h_first_error = nullptr;
+  std::vector<void*> ws;
+  std::vector<size_t> ws_bytes;
+  unsigned long long* prof = nullptr;
+};
+
+namespace pf {
+namespace host {
+
+int cuda_fail(cudaError_t e);
+void* workspace(pf_context* ctx, int slot, size_t bytes);
+int ensure_status(pf_context* ctx, int batch);
+int collect_status(pf_context* ctx, int batch, int flags, pf_status* out);
+int bad(pf_status* st);
+bool fill_method(const pf_method* m, SmallParams& p);
+int launch_small(pf_context* ctx, SmallParams& p);
+void gemm(pf_context* ctx, int m, int n, int k, int batch, double alpha, const double* A, int64_t lda, int64_t sA,
+          const double* B, int64_t ldb, int64_t sB, double beta, double* C, int64_t ldc, int64_t sC, double gamma,
+          const int* jmask = nullptr, int step = 0, const double* pass = nullptr);
+int max_j(pf_context* ctx, const int* dJ, int batch, int* out);
+
+// workspace slots (each slot is an independently grown device buffer)
+enum Slot {
+  kWsJ = 0,
+  kWsT1 = 1,
+  kWsT2 = 2,
+  kWsT3 = 3,
+  kWsT4 = 4,
+  kWsNorm = 5,
+  kWsLargeM = 10,
+  kWsLargeR = 11,
+  kWsLargeInv = 12,
+  kWsLargeAux = 13,
+  kWsLargePiv = 14,
+  kWsLargeB = 15,
+  kWsLargeX2 = 16,
+};
+
+// Large-n evaluation (pf_large.cu): outs[s] = r_s(2^-j A_b) for every weight set, any n.
+// dJ: per-matrix squaring counts (device) or nullptr for j = 0.
+int large_eval(pf_context* ctx, const pf_method* m, int n, int batch, const double* A, int64_t lda, int64_t strideA,
+               const int* dJ, double* const* outs, int64_t ldo, int64_t strideOut, int flags, pf_status* status);
+
+// n x k block action (pf_large.cu)
+int large_action(pf_context* ctx, const pf_method* m, int n, int k, const double* A, int64_t lda, const double* V,
+                 int64_t ldv, int substeps, double* out, int64_t ldo, int flags, pf_status* status);
+
+// DenseLu on any n (pf_large.cu)
+int large_lu_factor(pf_context* ctx, int n, int batch, double* A, int64_t lda, int64_t strideA, int* piv,
+                    double pivot_rel_tol, int flags, pf_status* status);
+int large_lu_solve(pf_context* ctx, int n, int k, int batch, const double* LU, int64_t lda, int64_t strideLU,
+                   const int* piv, double* R, int64_t ldr, int64_t strideR);
+
+}  // namespace host
+}  // namespace pf

@@ -1,0 +1,492 @@
+// Host orchestration of the large-n path (n > 128, and the DenseLu / action entry points):
+// recursive LU and triangular solves over batches of identity-padded systems, every off-diagonal
+// update on the DMMA GEMM (gemm.cu), 64 x 64 diagonal blocks on large.cu's base kernels.
+//
+//   LU(A)        = LU(A11); A12 <- L11^-1 A12; A21 <- A21 U11^-1; A22 -= A21 A12; LU(A22)
+//   L^-1 B       = [L11^-1 B1; L22^-1 (B2 - L21 B1)]
+//   U^-1 B       = [U11^-1 (B1 - U12 B2); U22^-1 B2]
+//   B U^-1       = [B1 U11^-1, (B2 - B1 U12) U22^-1]
+// The same arithmetic as dense.cpp's right-looking LU / substitution (dense.cpp:102-163), blocked.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "pf_host.h"
+
+namespace pf {
+
+__global__ void lu_base64_kernel(double* M, int64_t ld, int64_t strideM, int off, double* inv, int64_t inv_stride,
+                                 int factor);
+__global__ void apply_inv64_kernel(const double* inv, int64_t inv_stride, int blk, int upper, int right, double* Bm,
+                                   int64_t ld, int64_t strideB, int extent);
+__global__ void lu_pivot_kernel(double* M, int64_t ld, int64_t strideM, int n, int* piv, const double* tol,
+                                DevStatus* status, int* first_error);
+__global__ void form_shifted_kernel(const double* A, int64_t lda, int64_t strideA, int n, int np, int batch,
+                                    const double* shifts, const int* j, double* M, unsigned long long* mx);
+__global__ void certificate_kernel(const double* M, int np, int n, const unsigned long long* mx, double rel_tol,
+                                   int* ok);
+__global__ void form_rhs_kernel(const double* src, int64_t lds, int64_t strideS, int n, int np, int cols,
+                                int ncols_true, int batch, const double* shifts, const int* j, int residual,
+                                const int* perm, double* R, int64_t strideR);
+__global__ void accumulate_kernel(const double* X, int64_t xld, int64_t strideX, int n, int cols, int batch,
+                                  int n_terms, const int* term_z, const double* w, int add_poly, double constant,
+                                  double d1, double d2, const double* Bsrc, int64_t bld, int64_t strideBs,
+                                  const int* j, const double* B2, int64_t b2ld, int64_t strideB2, double* out,
+                                  int64_t ldo, int64_t strideOut);
+__global__ void action_accumulate_kernel(const double* R, int64_t rld, int64_t strideR, const double* X, int64_t xld,
+                                         int n, int k, int n_terms, const int* term_z, const double* w, int add_poly,
+                                         double constant, int hybrid, double d1, double d2, const double* BX,
+                                         const double* B2X, double* out, int64_t ldo);
+__global__ void perm_from_piv_kernel(const int* piv, int n, int* perm);
+__global__ void copy2d_kernel(int rows, int cols, double s, const double* X, int64_t ldx, int64_t strideX, double* Y,
+                              int64_t ldy, int64_t strideY);
+__global__ void scale_pad_kernel(const double* A, int64_t lda, int n, int np, double s, double* B);
+__global__ void fill_int_kernel(int* p, int count, int v);
+__global__ void load_padded_kernel(const double* A, int64_t lda, int64_t strideA, int n, int np, double* M,
+                                   unsigned long long* mx);
+__global__ void iota_kernel(int* p, int n);
+size_t apply_inv64_smem_bytes();
+
+namespace host {
+namespace {
+
+constexpr int kB = 64;
+
+int round64(int n) { return ((n + kB - 1) / kB) * kB; }
+unsigned grid_for(int64_t elems) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((elems + 255) / 256, 1184)); }
+
+// A batch of nsys systems of order np (row-major, stride np^2) plus their diagonal-block inverses.
+struct Sys {
+  double* M;
+  int np;
+  int nsys;
+  double* inv;
+  int64_t inv_stride;
+  int64_t stride() const { return (int64_t)np * np; }
+};
+
+void apply_inv(pf_context* ctx, const Sys& s, int blk, bool upper, bool right, double* B, int64_t ldb, int64_t sb,
+               int extent) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(apply_inv64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)apply_inv64_smem_bytes());
+    configured = true;
+  }
+  dim3 grid((extent + kB - 1) / kB, s.nsys);
+  apply_inv64_kernel<<<grid, 256, apply_inv64_smem_bytes(), ctx->stream>>>(s.inv, s.inv_stride, blk, upper ? 1 : 0, right ? 1 : 0, B, ldb, sb,
+                                                    extent);
+  ctx->launches++;
+}
+
+int half64(int n) { return std::max(kB, ((n / kB) / 2) * kB); }
+
+// B (n x cols) <- L^-1 B, L = unit-lower diagonal block [off, off + n) of s.M
+void trsm_left_lower(pf_context* ctx, const Sys& s, int off, int n, double* B, int64_t ldb, int64_t sb, int cols) {
+  if (n == kB) {
+    apply_inv(ctx, s, off / kB, false, false, B, ldb, sb, cols);
+    return;
+  }
+  const int n1 = half64(n), n2 = n - n1;
+  trsm_left_lower(ctx, s, off, n1, B, ldb, sb, cols);
+  const double* L21 = s.M + (int64_t)(off + n1) * s.np + off;
+  gemm(ctx, n2, cols, n1, s.nsys, -1.0, L21, s.np, s.stride(), B, ldb, sb, 1.0, B + (int64_t)n1 * ldb, ldb, sb, 0.0);
+  trsm_left_lower(ctx, s, off + n1, n2, B + (int64_t)n1 * ldb, ldb, sb, cols);
+}
+
+// B (n x cols) <- U^-1 B
+void trsm_left_upper(pf_context* ctx, const Sys& s, int off, int n, double* B, int64_t ldb, int64_t sb, int cols) {
+  if (n == kB) {
+    apply_inv(ctx, s, off / kB, true, false, B, ldb, sb, cols);
+    return;
+  }
+  const int n1 = half64(n), n2 = n - n1;
+  trsm_left_upper(ctx, s, off + n1, n2, B + (int64_t)n1 * ldb, ldb, sb, cols);
+  const double* U12 = s.M + (int64_t)off * s.np + off + n1;
+  gemm(ctx, n1, cols, n2, s.nsys, -1.0, U12, s.np, s.stride(), B + (int64_t)n1 * ldb, ldb, sb, 1.0, B, ldb, sb, 0.0);
+  trsm_left_upper(ctx, s, off, n1, B, ldb, sb, cols);
+}
+
+// B (rows x n) <- B U^-1
+void trsm_right_upper(pf_context* ctx, const Sys& s, int off, int n, double* B, int64_t ldb, int64_t sb, int rows) {
+  if (n == kB) {
+    apply_inv(ctx, s, off / kB, true, true, B, ldb, sb, rows);
+    return;
+  }
+  const int n1 = half64(n), n2 = n - n1;
+  trsm_right_upper(ctx, s, off, n1, B, ldb, sb, rows);
+  const double* U12 = s.M + (int64_t)off * s.np + off + n1;
+  gemm(ctx, rows, n2, n1, s.nsys, -1.0, B, ldb, sb, U12, s.np, s.stride(), 1.0, B + n1, ldb, sb, 0.0);
+  trsm_right_upper(ctx, s, off + n1, n2, B + n1, ldb, sb, rows);
+}
+
+void lu_rec(pf_context* ctx, const Sys& s, int off, int n) {
+  if (n == kB) {
+    lu_base64_kernel<<<s.nsys, 256, 0, ctx->stream>>>(s.M, s.np, s.stride(), off, s.inv, s.inv_stride, 1);
+    ctx->launches++;
+    return;
+  }
+  const int n1 = half64(n), n2 = n - n1;
+  lu_rec(ctx, s, off, n1);
+  double* A12 = s.M + (int64_t)off * s.np + off + n1;
+  double* A21 = s.M + (int64_t)(off + n1) * s.np + off;
+  double* A22 = s.M + (int64_t)(off + n1) * s.np + off + n1;
+  trsm_left_lower(ctx, s, off, n1, A12, s.np, s.stride(), n2);
+  trsm_right_upper(ctx, s, off, n1, A21, s.np, s.stride(), n2);
+  gemm(ctx, n2, n2, n1, s.nsys, -1.0, A21, s.np, s.stride(), A12, s.np, s.stride(), 1.0, A22, s.np, s.stride(), 0.0);
+  lu_rec(ctx, s, off + n1, n2);
+}
+
+void diag_inverses(pf_context* ctx, const Sys& s) {
+  for (int off = 0; off < s.np; off += kB) {
+    lu_base64_kernel<<<s.nsys, 256, 0, ctx->stream>>>(s.M, s.np, s.stride(), off, s.inv, s.inv_stride, 0);
+    ctx->launches++;
+  }
+}
+
+template <typename T>
+T* upload(pf_context* ctx, int slot, const std::vector<T>& v) {
+  T* d = static_cast<T*>(workspace(ctx, slot, sizeof(T) * std::max<size_t>(v.size(), 1)));
+  if (d && !v.empty()) cudaMemcpyAsync(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, ctx->stream);
+  return d;
+}
+
+// Factor the nsys systems already formed in s.M (true order n, padded np). Certified systems
+// (strict column diagonal dominance with margin) take the recursive no-exchange LU; otherwise every
+// system runs the genuine partial-pivoting kernel. On return perm (nsys x n) is the row order of
+// the RHS (nullptr when no system was pivoted). Failures are reported for system z.
+struct FactorResult {
+  int rc = PF_OK;
+  int z = -1;
+  pf::DevStatus st{};
+  bool pivoted = false;
+  std::vector<double> scale;
+};
+
+FactorResult factor_systems(pf_context* ctx, const Sys& s, int n, unsigned long long* d_mx, int flags,
+                            int* d_piv, int* d_perm, double pivot_rel_tol) {
+  FactorResult fr;
+  int* d_ok = static_cast<int*>(workspace(ctx, kWsLargeAux + 20, sizeof(int) * s.nsys));
+  fill_int_kernel<<<(s.nsys + 255) / 256, 256, 0, ctx->stream>>>(d_ok, s.nsys, 1);
+  certificate_kernel<<<dim3((n + 255) / 256, s.nsys), 256, 0, ctx->stream>>>(s.M, s.np, n, d_mx, pivot_rel_tol, d_ok);
+  ctx->launches += 2;
+  std::vector<int> ok(s.nsys);
+  std::vector<unsigned long long> mxbits(s.nsys);
+  cudaMemcpyAsync(ok.data(), d_ok, sizeof(int) * s.nsys, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaMemcpyAsync(mxbits.data(), d_mx, sizeof(unsigned long long) * s.nsys, cudaMemcpyDeviceToHost, ctx->stream);
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+    fr.rc = PF_ERR_CUDA;
+    return fr;
+  }
+  fr.scale.resize(s.nsys);
+  bool all_ok = (flags & PF_FLAG_FORCE_PIVOT) == 0;
+  for (int z = 0; z < s.nsys; ++z) {
+    double mx;
+    std::memcpy(&mx, &mxbits[z], sizeof(double));
+    fr.scale[z] = std::max(mx, 1e-300);
+    all_ok = all_ok && ok[z];
+  }
+  if (all_ok) {
+    lu_rec(ctx, s, 0, s.np);
+    return fr;
+  }
+  fr.pivoted = true;
+  std::vector<double> tol(s.nsys);
+  for (int z = 0; z < s.nsys; ++z) tol[z] = pivot_rel_tol * fr.scale[z];
+  double* d_tol = upload(ctx, kWsLargeAux + 21, tol);
+  int rc = ensure_status(ctx, s.nsys);
+  if (rc) {
+    fr.rc = rc;
+    return fr;
+  }
+  lu_pivot_kernel<<<s.nsys, 1024, 0, ctx->stream>>>(s.M, s.np, s.stride(), n, d_piv, d_tol, ctx->status,
+                                                    ctx->first_error);
+  ctx->launches++;
+  pf_status ps;
+  rc = collect_status(ctx, s.nsys, 0, &ps);
+  if (rc) {
+    fr.rc = rc;
+    fr.z = ps.batch_index;
+    fr.st.code = ps.code;
+    fr.st.column = ps.column;
+    fr.st.pivot_magnitude = ps.pivot_magnitude;
+    return fr;
+  }
+  perm_from_piv_kernel<<<s.nsys, 32, 0, ctx->stream>>>(d_piv, n, d_perm);
+  ctx->launches++;
+  diag_inverses(ctx, s);
+  return fr;
+}
+
+bool make_sys(pf_context* ctx, Sys& s, int n, int nsys, int slotM) {
+  s.np = round64(n);
+  s.nsys = nsys;
+  s.M = static_cast<double*>(workspace(ctx, slotM, sizeof(double) * s.stride() * std::max(nsys, 1)));
+  s.inv_stride = (int64_t)(s.np / kB) * 2 * kB * kB;
+  s.inv = static_cast<double*>(workspace(ctx, kWsLargeInv, sizeof(double) * s.inv_stride * std::max(nsys, 1)));
+  return s.M && s.inv;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+int large_eval(pf_context* ctx, const pf_method* m, int n, int batch, const double* A, int64_t lda, int64_t strideA,
+               const int* dJ, double* const* outs, int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
+  if (status) std::memset(status, 0, sizeof(*status));
+  if (batch == 0 || n == 0) return PF_OK;
+  std::vector<int> nz;
+  for (int i = 0; i < m->n_terms; ++i)
+    if (m->shifts[i] != 0.0) nz.push_back(i);
+  const int P = (int)nz.size();
+  const bool residual = m->form == PF_FORM_RESIDUAL;
+  Sys s;
+  const int nsys = P * batch;
+  if (!make_sys(ctx, s, n, nsys, kWsLargeM)) return PF_ERR_CUDA;
+  double* R = static_cast<double*>(workspace(ctx, kWsLargeR, sizeof(double) * s.stride() * std::max(nsys, 1)));
+  auto* d_mx = static_cast<unsigned long long*>(workspace(ctx, kWsLargeAux, sizeof(unsigned long long) * std::max(nsys, 1)));
+  int* d_piv = static_cast<int*>(workspace(ctx, kWsLargePiv, sizeof(int) * (size_t)n * std::max(nsys, 1) * 2));
+  if (!R || !d_mx || !d_piv) return PF_ERR_CUDA;
+  int* d_perm = d_piv + (size_t)n * std::max(nsys, 1);
+  std::vector<double> sh(P);
+  for (int q = 0; q < P; ++q) sh[q] = m->shifts[nz[q]];
+  double* d_sh = upload(ctx, kWsLargeAux + 1, sh);
+  bool pivoted = false;
+  if (nsys > 0) {
+    cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long) * nsys, ctx->stream);
+    form_shifted_kernel<<<dim3(grid_for(s.stride()), nsys), 256, 0, ctx->stream>>>(A, lda, strideA, n, s.np, batch,
+                                                                                   d_sh, dJ, s.M, d_mx);
+    ctx->launches++;
+    FactorResult fr = factor_systems(ctx, s, n, d_mx, flags, d_piv, d_perm, 1e-14);
+    if (fr.rc) {
+      if (status) {
+        status->code = fr.rc;
+        if (fr.z >= 0) {
+          status->batch_index = fr.z % batch;
+          status->shift_index = nz[fr.z / batch] + 1;
+          status->column = fr.st.column;
+          status->pivot_magnitude = fr.st.pivot_magnitude;
+          status->scale = fr.scale.empty() ? 0.0 : fr.scale[fr.z];
+        }
+      }
+      return fr.rc;
+    }
+    pivoted = fr.pivoted;
+    form_rhs_kernel<<<dim3(grid_for(s.stride()), nsys), 256, 0, ctx->stream>>>(
+        A, lda, strideA, n, s.np, s.np, n, batch, d_sh, dJ, residual ? 1 : 0, pivoted ? d_perm : nullptr, R,
+        s.stride());
+    ctx->launches++;
+    trsm_left_lower(ctx, s, 0, s.np, R, s.np, s.stride(), s.np);
+    trsm_left_upper(ctx, s, 0, s.np, R, s.np, s.stride(), s.np);
+  }
+  // poly part needs B^2 when any d2 != 0
+  double* B2 = nullptr;
+  bool need_b2 = false;
+  for (int q = 0; q < m->n_sets && m->has_poly; ++q) need_b2 |= m->poly[3 * q + 2] != 0.0;
+  if (need_b2) {
+    double* Bs = static_cast<double*>(workspace(ctx, kWsLargeB, sizeof(double) * (size_t)n * n * batch));
+    B2 = static_cast<double*>(workspace(ctx, kWsLargeX2, sizeof(double) * (size_t)n * n * batch));
+    if (!Bs || !B2) return PF_ERR_CUDA;
+    launch_ldexp_batched(n, batch, A, lda, strideA, dJ, Bs, n, (int64_t)n * n, ctx->stream);
+    ctx->launches++;
+    gemm(ctx, n, n, n, batch, 1.0, Bs, n, (int64_t)n * n, Bs, n, (int64_t)n * n, 0.0, B2, n, (int64_t)n * n, 0.0);
+  }
+  for (int q = 0; q < m->n_sets; ++q) {
+    std::vector<int> tz;
+    std::vector<double> w;
+    int slot = 0;
+    for (int i = 0; i < m->n_terms; ++i) {
+      const double wi = m->weights[q * m->n_terms + i];
+      if (m->shifts[i] != 0.0) {
+        tz.push_back(slot++);
+        w.push_back(wi);
+      } else if (!residual) {
+        tz.push_back(-1);
+        w.push_back(wi);
+      }
+    }
+    int* d_tz = upload(ctx, kWsLargeAux + 2 + 2 * q, tz);
+    double* d_w = upload(ctx, kWsLargeAux + 3 + 2 * q, w);
+    const bool add_poly = residual || m->has_poly;
+    const double constant = residual ? m->constant[q] : (m->has_poly ? m->poly[3 * q] : 0.0);
+    const double d1 = m->has_poly ? m->poly[3 * q + 1] : 0.0, d2 = m->has_poly ? m->poly[3 * q + 2] : 0.0;
+    accumulate_kernel<<<dim3(grid_for((int64_t)n * n), batch), 256, 0, ctx->stream>>>(
+        R, s.np, s.stride(), n, n, batch, (int)tz.size(), d_tz, d_w, add_poly ? 1 : 0, constant, d1, d2, A, lda,
+        strideA, dJ, B2, n, (int64_t)n * n, outs[q], ldo, strideOut);
+    ctx->launches++;
+  }
+  return cuda_fail(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------------------------
+int large_action(pf_context* ctx, const pf_method* m, int n, int k, const double* A, int64_t lda, const double* V,
+                 int64_t ldv, int substeps, double* out, int64_t ldo, int flags, pf_status* status) {
+  if (status) std::memset(status, 0, sizeof(*status));
+  std::vector<int> nz;
+  for (int i = 0; i < m->n_terms; ++i)
+    if (m->shifts[i] != 0.0) nz.push_back(i);
+  const int P = (int)nz.size();
+  const bool residual = m->form == PF_FORM_RESIDUAL;
+  const bool hybrid = m->has_poly != 0;
+  Sys s;
+  if (!make_sys(ctx, s, n, P, kWsLargeM)) return PF_ERR_CUDA;
+  const int np = s.np;
+  double* Bp = static_cast<double*>(workspace(ctx, kWsLargeB, sizeof(double) * s.stride()));
+  const size_t blk = (size_t)np * k;
+  double* R = static_cast<double*>(workspace(ctx, kWsLargeR, sizeof(double) * blk * std::max(P, 1)));
+  double* X = static_cast<double*>(workspace(ctx, kWsT1, sizeof(double) * blk * 4));
+  auto* d_mx = static_cast<unsigned long long*>(workspace(ctx, kWsLargeAux, sizeof(unsigned long long) * std::max(P, 1)));
+  int* d_piv = static_cast<int*>(workspace(ctx, kWsLargePiv, sizeof(int) * (size_t)n * std::max(P, 1) * 2));
+  if (!Bp || !R || !X || !d_mx || !d_piv) return PF_ERR_CUDA;
+  int* d_perm = d_piv + (size_t)n * std::max(P, 1);
+  double* BX = X + blk;
+  double* B2X = X + 2 * blk;
+  double* Xn = X + 3 * blk;
+  // B = A * (1.0 / N) (action.cpp:330-334), zero padded
+  const double inv = 1.0 / substeps;
+  scale_pad_kernel<<<grid_for(s.stride()), 256, 0, ctx->stream>>>(A, lda, n, np, inv, Bp);
+  ctx->launches++;
+  std::vector<double> sh(P);
+  for (int q = 0; q < P; ++q) sh[q] = m->shifts[nz[q]];
+  double* d_sh = upload(ctx, kWsLargeAux + 1, sh);
+  bool pivoted = false;
+  if (P > 0) {
+    cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long) * P, ctx->stream);
+    form_shifted_kernel<<<dim3(grid_for(s.stride()), P), 256, 0, ctx->stream>>>(Bp, np, 0, n, np, 1, d_sh, nullptr,
+                                                                               s.M, d_mx);
+    ctx->launches++;
+    FactorResult fr = factor_systems(ctx, s, n, d_mx, flags, d_piv, d_perm, 1e-14);
+    if (fr.rc) {
+      if (status) {
+        status->code = fr.rc;
+        if (fr.z >= 0) {
+          status->shift_index = nz[fr.z] + 1;
+          status->column = fr.st.column;
+          status->pivot_magnitude = fr.st.pivot_magnitude;
+          status->scale = fr.scale[fr.z];
+        }
+      }
+      return fr.rc;
+    }
+    pivoted = fr.pivoted;
+  }
+  // X = V (padded rows are zero)
+  cudaMemsetAsync(X, 0, sizeof(double) * blk, ctx->stream);
+  copy2d_kernel<<<dim3(grid_for((int64_t)n * k), 1), 256, 0, ctx->stream>>>(n, k, 1.0, V, ldv, 0, X, k, 0);
+  ctx->launches++;
+  std::vector<int> tz;
+  std::vector<double> w;
+  {
+    int slot = 0;
+    for (int i = 0; i < m->n_terms; ++i) {
+      if (m->shifts[i] != 0.0) {
+        tz.push_back(slot++);
+        w.push_back(m->weights[i]);
+      } else if (!residual) {
+        tz.push_back(-1);
+        w.push_back(m->weights[i]);
+      }
+    }
+  }
+  int* d_tz = upload(ctx, kWsLargeAux + 2, tz);
+  double* d_w = upload(ctx, kWsLargeAux + 3, w);
+  const double constant = residual ? m->constant[0] : (hybrid ? m->poly[0] : 0.0);
+  const double d1 = hybrid ? m->poly[1] : 0.0, d2 = hybrid ? m->poly[2] : 0.0;
+  for (int step = 0; step < substeps; ++step) {
+    if (residual || hybrid) gemm(ctx, np, k, np, 1, 1.0, Bp, np, 0, X, k, 0, 0.0, BX, k, 0, 0.0);
+    if (hybrid) gemm(ctx, np, k, np, 1, 1.0, Bp, np, 0, BX, k, 0, 0.0, B2X, k, 0, 0.0);
+    if (P > 0) {
+      // R_i = c_i B X (residual, action.cpp:252-258) or X (plain), rows permuted when pivoted
+      form_rhs_kernel<<<dim3(grid_for((int64_t)blk), P), 256, 0, ctx->stream>>>(
+          residual ? BX : X, k, 0, n, np, k, k, 1, d_sh, nullptr, 1, pivoted ? d_perm : nullptr, R, (int64_t)blk);
+      ctx->launches++;
+      if (!residual) {
+        // plain: RHS is X itself (form_rhs with c = 1 would need a unit shift table): rescale back
+        std::vector<double> ones(P, 1.0);
+        double* d_one = upload(ctx, kWsLargeAux + 9, ones);
+        form_rhs_kernel<<<dim3(grid_for((int64_t)blk), P), 256, 0, ctx->stream>>>(
+            X, k, 0, n, np, k, k, 1, d_one, nullptr, 1, pivoted ? d_perm : nullptr, R, (int64_t)blk);
+        ctx->launches++;
+      }
+      trsm_left_lower(ctx, s, 0, np, R, k, (int64_t)blk, k);
+      trsm_left_upper(ctx, s, 0, np, R, k, (int64_t)blk, k);
+    }
+    action_accumulate_kernel<<<grid_for((int64_t)n * k), 256, 0, ctx->stream>>>(
+        R, k, (int64_t)blk, X, k, n, k, (int)tz.size(), d_tz, d_w, (residual || hybrid) ? 1 : 0, constant,
+        hybrid ? 1 : 0, d1, d2, BX, B2X, Xn, k);
+    ctx->launches++;
+    std::swap(X, Xn);
+  }
+  copy2d_kernel<<<dim3(grid_for((int64_t)n * k), 1), 256, 0, ctx->stream>>>(n, k, 1.0, X, k, 0, out, ldo, 0);
+  ctx->launches++;
+  return cuda_fail(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------------------------
+int large_lu_factor(pf_context* ctx, int n, int batch, double* A, int64_t lda, int64_t strideA, int* piv,
+                    double pivot_rel_tol, int flags, pf_status* status) {
+  if (status) std::memset(status, 0, sizeof(*status));
+  if (batch == 0 || n == 0) return PF_OK;
+  Sys s;
+  if (!make_sys(ctx, s, n, batch, kWsLargeM)) return PF_ERR_CUDA;
+  auto* d_mx = static_cast<unsigned long long*>(workspace(ctx, kWsLargeAux, sizeof(unsigned long long) * batch));
+  int* d_piv = static_cast<int*>(workspace(ctx, kWsLargePiv, sizeof(int) * (size_t)n * batch * 2));
+  if (!d_mx || !d_piv) return PF_ERR_CUDA;
+  int* d_perm = d_piv + (size_t)n * batch;
+  cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long) * batch, ctx->stream);
+  load_padded_kernel<<<dim3(grid_for(s.stride()), batch), 256, 0, ctx->stream>>>(A, lda, strideA, n, s.np, s.M, d_mx);
+  ctx->launches++;
+  FactorResult fr = factor_systems(ctx, s, n, d_mx, flags, d_piv, d_perm, pivot_rel_tol);
+  if (fr.rc) {
+    if (status) {
+      status->code = fr.rc;
+      status->batch_index = std::max(fr.z, 0);
+      status->column = fr.st.column;
+      status->pivot_magnitude = fr.st.pivot_magnitude;
+      status->scale = fr.z >= 0 ? fr.scale[fr.z] : 0.0;
+    }
+    return fr.rc;
+  }
+  copy2d_kernel<<<dim3(grid_for((int64_t)n * n), batch), 256, 0, ctx->stream>>>(n, n, 1.0, s.M, s.np, s.stride(), A, lda,
+                                                                               strideA);
+  ctx->launches++;
+  if (piv) {
+    if (fr.pivoted) {
+      cudaMemcpyAsync(piv, d_piv, sizeof(int) * (size_t)n * batch, cudaMemcpyDeviceToDevice, ctx->stream);
+    } else {
+      iota_kernel<<<dim3((n + 255) / 256, batch), 256, 0, ctx->stream>>>(piv, n);
+      ctx->launches++;
+    }
+  }
+  return cuda_fail(cudaGetLastError());
+}
+
+int large_lu_solve(pf_context* ctx, int n, int k, int batch, const double* LU, int64_t lda, int64_t strideLU,
+                   const int* piv, double* R, int64_t ldr, int64_t strideR) {
+  if (batch == 0 || n == 0 || k == 0) return PF_OK;
+  Sys s;
+  if (!make_sys(ctx, s, n, batch, kWsLargeM)) return PF_ERR_CUDA;
+  auto* d_mx = static_cast<unsigned long long*>(workspace(ctx, kWsLargeAux, sizeof(unsigned long long) * batch));
+  int* d_perm = static_cast<int*>(workspace(ctx, kWsLargePiv, sizeof(int) * (size_t)n * batch * 2));
+  const size_t blk = (size_t)s.np * k;
+  double* X = static_cast<double*>(workspace(ctx, kWsLargeR, sizeof(double) * blk * batch));
+  if (!d_mx || !d_perm || !X) return PF_ERR_CUDA;
+  load_padded_kernel<<<dim3(grid_for(s.stride()), batch), 256, 0, ctx->stream>>>(LU, lda, strideLU, n, s.np, s.M, d_mx);
+  perm_from_piv_kernel<<<batch, 32, 0, ctx->stream>>>(piv, n, d_perm);
+  ctx->launches += 2;
+  diag_inverses(ctx, s);
+  std::vector<double> ones(batch, 1.0);
+  double* d_one = upload(ctx, kWsLargeAux + 9, ones);
+  // X = P R (padded zeros): form_rhs with c = 1, batch 1 per system via z = b (one shift slot)
+  form_rhs_kernel<<<dim3(grid_for((int64_t)blk), batch), 256, 0, ctx->stream>>>(R, ldr, strideR, n, s.np, k, k, batch,
+                                                                               d_one, nullptr, 1, d_perm, X,
+                                                                               (int64_t)blk);
+  ctx->launches++;
+  trsm_left_lower(ctx, s, 0, s.np, X, k, (int64_t)blk, k);
+  trsm_left_upper(ctx, s, 0, s.np, X, k, (int64_t)blk, k);
+  copy2d_kernel<<<dim3(grid_for((int64_t)n * k), batch), 256, 0, ctx->stream>>>(n, k, 1.0, X, k, (int64_t)blk, R, ldr,
+                                                                               strideR);
+  ctx->launches++;
+  return cuda_fail(cudaGetLastError());
+}
+
+}  // namespace host
+}  // namespace pf

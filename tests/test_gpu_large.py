@@ -1,0 +1,147 @@
+"""GPU parity of the large-n path (n > 128: recursive LU / triangular solves on the DMMA GEMM),
+the dense block action, DenseLu, and the phi1 / cos-sin compositions at mid sizes, against the
+CPU oracle on identical seeded inputs. Full BASELINE sizes are covered by size-independent
+properties in test_gpu_configs.py."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-11
+
+
+@pytest.fixture(scope="module")
+def dev(pf):
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need CUDA")
+    from paper_2210_03714_b200 import api
+
+    return api
+
+
+def rand(n, seed, norm):
+    from paper_2210_03714_b200 import workloads as W
+
+    return W.scaled_to_one_norm(W.randn_matrix(n, seed), norm)
+
+
+@pytest.mark.parametrize("n", [129, 200, 256, 333])
+@pytest.mark.parametrize("name,form", [("R4", 1), ("R8", 1), ("R8", 0), ("R10", 1)])
+def test_large_eval_dense(dev, oracle, n, name, form):
+    from paper_2210_03714_b200 import methods as M
+
+    m = M.catalog(name)
+    b = rand(n, 7 + n, 0.5)
+    ref = oracle.eval_dense(oracle.OMethod.from_method(m, form), b)
+    got = dev.eval_dense(m, b, dev.EvalOptions(form=form))
+    amp = float(sum(abs(w) for w in m.weights) + sum(abs(d) for d in m.poly))
+    tol = max(TOL, 100 * amp * 2.23e-16) if name.startswith("R10") else TOL
+    assert oracle.rel_diff_1norm(got, ref) <= tol
+
+
+def test_large_batched_eval_and_sets(dev, oracle):
+    from paper_2210_03714_b200 import methods as M
+
+    m = M.catalog("R8")
+    phi = M.same_shift_method(m, M.FunctionId.phi(1))
+    bs = np.stack([rand(192, 70 + i, 0.09) for i in range(3)])
+    e, p = dev.eval_dense(m, bs, dev.EvalOptions(form=1), extra_sets=[phi])
+    om = oracle.OMethod.from_method(m, 1, [phi])
+    for i in range(3):
+        ref = oracle.eval_dense(om, bs[i])
+        assert oracle.rel_diff_1norm(e[i], ref[0]) <= TOL
+        assert oracle.rel_diff_1norm(p[i], ref[1]) <= TOL
+
+
+def test_large_pivoting_path(dev, oracle):
+    """Non-dominant shifted systems run the genuine partial-pivoting kernel in the reference's
+    operation order."""
+    b = rand(200, 901, 80.0)
+    got = dev.solve_shifted(b, 0.2)
+    ref = oracle.solve_shifted(b, 0.2)
+    assert oracle.rel_diff_1norm(got, ref) <= 1e-12
+
+
+def test_large_singular(dev):
+    from paper_2210_03714_b200.errors import Errc, PfError
+
+    with pytest.raises(PfError) as ei:
+        dev.eval_dense("R10", 8.0 * np.eye(150))
+    assert ei.value.code == Errc.SingularShift
+    assert "shift" in str(ei.value)
+
+
+@pytest.mark.parametrize("n", [150, 256])
+@pytest.mark.parametrize("name", ["R4", "R8"])
+def test_large_expm(dev, oracle, n, name):
+    from paper_2210_03714_b200 import methods as M
+
+    a = np.stack([rand(n, 3 + i, 2.0 + 3 * i) for i in range(2)])
+    om = oracle.OMethod.from_method(M.catalog(name), 1)
+    got, js = dev.expm(a, name, return_squarings=True)
+    for i in range(2):
+        ref, j = oracle.expm(a[i], om, M.THETA_U53[name])
+        assert int(js[i]) == j
+        assert oracle.rel_diff_1norm(got[i], ref) <= TOL
+
+
+def test_large_expm_phi1(dev, oracle):
+    from paper_2210_03714_b200 import methods as M
+
+    m = M.catalog("R8")
+    phi = M.same_shift_method(m, M.FunctionId.phi(1))
+    th = min(M.THETA_U53["R8"], M.THETA_U53["R8_phi1set"])
+    a = rand(320, 5, 8.0)
+    e, p = dev.expm_phi1(a, "R8")
+    re, rp, _ = oracle.expm_phi1(a, oracle.OMethod.from_method(m, 1, [phi]), th)
+    assert oracle.rel_diff_1norm(e, re) <= TOL
+    assert oracle.rel_diff_1norm(p, rp) <= TOL
+
+
+def test_large_cossin(dev, oracle):
+    from paper_2210_03714_b200 import methods as M
+
+    pm = M.pair_method(M.catalog("R8"))
+    rng = np.random.default_rng(3)
+    q, _ = np.linalg.qr(rng.standard_normal((256, 256)))
+    a = np.stack([(q * rng.uniform(0, 50, 256)) @ q.T for _ in range(2)])
+    a = 0.5 * (a + a.transpose(0, 2, 1))
+    c, s = dev.cossin(a, "R8")
+    op = oracle.OPair.from_pair(pm)
+    for i in range(2):
+        rc, rs, _ = oracle.cossin(a[i], op, M.THETA_U53["R8"])
+        assert oracle.rel_diff_1norm(c[i], rc) <= TOL
+        assert oracle.rel_diff_1norm(s[i], rs) <= TOL
+
+
+@pytest.mark.parametrize("n,k", [(96, 4), (300, 8)])
+@pytest.mark.parametrize("name,form", [("R8", 1), ("R8", 0), ("R10", 1), ("R4", 1)])
+def test_action_block(dev, oracle, n, k, name, form):
+    from paper_2210_03714_b200 import methods as M, workloads as W
+
+    m = M.catalog(name)
+    a = W.randn_matrix(n, 40) / np.sqrt(n) - 2.0 * np.eye(n)
+    a *= 1.5 / W.one_norm(a)
+    v = W.randn(41, n * k).reshape(n, k)
+    nsub = M.substeps_for(1.5, M.THETA_U53.get(name, 0.1))
+    got = dev.action(a, v, m, substeps=nsub, form=form)
+    ref = oracle.action(a, v, oracle.OMethod.from_method(m, form), nsub)
+    amp = float(sum(abs(w) for w in m.weights) + sum(abs(d) for d in m.poly))
+    tol = max(TOL, 100 * amp * 2.23e-16) if name.startswith("R10") else TOL
+    assert oracle.rel_diff_1norm(got, ref) <= tol * nsub
+
+
+def test_dense_lu_api(dev, oracle):
+    """DenseLu: pivots bit-exact against the reference rule, factors and solves."""
+    for n, norm in [(40, 50.0), (200, 60.0), (100, 0.1)]:
+        b = rand(n, 77 + n, norm)
+        mm = np.eye(n) - 0.2 * b
+        lu = dev.DenseLu(mm)
+        LU, piv = lu.factors()
+        rlu, rpiv = oracle.lu(mm)
+        assert np.array_equal(piv, rpiv)
+        assert oracle.rel_diff_1norm(LU, rlu) <= 1e-12
+        rhs = rand(n, 5, 1.0)[:, :7]
+        x = lu.solve_matrix(rhs)
+        assert oracle.rel_diff_1norm(x, oracle.lu_solve_matrix(rlu, rpiv, rhs)) <= 1e-12
