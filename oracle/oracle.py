@@ -238,4 +238,9 @@ def rel_diff_1norm(a, b) -> float:
     a, b = _f64(a), _f64(b)
     if a.ndim == 3:
         return max(rel_diff_1norm(x, y) for x, y in zip(a, b))
+    if a.ndim == 1:
+        a, b = a[:, None], b[:, None]
+    if a.shape[0] != a.shape[1]:  # rectangular blocks (action, multi-RHS solves): max column sum
+        d = np.abs(a - b).sum(axis=0).max()
+        return float(d / max(np.abs(b).sum(axis=0).max(), 1e-300))
     return one_norm(a - b) / max(one_norm(b), 1e-300)

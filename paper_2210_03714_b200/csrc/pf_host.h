@@ -49,6 +49,7 @@ enum Slot {
   kWsLargePiv = 14,
   kWsLargeB = 15,
   kWsLargeX2 = 16,
+  kWsSmallArrays = 64,  // small uploaded tables: kWsSmallArrays + i, i < 32
 };
 
 // Large-n evaluation (pf_large.cu): outs[s] = r_s(2^-j A_b) for every weight set, any n.

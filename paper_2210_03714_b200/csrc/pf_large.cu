@@ -165,7 +165,7 @@ struct FactorResult {
 FactorResult factor_systems(pf_context* ctx, const Sys& s, int n, unsigned long long* d_mx, int flags,
                             int* d_piv, int* d_perm, double pivot_rel_tol) {
   FactorResult fr;
-  int* d_ok = static_cast<int*>(workspace(ctx, kWsLargeAux + 20, sizeof(int) * s.nsys));
+  int* d_ok = static_cast<int*>(workspace(ctx, kWsSmallArrays + 20, sizeof(int) * s.nsys));
   fill_int_kernel<<<(s.nsys + 255) / 256, 256, 0, ctx->stream>>>(d_ok, s.nsys, 1);
   certificate_kernel<<<dim3((n + 255) / 256, s.nsys), 256, 0, ctx->stream>>>(s.M, s.np, n, d_mx, pivot_rel_tol, d_ok);
   ctx->launches += 2;
@@ -192,7 +192,7 @@ FactorResult factor_systems(pf_context* ctx, const Sys& s, int n, unsigned long 
   fr.pivoted = true;
   std::vector<double> tol(s.nsys);
   for (int z = 0; z < s.nsys; ++z) tol[z] = pivot_rel_tol * fr.scale[z];
-  double* d_tol = upload(ctx, kWsLargeAux + 21, tol);
+  double* d_tol = upload(ctx, kWsSmallArrays + 21, tol);
   int rc = ensure_status(ctx, s.nsys);
   if (rc) {
     fr.rc = rc;
@@ -248,7 +248,7 @@ int large_eval(pf_context* ctx, const pf_method* m, int n, int batch, const doub
   int* d_perm = d_piv + (size_t)n * std::max(nsys, 1);
   std::vector<double> sh(P);
   for (int q = 0; q < P; ++q) sh[q] = m->shifts[nz[q]];
-  double* d_sh = upload(ctx, kWsLargeAux + 1, sh);
+  double* d_sh = upload(ctx, kWsSmallArrays + 1, sh);
   bool pivoted = false;
   if (nsys > 0) {
     cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long) * nsys, ctx->stream);
@@ -303,8 +303,8 @@ int large_eval(pf_context* ctx, const pf_method* m, int n, int batch, const doub
         w.push_back(wi);
       }
     }
-    int* d_tz = upload(ctx, kWsLargeAux + 2 + 2 * q, tz);
-    double* d_w = upload(ctx, kWsLargeAux + 3 + 2 * q, w);
+    int* d_tz = upload(ctx, kWsSmallArrays + 2 + 2 * q, tz);
+    double* d_w = upload(ctx, kWsSmallArrays + 3 + 2 * q, w);
     const bool add_poly = residual || m->has_poly;
     const double constant = residual ? m->constant[q] : (m->has_poly ? m->poly[3 * q] : 0.0);
     const double d1 = m->has_poly ? m->poly[3 * q + 1] : 0.0, d2 = m->has_poly ? m->poly[3 * q + 2] : 0.0;
@@ -346,7 +346,7 @@ int large_action(pf_context* ctx, const pf_method* m, int n, int k, const double
   ctx->launches++;
   std::vector<double> sh(P);
   for (int q = 0; q < P; ++q) sh[q] = m->shifts[nz[q]];
-  double* d_sh = upload(ctx, kWsLargeAux + 1, sh);
+  double* d_sh = upload(ctx, kWsSmallArrays + 1, sh);
   bool pivoted = false;
   if (P > 0) {
     cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long) * P, ctx->stream);
@@ -386,8 +386,10 @@ int large_action(pf_context* ctx, const pf_method* m, int n, int k, const double
       }
     }
   }
-  int* d_tz = upload(ctx, kWsLargeAux + 2, tz);
-  double* d_w = upload(ctx, kWsLargeAux + 3, w);
+  int* d_tz = upload(ctx, kWsSmallArrays + 2, tz);
+  double* d_w = upload(ctx, kWsSmallArrays + 3, w);
+  std::vector<double> ones(std::max(P, 1), 1.0);
+  double* d_one = upload(ctx, kWsSmallArrays + 9, ones);
   const double constant = residual ? m->constant[0] : (hybrid ? m->poly[0] : 0.0);
   const double d1 = hybrid ? m->poly[1] : 0.0, d2 = hybrid ? m->poly[2] : 0.0;
   for (int step = 0; step < substeps; ++step) {
@@ -395,17 +397,11 @@ int large_action(pf_context* ctx, const pf_method* m, int n, int k, const double
     if (hybrid) gemm(ctx, np, k, np, 1, 1.0, Bp, np, 0, BX, k, 0, 0.0, B2X, k, 0, 0.0);
     if (P > 0) {
       // R_i = c_i B X (residual, action.cpp:252-258) or X (plain), rows permuted when pivoted
+      // R_i = c_i (B X) (residual) or 1 * X (plain; unit "shift" table), rows permuted when pivoted
       form_rhs_kernel<<<dim3(grid_for((int64_t)blk), P), 256, 0, ctx->stream>>>(
-          residual ? BX : X, k, 0, n, np, k, k, 1, d_sh, nullptr, 1, pivoted ? d_perm : nullptr, R, (int64_t)blk);
+          residual ? BX : X, k, 0, n, np, k, k, 1, residual ? d_sh : d_one, nullptr, 1, pivoted ? d_perm : nullptr, R,
+          (int64_t)blk);
       ctx->launches++;
-      if (!residual) {
-        // plain: RHS is X itself (form_rhs with c = 1 would need a unit shift table): rescale back
-        std::vector<double> ones(P, 1.0);
-        double* d_one = upload(ctx, kWsLargeAux + 9, ones);
-        form_rhs_kernel<<<dim3(grid_for((int64_t)blk), P), 256, 0, ctx->stream>>>(
-            X, k, 0, n, np, k, k, 1, d_one, nullptr, 1, pivoted ? d_perm : nullptr, R, (int64_t)blk);
-        ctx->launches++;
-      }
       trsm_left_lower(ctx, s, 0, np, R, k, (int64_t)blk, k);
       trsm_left_upper(ctx, s, 0, np, R, k, (int64_t)blk, k);
     }
@@ -474,7 +470,7 @@ int large_lu_solve(pf_context* ctx, int n, int k, int batch, const double* LU, i
   ctx->launches += 2;
   diag_inverses(ctx, s);
   std::vector<double> ones(batch, 1.0);
-  double* d_one = upload(ctx, kWsLargeAux + 9, ones);
+  double* d_one = upload(ctx, kWsSmallArrays + 9, ones);
   // X = P R (padded zeros): form_rhs with c = 1, batch 1 per system via z = b (one shift slot)
   form_rhs_kernel<<<dim3(grid_for((int64_t)blk), batch), 256, 0, ctx->stream>>>(R, ldr, strideR, n, s.np, k, k, batch,
                                                                                d_one, nullptr, 1, d_perm, X,
