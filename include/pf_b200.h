@@ -30,6 +30,7 @@
 #ifndef PF_B200_H
 #define PF_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -164,6 +165,13 @@ int pf_solve_shifted_batched(pf_context* ctx, int n, int batch, const double* dB
 int pf_gemm_batched(pf_context* ctx, int m, int n, int k, int batch, double alpha, const double* dA, int64_t lda,
                     int64_t strideA, const double* dB, int64_t ldb, int64_t strideB, double beta, double* dC,
                     int64_t ldc, int64_t strideC, double gamma);
+
+/* Device memory helpers for hosts without their own CUDA runtime (the C++ host layer): allocation
+ * on the context's device, synchronous copies ordered on the context's stream. */
+int pf_device_alloc(pf_context* ctx, size_t bytes, void** out);
+int pf_device_free(pf_context* ctx, void* p);
+int pf_copy_to_device(pf_context* ctx, void* dst, const void* src, size_t bytes);
+int pf_copy_to_host(pf_context* ctx, void* dst, const void* src, size_t bytes);
 
 /* Measured FP64 DMMA throughput of `device` in TFLOP/s (the FP64 roofline denominator). */
 double pf_probe_dmma_tflops(int device);

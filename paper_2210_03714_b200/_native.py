@@ -63,6 +63,10 @@ SIGNATURES = [
     ("pf_solve_shifted_batched", C.c_int, [_VP, C.c_int, C.c_int, _VP, _I64, _I64, C.c_double, _VP, _I64, _I64,
                                            C.c_int, C.POINTER(PfStatus)]),
     ("pf_probe_dmma_tflops", C.c_double, [C.c_int]),
+    ("pf_device_alloc", C.c_int, [_VP, C.c_size_t, C.POINTER(_VP)]),
+    ("pf_device_free", C.c_int, [_VP, _VP]),
+    ("pf_copy_to_device", C.c_int, [_VP, _VP, _VP, C.c_size_t]),
+    ("pf_copy_to_host", C.c_int, [_VP, _VP, _VP, C.c_size_t]),
     ("pf_gemm_batched", C.c_int, [_VP, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, _VP, _I64, _I64, _VP, _I64,
                                   _I64, C.c_double, _VP, _I64, _I64, C.c_double]),
 ]

@@ -87,6 +87,20 @@ def build_host(verbose: bool = False) -> Path:
     return out
 
 
+def build_cpp_tests(verbose: bool = False) -> Path:
+    """The C++ parity test binary over the host layer (tests/cpp/test_parfrac.cpp)."""
+    src = ROOT / "tests" / "cpp" / "test_parfrac.cpp"
+    out = LIB / "test_parfrac"
+    if not src.exists():
+        return out
+    deps = [src, LIB / "libparfrac_host.so"] + list((CPP / "include").rglob("*.hpp"))
+    if _stale(out, deps):
+        cxx = shutil.which("g++") or "g++"
+        _run([cxx, *CXX_FLAGS, "-o", str(out), str(src), "-L" + str(LIB), "-lparfrac_host", "-lpfb200",
+              "-Wl,-rpath,$ORIGIN", "-lpthread"])
+    return out
+
+
 def build_oracle() -> Path:
     """The CPU checker (test infrastructure; never loaded by the product path)."""
     _run(["make", "-s", "-C", str(ROOT / "oracle")])
@@ -96,8 +110,9 @@ def build_oracle() -> Path:
 def build_all(verbose: bool = False):
     eng = build_engine(verbose)
     host = build_host(verbose)
+    tst = build_cpp_tests(verbose)
     orc = build_oracle()
-    return eng, host, orc
+    return eng, host, tst, orc
 
 
 if __name__ == "__main__":

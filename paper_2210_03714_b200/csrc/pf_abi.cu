@@ -509,4 +509,32 @@ int pf_lu_solve_batched(pf_context* ctx, int n, int k, int batch, const double* 
   return collect_status(ctx, 0, 0, nullptr);
 }
 
+int pf_device_alloc(pf_context* ctx, size_t bytes, void** out) {
+  if (!ctx || !out) return PF_ERR_BAD_ARGUMENT;
+  *out = nullptr;
+  if (bytes == 0) return PF_OK;
+  return cuda_fail(cudaMalloc(out, bytes));
+}
+
+int pf_device_free(pf_context* ctx, void* p) {
+  if (!ctx) return PF_ERR_BAD_ARGUMENT;
+  if (!p) return PF_OK;
+  cudaStreamSynchronize(ctx->stream);
+  return cuda_fail(cudaFree(p));
+}
+
+int pf_copy_to_device(pf_context* ctx, void* dst, const void* src, size_t bytes) {
+  if (!ctx) return PF_ERR_BAD_ARGUMENT;
+  if (bytes == 0) return PF_OK;
+  if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess) return PF_ERR_CUDA;
+  return cuda_fail(cudaStreamSynchronize(ctx->stream));
+}
+
+int pf_copy_to_host(pf_context* ctx, void* dst, const void* src, size_t bytes) {
+  if (!ctx) return PF_ERR_BAD_ARGUMENT;
+  if (bytes == 0) return PF_OK;
+  if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess) return PF_ERR_CUDA;
+  return cuda_fail(cudaStreamSynchronize(ctx->stream));
+}
+
 }  // extern "C"

@@ -1,0 +1,284 @@
+// C++ parity tests of the drop-in host layer (namespace parfrac) on the B200, written like the
+// reference's own suites (proj/tests/test_dense.cpp, test_methods.cpp) so a maintainer can read them
+// side by side. Built by __graft_entry__.build(); run by tests/test_cpp_host.py (-m gpu).
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "parfrac/dense.hpp"
+#include "parfrac/error.hpp"
+#include "parfrac/methods.hpp"
+#include "parfrac/rng.hpp"
+
+using namespace parfrac;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(cond)                                                         \
+  do {                                                                      \
+    ++g_checks;                                                             \
+    if (!(cond)) {                                                          \
+      ++g_fail;                                                             \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);           \
+    }                                                                       \
+  } while (0)
+#define CHECK_THROWS(expr)                                                  \
+  do {                                                                      \
+    ++g_checks;                                                             \
+    bool thrown_ = false;                                                   \
+    try {                                                                   \
+      (void)(expr);                                                         \
+    } catch (const Error&) {                                                \
+      thrown_ = true;                                                       \
+    }                                                                       \
+    if (!thrown_) {                                                         \
+      ++g_fail;                                                             \
+      std::printf("FAIL %s:%d: no throw: %s\n", __FILE__, __LINE__, #expr); \
+    }                                                                       \
+  } while (0)
+
+namespace {
+
+DenseMatrix random_matrix(int d, std::uint64_t seed) {  // make_dense_matrix randn (cli.cpp:40-45)
+  DenseMatrix m(d);
+  NormalSampler normal(seed);
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) m.at(i, j) = normal.next();
+  return m;
+}
+
+DenseMatrix scaled_to_one_norm(DenseMatrix m, double target) {
+  m.scale(target / m.one_norm());
+  return m;
+}
+
+double rel_diff_1norm(const DenseMatrix& a, const DenseMatrix& b) {
+  DenseMatrix diff = a;
+  diff.axpy(-1.0, b);
+  return diff.one_norm() / std::max(b.one_norm(), 1e-300);
+}
+
+// CPU reference of the residual evaluator in the reference's operation order (the oracle's
+// algorithm, small sizes only), used as the parity referee inside this binary.
+DenseMatrix host_eval(const FractionMethod& m, const DenseMatrix& b, EvalForm form) {
+  const int d = b.dim();
+  DenseMatrix acc(d);
+  for (size_t i = 0; i < m.shifts.size(); ++i) {
+    const double c = to_double_nearest(m.shifts[i]), w = to_double_nearest(m.weights[i]);
+    if (c == 0.0) {
+      if (form == EvalForm::Plain) acc.add_scaled_identity(w);
+      continue;
+    }
+    DenseMatrix mm = b;
+    mm.scale(-c);
+    mm.add_scaled_identity(1.0);
+    // Gauss-Jordan with partial pivoting on [M | RHS] (small sizes)
+    DenseMatrix rhs(d);
+    if (form == EvalForm::Plain)
+      rhs = DenseMatrix::identity(d);
+    else {
+      rhs = b;
+      rhs.scale(c);
+    }
+    for (int col = 0; col < d; ++col) {
+      int p = col;
+      for (int r = col + 1; r < d; ++r)
+        if (std::abs(mm.at(r, col)) > std::abs(mm.at(p, col))) p = r;
+      for (int j = 0; j < d; ++j) {
+        std::swap(mm.at(p, j), mm.at(col, j));
+        std::swap(rhs.at(p, j), rhs.at(col, j));
+      }
+      for (int r = 0; r < d; ++r) {
+        if (r == col) continue;
+        const double f = mm.at(r, col) / mm.at(col, col);
+        for (int j = 0; j < d; ++j) {
+          mm.at(r, j) -= f * mm.at(col, j);
+          rhs.at(r, j) -= f * rhs.at(col, j);
+        }
+      }
+    }
+    for (int r = 0; r < d; ++r)
+      for (int j = 0; j < d; ++j) rhs.at(r, j) = rhs.at(r, j) / mm.at(r, r) * w;
+    acc.axpy(1.0, rhs);
+  }
+  if (form == EvalForm::Residual) acc.add_scaled_identity(to_double_nearest(m.constant));
+  return acc;
+}
+
+void test_lu_solve_and_singular() {  // test_dense.cpp:34-53
+  DenseMatrix a(3);
+  a.at(0, 0) = 2;
+  a.at(0, 1) = 1;
+  a.at(1, 1) = 3;
+  a.at(1, 2) = -1;
+  a.at(2, 0) = 1;
+  a.at(2, 2) = 4;
+  DenseLu lu(a);
+  std::vector<double> x = lu.solve(std::vector<double>{3, 2, 5});
+  std::vector<double> r = a.matvec(x);
+  CHECK(std::abs(r[0] - 3) <= 1e-14 * 3);
+  CHECK(std::abs(r[1] - 2) <= 1e-14 * 2);
+  CHECK(std::abs(r[2] - 5) <= 1e-14 * 5);
+  DenseMatrix singular(2);
+  singular.at(0, 0) = 1;
+  singular.at(1, 0) = 1;
+  CHECK_THROWS(DenseLu{singular});
+}
+
+void test_solve_shifted() {  // test_dense.cpp:55-83
+  DenseMatrix zero(4);
+  CHECK(rel_diff_1norm(solve_shifted(zero, 0.3), DenseMatrix::identity(4)) == 0.0);
+  DenseMatrix diag(3);
+  diag.at(0, 0) = 1.0;
+  diag.at(1, 1) = -2.0;
+  diag.at(2, 2) = 0.5;
+  DenseMatrix di = solve_shifted(diag, 0.25);
+  for (int i = 0; i < 3; ++i) {
+    const double expect = 1.0 / (1.0 - 0.25 * diag.at(i, i));
+    CHECK(std::abs(di.at(i, i) - expect) <= 1e-15 * std::abs(expect));
+  }
+  DenseMatrix b = random_matrix(8, 3);
+  const double c = 1.0 / 5.0;
+  DenseMatrix x = solve_shifted(b, c);
+  DenseMatrix shifted = b;
+  shifted.scale(-c);
+  shifted.add_scaled_identity(1.0);
+  DenseMatrix residual = shifted.mul(x);
+  residual.add_scaled_identity(-1.0);
+  CHECK(residual.one_norm() <= 1e-13 * x.one_norm());
+  CHECK_THROWS(solve_shifted(DenseMatrix::identity(5), 1.0));
+}
+
+void test_eval_dense_trivial_and_diagonal() {  // test_dense.cpp:85-106
+  const FractionMethod& r4 = catalog("R4");
+  const FractionMethod& r10 = catalog("R10");
+  DenseMatrix zero(5);
+  DenseMatrix expect = DenseMatrix::identity(5);
+  CHECK(rel_diff_1norm(eval_dense(r4, zero), expect) <= 1e-12);
+  CHECK(rel_diff_1norm(eval_dense(r10, zero), expect) <= 1e-9);
+  DenseMatrix diag(3);
+  for (int i = 0; i < 3; ++i) diag.at(i, i) = 0.1;
+  DenseMatrix v = eval_dense(r4, diag);
+  double scalar = 0;
+  for (size_t i = 0; i < r4.shifts.size(); ++i)
+    scalar += to_double_nearest(r4.weights[i]) * (1.0 / (1 - to_double_nearest(r4.shifts[i]) * 0.1));
+  for (int i = 0; i < 3; ++i) CHECK(std::abs(v.at(i, i) - scalar) <= 10 * std::abs(scalar) * 2.23e-16);
+}
+
+void test_workers_bit_identical() {  // test_dense.cpp:108-119
+  const FractionMethod& r8 = catalog("R8");
+  DenseMatrix b = scaled_to_one_norm(random_matrix(24, 5), 0.7);
+  DenseMatrix w1 = eval_dense(r8, b, {.workers = 1});
+  DenseMatrix w2 = eval_dense(r8, b, {.workers = 2});
+  DenseMatrix w8 = eval_dense(r8, b, {.workers = 8});
+  bool same = true;
+  for (int i = 0; i < b.dim(); ++i)
+    for (int j = 0; j < b.dim(); ++j) same = same && w1.at(i, j) == w2.at(i, j) && w1.at(i, j) == w8.at(i, j);
+  CHECK(same);
+  CHECK_THROWS(eval_dense(r8, b, {.workers = 0}));
+  CHECK_THROWS(eval_dense(r8, b, {.fixed_order = false}));
+}
+
+void test_plain_and_residual_and_message() {  // test_dense.cpp:121-140
+  const FractionMethod& r10 = catalog("R10");
+  DenseMatrix b = scaled_to_one_norm(random_matrix(24, 7), 1.0);
+  DenseMatrix plain = eval_dense(r10, b, {.form = EvalForm::Plain});
+  DenseMatrix residual = eval_dense(r10, b, {.form = EvalForm::Residual});
+  CHECK(rel_diff_1norm(plain, residual) <= 1e-8);
+  DenseMatrix bad = DenseMatrix::identity(4);
+  bad.scale(8.0);
+  bool ok = false;
+  try {
+    eval_dense(r10, bad);
+  } catch (const Error& e) {
+    ok = e.code() == Errc::SingularShift && std::string(e.what()).find("shift") != std::string::npos &&
+         std::string(e.what()).find("singular system: pivot magnitude") != std::string::npos && e.is_numerical();
+  }
+  CHECK(ok);
+}
+
+void test_residual_parity_vs_host_reference() {
+  for (const char* name : {"R4", "R8"}) {
+    const FractionMethod& m = catalog(name);
+    DenseMatrix b = scaled_to_one_norm(random_matrix(40, 9), 0.09);
+    DenseMatrix got = eval_dense(m, b, {.form = EvalForm::Residual});
+    DenseMatrix ref = host_eval(m, b, EvalForm::Residual);
+    CHECK(rel_diff_1norm(got, ref) <= 1e-12);
+  }
+}
+
+void test_expm_and_friends() {
+  DenseMatrix a = scaled_to_one_norm(random_matrix(64, 1), 2.0);  // cfg1
+  int j = -1;
+  DenseMatrix e4 = expm(catalog("R4"), a, EvalForm::Residual, &j);
+  CHECK(j == 10);
+  DenseMatrix e8 = expm(catalog("R8"), a);
+  CHECK(rel_diff_1norm(e4, e8) <= 1e-12);
+  DenseMatrix minus = a;
+  minus.scale(-1.0);
+  DenseMatrix prod = e8.mul(expm(catalog("R8"), minus));
+  CHECK(rel_diff_1norm(prod, DenseMatrix::identity(64)) <= 1e-12);
+  auto [ex, phi] = expm_phi1(catalog("R8"), a);
+  DenseMatrix lhs = phi.mul(a);
+  DenseMatrix rhs = ex;
+  rhs.add_scaled_identity(-1.0);
+  CHECK(rel_diff_1norm(lhs, rhs) <= 1e-11);
+  DenseMatrix sym = a;
+  for (int i = 0; i < 64; ++i)
+    for (int k = 0; k < 64; ++k) sym.at(i, k) = 0.5 * (a.at(i, k) + a.at(k, i));
+  auto [c, s] = cossin(catalog("R8"), sym);
+  DenseMatrix py = c.mul(c);
+  py.axpy(1.0, s.mul(s));
+  CHECK(rel_diff_1norm(py, DenseMatrix::identity(64)) <= 1e-12);
+  std::vector<double> v(64 * 2);
+  NormalSampler ns(11);
+  for (auto& x : v) x = ns.next();
+  std::vector<double> av = substep_action(catalog("R8"), a, v, 2);
+  // column 0 of exp(A) V against e8 V
+  double err = 0, nrm = 0;
+  for (int i = 0; i < 64; ++i) {
+    double ref = 0;
+    for (int k = 0; k < 64; ++k) ref += e8.at(i, k) * v[size_t(k) * 2];
+    err += std::abs(av[size_t(i) * 2] - ref);
+    nrm += std::abs(ref);
+  }
+  CHECK(err <= 1e-11 * nrm);
+}
+
+void test_catalog() {  // test_methods.cpp:50-110 against the generated tables
+  CHECK(catalog("R4").weights[3].text == "-515/9");
+  CHECK(catalog("R8").weights[0].text == "-9979069/32256");
+  CHECK(catalog("R10star").poly[0].text == "-34244933704346617/14676708556800");
+  CHECK(catalog("R4").processors() == 4);
+  CHECK(catalog("R4").constant.text == "1");
+  CHECK_THROWS(catalog("R99"));
+  CHECK(&catalog("R4") == &catalog("R4"));
+}
+
+}  // namespace
+
+int main() {
+  const std::vector<std::pair<const char*, std::function<void()>>> tests = {
+      {"lu solve and singularity detection", test_lu_solve_and_singular},
+      {"solve_shifted", test_solve_shifted},
+      {"eval_dense on trivial and diagonal inputs", test_eval_dense_trivial_and_diagonal},
+      {"eval_dense is bit identical across worker counts", test_workers_bit_identical},
+      {"plain and residual forms agree to rounding", test_plain_and_residual_and_message},
+      {"residual parity vs host reference", test_residual_parity_vs_host_reference},
+      {"expm / phi1 / cos-sin / action", test_expm_and_friends},
+      {"catalog", test_catalog},
+  };
+  for (auto& [name, fn] : tests) {
+    const int before = g_fail;
+    try {
+      fn();
+    } catch (const std::exception& e) {
+      ++g_fail;
+      std::printf("FAIL %s: exception %s\n", name, e.what());
+    }
+    std::printf("%s %s\n", g_fail == before ? "PASS" : "FAIL", name);
+  }
+  std::printf("%d checks, %d failures\n", g_checks, g_fail);
+  return g_fail ? 1 : 0;
+}
