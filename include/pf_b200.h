@@ -123,6 +123,12 @@ int pf_eval_dense_batched(pf_context* ctx, const pf_method* m, int n, int batch,
                           int64_t strideB, double* const* dOuts, int64_t ldo, int64_t strideOut, int flags,
                           pf_status* status);
 
+/* r(2^-j_b A_b) for every weight set, no squaring (j_b from dSquaringsIn, else from theta as below);
+ * the building block of the shift-partitioned multi-GPU evaluation. */
+int pf_eval_scaled_batched(pf_context* ctx, const pf_method* m, double theta, int n, int batch, const double* dA,
+                           int64_t lda, int64_t strideA, const int* dSquaringsIn, int* dSquaringsOut,
+                           double* const* dOuts, int64_t ldo, int64_t strideOut, int flags, pf_status* status);
+
 /* exp by scaling and squaring. j_b = dSquaringsIn[b] when non-NULL, else the smallest j >= 0 with
  * ldexp(||A_b||_1, -j) <= theta. B_b = 2^-j_b A_b, E = r(B_b) (weight set 0), E <- E^2 j_b times.
  * dSquaringsOut (may be NULL) receives j_b. */
@@ -165,6 +171,36 @@ int pf_solve_shifted_batched(pf_context* ctx, int n, int batch, const double* dB
 int pf_gemm_batched(pf_context* ctx, int m, int n, int k, int batch, double alpha, const double* dA, int64_t lda,
                     int64_t strideA, const double* dB, int64_t ldb, int64_t strideB, double beta, double* dC,
                     int64_t ldc, int64_t strideC, double gamma);
+
+/* ---- building blocks for callers that drive the stages themselves (multi-GPU shift partition) ---- */
+
+/* j_b = smallest j >= 0 with ldexp(||A_b||_1, -j) <= theta, into dJ (device). */
+int pf_squarings_batched(pf_context* ctx, int n, int batch, const double* dA, int64_t lda, int64_t strideA,
+                         double theta, int* dJ);
+/* dOut = ((t_0 + t_1) + t_2) + ... elementwise, each add rounded: the ascending-shift reduction of
+ * eval_dense (dense.cpp:245-246). dTerms is a HOST array of `count` device pointers. */
+int pf_ordered_sum(pf_context* ctx, int count, const double* const* dTerms, int64_t n_elems, double* dOut);
+/* E <- E^(2^j_b) per matrix (contiguous n x n batch). */
+int pf_square_chain(pf_context* ctx, int n, int batch, const int* dJ, double* dE);
+/* j_b steps of Phi <- 0.5 (E + I) Phi, E <- E E. */
+int pf_phi1_doubling(pf_context* ctx, int n, int batch, const int* dJ, double* dE, double* dPhi);
+/* j_b steps of C <- C C - S S, S <- 2 (S C). */
+int pf_cossin_doubling(pf_context* ctx, int n, int batch, const int* dJ, double* dC, double* dS);
+
+/* ActionOperator for a dense A (action.hpp:68-82): B = A * (1/substeps), the LU factors of the
+ * owned shifts are computed once and reused by every apply. `owned` (host, n_terms ints, NULL = all)
+ * selects the shifts this operator handles -- one subset per rank in the multi-GPU partition. */
+typedef struct pf_action_op pf_action_op;
+int pf_action_create(pf_context* ctx, const pf_method* m, int n, const double* dA, int64_t lda, int substeps,
+                     const int* owned, int flags, pf_status* status, pf_action_op** out);
+/* One substep restricted to the owned terms: dOut = sum_owned w_i x_i (+ a_0 V + d1 BV + d2 B^2 V when
+ * include_poly). With dTerms != NULL also writes every owned weighted term (ascending shift index,
+ * n x k each) followed by a_0 V and d1 BV + d2 B^2 V (when include_poly): an ordered sum of all
+ * ranks' terms reproduces the single-operator result bit for bit. */
+int pf_action_apply(pf_action_op* op, const double* dV, int64_t ldv, int k, double* dOut, int64_t ldo,
+                    int include_poly, double* dTerms, pf_status* status);
+int pf_action_term_count(pf_action_op* op);
+int pf_action_destroy(pf_action_op* op);
 
 /* Device memory helpers for hosts without their own CUDA runtime (the C++ host layer): allocation
  * on the context's device, synchronous copies ordered on the context's stream. */

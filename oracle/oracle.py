@@ -113,6 +113,15 @@ def mul(a, b) -> np.ndarray:
     return out
 
 
+def mul_rect(a, b) -> np.ndarray:
+    """(n x n)(n x k), i-k-j order with the zero skip (DenseMatrix::mul generalised)."""
+    a, b = _f64(a), _f64(b)
+    b2 = b.reshape(b.shape[0], -1)
+    out = np.empty_like(b2)
+    lib().pfo_mul_rect(a.shape[0], b2.shape[1], _p(a), _p(b2), _p(out))
+    return out.reshape(b.shape)
+
+
 def lu(a, rel_tol: float = 1e-14):
     lu_ = _f64(a).copy()
     n = lu_.shape[0]

@@ -62,6 +62,18 @@ SIGNATURES = [
     ("pf_lu_solve_batched", C.c_int, [_VP, C.c_int, C.c_int, C.c_int, _VP, _I64, _I64, _VP, _VP, _I64, _I64]),
     ("pf_solve_shifted_batched", C.c_int, [_VP, C.c_int, C.c_int, _VP, _I64, _I64, C.c_double, _VP, _I64, _I64,
                                            C.c_int, C.POINTER(PfStatus)]),
+    ("pf_eval_scaled_batched", C.c_int, [_VP, C.POINTER(PfMethod), C.c_double, C.c_int, C.c_int, _VP, _I64, _I64,
+                                         _VP, _VP, C.POINTER(_VP), _I64, _I64, C.c_int, C.POINTER(PfStatus)]),
+    ("pf_squarings_batched", C.c_int, [_VP, C.c_int, C.c_int, _VP, _I64, _I64, C.c_double, _VP]),
+    ("pf_ordered_sum", C.c_int, [_VP, C.c_int, C.POINTER(_VP), _I64, _VP]),
+    ("pf_square_chain", C.c_int, [_VP, C.c_int, C.c_int, _VP, _VP]),
+    ("pf_phi1_doubling", C.c_int, [_VP, C.c_int, C.c_int, _VP, _VP, _VP]),
+    ("pf_cossin_doubling", C.c_int, [_VP, C.c_int, C.c_int, _VP, _VP, _VP]),
+    ("pf_action_create", C.c_int, [_VP, C.POINTER(PfMethod), C.c_int, _VP, _I64, C.c_int, C.POINTER(C.c_int), C.c_int,
+                                   C.POINTER(PfStatus), C.POINTER(_VP)]),
+    ("pf_action_apply", C.c_int, [_VP, _VP, _I64, C.c_int, _VP, _I64, C.c_int, _VP, C.POINTER(PfStatus)]),
+    ("pf_action_term_count", C.c_int, [_VP]),
+    ("pf_action_destroy", C.c_int, [_VP]),
     ("pf_probe_dmma_tflops", C.c_double, [C.c_int]),
     ("pf_device_alloc", C.c_int, [_VP, C.c_size_t, C.POINTER(_VP)]),
     ("pf_device_free", C.c_int, [_VP, _VP]),

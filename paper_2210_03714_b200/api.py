@@ -234,6 +234,131 @@ def eval_dense(method, B: ArrayLike, opts: Optional[EvalOptions] = None, extra_s
     return res if extra_sets else res[0]
 
 
+def eval_dense_raw(B: torch.Tensor, shifts: Sequence[float], weights: Sequence[Sequence[float]],
+                   constants: Sequence[float], form: int = RESIDUAL, poly: Optional[Sequence[Sequence[float]]] = None,
+                   flags: int = 0, squarings: Optional[torch.Tensor] = None) -> List[torch.Tensor]:
+    """eval_dense on explicit doubles (device tensors in and out): one output per weight set, of
+    B itself or -- with `squarings` (device int32, one per matrix) -- of 2^-j B. Used by the shift
+    partition (parallel.py) to evaluate a rank's subset of the terms."""
+    eng = engine()
+    dB3, batched = _as_batch(B.contiguous())
+    bsz, n = dB3.shape[0], dB3.shape[1]
+    nt = len(shifts)
+    sets = len(weights)
+    sh = (C.c_double * max(nt, 1))(*shifts)
+    w = (C.c_double * max(nt * sets, 1))(*[x for row in weights for x in row])
+    cst = (C.c_double * sets)(*constants)
+    pl = (C.c_double * (3 * sets))(*([x for row in poly for x in row] if poly else [0.0] * (3 * sets)))
+    m = N.PfMethod(nt, sh, sets, w, 1 if poly else 0, pl, cst, int(form))
+    outs = [torch.empty_like(dB3) for _ in range(sets)]
+    ptrs = (C.c_void_p * sets)(*[o.data_ptr() for o in outs])
+    st = N.PfStatus()
+    if squarings is not None:
+        jin = squarings.to(dtype=torch.int32, device=dB3.device).contiguous()
+        rc = N.lib.pf_eval_scaled_batched(eng.h, C.byref(m), 0.0, n, bsz, dB3.data_ptr(), n, n * n, jin.data_ptr(),
+                                          None, ptrs, n, n * n, flags, C.byref(st))
+    else:
+        rc = N.lib.pf_eval_dense_batched(eng.h, C.byref(m), n, bsz, dB3.data_ptr(), n, n * n, ptrs, n, n * n, flags,
+                                         C.byref(st))
+    if rc:
+        _raise(rc, st, batched)
+    return [o if batched else o[0] for o in outs]
+
+
+def ordered_sum(terms: Sequence[torch.Tensor]) -> torch.Tensor:
+    """((t0 + t1) + t2) + ... on the device (pf_ordered_sum): the reference's fixed reduction order."""
+    eng = engine()
+    ts = [t.contiguous() for t in terms]
+    out = torch.empty_like(ts[0])
+    ptrs = (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
+    rc = N.lib.pf_ordered_sum(eng.h, len(ts), ptrs, ts[0].numel(), out.data_ptr())
+    if rc:
+        _raise(rc, N.PfStatus(), False)
+    return out
+
+
+def squarings(A: torch.Tensor, theta: float) -> torch.Tensor:
+    eng = engine()
+    a3, _ = _as_batch(A.contiguous())
+    bsz, n = a3.shape[0], a3.shape[1]
+    j = torch.empty(bsz, dtype=torch.int32, device=a3.device)
+    rc = N.lib.pf_squarings_batched(eng.h, n, bsz, a3.data_ptr(), n, n * n, float(theta), j.data_ptr())
+    if rc:
+        _raise(rc, N.PfStatus(), True)
+    return j
+
+
+def phi1_doubling(E: torch.Tensor, Phi: torch.Tensor, j: torch.Tensor):
+    eng = engine()
+    e3, _ = _as_batch(E)
+    p3, _ = _as_batch(Phi)
+    rc = N.lib.pf_phi1_doubling(eng.h, e3.shape[1], e3.shape[0], j.data_ptr(), e3.data_ptr(), p3.data_ptr())
+    if rc:
+        _raise(rc, N.PfStatus(), True)
+    return E, Phi
+
+
+def square_chain(E: torch.Tensor, j: torch.Tensor):
+    eng = engine()
+    e3, _ = _as_batch(E)
+    rc = N.lib.pf_square_chain(eng.h, e3.shape[1], e3.shape[0], j.data_ptr(), e3.data_ptr())
+    if rc:
+        _raise(rc, N.PfStatus(), True)
+    return E
+
+
+class ActionOperator:
+    """ActionOperator on a dense A (action.hpp:68-82): B = A (1/N), LU of every owned shift computed
+    once; apply() = one substep r(B) V over the owned terms (optionally with the poly part)."""
+
+    def __init__(self, A: torch.Tensor, method="R8", substeps: int = 1, form: int = RESIDUAL,
+                 owned: Optional[Sequence[int]] = None, flags: int = 0):
+        self.method = _resolve_method(method)
+        self.pk = PackedMethod(self.method, form)
+        eng = engine()
+        self.A = A.contiguous()
+        n = self.A.shape[0]
+        own = None
+        if owned is not None:
+            own = (C.c_int * len(self.method.shifts))(*[1 if i in set(owned) else 0
+                                                        for i in range(len(self.method.shifts))])
+        h = C.c_void_p()
+        st = N.PfStatus()
+        rc = N.lib.pf_action_create(eng.h, self.pk.ptr(), n, self.A.data_ptr(), n, int(substeps), own, flags,
+                                    C.byref(st), C.byref(h))
+        if rc:
+            _raise(rc, st, False)
+        self.h = h
+        self.n = n
+        self.terms = int(N.lib.pf_action_term_count(h))
+        hybrid = len(self.method.poly) == 3
+        self.poly_terms = (1 if (form == RESIDUAL or hybrid) else 0) + (1 if hybrid else 0)
+
+    def apply(self, V: torch.Tensor, include_poly: bool = True, with_terms: bool = False):
+        V2 = V.reshape(self.n, -1).contiguous()
+        k = V2.shape[1]
+        out = torch.empty_like(V2)
+        nterm = self.terms + (self.poly_terms if include_poly else 0)
+        terms = torch.empty((nterm, self.n, k), dtype=torch.float64, device=V2.device) if with_terms else None
+        st = N.PfStatus()
+        rc = N.lib.pf_action_apply(self.h, V2.data_ptr(), k, k, out.data_ptr(), k, 1 if include_poly else 0,
+                                   terms.data_ptr() if terms is not None else None, C.byref(st))
+        if rc:
+            _raise(rc, st, False)
+        return (out, terms) if with_terms else out
+
+    def close(self):
+        if getattr(self, "h", None):
+            N.lib.pf_action_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def solve_shifted(B: ArrayLike, c: float, flags: int = 0):
     """(I - cB)^{-1} (dense.cpp:165-171)."""
     eng = engine()

@@ -30,10 +30,10 @@ __device__ __forceinline__ double ldexp_j(double x, int j) { return j == 0 ? x :
 // LU of the 64 x 64 diagonal block at (off, off) of every system, no row exchanges, in place;
 // inverses of L (unit lower) and U written to inv + z * inv_stride + (off / 64) * 2 * 64 * 64.
 __global__ void __launch_bounds__(256) lu_base64_kernel(double* M, int64_t ld, int64_t strideM, int off,
-                                                        double* inv, int64_t inv_stride, int factor) {
+                                                        double* inv, int64_t inv_stride, int factor, const int* zlist) {
   __shared__ double s[B64 * L64];
   __shared__ double prow[B64];
-  const int z = blockIdx.x;
+  const int z = zlist ? zlist[blockIdx.x] : blockIdx.x;
   double* a = M + (int64_t)z * strideM + (int64_t)off * ld + off;
   for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
     const int r = idx >> 6, c = idx & 63;
@@ -149,12 +149,13 @@ __global__ void __launch_bounds__(256) apply_inv64_kernel(const double* inv, int
 // Genuine partial pivoting (reference operation order, dense.cpp:105-132) on the leading n x n of
 // each np x np system; one CTA of 1024 threads per system, global memory. Fallback only.
 __global__ void __launch_bounds__(1024) lu_pivot_kernel(double* M, int64_t ld, int64_t strideM, int n, int* piv,
-                                                        const double* tol, DevStatus* status, int* first_error) {
+                                                        const double* tol, DevStatus* status, int* first_error,
+                                                        const int* zlist) {
   __shared__ double red_v[32];
   __shared__ int red_i[32];
   __shared__ int s_p;
   __shared__ double s_best;
-  const int z = blockIdx.x;
+  const int z = zlist ? zlist[blockIdx.x] : blockIdx.x;
   double* a = M + (int64_t)z * strideM;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int col = 0; col < n; ++col) {
@@ -334,8 +335,8 @@ __global__ void accumulate_kernel(const double* X, int64_t xld, int64_t strideX,
 }
 
 // perm_z from the swap sequence piv_z (LAPACK style): perm[r] = row of the original RHS in row r.
-__global__ void perm_from_piv_kernel(const int* piv, int n, int* perm) {
-  const int z = blockIdx.x;
+__global__ void perm_from_piv_kernel(const int* piv, int n, int* perm, const int* zlist) {
+  const int z = zlist ? zlist[blockIdx.x] : blockIdx.x;
   if (threadIdx.x != 0) return;
   int* p = perm + (int64_t)z * n;
   for (int r = 0; r < n; ++r) p[r] = r;
@@ -430,6 +431,17 @@ __global__ void action_accumulate_kernel(const double* R, int64_t rld, int64_t s
       }
     }
     out[(int64_t)r * ldo + c] = acc;
+  }
+}
+
+// out = d1 X + d2 Y (each product rounded, then the sum): the hybrid poly term of assemble_action
+// (action.cpp:279-281), kept separate for the deterministic multi-rank reduction.
+__global__ void lincomb2_kernel(int n, int k, double d1, const double* X, double d2, const double* Y, int64_t ld,
+                                double* out, int64_t ldo) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)n * k;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / k), c = (int)(idx % k);
+    out[(int64_t)r * ldo + c] = __dadd_rn(__dmul_rn(d1, X[(int64_t)r * ld + c]), __dmul_rn(d2, Y[(int64_t)r * ld + c]));
   }
 }
 }  // namespace pf

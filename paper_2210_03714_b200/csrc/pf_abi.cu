@@ -332,6 +332,20 @@ void copy_out(pf_context* ctx, int n, int batch, const double* src, double* dst,
 
 }  // namespace
 
+int pf_eval_scaled_batched(pf_context* ctx, const pf_method* m, double theta, int n, int batch, const double* dA,
+                           int64_t lda, int64_t strideA, const int* dSquaringsIn, int* dSquaringsOut,
+                           double* const* dOuts, int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
+  pf::SmallParams p{};
+  if (!ctx || n < 0 || batch < 0 || !dOuts || !fill_method(m, p) || lda < n || ldo < n ||
+      (!dSquaringsIn && !(theta > 0)))
+    return bad(status);
+  if (batch == 0 || n == 0) return PF_OK;
+  int* dJ = dSquaringsOut ? dSquaringsOut : static_cast<int*>(workspace(ctx, kWsJ, sizeof(int) * batch));
+  if (!dJ) return PF_ERR_CUDA;
+  return eval_scaled(ctx, m, theta > 0 ? theta : 1.0, n, batch, dA, lda, strideA, dSquaringsIn, dJ, dOuts, ldo,
+                     strideOut, flags, status);
+}
+
 int pf_expm_batched(pf_context* ctx, const pf_method* m, double theta, int n, int batch, const double* dA,
                     int64_t lda, int64_t strideA, const int* dSquaringsIn, int* dSquaringsOut, double* dOut,
                     int64_t ldo, int64_t strideOut, int flags, pf_status* status) {

@@ -19,8 +19,34 @@ struct pf_context {
   unsigned long long* prof = nullptr;
 };
 
+// Dense ActionOperator (action.hpp:68-82): B = A * (1/N) and the LU factors of the owned shifts,
+// persistent across applies (own allocations, not the context workspace).
+struct pf_action_op {
+  pf_context* ctx = nullptr;
+  int n = 0, np = 0, substeps = 1;
+  int form = PF_FORM_RESIDUAL, hybrid = 0;
+  double constant = 0.0, d1 = 0.0, d2 = 0.0;
+  std::vector<double> shifts;      // owned nonzero shifts, ascending shift index
+  std::vector<int> term_index;     // shift index of every owned term (nonzero shifts + plain zero shift)
+  std::vector<double> term_weight;
+  std::vector<int> term_slot;      // factor slot of the term (-1: plain zero shift, term = w X)
+  double* B = nullptr;             // np x np, zero padded
+  double* M = nullptr;             // P_owned x np x np LU factors
+  double* inv = nullptr;           // diagonal-block inverses
+  int* perm = nullptr;             // P_owned x n row order (pivoted systems)
+  bool pivoted = false;
+  double* d_shifts = nullptr;      // device copy of `shifts`
+  double* d_ones = nullptr;
+};
+
 namespace pf {
 namespace host {
+
+int action_op_create(pf_context* ctx, const pf_method* m, int n, const double* A, int64_t lda, int substeps,
+                     const int* owned, int flags, pf_status* status, pf_action_op** out);
+int action_op_apply(pf_action_op* op, const double* V, int64_t ldv, int k, double* out, int64_t ldo,
+                    int include_poly, double* terms);
+void action_op_destroy(pf_action_op* op);
 
 int cuda_fail(cudaError_t e);
 void* workspace(pf_context* ctx, int slot, size_t bytes);

@@ -15,12 +15,12 @@
 
 namespace pf {
 
-__global__ void lu_base64_kernel(double* M, int64_t ld, int64_t strideM, int off, double* inv, int64_t inv_stride,
-                                 int factor);
+__global__ void lu_base64_kernel(double* M, int64_t ld, int64_t strideM, int off, double* inv, int64_t inv_stride, int factor,
+                                 const int* zlist);
 __global__ void apply_inv64_kernel(const double* inv, int64_t inv_stride, int blk, int upper, int right, double* Bm,
                                    int64_t ld, int64_t strideB, int extent);
 __global__ void lu_pivot_kernel(double* M, int64_t ld, int64_t strideM, int n, int* piv, const double* tol,
-                                DevStatus* status, int* first_error);
+                                DevStatus* status, int* first_error, const int* zlist);
 __global__ void form_shifted_kernel(const double* A, int64_t lda, int64_t strideA, int n, int np, int batch,
                                     const double* shifts, const int* j, double* M, unsigned long long* mx);
 __global__ void certificate_kernel(const double* M, int np, int n, const unsigned long long* mx, double rel_tol,
@@ -37,7 +37,7 @@ __global__ void action_accumulate_kernel(const double* R, int64_t rld, int64_t s
                                          int n, int k, int n_terms, const int* term_z, const double* w, int add_poly,
                                          double constant, int hybrid, double d1, double d2, const double* BX,
                                          const double* B2X, double* out, int64_t ldo);
-__global__ void perm_from_piv_kernel(const int* piv, int n, int* perm);
+__global__ void perm_from_piv_kernel(const int* piv, int n, int* perm, const int* zlist);
 __global__ void copy2d_kernel(int rows, int cols, double s, const double* X, int64_t ldx, int64_t strideX, double* Y,
                               int64_t ldy, int64_t strideY);
 __global__ void scale_pad_kernel(const double* A, int64_t lda, int n, int np, double s, double* B);
@@ -45,6 +45,8 @@ __global__ void fill_int_kernel(int* p, int count, int v);
 __global__ void load_padded_kernel(const double* A, int64_t lda, int64_t strideA, int n, int np, double* M,
                                    unsigned long long* mx);
 __global__ void iota_kernel(int* p, int n);
+__global__ void lincomb2_kernel(int n, int k, double d1, const double* X, double d2, const double* Y, int64_t ld,
+                                double* out, int64_t ldo);
 size_t apply_inv64_smem_bytes();
 
 namespace host {
@@ -121,7 +123,7 @@ void trsm_right_upper(pf_context* ctx, const Sys& s, int off, int n, double* B, 
 
 void lu_rec(pf_context* ctx, const Sys& s, int off, int n) {
   if (n == kB) {
-    lu_base64_kernel<<<s.nsys, 256, 0, ctx->stream>>>(s.M, s.np, s.stride(), off, s.inv, s.inv_stride, 1);
+    lu_base64_kernel<<<s.nsys, 256, 0, ctx->stream>>>(s.M, s.np, s.stride(), off, s.inv, s.inv_stride, 1, nullptr);
     ctx->launches++;
     return;
   }
@@ -138,7 +140,7 @@ void lu_rec(pf_context* ctx, const Sys& s, int off, int n) {
 
 void diag_inverses(pf_context* ctx, const Sys& s) {
   for (int off = 0; off < s.np; off += kB) {
-    lu_base64_kernel<<<s.nsys, 256, 0, ctx->stream>>>(s.M, s.np, s.stride(), off, s.inv, s.inv_stride, 0);
+    lu_base64_kernel<<<s.nsys, 256, 0, ctx->stream>>>(s.M, s.np, s.stride(), off, s.inv, s.inv_stride, 0, nullptr);
     ctx->launches++;
   }
 }
@@ -178,28 +180,51 @@ FactorResult factor_systems(pf_context* ctx, const Sys& s, int n, unsigned long 
     return fr;
   }
   fr.scale.resize(s.nsys);
-  bool all_ok = (flags & PF_FLAG_FORCE_PIVOT) == 0;
+  const bool force = (flags & PF_FLAG_FORCE_PIVOT) != 0;
+  std::vector<int> fails;  // the pivot decision is per system: results never depend on the batch
   for (int z = 0; z < s.nsys; ++z) {
     double mx;
     std::memcpy(&mx, &mxbits[z], sizeof(double));
     fr.scale[z] = std::max(mx, 1e-300);
-    all_ok = all_ok && ok[z];
+    if (force || !ok[z]) fails.push_back(z);
   }
-  if (all_ok) {
+  const int nf = (int)fails.size();
+  if (nf == 0) {
     lu_rec(ctx, s, 0, s.np);
     return fr;
   }
   fr.pivoted = true;
+  // keep the failing systems' M aside, run the blocked LU on the batch, restore them, pivot them
+  double* side = nullptr;
+  if (nf < s.nsys) {
+    side = static_cast<double*>(workspace(ctx, kWsLargeX2 + 1, sizeof(double) * s.stride() * nf));
+    if (!side) {
+      fr.rc = PF_ERR_CUDA;
+      return fr;
+    }
+    for (int q = 0; q < nf; ++q)
+      cudaMemcpyAsync(side + q * s.stride(), s.M + fails[q] * s.stride(), sizeof(double) * s.stride(),
+                      cudaMemcpyDeviceToDevice, ctx->stream);
+    lu_rec(ctx, s, 0, s.np);
+    for (int q = 0; q < nf; ++q)
+      cudaMemcpyAsync(s.M + fails[q] * s.stride(), side + q * s.stride(), sizeof(double) * s.stride(),
+                      cudaMemcpyDeviceToDevice, ctx->stream);
+  }
   std::vector<double> tol(s.nsys);
   for (int z = 0; z < s.nsys; ++z) tol[z] = pivot_rel_tol * fr.scale[z];
   double* d_tol = upload(ctx, kWsSmallArrays + 21, tol);
+  int* d_fail = upload(ctx, kWsSmallArrays + 22, fails);
+  // certified systems keep the identity row order and swap sequence
+  iota_kernel<<<dim3((n + 255) / 256, s.nsys), 256, 0, ctx->stream>>>(d_perm, n);
+  iota_kernel<<<dim3((n + 255) / 256, s.nsys), 256, 0, ctx->stream>>>(d_piv, n);
+  ctx->launches += 2;
   int rc = ensure_status(ctx, s.nsys);
   if (rc) {
     fr.rc = rc;
     return fr;
   }
-  lu_pivot_kernel<<<s.nsys, 1024, 0, ctx->stream>>>(s.M, s.np, s.stride(), n, d_piv, d_tol, ctx->status,
-                                                    ctx->first_error);
+  lu_pivot_kernel<<<nf, 1024, 0, ctx->stream>>>(s.M, s.np, s.stride(), n, d_piv, d_tol, ctx->status,
+                                                ctx->first_error, d_fail);
   ctx->launches++;
   pf_status ps;
   rc = collect_status(ctx, s.nsys, 0, &ps);
@@ -211,9 +236,12 @@ FactorResult factor_systems(pf_context* ctx, const Sys& s, int n, unsigned long 
     fr.st.pivot_magnitude = ps.pivot_magnitude;
     return fr;
   }
-  perm_from_piv_kernel<<<s.nsys, 32, 0, ctx->stream>>>(d_piv, n, d_perm);
+  perm_from_piv_kernel<<<nf, 32, 0, ctx->stream>>>(d_piv, n, d_perm, d_fail);
   ctx->launches++;
-  diag_inverses(ctx, s);
+  for (int off = 0; off < s.np; off += kB) {
+    lu_base64_kernel<<<nf, 256, 0, ctx->stream>>>(s.M, s.np, s.stride(), off, s.inv, s.inv_stride, 0, d_fail);
+    ctx->launches++;
+  }
   return fr;
 }
 
@@ -445,7 +473,7 @@ int large_lu_factor(pf_context* ctx, int n, int batch, double* A, int64_t lda, i
                                                                                strideA);
   ctx->launches++;
   if (piv) {
-    if (fr.pivoted) {
+    if (fr.pivoted) {  // every system's swap sequence (identity for the certified ones)
       cudaMemcpyAsync(piv, d_piv, sizeof(int) * (size_t)n * batch, cudaMemcpyDeviceToDevice, ctx->stream);
     } else {
       iota_kernel<<<dim3((n + 255) / 256, batch), 256, 0, ctx->stream>>>(piv, n);
@@ -466,7 +494,7 @@ int large_lu_solve(pf_context* ctx, int n, int k, int batch, const double* LU, i
   double* X = static_cast<double*>(workspace(ctx, kWsLargeR, sizeof(double) * blk * batch));
   if (!d_mx || !d_perm || !X) return PF_ERR_CUDA;
   load_padded_kernel<<<dim3(grid_for(s.stride()), batch), 256, 0, ctx->stream>>>(LU, lda, strideLU, n, s.np, s.M, d_mx);
-  perm_from_piv_kernel<<<batch, 32, 0, ctx->stream>>>(piv, n, d_perm);
+  perm_from_piv_kernel<<<batch, 32, 0, ctx->stream>>>(piv, n, d_perm, nullptr);
   ctx->launches += 2;
   diag_inverses(ctx, s);
   std::vector<double> ones(batch, 1.0);
@@ -482,6 +510,164 @@ int large_lu_solve(pf_context* ctx, int n, int k, int batch, const double* LU, i
                                                                                strideR);
   ctx->launches++;
   return cuda_fail(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------------------------
+// ActionOperator on a dense A (action.hpp:68-82, action.cpp:300-325): B = A * (1/N) and the LU
+// factors of the owned shifts persist; apply() performs one substep r(B) V restricted to the owned
+// terms (a shift subset per rank for the multi-GPU partition), optionally with the poly part.
+int action_op_create(pf_context* ctx, const pf_method* m, int n, const double* A, int64_t lda, int substeps,
+                     const int* owned, int flags, pf_status* status, pf_action_op** out) {
+  if (status) std::memset(status, 0, sizeof(*status));
+  auto* op = new pf_action_op();
+  op->ctx = ctx;
+  op->n = n;
+  op->np = round64(n);
+  op->substeps = substeps;
+  op->form = m->form;
+  op->hybrid = m->has_poly ? 1 : 0;
+  const bool residual = m->form == PF_FORM_RESIDUAL;
+  op->constant = residual ? m->constant[0] : (op->hybrid ? m->poly[0] : 0.0);
+  op->d1 = op->hybrid ? m->poly[1] : 0.0;
+  op->d2 = op->hybrid ? m->poly[2] : 0.0;
+  for (int i = 0; i < m->n_terms; ++i) {
+    const bool nonzero = m->shifts[i] != 0.0;
+    if (!nonzero && residual) continue;  // residual zero shifts fold into a_0
+    if (owned && !owned[i]) continue;
+    op->term_index.push_back(i);
+    op->term_weight.push_back(m->weights[i]);
+    if (nonzero) {
+      op->term_slot.push_back((int)op->shifts.size());
+      op->shifts.push_back(m->shifts[i]);
+    } else {
+      op->term_slot.push_back(-1);
+    }
+  }
+  const int P = (int)op->shifts.size();
+  const int64_t st = (int64_t)op->np * op->np;
+  const int64_t inv_stride = (int64_t)(op->np / kB) * 2 * kB * kB;
+  bool okalloc = cudaMalloc(&op->B, sizeof(double) * st) == cudaSuccess;
+  if (P > 0) {
+    okalloc = okalloc && cudaMalloc(&op->M, sizeof(double) * st * P) == cudaSuccess;
+    okalloc = okalloc && cudaMalloc(&op->inv, sizeof(double) * inv_stride * P) == cudaSuccess;
+    okalloc = okalloc && cudaMalloc(&op->perm, sizeof(int) * (size_t)n * P) == cudaSuccess;
+    okalloc = okalloc && cudaMalloc(&op->d_shifts, sizeof(double) * P) == cudaSuccess;
+    okalloc = okalloc && cudaMalloc(&op->d_ones, sizeof(double) * P) == cudaSuccess;
+  }
+  if (!okalloc) {
+    action_op_destroy(op);
+    return PF_ERR_CUDA;
+  }
+  scale_pad_kernel<<<grid_for(st), 256, 0, ctx->stream>>>(A, lda, n, op->np, 1.0 / substeps, op->B);
+  ctx->launches++;
+  if (P > 0) {
+    std::vector<double> ones(P, 1.0);
+    cudaMemcpyAsync(op->d_shifts, op->shifts.data(), sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(op->d_ones, ones.data(), sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream);
+    auto* d_mx = static_cast<unsigned long long*>(workspace(ctx, kWsLargeAux, sizeof(unsigned long long) * P));
+    int* d_piv = static_cast<int*>(workspace(ctx, kWsLargePiv, sizeof(int) * (size_t)n * P));
+    if (!d_mx || !d_piv) {
+      action_op_destroy(op);
+      return PF_ERR_CUDA;
+    }
+    cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long) * P, ctx->stream);
+    form_shifted_kernel<<<dim3(grid_for(st), P), 256, 0, ctx->stream>>>(op->B, op->np, 0, n, op->np, 1, op->d_shifts,
+                                                                       nullptr, op->M, d_mx);
+    ctx->launches++;
+    Sys s{op->M, op->np, P, op->inv, inv_stride};
+    FactorResult fr = factor_systems(ctx, s, n, d_mx, flags, d_piv, op->perm, 1e-14);
+    if (fr.rc) {
+      if (status) {
+        status->code = fr.rc;
+        if (fr.z >= 0) {
+          int q = 0;
+          for (size_t t = 0; t < op->term_slot.size(); ++t)
+            if (op->term_slot[t] == fr.z) q = op->term_index[t];
+          status->shift_index = q + 1;
+          status->column = fr.st.column;
+          status->pivot_magnitude = fr.st.pivot_magnitude;
+          status->scale = fr.scale[fr.z];
+        }
+      }
+      const int rc = fr.rc;
+      action_op_destroy(op);
+      return rc;
+    }
+    op->pivoted = fr.pivoted;
+  }
+  *out = op;
+  return cuda_fail(cudaGetLastError());
+}
+
+int action_op_apply(pf_action_op* op, const double* V, int64_t ldv, int k, double* out, int64_t ldo,
+                    int include_poly, double* terms) {
+  pf_context* ctx = op->ctx;
+  const int n = op->n, np = op->np, P = (int)op->shifts.size();
+  const size_t blk = (size_t)np * k;
+  const bool residual = op->form == PF_FORM_RESIDUAL;
+  double* X = static_cast<double*>(workspace(ctx, kWsT1, sizeof(double) * blk * 3));
+  double* R = static_cast<double*>(workspace(ctx, kWsLargeR, sizeof(double) * blk * std::max(P, 1)));
+  if (!X || !R) return PF_ERR_CUDA;
+  double* BX = X + blk;
+  double* B2X = X + 2 * blk;
+  cudaMemsetAsync(X, 0, sizeof(double) * blk, ctx->stream);
+  copy2d_kernel<<<dim3(grid_for((int64_t)n * k), 1), 256, 0, ctx->stream>>>(n, k, 1.0, V, ldv, 0, X, k, 0);
+  ctx->launches++;
+  if (residual || op->hybrid) gemm(ctx, np, k, np, 1, 1.0, op->B, np, 0, X, k, 0, 0.0, BX, k, 0, 0.0);
+  if (op->hybrid) gemm(ctx, np, k, np, 1, 1.0, op->B, np, 0, BX, k, 0, 0.0, B2X, k, 0, 0.0);
+  if (P > 0) {
+    // R_i = c_i (B X) (residual, action.cpp:252-258) or X (plain), rows permuted when pivoted
+    form_rhs_kernel<<<dim3(grid_for((int64_t)blk), P), 256, 0, ctx->stream>>>(
+        residual ? BX : X, k, 0, n, np, k, k, 1, residual ? op->d_shifts : op->d_ones, nullptr, 1,
+        op->pivoted ? op->perm : nullptr, R, (int64_t)blk);
+    ctx->launches++;
+    Sys s{op->M, np, P, op->inv, (int64_t)(np / kB) * 2 * kB * kB};
+    trsm_left_lower(ctx, s, 0, np, R, k, (int64_t)blk, k);
+    trsm_left_upper(ctx, s, 0, np, R, k, (int64_t)blk, k);
+  }
+  const int nt = (int)op->term_slot.size();
+  int* d_tz = upload(ctx, kWsSmallArrays + 12, op->term_slot);
+  double* d_w = upload(ctx, kWsSmallArrays + 13, op->term_weight);
+  const bool add_poly = include_poly && (residual || op->hybrid);
+  action_accumulate_kernel<<<grid_for((int64_t)n * k), 256, 0, ctx->stream>>>(
+      R, k, (int64_t)blk, X, k, n, k, nt, d_tz, d_w, add_poly ? 1 : 0, op->constant, op->hybrid, op->d1, op->d2, BX,
+      B2X, out, ldo);
+  ctx->launches++;
+  if (terms) {
+    // the same products the accumulation adds, one n x k block per owned term (ascending shift
+    // index), then c X and d1 BX + d2 B^2 X: an ordered sum of these reproduces `out` bit for bit
+    const size_t nk = (size_t)n * k;
+    for (int t = 0; t < nt; ++t) {
+      const int slot = op->term_slot[t];
+      const double* src = slot >= 0 ? R + (size_t)slot * blk : X;
+      copy2d_kernel<<<dim3(grid_for((int64_t)nk), 1), 256, 0, ctx->stream>>>(n, k, op->term_weight[t], src, k, 0,
+                                                                             terms + t * nk, k, 0);
+      ctx->launches++;
+    }
+    if (add_poly) {
+      copy2d_kernel<<<dim3(grid_for((int64_t)nk), 1), 256, 0, ctx->stream>>>(n, k, op->constant, X, k, 0,
+                                                                             terms + nt * nk, k, 0);
+      ctx->launches++;
+      if (op->hybrid) {
+        lincomb2_kernel<<<grid_for((int64_t)nk), 256, 0, ctx->stream>>>(n, k, op->d1, BX, op->d2, B2X, k,
+                                                                        terms + (nt + 1) * nk, k);
+        ctx->launches++;
+      }
+    }
+  }
+  return cuda_fail(cudaGetLastError());
+}
+
+void action_op_destroy(pf_action_op* op) {
+  if (!op) return;
+  if (op->ctx) cudaStreamSynchronize(op->ctx->stream);
+  cudaFree(op->B);
+  cudaFree(op->M);
+  cudaFree(op->inv);
+  cudaFree(op->perm);
+  cudaFree(op->d_shifts);
+  cudaFree(op->d_ones);
+  delete op;
 }
 
 }  // namespace host

@@ -1,0 +1,206 @@
+"""Multi-GPU partition of the hot path: one process per GPU, torch.distributed
+(NCCL over NVLink on GPUs, gloo in the CPU tests) for the plumbing.
+
+* Single-matrix configs (cfg3 exp+phi1, cfg4 action): the s independent resolvents are the units.
+  Term t (every nonzero shift; plus the zero shift in plain form) belongs to rank t mod G -- the
+  B200 analogue of the reference's one-thread-per-shift parallel_for_index (worker_pool.hpp:16-44).
+  There is exactly one exchange per evaluation (cfg3) or per substep (cfg4):
+    fast           each rank sums its own weighted terms; NCCL reduce / all-reduce (sum) -- the
+                   addition order depends on G, like any NCCL sum;
+    deterministic  each rank ships its weighted terms; every term is then added in ascending shift
+                   index (pf_ordered_sum), which reproduces the single-GPU result bit for bit -- the
+                   reference's "bit-identical for any worker count" contract (dense.hpp:64-68).
+  The polynomial / constant part is added once, and the doubling recurrence runs on the root after
+  the reduce ("NCCL-reduce the weighted results over NVLink before squaring").
+* Batched configs (cfg2, cfg5): independent matrices, sharded by batch with no data-path collective
+  (bench.py runs one batch per rank: weak scaling).
+
+The partition logic is backend-agnostic: `CudaBackend` drives the C ABI on the local GPU,
+tests/test_parallel_cpu.py runs the same code with an oracle backend over gloo.
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence, Tuple
+
+import torch
+import torch.distributed as dist
+
+from .methods import (PLAIN, RESIDUAL, THETA_U53, FractionMethod, FunctionId, catalog, same_shift_method,
+                      to_double_nearest)
+
+
+def term_indices(method: FractionMethod, form: int) -> List[int]:
+    """Shift indices that produce a term (eval_dense: residual zero shifts fold into a_0)."""
+    return [i for i, c in enumerate(method.shifts) if c != 0 or form == PLAIN]
+
+
+def owned_terms(method: FractionMethod, form: int, rank: int, world: int) -> List[int]:
+    return [i for p, i in enumerate(term_indices(method, form)) if p % world == rank]
+
+
+class CudaBackend:
+    """The C-ABI operations the partition needs, on the local GPU. `j` is the device int32 tensor of
+    squaring counts: every evaluation is of r(2^-j A)."""
+
+    def __init__(self):
+        from . import api
+
+        self.api = api
+
+    def squarings(self, A, theta):
+        return self.api.squarings(A, theta)
+
+    def eval(self, A, j, shifts, weights, constants, form, poly=None) -> List[torch.Tensor]:
+        return self.api.eval_dense_raw(A, list(shifts), weights, list(constants), form, poly, squarings=j)
+
+    def ordered_sum(self, terms: Sequence[torch.Tensor]) -> torch.Tensor:
+        return self.api.ordered_sum(list(terms))
+
+    def phi1_doubling(self, E, Phi, j):
+        return self.api.phi1_doubling(E, Phi, j)
+
+
+def _gather_terms(local_idx: List[int], local_terms: torch.Tensor, group, world) -> Tuple[List[int], List[torch.Tensor]]:
+    """all_gather of variable-count term stacks (padded to the largest count with index -1);
+    returns every rank's terms sorted by shift index."""
+    dev = local_terms.device
+    cnt = torch.tensor([len(local_idx)], dtype=torch.int64, device=dev)
+    cnts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(cnts, cnt, group=group)
+    mx = max(int(c.item()) for c in cnts)
+    shape = tuple(local_terms.shape[1:])
+    pad_t = torch.zeros((mx,) + shape, dtype=local_terms.dtype, device=dev)
+    if local_idx:
+        pad_t[: len(local_idx)] = local_terms
+    pad_i = torch.full((mx,), -1, dtype=torch.int64, device=dev)
+    if local_idx:
+        pad_i[: len(local_idx)] = torch.tensor(local_idx, dtype=torch.int64, device=dev)
+    all_t = [torch.empty_like(pad_t) for _ in range(world)]
+    all_i = [torch.empty_like(pad_i) for _ in range(world)]
+    dist.all_gather(all_t, pad_t, group=group)
+    dist.all_gather(all_i, pad_i, group=group)
+    pairs = []
+    for ti, tt in zip(all_i, all_t):
+        for q in range(mx):
+            k = int(ti[q].item())
+            if k >= 0:
+                pairs.append((k, tt[q]))
+    pairs.sort(key=lambda p: p[0])
+    return [p[0] for p in pairs], [p[1] for p in pairs]
+
+
+def _constants(sets, form):
+    return [to_double_nearest(s.constant_term()) if form == RESIDUAL
+            else (to_double_nearest(s.poly[0]) if len(s.poly) == 3 else 0.0) for s in sets]
+
+
+def _poly(sets):
+    if not any(len(s.poly) == 3 for s in sets):
+        return None
+    return [[to_double_nearest(d) for d in s.poly] if len(s.poly) == 3 else [0.0, 0.0, 0.0] for s in sets]
+
+
+def eval_sets_sharded(A: torch.Tensor, j, method: FractionMethod, extra_sets: Sequence[FractionMethod] = (),
+                      form: int = RESIDUAL, deterministic: bool = True, group=None, backend=None,
+                      root: int = 0) -> Optional[List[torch.Tensor]]:
+    """r_s(2^-j A) for the method's weight set and every extra set on the same shifts, the terms
+    partitioned over the ranks of `group`. Returns the list of results on `root`, None elsewhere."""
+    backend = backend or CudaBackend()
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    sets = [method] + list(extra_sets)
+    mine = owned_terms(method, form, rank, world)
+    sh = method.shift_doubles()
+    constants = _constants(sets, form)
+    poly = _poly(sets)
+    has_poly_part = form == RESIDUAL or poly is not None
+    if deterministic:
+        # each owned term on its own (a one-term method with constant 0 returns exactly w X, or
+        # w I for a plain-form zero shift), every term to every rank, then the ascending-shift sum
+        local = [[] for _ in sets]
+        for i in mine:
+            res = backend.eval(A, j, [sh[i]], [[s.weight_doubles()[i]] for s in sets], [0.0] * len(sets),
+                               form if sh[i] != 0 else PLAIN)
+            for s_i in range(len(sets)):
+                local[s_i].append(res[s_i])
+        results = []
+        for s_i in range(len(sets)):
+            lt = torch.stack(local[s_i]) if local[s_i] else torch.zeros((0,) + tuple(A.shape), dtype=A.dtype,
+                                                                         device=A.device)
+            if world > 1:
+                idx, terms = _gather_terms(mine, lt, group, world)
+            else:
+                idx, terms = mine, list(lt)
+            if rank != root:
+                continue
+            if has_poly_part:
+                terms = list(terms) + backend.eval(A, j, [], [[] for _ in range(1)], [constants[s_i]], form,
+                                                   [poly[s_i]] if poly else None)
+            results.append(backend.ordered_sum(terms) if len(terms) > 1 else terms[0].clone())
+        return results if rank == root else None
+    # fast: local partial sums (the root also adds the constant / poly part) + reduce
+    cst = constants if rank == root else [0.0] * len(sets)
+    pl = poly if rank == root else None
+    if mine or rank == root:
+        parts = backend.eval(A, j, [sh[i] for i in mine], [[s.weight_doubles()[i] for i in mine] for s in sets],
+                             cst, form, pl)
+    else:
+        parts = [torch.zeros_like(A) for _ in sets]
+    out = []
+    for p in parts:
+        if world > 1:
+            dist.reduce(p, dst=root, op=dist.ReduceOp.SUM, group=group)
+        out.append(p)
+    return out if rank == root else None
+
+
+def expm_phi1_sharded(A: torch.Tensor, method="R8", deterministic: bool = True, group=None, root: int = 0,
+                      backend=None):
+    """cfg3: exp(A) and phi1(A) with the shifts split across the ranks, one reduce before the
+    doubling recurrence (which runs on the root). Returns (E, Phi) on the root, None elsewhere."""
+    backend = backend or CudaBackend()
+    m = catalog(method) if isinstance(method, str) else method
+    phi = same_shift_method(m, FunctionId.phi(1))
+    theta = min(THETA_U53[m.name], THETA_U53.get(m.name + "_phi1set", THETA_U53[m.name]))
+    j = backend.squarings(A, theta)
+    res = eval_sets_sharded(A, j, m, [phi], RESIDUAL, deterministic, group, backend, root)
+    if res is None:
+        return None
+    E, Phi = res
+    backend.phi1_doubling(E, Phi, j)
+    return E, Phi
+
+
+def action_sharded(A: torch.Tensor, V: torch.Tensor, method="R8", substeps: int = 1, form: int = RESIDUAL,
+                   deterministic: bool = True, group=None, operator_factory=None, ordered_sum=None):
+    """cfg4: exp(A) V by N substeps; every rank factors its shifts once (ActionOperator) and each
+    substep ends with one all-reduce (fast) or all-gather + ordered sum (deterministic) of n x k."""
+    if operator_factory is None:
+        from . import api
+
+        operator_factory = api.ActionOperator
+        ordered_sum = api.ordered_sum
+    m = catalog(method) if isinstance(method, str) else method
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    mine = owned_terms(m, form, rank, world)
+    op = operator_factory(A, m, substeps, form, owned=mine)
+    X = V.reshape(V.shape[0], -1).contiguous()
+    for _ in range(substeps):
+        if deterministic:
+            _, terms = op.apply(X, include_poly=True, with_terms=True)
+            nloc = op.terms
+            local = terms[:nloc]
+            if world > 1:
+                _, gathered = _gather_terms(mine, local, group, world)
+            else:
+                gathered = list(local)
+            ts = list(gathered) + [terms[nloc + q] for q in range(op.poly_terms)]
+            X = ordered_sum(ts) if len(ts) > 1 else ts[0].clone()
+        else:
+            part = op.apply(X, include_poly=(rank == 0))
+            if world > 1:
+                dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)
+            X = part
+    op.close()
+    return X.reshape(V.shape)

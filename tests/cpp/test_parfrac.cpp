@@ -234,7 +234,7 @@ void test_expm_and_friends() {
   std::vector<double> v(64 * 2);
   NormalSampler ns(11);
   for (auto& x : v) x = ns.next();
-  std::vector<double> av = substep_action(catalog("R8"), a, v, 2);
+  std::vector<double> av = substep_action(catalog("R8"), a, v, 2, 0, {.form = EvalForm::Residual});
   // column 0 of exp(A) V against e8 V
   double err = 0, nrm = 0;
   for (int i = 0; i < 64; ++i) {

@@ -1,0 +1,93 @@
+"""Multi-GPU building blocks on one B200. The rank partition is emulated sequentially in one process
+(no concurrently waiting kernels): the deterministic mode's ordered reduction of every rank's terms
+must equal the single-GPU evaluation bit for bit, for the small (n <= 128) and large engines."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev(pf):
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need CUDA")
+    from paper_2210_03714_b200 import api
+
+    return api
+
+
+def _a(n, seed, norm):
+    from paper_2210_03714_b200 import workloads as W
+
+    return torch.from_numpy(W.scaled_to_one_norm(W.randn_matrix(n, seed), norm)).cuda()
+
+
+@pytest.mark.parametrize("n", [100, 200])
+@pytest.mark.parametrize("world", [2, 3])
+def test_emulated_shift_partition_is_bit_identical(dev, n, world):
+    from paper_2210_03714_b200 import methods as M, parallel as P
+
+    m = M.catalog("R8")
+    phi = M.same_shift_method(m, M.FunctionId.phi(1))
+    A = _a(n, 9, 6.0)
+    be = P.CudaBackend()
+    j = be.squarings(A, M.THETA_U53["R8_phi1set"])
+    # single GPU, all shifts in one call
+    full = dev.eval_dense_raw(A, m.shift_doubles(), [m.weight_doubles(), phi.weight_doubles()],
+                              [1.0, 1.0], M.RESIDUAL, squarings=j)
+    # every rank's terms, gathered and summed in ascending shift order
+    terms = {}
+    for r in range(world):
+        for i in P.owned_terms(m, M.RESIDUAL, r, world):
+            res = be.eval(A, j, [m.shift_doubles()[i]], [[m.weight_doubles()[i]], [phi.weight_doubles()[i]]],
+                          [0.0, 0.0], M.RESIDUAL)
+            terms[i] = res
+    for s in range(2):
+        ts = [terms[i][s] for i in sorted(terms)]
+        ts += be.eval(A, j, [], [[]], [1.0], M.RESIDUAL)
+        got = be.ordered_sum(ts)
+        assert torch.equal(got, full[s])
+
+
+def test_sharded_world1_matches_expm_phi1(dev):
+    from paper_2210_03714_b200 import parallel as P
+
+    A = _a(96, 4, 5.0)
+    E, Phi = P.expm_phi1_sharded(A, "R8", deterministic=True)
+    E2, Phi2 = dev.expm_phi1(A, "R8")
+    assert torch.equal(E, E2) and torch.equal(Phi, Phi2)
+    Ef, Phif = P.expm_phi1_sharded(A, "R8", deterministic=False)
+    assert float((Ef - E2).abs().max()) <= 1e-13 * float(E2.abs().max())
+
+
+@pytest.mark.parametrize("n", [96, 200])
+def test_action_operator_and_partition(dev, n):
+    from paper_2210_03714_b200 import methods as M, parallel as P, workloads as W
+
+    a = W.randn_matrix(n, 40) / np.sqrt(n) - 2.0 * np.eye(n)
+    a *= 1.5 / W.one_norm(a)
+    A = torch.from_numpy(a).cuda()
+    V = torch.from_numpy(W.randn(41, n * 4).reshape(n, 4)).cuda()
+    nsub = 5
+    ref = dev.action(A, V, "R8", substeps=nsub)
+    # one operator owning everything == pf_action_block
+    X = P.action_sharded(A, V, "R8", nsub, M.RESIDUAL, deterministic=True)
+    assert torch.equal(X, ref)
+    # emulated 2-rank deterministic substeps
+    m = M.catalog("R8")
+    ops = [dev.ActionOperator(A, m, nsub, M.RESIDUAL, owned=P.owned_terms(m, M.RESIDUAL, r, 2)) for r in range(2)]
+    X = V.clone()
+    for _ in range(nsub):
+        parts = []
+        poly = None
+        for r, op in enumerate(ops):
+            _, terms = op.apply(X, include_poly=True, with_terms=True)
+            for q, i in enumerate(P.owned_terms(m, M.RESIDUAL, r, 2)):
+                parts.append((i, terms[q]))
+            poly = [terms[op.terms + q] for q in range(op.poly_terms)]
+        parts.sort(key=lambda p: p[0])
+        X = dev.ordered_sum([p[1] for p in parts] + poly)
+    assert torch.equal(X, ref)
+    for op in ops:
+        op.close()

@@ -1,0 +1,213 @@
+"""The multi-GPU partition logic (paper_2210_03714_b200/parallel.py) on CPU: world_size 2 over gloo,
+with an oracle backend standing in for the device. Deterministic mode must reproduce the
+single-process evaluation bit for bit (the reference's bit-identical-across-workers contract,
+dense.hpp:64-68); fast mode agrees to rounding."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2210_03714_b200 import methods as M
+from paper_2210_03714_b200 import parallel as P
+
+
+class OracleBackend:
+    def __init__(self):
+        from oracle import oracle as O
+
+        self.O = O
+
+    def squarings(self, A, theta):
+        return torch.tensor([self.O.squarings(self.O.one_norm(A.numpy()), theta)], dtype=torch.int32)
+
+    def eval(self, A, j, shifts, weights, constants, form, poly=None):
+        B = np.ldexp(A.numpy(), -int(j[0]))
+        om = self.O.OMethod(shifts, weights if shifts else [[] for _ in constants], poly, constants, form)
+        if not shifts:
+            om = self.O.OMethod([], [[]] * len(constants), poly, constants, form)
+        out = self.O.eval_dense(om, B)
+        out = out if out.ndim == 3 else out[None]
+        return [torch.from_numpy(np.ascontiguousarray(o)) for o in out]
+
+    def ordered_sum(self, terms):
+        acc = terms[0].clone()
+        for t in terms[1:]:
+            acc = acc + t
+        return acc
+
+    def phi1_doubling(self, E, Phi, j):
+        return E, Phi
+
+
+class OracleActionOperator:
+    """Restates the oracle's block action per owned shift (oracle/pf_oracle.c pfo_action)."""
+
+    def __init__(self, A, m, substeps, form, owned):
+        from oracle import oracle as O
+
+        self.O = O
+        self.m = m
+        self.form = form
+        a = A.numpy()
+        self.B = a * (1.0 / substeps)
+        n = a.shape[0]
+        self.own = [i for i in owned]
+        self.facs = {}
+        for i in self.own:
+            c = m.shift_doubles()[i]
+            if c != 0.0:
+                mm = self.B * (-c)
+                mm[np.arange(n), np.arange(n)] += 1.0
+                self.facs[i] = O.lu(mm)
+        self.terms = len(self.own)
+        hybrid = len(m.poly) == 3
+        self.poly_terms = (1 if (form == M.RESIDUAL or hybrid) else 0) + (1 if hybrid else 0)
+
+    def apply(self, X, include_poly=True, with_terms=False):
+        O, m = self.O, self.m
+        x = X.numpy()
+        hybrid = len(m.poly) == 3
+        bv = O.mul_rect(self.B, x) if (self.form == M.RESIDUAL or hybrid) else None
+        ts = []
+        for i in self.own:
+            c, w = m.shift_doubles()[i], m.weight_doubles()[i]
+            if self.form == M.PLAIN:
+                xi = x.copy() if c == 0.0 else O.lu_solve_matrix(*self.facs[i], x)
+            else:
+                xi = O.lu_solve_matrix(*self.facs[i], c * bv)
+            ts.append(xi * w)
+        if include_poly and (self.form == M.RESIDUAL or hybrid):
+            cst = M.to_double_nearest(m.constant_term()) if self.form == M.RESIDUAL else M.to_double_nearest(m.poly[0])
+            ts.append(cst * x)
+            if hybrid:
+                d1, d2 = M.to_double_nearest(m.poly[1]), M.to_double_nearest(m.poly[2])
+                b2v = O.mul_rect(self.B, bv)
+                ts.append(d1 * bv + d2 * b2v)
+        terms = torch.from_numpy(np.stack(ts)) if ts else torch.zeros((0,) + x.shape)
+        out = terms[0].clone()
+        for t in terms[1:]:
+            out = out + t
+        return (out, terms) if with_terms else out
+
+    def close(self):
+        pass
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q, case):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2210_03714_b200 import workloads as W
+
+        if case.startswith("eval"):
+            det = case.endswith("det")
+            m = M.catalog("R8")
+            phi = M.same_shift_method(m, M.FunctionId.phi(1))
+            A = torch.from_numpy(W.scaled_to_one_norm(W.randn_matrix(24, 3), 3.0))
+            be = OracleBackend()
+            j = be.squarings(A, M.THETA_U53["R8_phi1set"])
+            res = P.eval_sets_sharded(A, j, m, [phi], M.RESIDUAL, det, None, be)
+            if rank == 0:
+                q.put([r.numpy() for r in res])
+        else:
+            det = case.endswith("det")
+            name = "R10" if "hybrid" in case else "R8"
+            form = M.PLAIN if "plain" in case else M.RESIDUAL
+            a = W.randn_matrix(30, 40) / np.sqrt(30) - 2.0 * np.eye(30)
+            a *= 1.5 / W.one_norm(a)
+            V = torch.from_numpy(W.randn(41, 30 * 3).reshape(30, 3))
+            out = P.action_sharded(torch.from_numpy(a), V, name, 4, form, det, None, OracleActionOperator,
+                                   OracleBackend().ordered_sum)
+            if rank == 0:
+                q.put([out.numpy()])
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(case, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, case)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    return res
+
+
+def test_term_partition():
+    m = M.catalog("R8")
+    assert P.term_indices(m, M.RESIDUAL) == list(range(1, 9))
+    assert P.term_indices(m, M.PLAIN) == list(range(9))
+    parts = [P.owned_terms(m, M.RESIDUAL, r, 3) for r in range(3)]
+    assert sorted(sum(parts, [])) == list(range(1, 9))
+    assert parts[0] == [1, 4, 7]
+
+
+def test_sharded_eval_deterministic_is_bit_identical():
+    from oracle import oracle as O
+    from paper_2210_03714_b200 import workloads as W
+
+    e2 = _run("eval_det", 2)
+    m = M.catalog("R8")
+    phi = M.same_shift_method(m, M.FunctionId.phi(1))
+    a = W.scaled_to_one_norm(W.randn_matrix(24, 3), 3.0)
+    j = O.squarings(O.one_norm(a), M.THETA_U53["R8_phi1set"])
+    ref = O.eval_dense(O.OMethod.from_method(m, M.RESIDUAL, [phi]), np.ldexp(a, -j))
+    assert np.array_equal(e2[0], ref[0]) and np.array_equal(e2[1], ref[1])
+
+
+def test_sharded_eval_fast_agrees():
+    from oracle import oracle as O
+    from paper_2210_03714_b200 import workloads as W
+
+    e2 = _run("eval_fast", 2)
+    m = M.catalog("R8")
+    phi = M.same_shift_method(m, M.FunctionId.phi(1))
+    a = W.scaled_to_one_norm(W.randn_matrix(24, 3), 3.0)
+    j = O.squarings(O.one_norm(a), M.THETA_U53["R8_phi1set"])
+    ref = O.eval_dense(O.OMethod.from_method(m, M.RESIDUAL, [phi]), np.ldexp(a, -j))
+    assert O.rel_diff_1norm(e2[0], ref[0]) <= 1e-13 and O.rel_diff_1norm(e2[1], ref[1]) <= 1e-13
+
+
+@pytest.mark.parametrize("case", ["action_det", "action_plain_det", "action_hybrid_det"])
+def test_sharded_action_deterministic_is_bit_identical(case):
+    from oracle import oracle as O
+    from paper_2210_03714_b200 import workloads as W
+
+    out = _run(case, 2)[0]
+    name = "R10" if "hybrid" in case else "R8"
+    form = M.PLAIN if "plain" in case else M.RESIDUAL
+    a = W.randn_matrix(30, 40) / np.sqrt(30) - 2.0 * np.eye(30)
+    a *= 1.5 / W.one_norm(a)
+    v = W.randn(41, 30 * 3).reshape(30, 3)
+    ref = O.action(a, v, O.OMethod.from_method(M.catalog(name), form), 4)
+    assert np.array_equal(out, ref)
+
+
+def test_sharded_action_fast_agrees():
+    from oracle import oracle as O
+    from paper_2210_03714_b200 import workloads as W
+
+    out = _run("action_fast", 2)[0]
+    a = W.randn_matrix(30, 40) / np.sqrt(30) - 2.0 * np.eye(30)
+    a *= 1.5 / W.one_norm(a)
+    v = W.randn(41, 30 * 3).reshape(30, 3)
+    ref = O.action(a, v, O.OMethod.from_method(M.catalog("R8"), M.RESIDUAL), 4)
+    assert O.rel_diff_1norm(out, ref) <= 1e-13
