@@ -21,10 +21,12 @@
  *   factor-once substepping (assemble_action / ActionOperator / substep_action,
  *   action.cpp:224-339).
  *
- * Parity pinning: the reference cannot be compiled here (no gmpxx, no vendor/), so this
- * restatement is pinned by the reference's own known-answer tests and properties
- * (tests/test_oracle.py: test_dense.cpp:34-156, test_action.cpp:124-188) and by an
- * mpmath high-precision expm referee; golden fixtures in tests/golden/ freeze its output.
+ * Parity pinning: PARITY UNPINNED against reference outputs. The reference cannot be compiled
+ * here (gmpxx.h / libgmpxx and vendor/ are absent) and ships no golden output matrices, so this
+ * restatement is pinned instead by the reference's own known-answer tests and properties
+ * (tests/test_oracle.py: test_dense.cpp:34-156, test_action.cpp:124-188, the published
+ * SplitMix64 sequence) and by independent referees (scipy expm, eigh); golden fixtures in
+ * tests/golden/ freeze its output so drift is caught.
  */
 #ifndef PF_ORACLE_H
 #define PF_ORACLE_H
