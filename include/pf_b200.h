@@ -109,6 +109,11 @@ int pf_context_destroy(pf_context* ctx);
 int pf_context_set_stream(pf_context* ctx, void* stream);
 /* Number of kernels this context launched so far (bench evidence). */
 int64_t pf_context_launch_count(pf_context* ctx);
+/* Pipelined use (several PF_FLAG_ASYNC calls in flight): sticky != 0 resets the device error flag
+ * once and keeps it across launches; pf_context_pending_error synchronises the context's stream and
+ * returns 1 if any launch since the reset failed (re-run synchronously to get the pf_status). */
+int pf_context_set_sticky_status(pf_context* ctx, int sticky);
+int pf_context_pending_error(pf_context* ctx);
 /* Diagnostics: when non-NULL, the fused small-n kernel adds per-phase SM cycles (thread 0 of each
  * CTA, clock64) into dev_counters[0..9]: norm, shift-matrix load, LU, diagonal inverses, RHS load,
  * solve+accumulate, E formation, squaring, output. NULL disables (the default). */

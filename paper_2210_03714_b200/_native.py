@@ -46,6 +46,8 @@ SIGNATURES = [
     ("pf_context_set_stream", C.c_int, [_VP, _VP]),
     ("pf_context_launch_count", C.c_int64, [_VP]),
     ("pf_context_set_profile", C.c_int, [_VP, _VP]),
+    ("pf_context_set_sticky_status", C.c_int, [_VP, C.c_int]),
+    ("pf_context_pending_error", C.c_int, [_VP]),
     ("pf_one_norm_batched", C.c_int, [_VP, C.c_int, C.c_int, _VP, _I64, _I64, _VP]),
     ("pf_eval_dense_batched", C.c_int, [_VP, C.POINTER(PfMethod), C.c_int, C.c_int, _VP, _I64, _I64,
                                         C.POINTER(_VP), _I64, _I64, C.c_int, C.POINTER(PfStatus)]),

@@ -403,6 +403,60 @@ def expm(A: ArrayLike, method="R4", theta: Optional[float] = None, squarings: Op
     return res
 
 
+class HostPipeline:
+    """Batched expm of HOST matrices with the host->device copy, the evaluation and the
+    device->host copy overlapped across chunks: `streams` CUDA streams, one pf_context each (so
+    every stream has its own status buffers), chunk c on stream c mod streams. Inputs/outputs
+    should be pinned for the copies to be asynchronous."""
+
+    def __init__(self, n: int, batch: int, chunk: int = 512, streams: int = 3, device: Optional[int] = None):
+        if not torch.cuda.is_available():
+            raise PfError(Errc.CudaError, "paper_2210_03714_b200 needs a CUDA device (there is no CPU path)")
+        self.device = torch.cuda.current_device() if device is None else device
+        self.n, self.batch, self.chunk = n, batch, min(chunk, batch)
+        self.streams = [torch.cuda.Stream(self.device) for _ in range(streams)]
+        self.engines = [Engine(self.device) for _ in range(streams)]
+        for e, s in zip(self.engines, self.streams):
+            N.lib.pf_context_set_stream(e.h, C.c_void_p(s.cuda_stream))
+        shape = (self.chunk, n, n)
+        self.dA = [torch.empty(shape, dtype=torch.float64, device=self.device) for _ in range(streams)]
+        self.dO = [torch.empty(shape, dtype=torch.float64, device=self.device) for _ in range(streams)]
+
+    def launch_count(self) -> int:
+        return sum(e.launch_count() for e in self.engines)
+
+    def expm(self, host_in: torch.Tensor, host_out: torch.Tensor, method="R4", theta: Optional[float] = None,
+             form: int = RESIDUAL):
+        m = _resolve_method(method)
+        th = _theta_for(m, theta)
+        pk = PackedMethod(m, form)
+        n, S = self.n, len(self.streams)
+        cur = torch.cuda.current_stream(self.device)
+        for e in self.engines:
+            N.lib.pf_context_set_sticky_status(e.h, 1)
+        for s in self.streams:
+            s.wait_stream(cur)
+        st = N.PfStatus()
+        for c, start in enumerate(range(0, self.batch, self.chunk)):
+            k = c % S
+            mb = min(self.chunk, self.batch - start)
+            with torch.cuda.stream(self.streams[k]):
+                self.dA[k][:mb].copy_(host_in[start:start + mb], non_blocking=True)
+                rc = N.lib.pf_expm_batched(self.engines[k].h, pk.ptr(), th, n, mb, self.dA[k].data_ptr(), n, n * n,
+                                           None, None, self.dO[k].data_ptr(), n, n * n, N.PF_FLAG_ASYNC, C.byref(st))
+                if rc:
+                    _raise(rc, st, True)
+                host_out[start:start + mb].copy_(self.dO[k][:mb], non_blocking=True)
+        for s in self.streams:
+            cur.wait_stream(s)
+        failed = [N.lib.pf_context_pending_error(e.h) for e in self.engines]
+        for e in self.engines:
+            N.lib.pf_context_set_sticky_status(e.h, 0)
+        if any(failed):  # locate and raise the precise error synchronously
+            expm(host_in.cuda(), m, th, form=form)
+        return host_out
+
+
 def expm_phi1(A: ArrayLike, method="R8", theta: Optional[float] = None, form: int = RESIDUAL, flags: int = 0,
               return_squarings: bool = False):
     """(exp(A), phi1(A)) from one solve per shift (weight sets exp and phi1 on the method's

@@ -44,6 +44,7 @@ int ensure_status(pf_context* ctx, int batch) {
     if (cudaMalloc(&ctx->status, sizeof(pf::DevStatus) * cap) != cudaSuccess) return PF_ERR_CUDA;
     ctx->status_cap = cap;
   }
+  if (ctx->sticky) return PF_OK;  // PF_FLAG_STICKY_STATUS callers reset once per pipeline
   return cuda_fail(cudaMemsetAsync(ctx->first_error, 0x7f, sizeof(int), ctx->stream));
 }
 
@@ -218,6 +219,21 @@ int pf_context_set_stream(pf_context* ctx, void* stream) {
 }
 
 int64_t pf_context_launch_count(pf_context* ctx) { return ctx ? ctx->launches : 0; }
+
+int pf_context_set_sticky_status(pf_context* ctx, int sticky) {
+  if (!ctx) return PF_ERR_BAD_ARGUMENT;
+  ctx->sticky = sticky != 0;
+  return cuda_fail(cudaMemsetAsync(ctx->first_error, 0x7f, sizeof(int), ctx->stream));
+}
+
+int pf_context_pending_error(pf_context* ctx) {
+  if (!ctx) return PF_ERR_BAD_ARGUMENT;
+  if (cudaMemcpyAsync(ctx->h_first_error, ctx->first_error, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+    return PF_ERR_CUDA;
+  return *ctx->h_first_error != 0x7f7f7f7f ? 1 : 0;
+}
 
 int pf_context_set_profile(pf_context* ctx, unsigned long long* dev_counters) {
   if (!ctx) return PF_ERR_BAD_ARGUMENT;

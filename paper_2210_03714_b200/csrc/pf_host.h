@@ -17,6 +17,7 @@ struct pf_context {
   std::vector<void*> ws;
   std::vector<size_t> ws_bytes;
   unsigned long long* prof = nullptr;
+  bool sticky = false;  // keep first_error across launches (pipelined async use)
 };
 
 // Dense ActionOperator (action.hpp:68-82): B = A * (1/N) and the LU factors of the owned shifts,
