@@ -115,6 +115,14 @@ int launch_small(pf_context* ctx, pf::SmallParams& p) {
   p.status = ctx->status;
   p.first_error = ctx->first_error;
   p.prof = ctx->prof;
+  // per-SM accumulator slots: one CTA per SM (smem-bound), so %smid indexes a private slot that
+  // stays in L2 across the shifts; slots beyond the guard fall back to the output buffer
+  static int sms = 0;
+  if (sms == 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  p.scratch_slots = 2 * sms;
+  p.scratch = static_cast<double*>(
+      workspace(ctx, kWsScratch, sizeof(double) * 2 * PF_SMALL_N * PF_SMALL_N * (size_t)p.scratch_slots));
+  if (!p.scratch) p.scratch_slots = 0;
   if (p.batch == 0) return PF_OK;
   pf::small_eval_kernel<<<p.batch, pf::small_eval_threads(), pf::small_eval_smem_bytes(), ctx->stream>>>(p);
   ctx->launches++;

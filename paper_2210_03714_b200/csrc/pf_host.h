@@ -76,6 +76,7 @@ enum Slot {
   kWsLargePiv = 14,
   kWsLargeB = 15,
   kWsLargeX2 = 16,
+  kWsScratch = 20,      // per-SM accumulator slots of the small kernel
   kWsSmallArrays = 64,  // small uploaded tables: kWsSmallArrays + i, i < 32
 };
 

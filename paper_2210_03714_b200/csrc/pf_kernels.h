@@ -34,6 +34,8 @@ struct SmallParams {
   DevStatus* status;
   int* first_error;
   unsigned long long* prof;  // optional phase profile (diagnostics), nullptr normally
+  double* scratch;           // per-SM accumulator slots (2 x 128 x 128 doubles each), or nullptr
+  int scratch_slots;
 };
 
 __global__ void small_eval_kernel(SmallParams p);
