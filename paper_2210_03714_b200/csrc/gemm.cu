@@ -1,20 +1,22 @@
 // K5: batched FP64 GEMM on DMMA.8x8x4, C = alpha * A B + beta * C + gamma * I (row-major).
 //
 // Replaces DenseMatrix::mul (proj/core/src/dense.cpp:17-29) for the squaring chain, B^2, the
-// phi1 / cos-sin recurrences and B V. CTA tile 128 x 128 x 16, 8 warps (4 x 2) of 32 x 64,
-// 3-stage cp.async pipeline; 8-byte async copies with zero fill make any shape / leading
-// dimension legal (FP64 rows are only 8-byte aligned in general).
+// phi1 / cos-sin recurrences, B V, and every off-diagonal update of the large-n LU / triangular
+// solves. CTA tile BM x BN x 16 with BN = 128 (8 warps of 32 x 64) or BN = 64 for thin right-hand
+// sides (8 warps of 32 x 32, two CTAs per SM); 3-stage cp.async pipeline, 16-byte copies when the
+// operands allow it (8-byte copies with zero fill otherwise: any shape / leading dimension is legal).
 #include "pf_common.cuh"
 #include "pf_kernels.h"
 
 namespace pf {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3, NT = 256;
-constexpr int LA = BK + 4;  // A tile row stride (doubles)
-constexpr int LB = BN + 4;  // B tile row stride
+constexpr int BM = 128, BK = 16, STAGES = 3, NT = 256;
+constexpr int LA = BK + 4;  // A tile row stride (doubles): 32-byte skew
 
+template <int BN>
 struct GemmSmem {
+  static constexpr int LB = BN + 4;
   double a[STAGES][BM * LA];
   double b[STAGES][BK * LB];
 };
@@ -24,38 +26,67 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool
   const int bytes = pred ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
 }
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, int bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-__device__ __forceinline__ void load_stage(GemmSmem& sm, int stage, const GemmParams& p, const double* A,
+template <int BN, bool V16>
+__device__ __forceinline__ void load_stage(GemmSmem<BN>& sm, int stage, const GemmParams& p, const double* A,
                                            const double* B, int m0, int n0, int k0) {
-  // A tile: BM x BK = 2048 doubles, 8 per thread
+  constexpr int LB = GemmSmem<BN>::LB;
+  if constexpr (V16) {
 #pragma unroll
-  for (int it = 0; it < (BM * BK) / NT; ++it) {
-    const int idx = threadIdx.x + it * NT;
-    const int r = idx / BK, c = idx % BK;
-    const int gr = m0 + r, gc = k0 + c;
-    const bool ok = gr < p.m && gc < p.k;
-    cp_async8(&sm.a[stage][r * LA + c], ok ? A + (int64_t)gr * p.lda + gc : A, ok);
-  }
+    for (int it = 0; it < (BM * BK / 2) / NT; ++it) {
+      const int idx = threadIdx.x + it * NT;
+      const int r = idx / (BK / 2), c = 2 * (idx % (BK / 2));
+      const int gr = m0 + r, gc = k0 + c;
+      const int bytes = gr < p.m ? (gc + 1 < p.k ? 16 : (gc < p.k ? 8 : 0)) : 0;
+      cp_async16(&sm.a[stage][r * LA + c], bytes ? A + (int64_t)gr * p.lda + gc : A, bytes);
+    }
 #pragma unroll
-  for (int it = 0; it < (BK * BN) / NT; ++it) {
-    const int idx = threadIdx.x + it * NT;
-    const int r = idx / BN, c = idx % BN;
-    const int gr = k0 + r, gc = n0 + c;
-    const bool ok = gr < p.k && gc < p.n;
-    cp_async8(&sm.b[stage][r * LB + c], ok ? B + (int64_t)gr * p.ldb + gc : B, ok);
+    for (int it = 0; it < (BK * BN / 2) / NT; ++it) {
+      const int idx = threadIdx.x + it * NT;
+      const int r = idx / (BN / 2), c = 2 * (idx % (BN / 2));
+      const int gr = k0 + r, gc = n0 + c;
+      const int bytes = gr < p.k ? (gc + 1 < p.n ? 16 : (gc < p.n ? 8 : 0)) : 0;
+      cp_async16(&sm.b[stage][r * LB + c], bytes ? B + (int64_t)gr * p.ldb + gc : B, bytes);
+    }
+  } else {
+#pragma unroll
+    for (int it = 0; it < (BM * BK) / NT; ++it) {
+      const int idx = threadIdx.x + it * NT;
+      const int r = idx / BK, c = idx % BK;
+      const int gr = m0 + r, gc = k0 + c;
+      const bool ok = gr < p.m && gc < p.k;
+      cp_async8(&sm.a[stage][r * LA + c], ok ? A + (int64_t)gr * p.lda + gc : A, ok);
+    }
+#pragma unroll
+    for (int it = 0; it < (BK * BN) / NT; ++it) {
+      const int idx = threadIdx.x + it * NT;
+      const int r = idx / BN, c = idx % BN;
+      const int gr = k0 + r, gc = n0 + c;
+      const bool ok = gr < p.k && gc < p.n;
+      cp_async8(&sm.b[stage][r * LB + c], ok ? B + (int64_t)gr * p.ldb + gc : B, ok);
+    }
   }
 }
 
 }  // namespace
 
-__global__ void __launch_bounds__(NT, 1) gemm_kernel(GemmParams p, int tiles_n) {
+// BN = 128: warps 4 (M) x 2 (N) of 32 x 64; BN = 64: warps 4 x 2 of 32 x 32.
+template <int BN, bool V16>
+__global__ void __launch_bounds__(NT, BN == 64 ? 2 : 1) gemm_kernel(GemmParams p, int tiles_n) {
+  constexpr int LB = GemmSmem<BN>::LB;
+  constexpr int WN = BN / 2;      // warp tile width
+  constexpr int NJ = WN / 8;      // DMMA tiles across
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  GemmSmem& sm = *reinterpret_cast<GemmSmem*>(smem_raw);
+  GemmSmem<BN>& sm = *reinterpret_cast<GemmSmem<BN>*>(smem_raw);
   const int bz = blockIdx.y;
   const int m0 = (blockIdx.x / tiles_n) * BM, n0 = (blockIdx.x % tiles_n) * BN;
   const double* A = p.A + (int64_t)bz * p.strideA;
@@ -73,39 +104,39 @@ __global__ void __launch_bounds__(NT, 1) gemm_kernel(GemmParams p, int tiles_n) 
   }
   const int lane = lane_id(), warp = warp_id();
   const int g = lane >> 2, t = lane & 3;
-  const int wm = 32 * (warp >> 1), wn = 64 * (warp & 1);
+  const int wm = 32 * (warp >> 1), wn = WN * (warp & 1);
 
-  double acc[4][8][2];
+  double acc[4][NJ][2];
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-    for (int nj = 0; nj < 8; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
+    for (int nj = 0; nj < NJ; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
 
   const int nk = (p.k + BK - 1) / BK;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) load_stage(sm, s, p, A, B, m0, n0, s * BK);
+    if (s < nk) load_stage<BN, V16>(sm, s, p, A, B, m0, n0, s * BK);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     const int nxt = kt + STAGES - 1;
-    if (nxt < nk) load_stage(sm, nxt % STAGES, p, A, B, m0, n0, nxt * BK);
+    if (nxt < nk) load_stage<BN, V16>(sm, nxt % STAGES, p, A, B, m0, n0, nxt * BK);
     cp_async_commit();
     const double* as = sm.a[kt % STAGES];
     const double* bs = sm.b[kt % STAGES];
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[4], bf[8];
+      double af[4], bf[NJ];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) af[mi] = as[(wm + 8 * mi + g) * LA + kk + t];
 #pragma unroll
-      for (int nj = 0; nj < 8; ++nj) bf[nj] = bs[(kk + t) * LB + wn + 8 * nj + g];
+      for (int nj = 0; nj < NJ; ++nj) bf[nj] = bs[(kk + t) * LB + wn + 8 * nj + g];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int nj = 0; nj < 8; ++nj) dmma(acc[mi][nj], af[mi], bf[nj]);
+        for (int nj = 0; nj < NJ; ++nj) dmma(acc[mi][nj], af[mi], bf[nj]);
     }
   }
   cp_async_wait<0>();
@@ -114,7 +145,7 @@ __global__ void __launch_bounds__(NT, 1) gemm_kernel(GemmParams p, int tiles_n) 
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-    for (int nj = 0; nj < 8; ++nj)
+    for (int nj = 0; nj < NJ; ++nj)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int r = m0 + wm + 8 * mi + g, c = n0 + wn + 8 * nj + 2 * t + e;
@@ -128,15 +159,36 @@ __global__ void __launch_bounds__(NT, 1) gemm_kernel(GemmParams p, int tiles_n) 
       }
 }
 
-void launch_gemm(const GemmParams& p, cudaStream_t stream) {
+namespace {
+template <int BN, bool V16>
+void launch_tile(const GemmParams& p, cudaStream_t stream) {
   static bool configured = false;
+  const int smem = (int)sizeof(GemmSmem<BN>);
   if (!configured) {
-    cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(GemmSmem));
+    cudaFuncSetAttribute(gemm_kernel<BN, V16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     configured = true;
   }
   const int tiles_m = (p.m + BM - 1) / BM, tiles_n = (p.n + BN - 1) / BN;
   dim3 grid(tiles_m * tiles_n, p.batch);
-  gemm_kernel<<<grid, NT, sizeof(GemmSmem), stream>>>(p, tiles_n);
+  gemm_kernel<BN, V16><<<grid, NT, smem, stream>>>(p, tiles_n);
+}
+}  // namespace
+
+void launch_gemm(const GemmParams& p, cudaStream_t stream) {
+  // 16-byte copies need even leading dimensions / batch strides and 16-byte aligned bases
+  const bool v16 = ((p.lda | p.ldb | p.strideA | p.strideB) & 1) == 0 &&
+                   ((reinterpret_cast<uintptr_t>(p.A) | reinterpret_cast<uintptr_t>(p.B)) & 15) == 0;
+  if (p.n <= 64) {
+    if (v16)
+      launch_tile<64, true>(p, stream);
+    else
+      launch_tile<64, false>(p, stream);
+  } else {
+    if (v16)
+      launch_tile<128, true>(p, stream);
+    else
+      launch_tile<128, false>(p, stream);
+  }
 }
 
 }  // namespace pf

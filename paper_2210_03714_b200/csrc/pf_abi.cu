@@ -2,6 +2,7 @@
 // compositions (scaling and squaring, phi1 doubling, cos/sin recurrence) over the kernels.
 // No exceptions cross this boundary; every error is a pf_err code + pf_status.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -99,6 +100,27 @@ bool fill_method(const pf_method* m, pf::SmallParams& p) {
     for (int k = 0; k < 3; ++k) p.poly[s][k] = (m->has_poly && s < m->n_sets) ? m->poly[3 * s + k] : 0.0;
     p.constant[s] = (m->constant && s < m->n_sets) ? m->constant[s] : 0.0;
   }
+  // (c, -c) shift pairs for the merged residual-form solve (small kernel; the kernel still checks
+  // both systems' certificates per matrix and falls back to the per-shift path)
+  static const bool no_pairs = std::getenv("PF_NO_PAIRS") != nullptr;
+  p.pair_mode = 0;
+  for (int i = 0; i < PF_MAX_TERMS; ++i) {
+    p.pair_of[i] = 0;
+    for (int s = 0; s < 2; ++s) p.pair_cm[s][i] = p.pair_cp[s][i] = 0.0;
+  }
+  if (m->form == PF_FORM_RESIDUAL && !no_pairs) {
+    for (int i = 0; i + 1 < m->n_terms; ++i) {
+      const double c = p.shifts[i];
+      if (c == 0.0 || p.shifts[i + 1] != -c) continue;
+      p.pair_of[i] = 1;
+      for (int s = 0; s < 2; ++s) {
+        p.pair_cm[s][i] = p.weights[s][i] - p.weights[s][i + 1];
+        p.pair_cp[s][i] = p.weights[s][i] + p.weights[s][i + 1];
+      }
+      p.pair_mode = 1;
+      ++i;
+    }
+  }
   return true;
 }
 
@@ -121,7 +143,7 @@ int launch_small(pf_context* ctx, pf::SmallParams& p) {
   if (sms == 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
   p.scratch_slots = 2 * sms;
   p.scratch = static_cast<double*>(
-      workspace(ctx, kWsScratch, sizeof(double) * 2 * PF_SMALL_N * PF_SMALL_N * (size_t)p.scratch_slots));
+      workspace(ctx, kWsScratch, sizeof(double) * 3 * PF_SMALL_N * PF_SMALL_N * (size_t)p.scratch_slots));
   if (!p.scratch) p.scratch_slots = 0;
   if (p.batch == 0) return PF_OK;
   pf::small_eval_kernel<<<p.batch, pf::small_eval_threads(), pf::small_eval_smem_bytes(), ctx->stream>>>(p);

@@ -34,8 +34,14 @@ struct SmallParams {
   DevStatus* status;
   int* first_error;
   unsigned long long* prof;  // optional phase profile (diagnostics), nullptr normally
-  double* scratch;           // per-SM accumulator slots (2 x 128 x 128 doubles each), or nullptr
+  double* scratch;           // per-SM slots of 3 x 128 x 128 doubles (acc set 0, acc set 1, B^2), or nullptr
   int scratch_slots;
+  // pair mode (residual form): shifts i, i+1 = (c, -c) merged into one solve of (I - c^2 B^2);
+  // pair_of[i] = 1 marks the first shift of a pair, cm = w_i - w_{i+1}, cp = w_i + w_{i+1}
+  int pair_mode;
+  int pair_of[PF_MAX_TERMS];
+  double pair_cm[2][PF_MAX_TERMS];
+  double pair_cp[2][PF_MAX_TERMS];
 };
 
 __global__ void small_eval_kernel(SmallParams p);
