@@ -2,21 +2,25 @@
 //
 // Replaces DenseMatrix::mul (proj/core/src/dense.cpp:17-29) for the squaring chain, B^2, the
 // phi1 / cos-sin recurrences, B V, and every off-diagonal update of the large-n LU / triangular
-// solves. CTA tile BM x BN x 16 with BN = 128 (8 warps of 32 x 64) or BN = 64 for thin right-hand
-// sides (8 warps of 32 x 32, two CTAs per SM); 3-stage cp.async pipeline, 16-byte copies when the
-// operands allow it (8-byte copies with zero fill otherwise: any shape / leading dimension is legal).
+// solves. CTA tile BM x BN x 16: 128 x 128 (8 warps of 32 x 64), 128 x 64 for thin right-hand sides
+// (8 warps of 32 x 32, two CTAs per SM), or 64 x 64 (4 warps of 32 x 32) when the larger tiles would
+// leave most of the 148 SMs idle (the small updates deep in the LU / TRSM recursion: one SM's DMMA
+// rate is 250 GFLOP/s, so a single 128^3 tile takes 17 us); 3-stage cp.async pipeline, 16-byte
+// copies when the operands allow it (8-byte copies with zero fill otherwise: any shape / leading
+// dimension is legal).
 #include "pf_common.cuh"
 #include "pf_kernels.h"
 
 namespace pf {
 namespace {
 
-constexpr int BM = 128, BK = 16, STAGES = 3, NT = 256;
+constexpr int BK = 16, STAGES = 3;
 constexpr int LA = BK + 4;  // A tile row stride (doubles): 32-byte skew
 
-template <int BN>
+template <int BM, int BN>
 struct GemmSmem {
   static constexpr int LB = BN + 4;
+  static constexpr int NT = BM * 2;  // (BM / 32) x 2 warps
   double a[STAGES][BM * LA];
   double b[STAGES][BK * LB];
 };
@@ -36,10 +40,11 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-template <int BN, bool V16>
-__device__ __forceinline__ void load_stage(GemmSmem<BN>& sm, int stage, const GemmParams& p, const double* A,
+template <int BM, int BN, bool V16>
+__device__ __forceinline__ void load_stage(GemmSmem<BM, BN>& sm, int stage, const GemmParams& p, const double* A,
                                            const double* B, int m0, int n0, int k0) {
-  constexpr int LB = GemmSmem<BN>::LB;
+  constexpr int LB = GemmSmem<BM, BN>::LB;
+  constexpr int NT = GemmSmem<BM, BN>::NT;
   if constexpr (V16) {
 #pragma unroll
     for (int it = 0; it < (BM * BK / 2) / NT; ++it) {
@@ -79,14 +84,15 @@ __device__ __forceinline__ void load_stage(GemmSmem<BN>& sm, int stage, const Ge
 
 }  // namespace
 
-// BN = 128: warps 4 (M) x 2 (N) of 32 x 64; BN = 64: warps 4 x 2 of 32 x 32.
-template <int BN, bool V16>
-__global__ void __launch_bounds__(NT, BN == 64 ? 2 : 1) gemm_kernel(GemmParams p, int tiles_n) {
-  constexpr int LB = GemmSmem<BN>::LB;
+// warps (BM / 32) (M) x 2 (N) of 32 x BN / 2.
+template <int BM, int BN, bool V16>
+__global__ void __launch_bounds__(BM * 2, BN == 64 ? (BM == 64 ? 4 : 2) : 1) gemm_kernel(GemmParams p, int tiles_n) {
+  constexpr int LB = GemmSmem<BM, BN>::LB;
+  constexpr int NT = GemmSmem<BM, BN>::NT;
   constexpr int WN = BN / 2;      // warp tile width
   constexpr int NJ = WN / 8;      // DMMA tiles across
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  GemmSmem<BN>& sm = *reinterpret_cast<GemmSmem<BN>*>(smem_raw);
+  GemmSmem<BM, BN>& sm = *reinterpret_cast<GemmSmem<BM, BN>*>(smem_raw);
   const int bz = blockIdx.y;
   const int m0 = (blockIdx.x / tiles_n) * BM, n0 = (blockIdx.x % tiles_n) * BN;
   const double* A = p.A + (int64_t)bz * p.strideA;
@@ -115,14 +121,14 @@ __global__ void __launch_bounds__(NT, BN == 64 ? 2 : 1) gemm_kernel(GemmParams p
   const int nk = (p.k + BK - 1) / BK;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) load_stage<BN, V16>(sm, s, p, A, B, m0, n0, s * BK);
+    if (s < nk) load_stage<BM, BN, V16>(sm, s, p, A, B, m0, n0, s * BK);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     const int nxt = kt + STAGES - 1;
-    if (nxt < nk) load_stage<BN, V16>(sm, nxt % STAGES, p, A, B, m0, n0, nxt * BK);
+    if (nxt < nk) load_stage<BM, BN, V16>(sm, nxt % STAGES, p, A, B, m0, n0, nxt * BK);
     cp_async_commit();
     const double* as = sm.a[kt % STAGES];
     const double* bs = sm.b[kt % STAGES];
@@ -160,17 +166,25 @@ __global__ void __launch_bounds__(NT, BN == 64 ? 2 : 1) gemm_kernel(GemmParams p
 }
 
 namespace {
-template <int BN, bool V16>
+template <int BM, int BN, bool V16>
 void launch_tile(const GemmParams& p, cudaStream_t stream) {
   static bool configured = false;
-  const int smem = (int)sizeof(GemmSmem<BN>);
+  const int smem = (int)sizeof(GemmSmem<BM, BN>);
   if (!configured) {
-    cudaFuncSetAttribute(gemm_kernel<BN, V16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(gemm_kernel<BM, BN, V16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     configured = true;
   }
   const int tiles_m = (p.m + BM - 1) / BM, tiles_n = (p.n + BN - 1) / BN;
   dim3 grid(tiles_m * tiles_n, p.batch);
-  gemm_kernel<BN, V16><<<grid, NT, smem, stream>>>(p, tiles_n);
+  gemm_kernel<BM, BN, V16><<<grid, GemmSmem<BM, BN>::NT, smem, stream>>>(p, tiles_n);
+}
+
+template <int BM, int BN>
+void launch_v(const GemmParams& p, bool v16, cudaStream_t stream) {
+  if (v16)
+    launch_tile<BM, BN, true>(p, stream);
+  else
+    launch_tile<BM, BN, false>(p, stream);
 }
 }  // namespace
 
@@ -178,16 +192,19 @@ void launch_gemm(const GemmParams& p, cudaStream_t stream) {
   // 16-byte copies need even leading dimensions / batch strides and 16-byte aligned bases
   const bool v16 = ((p.lda | p.ldb | p.strideA | p.strideB) & 1) == 0 &&
                    ((reinterpret_cast<uintptr_t>(p.A) | reinterpret_cast<uintptr_t>(p.B)) & 15) == 0;
-  if (p.n <= 64) {
-    if (v16)
-      launch_tile<64, true>(p, stream);
-    else
-      launch_tile<64, false>(p, stream);
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t big_tiles = (int64_t)((p.m + 127) / 128) * ((p.n + (p.n <= 64 ? 63 : 127)) / (p.n <= 64 ? 64 : 128)) * p.batch;
+  if (big_tiles < sms) {
+    launch_v<64, 64>(p, v16, stream);  // too few CTAs for the SMs: 64 x 64 tiles
+  } else if (p.n <= 64) {
+    launch_v<128, 64>(p, v16, stream);
   } else {
-    if (v16)
-      launch_tile<128, true>(p, stream);
-    else
-      launch_tile<128, false>(p, stream);
+    launch_v<128, 128>(p, v16, stream);
   }
 }
 

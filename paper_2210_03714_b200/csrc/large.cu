@@ -29,62 +29,162 @@ __device__ __forceinline__ double ldexp_j(double x, int j) { return j == 0 ? x :
 // ---------------------------------------------------------------------------------------------
 // LU of the 64 x 64 diagonal block at (off, off) of every system, no row exchanges, in place;
 // inverses of L (unit lower) and U written to inv + z * inv_stride + (off / 64) * 2 * 64 * 64.
+//  factor: right-looking, thread (r, q) keeps row r's columns q, q + 4, ... in registers; the
+//          multiplier comes from the row's quad by shuffle and the pivot row from smem, one barrier
+//          per pivot (the previous smem-only version with two barriers and an IEEE division per
+//          step, plus 128-thread substitution inverses, took 86 us per call);
+//  inverses: the eight 16 x 16 diagonal blocks of L and U by eight warps at once (16-step
+//          substitution chains), then the off-diagonal blocks by block substitution on DMMA in
+//          three dependency levels: X_ij = -X_ii (sum_k L_ik X_kj), Y_ij = -Y_ii (sum_k U_ik Y_kj).
+namespace {
+constexpr int TSW = 20;  // per-warp 16 x 16 scratch row stride
+
+// acc += A (16 x K) B (K x 16), A / B row-major in smem (K a multiple of 4)
+__device__ __forceinline__ void mm16(const double* A, int lda, const double* B, int ldb, int K, double (&acc)[2][2][2]) {
+  const int lane = lane_id();
+  const int g = lane >> 2, t = lane & 3;
+  for (int k = 0; k < K; k += 4) {
+    double af[2], bf[2];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) af[mi] = A[(8 * mi + g) * lda + k + t];
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj) bf[nj] = B[(k + t) * ldb + 8 * nj + g];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj) dmma(acc[mi][nj], af[mi], bf[nj]);
+  }
+}
+
+__device__ __forceinline__ void store16(double* D, int ldd, const double (&acc)[2][2][2], double scale) {
+  const int lane = lane_id();
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) D[(8 * mi + g) * ldd + 8 * nj + 2 * t + e] = scale * acc[mi][nj][e];
+}
+
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+}  // namespace
+
+size_t lu_base64_smem_bytes() { return sizeof(double) * (3 * B64 * L64 + 8 * 16 * TSW); }
+
 __global__ void __launch_bounds__(256) lu_base64_kernel(double* M, int64_t ld, int64_t strideM, int off,
                                                         double* inv, int64_t inv_stride, int factor, const int* zlist) {
-  __shared__ double s[B64 * L64];
-  __shared__ double prow[B64];
+  extern __shared__ __align__(16) double lu_smem[];
+  double* s = lu_smem;             // the block, LU in place
+  double* xl = s + B64 * L64;      // L^-1
+  double* xu = xl + B64 * L64;     // U^-1
+  double* scratch = xu + B64 * L64;
   const int z = zlist ? zlist[blockIdx.x] : blockIdx.x;
   double* a = M + (int64_t)z * strideM + (int64_t)off * ld + off;
   for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
     const int r = idx >> 6, c = idx & 63;
     s[r * L64 + c] = a[(int64_t)r * ld + c];
+    xl[r * L64 + c] = 0.0;
+    xu[r * L64 + c] = 0.0;
   }
   __syncthreads();
+  const int lane = lane_id(), warp = warp_id();
   if (factor) {
-    // right-looking, one column per step: 4 threads per row, 16 columns each
     const int r = threadIdx.x >> 2, q = threadIdx.x & 3;
-    for (int m = 0; m < B64; ++m) {
-      if (threadIdx.x >= m && threadIdx.x < B64) prow[threadIdx.x] = s[m * L64 + threadIdx.x];
-      __syncthreads();
-      double f = 0.0;
+    double v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = s[r * L64 + q + 4 * k];
+#pragma unroll
+    for (int m = 0; m < B64 - 1; ++m) {
+      const double ip = rcp_nr(s[m * L64 + m]);
+      const double xm = __shfl_sync(0xffffffffu, v[m >> 2], (lane & ~3) | (m & 3));
       if (r > m) {
-        f = s[r * L64 + m] * (1.0 / prow[m]);
-        for (int c = m + 1 + q; c < B64; c += 4) s[r * L64 + c] = fma(-f, prow[c], s[r * L64 + c]);
+        const double f = xm * ip;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (q + 4 * k > m) v[k] = fma(-f, s[m * L64 + q + 4 * k], v[k]);
+        if (q == (m & 3)) v[m >> 2] = f;
+      }
+      if (r == m + 1) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) s[r * L64 + q + 4 * k] = v[k];
       }
       __syncthreads();
-      if (r > m && q == 0) s[r * L64 + m] = f;
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      s[r * L64 + q + 4 * k] = v[k];
+      a[(int64_t)r * ld + q + 4 * k] = v[k];
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
-      const int rr = idx >> 6, c = idx & 63;
-      a[(int64_t)rr * ld + c] = s[rr * L64 + c];
-    }
   }
-  // inverses: threads 0-63 column l of L^-1, threads 64-127 column l of U^-1 (right-looking)
-  double* out = inv + (int64_t)z * inv_stride + (int64_t)(off / B64) * 2 * B64 * B64;
-  if (threadIdx.x < 2 * B64) {
-    const bool lower = threadIdx.x < B64;
-    const int l = threadIdx.x & 63;
-    double x[B64];
+  // diagonal 16 x 16 blocks: warps 0-3 L_bb^-1, warps 4-7 U_bb^-1 (lane l < 16: column l)
+  {
+    const int bb = warp & 3, o = 16 * bb, l = lane & 15;
+    double x[16];
 #pragma unroll
-    for (int i = 0; i < B64; ++i) x[i] = (i == l) ? 1.0 : 0.0;
-    if (lower) {
+    for (int i = 0; i < 16; ++i) x[i] = (i == l) ? 1.0 : 0.0;
+    if (warp < 4) {
 #pragma unroll
-      for (int m = 0; m < B64 - 1; ++m)
+      for (int m = 0; m < 15; ++m)
 #pragma unroll
-        for (int i = m + 1; i < B64; ++i) x[i] = fma(-s[i * L64 + m], x[m], x[i]);
+        for (int i = m + 1; i < 16; ++i) x[i] = fma(-s[(o + i) * L64 + o + m], x[m], x[i]);
+      if (lane < 16)
 #pragma unroll
-      for (int i = 0; i < B64; ++i) out[i * B64 + l] = x[i];
+        for (int i = 0; i < 16; ++i) xl[(o + i) * L64 + o + l] = x[i];
     } else {
 #pragma unroll
-      for (int m = B64 - 1; m >= 0; --m) {
-        x[m] = x[m] / s[m * L64 + m];
+      for (int m = 15; m >= 0; --m) {
+        x[m] = x[m] * rcp_nr(s[(o + m) * L64 + o + m]);
 #pragma unroll
-        for (int i = 0; i < m; ++i) x[i] = fma(-s[i * L64 + m], x[m], x[i]);
+        for (int i = 0; i < m; ++i) x[i] = fma(-s[(o + i) * L64 + o + m], x[m], x[i]);
       }
+      if (lane < 16)
 #pragma unroll
-      for (int i = 0; i < B64; ++i) out[B64 * B64 + i * B64 + l] = x[i];
+        for (int i = 0; i < 16; ++i) xu[(o + i) * L64 + o + l] = x[i];
     }
+  }
+  __syncthreads();
+  // off-diagonal blocks, level d = 1, 2, 3: tasks (L, j) j < 4 - d and (U, i) i < 4 - d
+  double* ws = scratch + warp * 16 * TSW;
+  for (int d = 1; d < 4; ++d) {
+    const int ntask = 4 - d;
+    if (warp < 2 * ntask) {
+      const bool lower = warp < ntask;
+      const int b0 = lower ? warp : warp - ntask;
+      double acc[2][2][2] = {};
+      if (lower) {  // X_ij, i = b0 + d, j = b0: P = L[i, j..i-1] X[j..i-1, j]
+        const int i = b0 + d, j = b0;
+        mm16(s + 16 * i * L64 + 16 * j, L64, xl + 16 * j * L64 + 16 * j, L64, 16 * d, acc);
+        store16(ws, TSW, acc, 1.0);
+        __syncwarp();
+        double acc2[2][2][2] = {};
+        mm16(xl + 16 * i * L64 + 16 * i, L64, ws, TSW, 16, acc2);
+        store16(xl + 16 * i * L64 + 16 * j, L64, acc2, -1.0);
+      } else {  // Y_ij, i = b0, j = b0 + d: P = U[i, i+1..j] Y[i+1..j, j]
+        const int i = b0, j = b0 + d;
+        mm16(s + 16 * i * L64 + 16 * (i + 1), L64, xu + 16 * (i + 1) * L64 + 16 * j, L64, 16 * d, acc);
+        store16(ws, TSW, acc, 1.0);
+        __syncwarp();
+        double acc2[2][2][2] = {};
+        mm16(xu + 16 * i * L64 + 16 * i, L64, ws, TSW, 16, acc2);
+        store16(xu + 16 * i * L64 + 16 * j, L64, acc2, -1.0);
+      }
+    }
+    __syncthreads();
+  }
+  double* out = inv + (int64_t)z * inv_stride + (int64_t)(off / B64) * 2 * B64 * B64;
+  for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
+    const int r = idx >> 6, c = idx & 63;
+    out[idx] = xl[r * L64 + c];
+    out[B64 * B64 + idx] = xu[r * L64 + c];
   }
 }
 
@@ -256,16 +356,36 @@ __global__ void form_shifted_kernel(const double* A, int64_t lda, int64_t stride
 }
 
 // Strict column diagonal dominance with margin (see small_eval.cu): ok[z] stays 1 only if every
-// column passes. One thread per column, rows summed in order.
-__global__ void certificate_kernel(const double* M, int np, int n, const unsigned long long* mx, double rel_tol,
-                                   int* ok) {
+// column passes. Off-diagonal column sums in two passes: certificate_partial_kernel sums row chunk
+// blockIdx.y of every column (one thread per column, coalesced rows), certificate_kernel adds the
+// chunks in ascending order -- a fixed order, so the decision is deterministic. (One thread summing
+// all n rows of its column took 1.8 ms for 8 x 4096^2: a 4096-long dependent add chain per thread.)
+__global__ void certificate_partial_kernel(const double* M, int np, int n, int chunk, double* part) {
+  const int z = blockIdx.z, q = blockIdx.y;
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= n) return;
+  const double* m = M + (int64_t)z * np * np;
+  const int r0 = q * chunk, r1 = min(n, r0 + chunk);
+  double s0 = 0.0, s1 = 0.0;  // two interleaved chains, combined at the end
+  int r = r0;
+  for (; r + 1 < r1; r += 2) {
+    const double a0 = (r != col) ? fabs(m[(int64_t)r * np + col]) : 0.0;
+    const double a1 = (r + 1 != col) ? fabs(m[(int64_t)(r + 1) * np + col]) : 0.0;
+    s0 += a0;
+    s1 += a1;
+  }
+  if (r < r1 && r != col) s0 += fabs(m[(int64_t)r * np + col]);
+  part[((int64_t)z * gridDim.y + q) * n + col] = s0 + s1;
+}
+
+__global__ void certificate_kernel(const double* M, int np, int n, int nchunks, const double* part,
+                                   const unsigned long long* mx, double rel_tol, int* ok) {
   const int z = blockIdx.y;
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= n) return;
   const double* m = M + (int64_t)z * np * np;
   double off = 0.0;
-  for (int r = 0; r < n; ++r)
-    if (r != col) off += fabs(m[(int64_t)r * np + col]);
+  for (int q = 0; q < nchunks; ++q) off += part[((int64_t)z * nchunks + q) * n + col];
   const double mxz = __longlong_as_double((long long)mx[z]);
   const double margin = fabs(m[(int64_t)col * np + col]) - off;
   const bool pass = (margin >= 1e-10 * mxz) && (margin > 2.0 * rel_tol * fmax(mxz, 1e-300)) && (mxz > 1e-250) &&

@@ -38,6 +38,10 @@ struct pf_action_op {
   bool pivoted = false;
   double* d_shifts = nullptr;      // device copy of `shifts`
   double* d_ones = nullptr;
+  // explicit inverses of the nbig x nbig diagonal blocks of L and U (per system: for block q,
+  // Linv at q * 2 * nbig^2, Uinv at (2q + 1) * nbig^2), for the blocked thin-RHS solves
+  int nbig = 0;
+  double* binv = nullptr;
 };
 
 namespace pf {
@@ -76,6 +80,7 @@ enum Slot {
   kWsLargePiv = 14,
   kWsLargeB = 15,
   kWsLargeX2 = 16,
+  kWsLargeBinv = 18,    // explicit inverses of the big diagonal blocks (thin-RHS solves)
   kWsScratch = 20,      // per-SM accumulator slots of the small kernel
   kWsSmallArrays = 64,  // small uploaded tables: kWsSmallArrays + i, i < 32
 };

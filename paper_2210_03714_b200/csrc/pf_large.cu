@@ -8,6 +8,7 @@
 //   B U^-1       = [B1 U11^-1, (B2 - B1 U12) U22^-1]
 // The same arithmetic as dense.cpp's right-looking LU / substitution (dense.cpp:102-163), blocked.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -23,8 +24,9 @@ __global__ void lu_pivot_kernel(double* M, int64_t ld, int64_t strideM, int n, i
                                 DevStatus* status, int* first_error, const int* zlist);
 __global__ void form_shifted_kernel(const double* A, int64_t lda, int64_t strideA, int n, int np, int batch,
                                     const double* shifts, const int* j, double* M, unsigned long long* mx);
-__global__ void certificate_kernel(const double* M, int np, int n, const unsigned long long* mx, double rel_tol,
-                                   int* ok);
+__global__ void certificate_partial_kernel(const double* M, int np, int n, int chunk, double* part);
+__global__ void certificate_kernel(const double* M, int np, int n, int nchunks, const double* part,
+                                   const unsigned long long* mx, double rel_tol, int* ok);
 __global__ void form_rhs_kernel(const double* src, int64_t lds, int64_t strideS, int n, int np, int cols,
                                 int ncols_true, int batch, const double* shifts, const int* j, int residual,
                                 const int* perm, double* R, int64_t strideR);
@@ -48,6 +50,7 @@ __global__ void iota_kernel(int* p, int n);
 __global__ void lincomb2_kernel(int n, int k, double d1, const double* X, double d2, const double* Y, int64_t ld,
                                 double* out, int64_t ldo);
 size_t apply_inv64_smem_bytes();
+size_t lu_base64_smem_bytes();
 
 namespace host {
 namespace {
@@ -77,6 +80,18 @@ void apply_inv(pf_context* ctx, const Sys& s, int blk, bool upper, bool right, d
   dim3 grid((extent + kB - 1) / kB, s.nsys);
   apply_inv64_kernel<<<grid, 256, apply_inv64_smem_bytes(), ctx->stream>>>(s.inv, s.inv_stride, blk, upper ? 1 : 0, right ? 1 : 0, B, ldb, sb,
                                                     extent);
+  ctx->launches++;
+}
+
+// 64 x 64 diagonal block: LU in place (factor) and the explicit inverses of its L and U
+void lu_base(pf_context* ctx, const Sys& s, int nblocks, int off, int factor, const int* zlist) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(lu_base64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lu_base64_smem_bytes());
+    configured = true;
+  }
+  lu_base64_kernel<<<nblocks, 256, lu_base64_smem_bytes(), ctx->stream>>>(s.M, s.np, s.stride(), off, s.inv,
+                                                                          s.inv_stride, factor, zlist);
   ctx->launches++;
 }
 
@@ -123,8 +138,7 @@ void trsm_right_upper(pf_context* ctx, const Sys& s, int off, int n, double* B, 
 
 void lu_rec(pf_context* ctx, const Sys& s, int off, int n) {
   if (n == kB) {
-    lu_base64_kernel<<<s.nsys, 256, 0, ctx->stream>>>(s.M, s.np, s.stride(), off, s.inv, s.inv_stride, 1, nullptr);
-    ctx->launches++;
+    lu_base(ctx, s, s.nsys, off, 1, nullptr);
     return;
   }
   const int n1 = half64(n), n2 = n - n1;
@@ -140,8 +154,7 @@ void lu_rec(pf_context* ctx, const Sys& s, int off, int n) {
 
 void diag_inverses(pf_context* ctx, const Sys& s) {
   for (int off = 0; off < s.np; off += kB) {
-    lu_base64_kernel<<<s.nsys, 256, 0, ctx->stream>>>(s.M, s.np, s.stride(), off, s.inv, s.inv_stride, 0, nullptr);
-    ctx->launches++;
+    lu_base(ctx, s, s.nsys, off, 0, nullptr);
   }
 }
 
@@ -169,8 +182,18 @@ FactorResult factor_systems(pf_context* ctx, const Sys& s, int n, unsigned long 
   FactorResult fr;
   int* d_ok = static_cast<int*>(workspace(ctx, kWsSmallArrays + 20, sizeof(int) * s.nsys));
   fill_int_kernel<<<(s.nsys + 255) / 256, 256, 0, ctx->stream>>>(d_ok, s.nsys, 1);
-  certificate_kernel<<<dim3((n + 255) / 256, s.nsys), 256, 0, ctx->stream>>>(s.M, s.np, n, d_mx, pivot_rel_tol, d_ok);
-  ctx->launches += 2;
+  const int nchunks = std::max(1, std::min(64, n / 64));
+  const int chunk = (n + nchunks - 1) / nchunks;
+  double* d_part = static_cast<double*>(workspace(ctx, kWsSmallArrays + 23, sizeof(double) * (size_t)s.nsys * nchunks * n));
+  if (!d_part) {
+    fr.rc = PF_ERR_CUDA;
+    return fr;
+  }
+  certificate_partial_kernel<<<dim3((n + 255) / 256, nchunks, s.nsys), 256, 0, ctx->stream>>>(s.M, s.np, n, chunk,
+                                                                                             d_part);
+  certificate_kernel<<<dim3((n + 255) / 256, s.nsys), 256, 0, ctx->stream>>>(s.M, s.np, n, nchunks, d_part, d_mx,
+                                                                             pivot_rel_tol, d_ok);
+  ctx->launches += 3;
   std::vector<int> ok(s.nsys);
   std::vector<unsigned long long> mxbits(s.nsys);
   cudaMemcpyAsync(ok.data(), d_ok, sizeof(int) * s.nsys, cudaMemcpyDeviceToHost, ctx->stream);
@@ -239,10 +262,124 @@ FactorResult factor_systems(pf_context* ctx, const Sys& s, int n, unsigned long 
   perm_from_piv_kernel<<<nf, 32, 0, ctx->stream>>>(d_piv, n, d_perm, d_fail);
   ctx->launches++;
   for (int off = 0; off < s.np; off += kB) {
-    lu_base64_kernel<<<nf, 256, 0, ctx->stream>>>(s.M, s.np, s.stride(), off, s.inv, s.inv_stride, 0, d_fail);
-    ctx->launches++;
+    lu_base(ctx, s, nf, off, 0, d_fail);
   }
   return fr;
+}
+
+// ---- explicit inverses of large diagonal blocks (thin right-hand sides: the action operator)
+// A solve with k = 64 columns through the 64-leaf recursion is a chain of ~512 dependent small
+// launches per triangle (cfg4: 1026 launches, 25 ms per substep). The operator is factored once and
+// applied many times, so the inverses of its nbig x nbig diagonal blocks are formed once here
+// (recursive block inversion on DMMA GEMMs from the 64 x 64 leaf inverses):
+//   [L11 0; L21 L22]^-1 = [X11 0; -X22 L21 X11  X22],  [U11 U12; 0 U22]^-1 = [Y11 -Y11 U12 Y22; 0 Y22]
+// and every apply is a left-looking blocked substitution with two GEMMs per block.
+// dst (b x b, leading dimension ldd, batch stride sd) = inverse of the unit-lower / upper diagonal
+// block [off, off + b) of every system; tmp holds (b/2)^2 per system.
+void tri_inv(pf_context* ctx, const Sys& s, bool upper, int off, int b, double* dst, int64_t ldd, int64_t sd,
+             double* tmp, int64_t st) {
+  if (b == kB) {
+    const double* src = s.inv + (int64_t)(off / kB) * 2 * kB * kB + (upper ? kB * kB : 0);
+    copy2d_kernel<<<dim3(grid_for((int64_t)kB * kB), s.nsys), 256, 0, ctx->stream>>>(kB, kB, 1.0, src, kB,
+                                                                                      s.inv_stride, dst, ldd, sd);
+    ctx->launches++;
+    return;
+  }
+  const int b1 = half64(b), b2 = b - b1;
+  double* X11 = dst;
+  double* X22 = dst + (int64_t)b1 * ldd + b1;
+  tri_inv(ctx, s, upper, off, b1, X11, ldd, sd, tmp, st);
+  tri_inv(ctx, s, upper, off + b1, b2, X22, ldd, sd, tmp, st);
+  if (!upper) {
+    // T = L21 X11 (b2 x b1); X21 = -X22 T
+    const double* L21 = s.M + (int64_t)(off + b1) * s.np + off;
+    gemm(ctx, b2, b1, b1, s.nsys, 1.0, L21, s.np, s.stride(), X11, ldd, sd, 0.0, tmp, b1, st, 0.0);
+    gemm(ctx, b2, b1, b2, s.nsys, -1.0, X22, ldd, sd, tmp, b1, st, 0.0, dst + (int64_t)b1 * ldd, ldd, sd, 0.0);
+  } else {
+    // T = U12 X22 (b1 x b2); X12 = -X11 T
+    const double* U12 = s.M + (int64_t)off * s.np + off + b1;
+    gemm(ctx, b1, b2, b2, s.nsys, 1.0, U12, s.np, s.stride(), X22, ldd, sd, 0.0, tmp, b2, st, 0.0);
+    gemm(ctx, b1, b2, b1, s.nsys, -1.0, X11, ldd, sd, tmp, b2, st, 0.0, dst + b1, ldd, sd, 0.0);
+  }
+}
+
+int big_block(int np) {
+  if (np >= 4096) return 1024;
+  if (np >= 2048) return 512;
+  if (np >= 1024) return 256;
+  return 0;  // small systems keep the 64-leaf recursion
+}
+
+int64_t big_inverse_stride(int np, int nb) { return (int64_t)((np + nb - 1) / nb) * 2 * nb * nb; }
+
+// binv (per system big_inverse_stride doubles) <- block q: Linv at 2q nb^2, Uinv at (2q + 1) nb^2
+bool build_big_inverses(pf_context* ctx, const Sys& s, int nb, double* binv) {
+  const int nblk = (s.np + nb - 1) / nb;
+  const int64_t bstride = big_inverse_stride(s.np, nb);
+  double* tmp = static_cast<double*>(workspace(ctx, kWsT2, sizeof(double) * (size_t)(nb / 2) * (nb / 2) * s.nsys));
+  if (!tmp) return false;
+  cudaMemsetAsync(binv, 0, sizeof(double) * bstride * s.nsys, ctx->stream);
+  for (int q = 0; q < nblk; ++q) {
+    const int off = q * nb, b = std::min(nb, s.np - off);
+    for (int u = 0; u < 2; ++u)
+      tri_inv(ctx, s, u == 1, off, b, binv + (int64_t)(2 * q + u) * nb * nb, b, bstride, tmp,
+              (int64_t)(nb / 2) * (nb / 2));
+  }
+  return true;
+}
+
+// R (np x k per system, batch stride rs) <- U^-1 L^-1 R: left-looking blocked substitution with the
+// explicit block inverses (forward into Y, backward back into R; two GEMMs per block) when binv is
+// given, else the 64-leaf recursion.
+int solve_lu(pf_context* ctx, const Sys& s, const double* binv, int nb, double* R, int k, int64_t rs) {
+  if (!binv) {
+    trsm_left_lower(ctx, s, 0, s.np, R, k, rs, k);
+    trsm_left_upper(ctx, s, 0, s.np, R, k, rs, k);
+    return PF_OK;
+  }
+  const int np = s.np, P = s.nsys, nblk = (np + nb - 1) / nb;
+  const int64_t bstride = big_inverse_stride(np, nb), st = s.stride();
+  double* Y = static_cast<double*>(workspace(ctx, kWsLargeX2, sizeof(double) * rs * P));
+  if (!Y) return PF_ERR_CUDA;
+  static const bool left_looking = std::getenv("PF_LEFT_LOOKING") != nullptr;
+  if (!left_looking) {
+    // right-looking: after each block, one GEMM updates every remaining row (np - end rows: many
+    // CTAs, K = nb) instead of a K = q nb reduction over few CTAs per block
+    for (int q = 0; q < nblk; ++q) {
+      const int off = q * nb, b = std::min(nb, np - off), end = off + b;
+      gemm(ctx, b, k, b, P, 1.0, binv + (int64_t)(2 * q) * nb * nb, b, bstride, R + (int64_t)off * k, k, rs, 0.0,
+           Y + (int64_t)off * k, k, rs, 0.0);
+      if (end < np)  // R[>q] -= L[>q, q] Y_q
+        gemm(ctx, np - end, k, b, P, -1.0, s.M + (int64_t)end * np + off, np, st, Y + (int64_t)off * k, k, rs, 1.0,
+             R + (int64_t)end * k, k, rs, 0.0);
+    }
+    for (int q = nblk - 1; q >= 0; --q) {
+      const int off = q * nb, b = std::min(nb, np - off);
+      gemm(ctx, b, k, b, P, 1.0, binv + (int64_t)(2 * q + 1) * nb * nb, b, bstride, Y + (int64_t)off * k, k, rs,
+           0.0, R + (int64_t)off * k, k, rs, 0.0);
+      if (off > 0)  // Y[<q] -= U[<q, q] X_q
+        gemm(ctx, off, k, b, P, -1.0, s.M + off, np, st, R + (int64_t)off * k, k, rs, 1.0, Y, k, rs, 0.0);
+    }
+    return PF_OK;
+  }
+  for (int q = 0; q < nblk; ++q) {
+    const int off = q * nb, b = std::min(nb, np - off);
+    double* Rq = R + (int64_t)off * k;
+    if (off > 0)  // R_q -= L[q, <q] Y[<q]
+      gemm(ctx, b, k, off, P, -1.0, s.M + (int64_t)off * np, np, st, Y, k, rs, 1.0, Rq, k, rs, 0.0);
+    gemm(ctx, b, k, b, P, 1.0, binv + (int64_t)(2 * q) * nb * nb, b, bstride, Rq, k, rs, 0.0, Y + (int64_t)off * k, k,
+         rs, 0.0);
+  }
+  for (int q = nblk - 1; q >= 0; --q) {
+    const int off = q * nb, b = std::min(nb, np - off), end = off + b;
+    double* Yq = Y + (int64_t)off * k;
+    if (end < np)  // Y_q -= U[q, >q] X[>q]
+      gemm(ctx, b, k, np - end, P, -1.0, s.M + (int64_t)off * np + end, np, st, R + (int64_t)end * k, k, rs, 1.0,
+           Yq, k, rs, 0.0);
+    gemm(ctx, b, k, b, P, 1.0, binv + (int64_t)(2 * q + 1) * nb * nb, b, bstride, Yq, k, rs, 0.0,
+         R + (int64_t)off * k, k, rs, 0.0);
+  }
+  return PF_OK;
 }
 
 bool make_sys(pf_context* ctx, Sys& s, int n, int nsys, int slotM) {
@@ -396,6 +533,13 @@ int large_action(pf_context* ctx, const pf_method* m, int n, int k, const double
     }
     pivoted = fr.pivoted;
   }
+  // factored once, solved `substeps` times: explicit inverses of the big diagonal blocks
+  const int nb = P > 0 ? big_block(np) : 0;
+  double* binv = nullptr;
+  if (nb) {
+    binv = static_cast<double*>(workspace(ctx, kWsLargeBinv, sizeof(double) * big_inverse_stride(np, nb) * P));
+    if (!binv || !build_big_inverses(ctx, s, nb, binv)) return PF_ERR_CUDA;
+  }
   // X = V (padded rows are zero)
   cudaMemsetAsync(X, 0, sizeof(double) * blk, ctx->stream);
   copy2d_kernel<<<dim3(grid_for((int64_t)n * k), 1), 256, 0, ctx->stream>>>(n, k, 1.0, V, ldv, 0, X, k, 0);
@@ -430,8 +574,8 @@ int large_action(pf_context* ctx, const pf_method* m, int n, int k, const double
           residual ? BX : X, k, 0, n, np, k, k, 1, residual ? d_sh : d_one, nullptr, 1, pivoted ? d_perm : nullptr, R,
           (int64_t)blk);
       ctx->launches++;
-      trsm_left_lower(ctx, s, 0, np, R, k, (int64_t)blk, k);
-      trsm_left_upper(ctx, s, 0, np, R, k, (int64_t)blk, k);
+      const int rc = solve_lu(ctx, s, binv, nb, R, k, (int64_t)blk);
+      if (rc) return rc;
     }
     action_accumulate_kernel<<<grid_for((int64_t)n * k), 256, 0, ctx->stream>>>(
         R, k, (int64_t)blk, X, k, n, k, (int)tz.size(), d_tz, d_w, (residual || hybrid) ? 1 : 0, constant,
@@ -594,6 +738,14 @@ int action_op_create(pf_context* ctx, const pf_method* m, int n, const double* A
       return rc;
     }
     op->pivoted = fr.pivoted;
+    op->nbig = big_block(op->np);
+    if (op->nbig) {
+      if (cudaMalloc(&op->binv, sizeof(double) * big_inverse_stride(op->np, op->nbig) * P) != cudaSuccess ||
+          !build_big_inverses(ctx, s, op->nbig, op->binv)) {
+        action_op_destroy(op);
+        return PF_ERR_CUDA;
+      }
+    }
   }
   *out = op;
   return cuda_fail(cudaGetLastError());
@@ -622,8 +774,8 @@ int action_op_apply(pf_action_op* op, const double* V, int64_t ldv, int k, doubl
         op->pivoted ? op->perm : nullptr, R, (int64_t)blk);
     ctx->launches++;
     Sys s{op->M, np, P, op->inv, (int64_t)(np / kB) * 2 * kB * kB};
-    trsm_left_lower(ctx, s, 0, np, R, k, (int64_t)blk, k);
-    trsm_left_upper(ctx, s, 0, np, R, k, (int64_t)blk, k);
+    const int rc = solve_lu(ctx, s, op->binv, op->nbig, R, k, (int64_t)blk);
+    if (rc) return rc;
   }
   const int nt = (int)op->term_slot.size();
   int* d_tz = upload(ctx, kWsSmallArrays + 12, op->term_slot);
@@ -667,6 +819,7 @@ void action_op_destroy(pf_action_op* op) {
   cudaFree(op->perm);
   cudaFree(op->d_shifts);
   cudaFree(op->d_ones);
+  cudaFree(op->binv);
   delete op;
 }
 
