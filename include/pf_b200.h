@@ -58,7 +58,10 @@ enum pf_form { PF_FORM_PLAIN = 0, PF_FORM_RESIDUAL = 1 };
 enum pf_flags {
   PF_FLAG_NONE = 0,
   PF_FLAG_ASYNC = 1,     /* do not synchronise to read device status */
-  PF_FLAG_FORCE_PIVOT = 2 /* always run the genuine partial-pivoting LU (testing) */
+  PF_FLAG_FORCE_PIVOT = 2, /* always run the genuine partial-pivoting LU (testing) */
+  PF_FLAG_PER_SHIFT = 4    /* no (c, -c) pair merging: one solve per shift, weighted terms added in
+                              ascending shift order -- dense.cpp's rounding sequence; results are then
+                              bit-identical to any shift partition summed in that order */
 };
 
 /* Failure detail; enough for the C++ wrapper to rebuild the reference message

@@ -2,8 +2,8 @@
 //
 // Replaces DenseMatrix::mul (proj/core/src/dense.cpp:17-29) for the squaring chain, B^2, the
 // phi1 / cos-sin recurrences, B V, and every off-diagonal update of the large-n LU / triangular
-// solves. CTA tile BM x BN x 16: 128 x 128 (8 warps of 32 x 64), 128 x 64 for thin right-hand sides
-// (8 warps of 32 x 32, two CTAs per SM), or 64 x 64 (4 warps of 32 x 32) when the larger tiles would
+// solves. CTA tile BM x BN x BK: 128 x 128 x 32 (8 warps of 32 x 64), 128 x 64 x 16 for thin right-hand sides
+// (8 warps of 32 x 32, two CTAs per SM), or 64 x 64 x 16 (4 warps of 32 x 32) when the larger tiles would
 // leave most of the 148 SMs idle (the small updates deep in the LU / TRSM recursion: one SM's DMMA
 // rate is 250 GFLOP/s, so a single 128^3 tile takes 17 us); 3-stage cp.async pipeline, 16-byte
 // copies when the operands allow it (8-byte copies with zero fill otherwise: any shape / leading
@@ -14,13 +14,12 @@
 namespace pf {
 namespace {
 
-constexpr int BK = 16, STAGES = 3;
-constexpr int LA = BK + 4;  // A tile row stride (doubles): 32-byte skew
+constexpr int STAGES = 3;
 
-template <int BM, int BN>
+template <int BM, int BN, int BK>
 struct GemmSmem {
+  static constexpr int LA = BK + 4;  // A tile row stride (doubles): 32-byte skew
   static constexpr int LB = BN + 4;
-  static constexpr int NT = BM * 2;  // (BM / 32) x 2 warps
   double a[STAGES][BM * LA];
   double b[STAGES][BK * LB];
 };
@@ -40,11 +39,11 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-template <int BM, int BN, bool V16>
-__device__ __forceinline__ void load_stage(GemmSmem<BM, BN>& sm, int stage, const GemmParams& p, const double* A,
+template <int BM, int BN, int BK, int NT, bool V16>
+__device__ __forceinline__ void load_stage(GemmSmem<BM, BN, BK>& sm, int stage, const GemmParams& p, const double* A,
                                            const double* B, int m0, int n0, int k0) {
-  constexpr int LB = GemmSmem<BM, BN>::LB;
-  constexpr int NT = GemmSmem<BM, BN>::NT;
+  constexpr int LA = GemmSmem<BM, BN, BK>::LA;
+  constexpr int LB = GemmSmem<BM, BN, BK>::LB;
   if constexpr (V16) {
 #pragma unroll
     for (int it = 0; it < (BM * BK / 2) / NT; ++it) {
@@ -84,15 +83,17 @@ __device__ __forceinline__ void load_stage(GemmSmem<BM, BN>& sm, int stage, cons
 
 }  // namespace
 
-// warps (BM / 32) (M) x 2 (N) of 32 x BN / 2.
-template <int BM, int BN, bool V16>
-__global__ void __launch_bounds__(BM * 2, BN == 64 ? (BM == 64 ? 4 : 2) : 1) gemm_kernel(GemmParams p, int tiles_n) {
-  constexpr int LB = GemmSmem<BM, BN>::LB;
-  constexpr int NT = GemmSmem<BM, BN>::NT;
-  constexpr int WN = BN / 2;      // warp tile width
+// warps (BM / WM) (M) x (BN / WN) (N), each a WM x WN tile of (WM / 8) x (WN / 8) DMMA tiles.
+template <int BM, int BN, int BK, int WM, int WN, int MINB, bool V16>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB) gemm_kernel(GemmParams p, int tiles_n) {
+  constexpr int LA = GemmSmem<BM, BN, BK>::LA;
+  constexpr int LB = GemmSmem<BM, BN, BK>::LB;
+  constexpr int NT = (BM / WM) * (BN / WN) * 32;
+  constexpr int MI = WM / 8;      // DMMA tiles down
   constexpr int NJ = WN / 8;      // DMMA tiles across
+  constexpr int WCOLS = BN / WN;  // warps across
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  GemmSmem<BM, BN>& sm = *reinterpret_cast<GemmSmem<BM, BN>*>(smem_raw);
+  GemmSmem<BM, BN, BK>& sm = *reinterpret_cast<GemmSmem<BM, BN, BK>*>(smem_raw);
   const int bz = blockIdx.y;
   const int m0 = (blockIdx.x / tiles_n) * BM, n0 = (blockIdx.x % tiles_n) * BN;
   const double* A = p.A + (int64_t)bz * p.strideA;
@@ -110,37 +111,37 @@ __global__ void __launch_bounds__(BM * 2, BN == 64 ? (BM == 64 ? 4 : 2) : 1) gem
   }
   const int lane = lane_id(), warp = warp_id();
   const int g = lane >> 2, t = lane & 3;
-  const int wm = 32 * (warp >> 1), wn = WN * (warp & 1);
+  const int wm = WM * (warp / WCOLS), wn = WN * (warp % WCOLS);
 
-  double acc[4][NJ][2];
+  double acc[MI][NJ][2];
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
     for (int nj = 0; nj < NJ; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
 
   const int nk = (p.k + BK - 1) / BK;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) load_stage<BM, BN, V16>(sm, s, p, A, B, m0, n0, s * BK);
+    if (s < nk) load_stage<BM, BN, BK, NT, V16>(sm, s, p, A, B, m0, n0, s * BK);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     const int nxt = kt + STAGES - 1;
-    if (nxt < nk) load_stage<BM, BN, V16>(sm, nxt % STAGES, p, A, B, m0, n0, nxt * BK);
+    if (nxt < nk) load_stage<BM, BN, BK, NT, V16>(sm, nxt % STAGES, p, A, B, m0, n0, nxt * BK);
     cp_async_commit();
     const double* as = sm.a[kt % STAGES];
     const double* bs = sm.b[kt % STAGES];
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[4], bf[NJ];
+      double af[MI], bf[NJ];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) af[mi] = as[(wm + 8 * mi + g) * LA + kk + t];
+      for (int mi = 0; mi < MI; ++mi) af[mi] = as[(wm + 8 * mi + g) * LA + kk + t];
 #pragma unroll
       for (int nj = 0; nj < NJ; ++nj) bf[nj] = bs[(kk + t) * LB + wn + 8 * nj + g];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
+      for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
         for (int nj = 0; nj < NJ; ++nj) dmma(acc[mi][nj], af[mi], bf[nj]);
     }
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(BM * 2, BN == 64 ? (BM == 64 ? 4 : 2) : 1) gem
 
   // epilogue: alpha * acc (+ beta * C) (+ gamma on the diagonal)
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
     for (int nj = 0; nj < NJ; ++nj)
 #pragma unroll
@@ -166,25 +167,26 @@ __global__ void __launch_bounds__(BM * 2, BN == 64 ? (BM == 64 ? 4 : 2) : 1) gem
 }
 
 namespace {
-template <int BM, int BN, bool V16>
+template <int BM, int BN, int BK, int WM, int WN, int MINB, bool V16>
 void launch_tile(const GemmParams& p, cudaStream_t stream) {
   static bool configured = false;
-  const int smem = (int)sizeof(GemmSmem<BM, BN>);
+  const int smem = (int)sizeof(GemmSmem<BM, BN, BK>);
   if (!configured) {
-    cudaFuncSetAttribute(gemm_kernel<BM, BN, V16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(gemm_kernel<BM, BN, BK, WM, WN, MINB, V16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
     configured = true;
   }
   const int tiles_m = (p.m + BM - 1) / BM, tiles_n = (p.n + BN - 1) / BN;
   dim3 grid(tiles_m * tiles_n, p.batch);
-  gemm_kernel<BM, BN, V16><<<grid, GemmSmem<BM, BN>::NT, smem, stream>>>(p, tiles_n);
+  gemm_kernel<BM, BN, BK, WM, WN, MINB, V16><<<grid, (BM / WM) * (BN / WN) * 32, smem, stream>>>(p, tiles_n);
 }
 
-template <int BM, int BN>
+template <int BM, int BN, int BK, int WM, int WN, int MINB>
 void launch_v(const GemmParams& p, bool v16, cudaStream_t stream) {
   if (v16)
-    launch_tile<BM, BN, true>(p, stream);
+    launch_tile<BM, BN, BK, WM, WN, MINB, true>(p, stream);
   else
-    launch_tile<BM, BN, false>(p, stream);
+    launch_tile<BM, BN, BK, WM, WN, MINB, false>(p, stream);
 }
 }  // namespace
 
@@ -199,12 +201,14 @@ void launch_gemm(const GemmParams& p, cudaStream_t stream) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int64_t big_tiles = (int64_t)((p.m + 127) / 128) * ((p.n + (p.n <= 64 ? 63 : 127)) / (p.n <= 64 ? 64 : 128)) * p.batch;
+  // measured on B200 (tools/large_timing.py gemm): 128 x 128 x 32 tiles 31.6 / 31.9 TF/s at 4096^3 /
+  // 8192^3 vs 30.6 / 30.9 with BK = 16; 4 warps of 64 x 64 spill at 255 registers (18.5 TF/s)
   if (big_tiles < sms) {
-    launch_v<64, 64>(p, v16, stream);  // too few CTAs for the SMs: 64 x 64 tiles
+    launch_v<64, 64, 16, 32, 32, 4>(p, v16, stream);  // too few CTAs for the SMs: 64 x 64 tiles
   } else if (p.n <= 64) {
-    launch_v<128, 64>(p, v16, stream);
+    launch_v<128, 64, 16, 32, 32, 2>(p, v16, stream);
   } else {
-    launch_v<128, 128>(p, v16, stream);
+    launch_v<128, 128, 32, 32, 64, 1>(p, v16, stream);
   }
 }
 

@@ -393,6 +393,52 @@ __global__ void certificate_kernel(const double* M, int np, int n, int nchunks, 
   if (!pass) atomicAnd(ok + z, 0);
 }
 
+// Pair mode (pf_large.cu large_eval_pairs): the reference's systems I - cB and I + cB must be
+// certified for every pair c. Column statistics of B in two passes like the certificate above:
+// off-diagonal |b| sums per row chunk, and max|B| per matrix (atomicMax on the bit pattern).
+__global__ void colstat_partial_kernel(const double* B, int64_t ld, int64_t strideB, int n, int chunk, double* part,
+                                       unsigned long long* bmax) {
+  const int z = blockIdx.z, q = blockIdx.y;
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  double mx = 0.0;
+  if (col < n) {
+    const double* m = B + (int64_t)z * strideB;
+    const int r0 = q * chunk, r1 = min(n, r0 + chunk);
+    double s0 = 0.0;
+    for (int r = r0; r < r1; ++r) {
+      const double a = fabs(m[(int64_t)r * ld + col]);
+      mx = fmax(mx, a);
+      if (r != col) s0 += a;
+    }
+    part[((int64_t)z * gridDim.y + q) * n + col] = s0;
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(bmax + z, (unsigned long long)__double_as_longlong(mx));
+}
+
+// |1 -/+ c b_jj| - |c| sum_{i != j} |b_ij| > bound (1 + |c| max|B|) for every pair c and column j:
+// strict column diagonal dominance of I - cB and I + cB with the per-shift certificate's margin
+// taken at the upper bound 1 + |c| max|B| of max|I -/+ cB|.
+__global__ void pair_certificate_kernel(const double* B, int64_t ld, int64_t strideB, int n, int nchunks,
+                                        const double* part, const unsigned long long* bmax, const double* c, int npairs,
+                                        double rel, int* ok) {
+  const int z = blockIdx.y;
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= n) return;
+  double off = 0.0;
+  for (int q = 0; q < nchunks; ++q) off += part[((int64_t)z * nchunks + q) * n + col];
+  const double d = B[(int64_t)z * strideB + (int64_t)col * ld + col];
+  const double bm = __longlong_as_double((long long)bmax[z]);
+  bool pass = bm < 1e250;
+  for (int p = 0; p < npairs && pass; ++p) {
+    const double cc = c[p], scale = 1.0 + fabs(cc) * bm;
+    const double bound = fmax(1e-10, 2.0 * rel) * scale;
+    const double o = fabs(cc) * off;
+    pass = (fabs(1.0 - cc * d) - o > bound) && (fabs(1.0 + cc * d) - o > bound);
+  }
+  if (!pass) atomicAnd(ok + z, 0);
+}
+
 // R_z = c_i 2^-j A_b[perm] (residual) or P I (plain), padded np x cols (cols = np for matrices).
 // For the action, A_b is replaced by the block V (n x k): src_ld / src_stride describe it.
 __global__ void form_rhs_kernel(const double* src, int64_t lds, int64_t strideS, int n, int np, int cols, int ncols_true,

@@ -303,6 +303,7 @@ int pf_eval_dense_batched(pf_context* ctx, const pf_method* m, int n, int batch,
   p.batch = batch;
   p.mode = pf::kModeEval;
   p.force_pivot = (flags & PF_FLAG_FORCE_PIVOT) ? 1 : 0;
+  if (flags & PF_FLAG_PER_SHIFT) p.pair_mode = 0;
   p.A = dB;
   p.lda = ldb;
   p.strideA = strideB;
@@ -348,6 +349,7 @@ int eval_scaled(pf_context* ctx, const pf_method* m, double theta, int n, int ba
   p.batch = batch;
   p.mode = pf::kModeScaledEval;
   p.force_pivot = (flags & PF_FLAG_FORCE_PIVOT) ? 1 : 0;
+  if (flags & PF_FLAG_PER_SHIFT) p.pair_mode = 0;
   p.A = dA;
   p.lda = lda;
   p.strideA = strideA;
@@ -426,6 +428,7 @@ int pf_expm_batched(pf_context* ctx, const pf_method* m, double theta, int n, in
   p.batch = batch;
   p.mode = pf::kModeExpm;
   p.force_pivot = (flags & PF_FLAG_FORCE_PIVOT) ? 1 : 0;
+  if (flags & PF_FLAG_PER_SHIFT) p.pair_mode = 0;
   p.A = dA;
   p.lda = lda;
   p.strideA = strideA;

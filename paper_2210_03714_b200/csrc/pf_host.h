@@ -81,6 +81,9 @@ enum Slot {
   kWsLargeB = 15,
   kWsLargeX2 = 16,
   kWsLargeBinv = 18,    // explicit inverses of the big diagonal blocks (thin-RHS solves)
+  kWsPairB = 19,        // large pair mode: B = 2^-j A, B^2, E_A
+  kWsPairB2 = 21,
+  kWsPairT = 22,
   kWsScratch = 20,      // per-SM accumulator slots of the small kernel
   kWsSmallArrays = 64,  // small uploaded tables: kWsSmallArrays + i, i < 32
 };

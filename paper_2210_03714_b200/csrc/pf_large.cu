@@ -25,6 +25,11 @@ __global__ void lu_pivot_kernel(double* M, int64_t ld, int64_t strideM, int n, i
 __global__ void form_shifted_kernel(const double* A, int64_t lda, int64_t strideA, int n, int np, int batch,
                                     const double* shifts, const int* j, double* M, unsigned long long* mx);
 __global__ void certificate_partial_kernel(const double* M, int np, int n, int chunk, double* part);
+__global__ void colstat_partial_kernel(const double* B, int64_t ld, int64_t strideB, int n, int chunk, double* part,
+                                       unsigned long long* bmax);
+__global__ void pair_certificate_kernel(const double* B, int64_t ld, int64_t strideB, int n, int nchunks,
+                                        const double* part, const unsigned long long* bmax, const double* c, int npairs,
+                                        double rel, int* ok);
 __global__ void certificate_kernel(const double* M, int np, int n, int nchunks, const double* part,
                                    const unsigned long long* mx, double rel_tol, int* ok);
 __global__ void form_rhs_kernel(const double* src, int64_t lds, int64_t strideS, int n, int np, int cols,
@@ -177,8 +182,10 @@ struct FactorResult {
   std::vector<double> scale;
 };
 
+constexpr int kDeclined = -1000;  // pair mode declined: the caller takes the per-shift path
+
 FactorResult factor_systems(pf_context* ctx, const Sys& s, int n, unsigned long long* d_mx, int flags,
-                            int* d_piv, int* d_perm, double pivot_rel_tol) {
+                            int* d_piv, int* d_perm, double pivot_rel_tol, bool decline = false) {
   FactorResult fr;
   int* d_ok = static_cast<int*>(workspace(ctx, kWsSmallArrays + 20, sizeof(int) * s.nsys));
   fill_int_kernel<<<(s.nsys + 255) / 256, 256, 0, ctx->stream>>>(d_ok, s.nsys, 1);
@@ -212,6 +219,10 @@ FactorResult factor_systems(pf_context* ctx, const Sys& s, int n, unsigned long 
     if (force || !ok[z]) fails.push_back(z);
   }
   const int nf = (int)fails.size();
+  if (decline && nf > 0) {  // pair mode only runs the exchange-free LU
+    fr.rc = kDeclined;
+    return fr;
+  }
   if (nf == 0) {
     lu_rec(ctx, s, 0, s.np);
     return fr;
@@ -394,10 +405,133 @@ bool make_sys(pf_context* ctx, Sys& s, int n, int nsys, int slotM) {
 }  // namespace
 
 // ---------------------------------------------------------------------------------------------
+// Pair mode (residual form, every nonzero shift in a pair c, -c; small_eval.cu does the same per
+// matrix). With Z_p = (I - c_p^2 B^2)^-1 c_p^2 B^2 (the residual term of shift c_p^2 on B^2):
+//   w+ X+ + w- X- = (w+ - w-) c (I + Z) B + (w+ + w-) Z,
+// so for every weight set  f = a0 I + E_A B + E_B,  E_A = sum_p cm_p c_p (I + Z_p),  E_B = sum_p cp_p Z_p:
+// half the LUs and solves of the per-shift path, plus B^2 and one product per weight set. Taken only
+// when the reference's own systems I -/+ c B are certified for every pair (the reference would not
+// pivot and raises nothing) and every I - c^2 B^2 passes the certificate; otherwise kDeclined.
+int large_eval_pairs(pf_context* ctx, const pf_method* m, int n, int batch, const double* A, int64_t lda,
+                     int64_t strideA, const int* dJ, double* const* outs, int64_t ldo, int64_t strideOut, int flags,
+                     pf_status* status) {
+  static const bool no_pairs = std::getenv("PF_NO_PAIRS") != nullptr;
+  if (no_pairs || m->form != PF_FORM_RESIDUAL || m->has_poly || (flags & (PF_FLAG_FORCE_PIVOT | PF_FLAG_PER_SHIFT)))
+    return kDeclined;
+  std::vector<double> c;
+  std::vector<int> ip, im;
+  std::vector<char> used(m->n_terms, 0);
+  for (int i = 0; i < m->n_terms; ++i) {
+    if (used[i] || m->shifts[i] == 0.0) continue;
+    int jp = -1;
+    for (int j = i + 1; j < m->n_terms; ++j)
+      if (!used[j] && m->shifts[j] == -m->shifts[i]) {
+        jp = j;
+        break;
+      }
+    if (jp < 0) return kDeclined;
+    used[i] = used[jp] = 1;
+    c.push_back(m->shifts[i]);
+    ip.push_back(i);
+    im.push_back(jp);
+  }
+  const int npairs = (int)c.size();
+  if (npairs == 0) return kDeclined;
+  const int64_t nn = (int64_t)n * n;
+  double* Bs = static_cast<double*>(workspace(ctx, kWsPairB, sizeof(double) * nn * batch));
+  double* B2 = static_cast<double*>(workspace(ctx, kWsPairB2, sizeof(double) * nn * batch));
+  double* T = static_cast<double*>(workspace(ctx, kWsPairT, sizeof(double) * nn * batch));
+  const int nchunks = std::max(1, std::min(64, n / 64));
+  const int chunk = (n + nchunks - 1) / nchunks;
+  double* d_part = static_cast<double*>(workspace(ctx, kWsSmallArrays + 24, sizeof(double) * (size_t)batch * nchunks * n));
+  auto* d_bmax = static_cast<unsigned long long*>(workspace(ctx, kWsSmallArrays + 25, sizeof(unsigned long long) * batch));
+  int* d_ok = static_cast<int*>(workspace(ctx, kWsSmallArrays + 26, sizeof(int) * batch));
+  double* d_c = upload(ctx, kWsSmallArrays + 27, c);
+  if (!Bs || !B2 || !T || !d_part || !d_bmax || !d_ok || !d_c) return PF_ERR_CUDA;
+  launch_ldexp_batched(n, batch, A, lda, strideA, dJ, Bs, n, nn, ctx->stream);
+  cudaMemsetAsync(d_bmax, 0, sizeof(unsigned long long) * batch, ctx->stream);
+  fill_int_kernel<<<(batch + 255) / 256, 256, 0, ctx->stream>>>(d_ok, batch, 1);
+  colstat_partial_kernel<<<dim3((n + 255) / 256, nchunks, batch), 256, 0, ctx->stream>>>(Bs, n, nn, n, chunk, d_part,
+                                                                                        d_bmax);
+  pair_certificate_kernel<<<dim3((n + 255) / 256, batch), 256, 0, ctx->stream>>>(Bs, n, nn, n, nchunks, d_part, d_bmax,
+                                                                                 d_c, npairs, 1e-14, d_ok);
+  ctx->launches += 4;
+  std::vector<int> ok(batch);
+  cudaMemcpyAsync(ok.data(), d_ok, sizeof(int) * batch, cudaMemcpyDeviceToHost, ctx->stream);
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return PF_ERR_CUDA;
+  int nok = 0;
+  for (int v : ok) nok += v ? 1 : 0;
+  if (nok == 0) return kDeclined;
+  if (nok < batch) {  // mixed batch: every matrix decides for itself
+    for (int b = 0; b < batch; ++b) {
+      double* ob[2] = {outs[0] + b * strideOut, m->n_sets > 1 ? outs[1] + b * strideOut : nullptr};
+      const int rc = large_eval(ctx, m, n, 1, A + b * strideA, lda, 0, dJ ? dJ + b : nullptr, ob, ldo, 0, flags,
+                                status);
+      if (rc) {
+        if (status) status->batch_index = b;
+        return rc;
+      }
+    }
+    return PF_OK;
+  }
+  gemm(ctx, n, n, n, batch, 1.0, Bs, n, nn, Bs, n, nn, 0.0, B2, n, nn, 0.0);
+  Sys s;
+  const int nsys = npairs * batch;
+  if (!make_sys(ctx, s, n, nsys, kWsLargeM)) return PF_ERR_CUDA;
+  double* R = static_cast<double*>(workspace(ctx, kWsLargeR, sizeof(double) * s.stride() * nsys));
+  auto* d_mx = static_cast<unsigned long long*>(workspace(ctx, kWsLargeAux, sizeof(unsigned long long) * nsys));
+  int* d_piv = static_cast<int*>(workspace(ctx, kWsLargePiv, sizeof(int) * (size_t)n * nsys * 2));
+  if (!R || !d_mx || !d_piv) return PF_ERR_CUDA;
+  std::vector<double> c2(npairs);
+  for (int q = 0; q < npairs; ++q) c2[q] = c[q] * c[q];
+  double* d_c2 = upload(ctx, kWsSmallArrays + 1, c2);
+  cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long) * nsys, ctx->stream);
+  form_shifted_kernel<<<dim3(grid_for(s.stride()), nsys), 256, 0, ctx->stream>>>(B2, n, nn, n, s.np, batch, d_c2,
+                                                                                 nullptr, s.M, d_mx);
+  ctx->launches++;
+  FactorResult fr = factor_systems(ctx, s, n, d_mx, flags, d_piv, d_piv + (size_t)n * nsys, 1e-14, true);
+  if (fr.rc) return fr.rc;  // kDeclined (an I - c^2 B^2 failed the certificate) or a CUDA error
+  form_rhs_kernel<<<dim3(grid_for(s.stride()), nsys), 256, 0, ctx->stream>>>(B2, n, nn, n, s.np, s.np, n, batch, d_c2,
+                                                                             nullptr, 1, nullptr, R, s.stride());
+  ctx->launches++;
+  trsm_left_lower(ctx, s, 0, s.np, R, s.np, s.stride(), s.np);
+  trsm_left_upper(ctx, s, 0, s.np, R, s.np, s.stride(), s.np);
+  std::vector<int> tz(npairs);
+  for (int q = 0; q < npairs; ++q) tz[q] = q;
+  int* d_tz = upload(ctx, kWsSmallArrays + 2, tz);
+  for (int q = 0; q < m->n_sets; ++q) {
+    std::vector<double> wa(npairs), wb(npairs);
+    double consta = 0.0;
+    for (int t = 0; t < npairs; ++t) {
+      const double wp = m->weights[q * m->n_terms + ip[t]], wm = m->weights[q * m->n_terms + im[t]];
+      wa[t] = (wp - wm) * c[t];
+      wb[t] = wp + wm;
+      consta += wa[t];
+    }
+    double* d_wa = upload(ctx, kWsSmallArrays + 3 + 2 * q, wa);
+    double* d_wb = upload(ctx, kWsSmallArrays + 28 + q, wb);
+    // E_B into the output, E_A into T, then out = E_A B + E_B + a0 I
+    accumulate_kernel<<<dim3(grid_for(nn), batch), 256, 0, ctx->stream>>>(
+        R, s.np, s.stride(), n, n, batch, npairs, d_tz, d_wb, 0, 0.0, 0.0, 0.0, nullptr, 0, 0, nullptr, nullptr, 0, 0,
+        outs[q], ldo, strideOut);
+    accumulate_kernel<<<dim3(grid_for(nn), batch), 256, 0, ctx->stream>>>(
+        R, s.np, s.stride(), n, n, batch, npairs, d_tz, d_wa, 1, consta, 0.0, 0.0, nullptr, 0, 0, nullptr, nullptr, 0,
+        0, T, n, nn);
+    ctx->launches += 2;
+    gemm(ctx, n, n, n, batch, 1.0, T, n, nn, Bs, n, nn, 1.0, outs[q], ldo, strideOut, m->constant[q]);
+  }
+  return cuda_fail(cudaGetLastError());
+}
+
 int large_eval(pf_context* ctx, const pf_method* m, int n, int batch, const double* A, int64_t lda, int64_t strideA,
                const int* dJ, double* const* outs, int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
   if (status) std::memset(status, 0, sizeof(*status));
   if (batch == 0 || n == 0) return PF_OK;
+  {
+    const int rc = large_eval_pairs(ctx, m, n, batch, A, lda, strideA, dJ, outs, ldo, strideOut, flags, status);
+    if (rc != kDeclined) return rc;
+    if (status) std::memset(status, 0, sizeof(*status));
+  }
   std::vector<int> nz;
   for (int i = 0; i < m->n_terms; ++i)
     if (m->shifts[i] != 0.0) nz.push_back(i);

@@ -8,8 +8,13 @@
     fast           each rank sums its own weighted terms; NCCL reduce / all-reduce (sum) -- the
                    addition order depends on G, like any NCCL sum;
     deterministic  each rank ships its weighted terms; every term is then added in ascending shift
-                   index (pf_ordered_sum), which reproduces the single-GPU result bit for bit -- the
-                   reference's "bit-identical for any worker count" contract (dense.hpp:64-68).
+                   index (pf_ordered_sum), which reproduces the single-GPU per-shift evaluation
+                   (PF_FLAG_PER_SHIFT) bit for bit for any G -- the reference's "bit-identical for
+                   any worker count" contract (dense.hpp:64-68). The default single-GPU evaluation
+                   merges (c, -c) shift pairs into one solve (faster, equal up to rounding), so it
+                   is not the deterministic mode's bit-level reference.
+  Units are (c, -c) pairs when the method's nonzero shifts pair up (every frac4/frac8 set), single
+  terms otherwise, so that a rank evaluates whole pairs in the fast mode.
   The polynomial / constant part is added once, and the doubling recurrence runs on the root after
   the reduce ("NCCL-reduce the weighted results over NVLink before squaring").
 * Batched configs (cfg2, cfg5): independent matrices, sharded by batch with no data-path collective
@@ -34,8 +39,27 @@ def term_indices(method: FractionMethod, form: int) -> List[int]:
     return [i for i, c in enumerate(method.shifts) if c != 0 or form == PLAIN]
 
 
+def term_units(method: FractionMethod, form: int) -> List[List[int]]:
+    """Partition units: (c, -c) shift pairs (residual form, every nonzero shift paired), else terms."""
+    terms = term_indices(method, form)
+    sh = method.shift_doubles()
+    if form == RESIDUAL and terms:
+        units, used = [], set()
+        for i in terms:
+            if i in used:
+                continue
+            j = next((k for k in terms if k > i and k not in used and sh[k] == -sh[i]), None)
+            if j is None:
+                break
+            used.update((i, j))
+            units.append([i, j])
+        else:
+            return units
+    return [[i] for i in terms]
+
+
 def owned_terms(method: FractionMethod, form: int, rank: int, world: int) -> List[int]:
-    return [i for p, i in enumerate(term_indices(method, form)) if p % world == rank]
+    return sorted(i for u, unit in enumerate(term_units(method, form)) if u % world == rank for i in unit)
 
 
 class CudaBackend:

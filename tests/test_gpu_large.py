@@ -145,3 +145,26 @@ def test_dense_lu_api(dev, oracle):
         rhs = rand(n, 5, 1.0)[:, :7]
         x = lu.solve_matrix(rhs)
         assert oracle.rel_diff_1norm(x, oracle.lu_solve_matrix(rlu, rpiv, rhs)) <= 1e-12
+
+
+def test_large_pair_mode_and_decline(dev, oracle):
+    """(c, -c) pair merging on the large path: equal to the per-shift evaluation to rounding when
+    every I -/+ cB is certified; bit-identical to the per-shift path when it declines (a matrix whose
+    shifted systems are not diagonally dominant); a mixed batch equals per-matrix evaluation."""
+    from paper_2210_03714_b200 import _native as N, methods as M
+
+    m = M.catalog("R8")
+    good = rand(200, 31, 0.09)  # ||B||_1 small: every I -/+ cB certified -> pair path
+    bad = rand(200, 32, 80.0)   # not dominant -> declined (and pivoting per shift)
+    opts = dev.EvalOptions(form=1)
+    pg = dev.eval_dense(m, good, opts)
+    sg = dev.eval_dense(m, good, opts, flags=N.PF_FLAG_PER_SHIFT)
+    ref = oracle.eval_dense(oracle.OMethod.from_method(m, 1), good)
+    assert oracle.rel_diff_1norm(pg, ref) <= TOL and oracle.rel_diff_1norm(sg, ref) <= TOL
+    assert not np.array_equal(np.asarray(pg), np.asarray(sg))  # the pair path really ran
+    pb = dev.eval_dense(m, bad, opts)
+    sb = dev.eval_dense(m, bad, opts, flags=N.PF_FLAG_PER_SHIFT)
+    assert np.array_equal(np.asarray(pb), np.asarray(sb))
+    both = dev.eval_dense(m, np.stack([good, bad]), opts)
+    assert np.array_equal(np.asarray(both[0]), np.asarray(pg))
+    assert np.array_equal(np.asarray(both[1]), np.asarray(pb))

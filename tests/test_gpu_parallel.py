@@ -33,9 +33,16 @@ def test_emulated_shift_partition_is_bit_identical(dev, n, world):
     A = _a(n, 9, 6.0)
     be = P.CudaBackend()
     j = be.squarings(A, M.THETA_U53["R8_phi1set"])
-    # single GPU, all shifts in one call
+    # single GPU, all shifts in one call, per-shift evaluation (the deterministic mode's reference;
+    # the default merges (c, -c) pairs into one solve)
+    from paper_2210_03714_b200 import _native as N
+
     full = dev.eval_dense_raw(A, m.shift_doubles(), [m.weight_doubles(), phi.weight_doubles()],
-                              [1.0, 1.0], M.RESIDUAL, squarings=j)
+                              [1.0, 1.0], M.RESIDUAL, squarings=j, flags=N.PF_FLAG_PER_SHIFT)
+    paired = dev.eval_dense_raw(A, m.shift_doubles(), [m.weight_doubles(), phi.weight_doubles()],
+                                [1.0, 1.0], M.RESIDUAL, squarings=j)
+    for s in range(2):  # the pair path agrees to rounding
+        assert float((paired[s] - full[s]).abs().sum(0).max()) <= 1e-12 * float(full[s].abs().sum(0).max())
     # every rank's terms, gathered and summed in ascending shift order
     terms = {}
     for r in range(world):
@@ -53,9 +60,11 @@ def test_emulated_shift_partition_is_bit_identical(dev, n, world):
 def test_sharded_world1_matches_expm_phi1(dev):
     from paper_2210_03714_b200 import parallel as P
 
+    from paper_2210_03714_b200 import _native as N
+
     A = _a(96, 4, 5.0)
     E, Phi = P.expm_phi1_sharded(A, "R8", deterministic=True)
-    E2, Phi2 = dev.expm_phi1(A, "R8")
+    E2, Phi2 = dev.expm_phi1(A, "R8", flags=N.PF_FLAG_PER_SHIFT)
     assert torch.equal(E, E2) and torch.equal(Phi, Phi2)
     Ef, Phif = P.expm_phi1_sharded(A, "R8", deterministic=False)
     assert float((Ef - E2).abs().max()) <= 1e-13 * float(E2.abs().max())

@@ -155,9 +155,14 @@ def test_term_partition():
     m = M.catalog("R8")
     assert P.term_indices(m, M.RESIDUAL) == list(range(1, 9))
     assert P.term_indices(m, M.PLAIN) == list(range(9))
+    # residual R8: the units are the (c, -c) pairs (1,2) (3,4) (5,6) (7,8), pair u -> rank u mod G
+    assert P.term_units(m, M.RESIDUAL) == [[1, 2], [3, 4], [5, 6], [7, 8]]
     parts = [P.owned_terms(m, M.RESIDUAL, r, 3) for r in range(3)]
     assert sorted(sum(parts, [])) == list(range(1, 9))
-    assert parts[0] == [1, 4, 7]
+    assert parts == [[1, 2, 7, 8], [3, 4], [5, 6]]
+    # plain form: single terms (the zero shift is a term)
+    assert P.term_units(m, M.PLAIN) == [[i] for i in range(9)]
+    assert P.owned_terms(m, M.PLAIN, 0, 3) == [0, 3, 6]
 
 
 def test_sharded_eval_deterministic_is_bit_identical():
