@@ -412,14 +412,12 @@ bool make_sys(pf_context* ctx, Sys& s, int n, int nsys, int slotM) {
 // half the LUs and solves of the per-shift path, plus B^2 and one product per weight set. Taken only
 // when the reference's own systems I -/+ c B are certified for every pair (the reference would not
 // pivot and raises nothing) and every I - c^2 B^2 passes the certificate; otherwise kDeclined.
-int large_eval_pairs(pf_context* ctx, const pf_method* m, int n, int batch, const double* A, int64_t lda,
-                     int64_t strideA, const int* dJ, double* const* outs, int64_t ldo, int64_t strideOut, int flags,
-                     pf_status* status) {
+// Pairs (c, -c) of a residual-form method without poly part: c of the first, indices of both;
+// false when pair mode does not apply (or PF_NO_PAIRS / PF_FLAG_PER_SHIFT / PF_FLAG_FORCE_PIVOT).
+bool plan_pairs(const pf_method* m, int flags, std::vector<double>& c, std::vector<int>& ip, std::vector<int>& im) {
   static const bool no_pairs = std::getenv("PF_NO_PAIRS") != nullptr;
   if (no_pairs || m->form != PF_FORM_RESIDUAL || m->has_poly || (flags & (PF_FLAG_FORCE_PIVOT | PF_FLAG_PER_SHIFT)))
-    return kDeclined;
-  std::vector<double> c;
-  std::vector<int> ip, im;
+    return false;
   std::vector<char> used(m->n_terms, 0);
   for (int i = 0; i < m->n_terms; ++i) {
     if (used[i] || m->shifts[i] == 0.0) continue;
@@ -429,36 +427,56 @@ int large_eval_pairs(pf_context* ctx, const pf_method* m, int n, int batch, cons
         jp = j;
         break;
       }
-    if (jp < 0) return kDeclined;
+    if (jp < 0) return false;
     used[i] = used[jp] = 1;
     c.push_back(m->shifts[i]);
     ip.push_back(i);
     im.push_back(jp);
   }
-  const int npairs = (int)c.size();
-  if (npairs == 0) return kDeclined;
-  const int64_t nn = (int64_t)n * n;
-  double* Bs = static_cast<double*>(workspace(ctx, kWsPairB, sizeof(double) * nn * batch));
-  double* B2 = static_cast<double*>(workspace(ctx, kWsPairB2, sizeof(double) * nn * batch));
-  double* T = static_cast<double*>(workspace(ctx, kWsPairT, sizeof(double) * nn * batch));
+  return !c.empty();
+}
+
+// ok[b] = every I -/+ c_p B_b certified (B_b = B + b * strideB, n x n of leading dimension ld)
+int pair_certificates(pf_context* ctx, const double* B, int64_t ld, int64_t strideB, int n, int batch,
+                      const std::vector<double>& c, std::vector<int>& ok) {
   const int nchunks = std::max(1, std::min(64, n / 64));
   const int chunk = (n + nchunks - 1) / nchunks;
   double* d_part = static_cast<double*>(workspace(ctx, kWsSmallArrays + 24, sizeof(double) * (size_t)batch * nchunks * n));
   auto* d_bmax = static_cast<unsigned long long*>(workspace(ctx, kWsSmallArrays + 25, sizeof(unsigned long long) * batch));
   int* d_ok = static_cast<int*>(workspace(ctx, kWsSmallArrays + 26, sizeof(int) * batch));
   double* d_c = upload(ctx, kWsSmallArrays + 27, c);
-  if (!Bs || !B2 || !T || !d_part || !d_bmax || !d_ok || !d_c) return PF_ERR_CUDA;
-  launch_ldexp_batched(n, batch, A, lda, strideA, dJ, Bs, n, nn, ctx->stream);
+  if (!d_part || !d_bmax || !d_ok || !d_c) return PF_ERR_CUDA;
   cudaMemsetAsync(d_bmax, 0, sizeof(unsigned long long) * batch, ctx->stream);
   fill_int_kernel<<<(batch + 255) / 256, 256, 0, ctx->stream>>>(d_ok, batch, 1);
-  colstat_partial_kernel<<<dim3((n + 255) / 256, nchunks, batch), 256, 0, ctx->stream>>>(Bs, n, nn, n, chunk, d_part,
-                                                                                        d_bmax);
-  pair_certificate_kernel<<<dim3((n + 255) / 256, batch), 256, 0, ctx->stream>>>(Bs, n, nn, n, nchunks, d_part, d_bmax,
-                                                                                 d_c, npairs, 1e-14, d_ok);
-  ctx->launches += 4;
-  std::vector<int> ok(batch);
+  colstat_partial_kernel<<<dim3((n + 255) / 256, nchunks, batch), 256, 0, ctx->stream>>>(B, ld, strideB, n, chunk,
+                                                                                        d_part, d_bmax);
+  pair_certificate_kernel<<<dim3((n + 255) / 256, batch), 256, 0, ctx->stream>>>(
+      B, ld, strideB, n, nchunks, d_part, d_bmax, d_c, (int)c.size(), 1e-14, d_ok);
+  ctx->launches += 3;
+  ok.assign(batch, 0);
   cudaMemcpyAsync(ok.data(), d_ok, sizeof(int) * batch, cudaMemcpyDeviceToHost, ctx->stream);
-  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return PF_ERR_CUDA;
+  return cudaStreamSynchronize(ctx->stream) == cudaSuccess ? PF_OK : PF_ERR_CUDA;
+}
+
+int large_eval_pairs(pf_context* ctx, const pf_method* m, int n, int batch, const double* A, int64_t lda,
+                     int64_t strideA, const int* dJ, double* const* outs, int64_t ldo, int64_t strideOut, int flags,
+                     pf_status* status) {
+  std::vector<double> c;
+  std::vector<int> ip, im;
+  if (!plan_pairs(m, flags, c, ip, im)) return kDeclined;
+  const int npairs = (int)c.size();
+  const int64_t nn = (int64_t)n * n;
+  double* Bs = static_cast<double*>(workspace(ctx, kWsPairB, sizeof(double) * nn * batch));
+  double* B2 = static_cast<double*>(workspace(ctx, kWsPairB2, sizeof(double) * nn * batch));
+  double* T = static_cast<double*>(workspace(ctx, kWsPairT, sizeof(double) * nn * batch));
+  if (!Bs || !B2 || !T) return PF_ERR_CUDA;
+  launch_ldexp_batched(n, batch, A, lda, strideA, dJ, Bs, n, nn, ctx->stream);
+  ctx->launches++;
+  std::vector<int> ok;
+  {
+    const int rc = pair_certificates(ctx, Bs, n, nn, n, batch, c, ok);
+    if (rc) return rc;
+  }
   int nok = 0;
   for (int v : ok) nok += v ? 1 : 0;
   if (nok == 0) return kDeclined;
@@ -616,9 +634,99 @@ int large_eval(pf_context* ctx, const pf_method* m, int n, int batch, const doub
 }
 
 // ---------------------------------------------------------------------------------------------
+// Block action in pair mode (see large_eval_pairs): B = A / N; every pair's system I - c^2 B^2 is
+// factored once; per substep Y_p = (I - c_p^2 B^2)^-1 (c_p B X) for all pairs in one batched solve,
+// U = a0 X + sum_p cm_p Y_p, V = sum_p cp_p c_p Y_p, and X <- U + B V (one extra n^2 k product per
+// substep instead of the second solve of every pair).
+int large_action_pairs(pf_context* ctx, const pf_method* m, int n, int k, const double* A, int64_t lda,
+                       const double* V, int64_t ldv, int substeps, double* out, int64_t ldo, int flags) {
+  std::vector<double> c;
+  std::vector<int> ip, im;
+  if (!plan_pairs(m, flags, c, ip, im)) return kDeclined;
+  const int npairs = (int)c.size();
+  const int np = round64(n);
+  const int64_t st = (int64_t)np * np;
+  double* Bp = static_cast<double*>(workspace(ctx, kWsLargeB, sizeof(double) * st));
+  if (!Bp) return PF_ERR_CUDA;
+  scale_pad_kernel<<<grid_for(st), 256, 0, ctx->stream>>>(A, lda, n, np, 1.0 / substeps, Bp);
+  ctx->launches++;
+  std::vector<int> ok;
+  {
+    const int rc = pair_certificates(ctx, Bp, np, 0, n, 1, c, ok);
+    if (rc) return rc;
+    if (!ok[0]) return kDeclined;
+  }
+  double* B2 = static_cast<double*>(workspace(ctx, kWsPairB2, sizeof(double) * st));
+  if (!B2) return PF_ERR_CUDA;
+  gemm(ctx, np, np, np, 1, 1.0, Bp, np, 0, Bp, np, 0, 0.0, B2, np, 0, 0.0);
+  Sys s;
+  if (!make_sys(ctx, s, n, npairs, kWsLargeM)) return PF_ERR_CUDA;
+  const size_t blk = (size_t)np * k;
+  double* R = static_cast<double*>(workspace(ctx, kWsLargeR, sizeof(double) * blk * npairs));
+  double* X = static_cast<double*>(workspace(ctx, kWsT1, sizeof(double) * blk * 4));
+  auto* d_mx = static_cast<unsigned long long*>(workspace(ctx, kWsLargeAux, sizeof(unsigned long long) * npairs));
+  int* d_piv = static_cast<int*>(workspace(ctx, kWsLargePiv, sizeof(int) * (size_t)n * npairs * 2));
+  if (!R || !X || !d_mx || !d_piv) return PF_ERR_CUDA;
+  std::vector<double> c2(npairs);
+  for (int q = 0; q < npairs; ++q) c2[q] = c[q] * c[q];
+  double* d_c2 = upload(ctx, kWsSmallArrays + 1, c2);
+  double* d_c = upload(ctx, kWsSmallArrays + 4, c);
+  cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long) * npairs, ctx->stream);
+  form_shifted_kernel<<<dim3(grid_for(st), npairs), 256, 0, ctx->stream>>>(B2, np, 0, n, np, 1, d_c2, nullptr, s.M,
+                                                                           d_mx);
+  ctx->launches++;
+  FactorResult fr = factor_systems(ctx, s, n, d_mx, flags, d_piv, d_piv + (size_t)n * npairs, 1e-14, true);
+  if (fr.rc) return fr.rc;  // kDeclined or a CUDA error
+  const int nb = big_block(np);
+  double* binv = nullptr;
+  if (nb) {
+    binv = static_cast<double*>(workspace(ctx, kWsLargeBinv, sizeof(double) * big_inverse_stride(np, nb) * npairs));
+    if (!binv || !build_big_inverses(ctx, s, nb, binv)) return PF_ERR_CUDA;
+  }
+  double* BX = X + blk;
+  double* Vs = X + 2 * blk;
+  double* Xn = X + 3 * blk;
+  cudaMemsetAsync(X, 0, sizeof(double) * blk * 4, ctx->stream);  // padding rows stay zero
+  copy2d_kernel<<<dim3(grid_for((int64_t)n * k), 1), 256, 0, ctx->stream>>>(n, k, 1.0, V, ldv, 0, X, k, 0);
+  ctx->launches++;
+  std::vector<int> tz(npairs);
+  std::vector<double> wu(npairs), wv(npairs);
+  for (int q = 0; q < npairs; ++q) {
+    tz[q] = q;
+    const double wp = m->weights[ip[q]], wm = m->weights[im[q]];
+    wu[q] = wp - wm;
+    wv[q] = (wp + wm) * c[q];
+  }
+  int* d_tz = upload(ctx, kWsSmallArrays + 2, tz);
+  double* d_wu = upload(ctx, kWsSmallArrays + 3, wu);
+  double* d_wv = upload(ctx, kWsSmallArrays + 5, wv);
+  for (int step = 0; step < substeps; ++step) {
+    gemm(ctx, np, k, np, 1, 1.0, Bp, np, 0, X, k, 0, 0.0, BX, k, 0, 0.0);
+    form_rhs_kernel<<<dim3(grid_for((int64_t)blk), npairs), 256, 0, ctx->stream>>>(BX, k, 0, n, np, k, k, 1, d_c, nullptr,
+                                                                                  1, nullptr, R, (int64_t)blk);
+    ctx->launches++;
+    const int rc = solve_lu(ctx, s, binv, nb, R, k, (int64_t)blk);
+    if (rc) return rc;
+    action_accumulate_kernel<<<grid_for((int64_t)n * k), 256, 0, ctx->stream>>>(
+        R, k, (int64_t)blk, X, k, n, k, npairs, d_tz, d_wu, 1, m->constant[0], 0, 0.0, 0.0, nullptr, nullptr, Xn, k);
+    action_accumulate_kernel<<<grid_for((int64_t)n * k), 256, 0, ctx->stream>>>(
+        R, k, (int64_t)blk, X, k, n, k, npairs, d_tz, d_wv, 0, 0.0, 0, 0.0, 0.0, nullptr, nullptr, Vs, k);
+    ctx->launches += 2;
+    gemm(ctx, np, k, np, 1, 1.0, Bp, np, 0, Vs, k, 0, 1.0, Xn, k, 0, 0.0);  // X <- a0 X + U + B V
+    std::swap(X, Xn);
+  }
+  copy2d_kernel<<<dim3(grid_for((int64_t)n * k), 1), 256, 0, ctx->stream>>>(n, k, 1.0, X, k, 0, out, ldo, 0);
+  ctx->launches++;
+  return cuda_fail(cudaGetLastError());
+}
+
 int large_action(pf_context* ctx, const pf_method* m, int n, int k, const double* A, int64_t lda, const double* V,
                  int64_t ldv, int substeps, double* out, int64_t ldo, int flags, pf_status* status) {
   if (status) std::memset(status, 0, sizeof(*status));
+  {
+    const int rc = large_action_pairs(ctx, m, n, k, A, lda, V, ldv, substeps, out, ldo, flags);
+    if (rc != kDeclined) return rc;
+  }
   std::vector<int> nz;
   for (int i = 0; i < m->n_terms; ++i)
     if (m->shifts[i] != 0.0) nz.push_back(i);
@@ -674,8 +782,9 @@ int large_action(pf_context* ctx, const pf_method* m, int n, int k, const double
     binv = static_cast<double*>(workspace(ctx, kWsLargeBinv, sizeof(double) * big_inverse_stride(np, nb) * P));
     if (!binv || !build_big_inverses(ctx, s, nb, binv)) return PF_ERR_CUDA;
   }
-  // X = V (padded rows are zero)
+  // X = V (padded rows are zero, in both iterate buffers)
   cudaMemsetAsync(X, 0, sizeof(double) * blk, ctx->stream);
+  cudaMemsetAsync(Xn, 0, sizeof(double) * blk, ctx->stream);
   copy2d_kernel<<<dim3(grid_for((int64_t)n * k), 1), 256, 0, ctx->stream>>>(n, k, 1.0, V, ldv, 0, X, k, 0);
   ctx->launches++;
   std::vector<int> tz;

@@ -79,7 +79,13 @@ def test_action_operator_and_partition(dev, n):
     A = torch.from_numpy(a).cuda()
     V = torch.from_numpy(W.randn(41, n * 4).reshape(n, 4)).cuda()
     nsub = 5
-    ref = dev.action(A, V, "R8", substeps=nsub)
+    from paper_2210_03714_b200 import _native as N
+
+    # the deterministic partition reproduces the per-shift evaluation; the default pf_action_block
+    # merges (c, -c) pairs (equal to rounding)
+    ref = dev.action(A, V, "R8", substeps=nsub, flags=N.PF_FLAG_PER_SHIFT)
+    paired = dev.action(A, V, "R8", substeps=nsub)
+    assert float((paired - ref).abs().sum(0).max()) <= 1e-12 * float(ref.abs().sum(0).max())
     # one operator owning everything == pf_action_block
     X = P.action_sharded(A, V, "R8", nsub, M.RESIDUAL, deterministic=True)
     assert torch.equal(X, ref)
