@@ -1,3 +1,4 @@
+#include <algorithm>
 // K6 and elementwise helpers: batched 1-norm, squaring-count selection, exact 2^-j scaling,
 // Y = alpha X + diag I. HBM-bound; one thread per column / element, coalesced along rows.
 #include "pf_common.cuh"
@@ -87,6 +88,20 @@ void launch_ldexp_batched(int n, int batch, const double* X, int64_t ldx, int64_
   if (blocks > 1184) blocks = 1184;
   dim3 grid(blocks, batch);
   ldexp_kernel<<<grid, 256, 0, stream>>>(n, X, ldx, strideX, j, Y, ldy, strideY);
+}
+
+// D = C - S, E = C + S (the cos/sin double-angle step as (C - S)(C + S), see pf_cossin_batched)
+__global__ void sum_diff_kernel(int64_t count, const double* C, const double* S, double* D, double* E) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const double c = C[i], s = S[i];
+    D[i] = c - s;
+    E[i] = c + s;
+  }
+}
+
+void launch_sum_diff(int64_t count, const double* C, const double* S, double* D, double* E, cudaStream_t stream) {
+  const int64_t blocks = std::min<int64_t>((count + 255) / 256, 4736);
+  sum_diff_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, stream>>>(count, C, S, D, E);
 }
 
 }  // namespace pf

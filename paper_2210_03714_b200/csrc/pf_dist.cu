@@ -151,10 +151,16 @@ int pf_cossin_doubling(pf_context* ctx, int n, int batch, const int* dJ, double*
   if (rc) return rc;
   cudaMemcpyAsync(C, dC, bytes, cudaMemcpyDeviceToDevice, ctx->stream);
   cudaMemcpyAsync(S, dS, bytes, cudaMemcpyDeviceToDevice, ctx->stream);
-  // C <- C C - S S ; S <- 2 (S C)
+  // C <- C C - S S = (C - S)(C + S) ; S <- 2 (S C)  (same steps as pf_cossin_batched)
+  // double angle: C <- C^2 - S^2 = (C - S)(C + S) (C and S are functions of the same matrix, so they
+  // commute), S <- 2 S C: two GEMMs per step instead of three; matrices past their own j pass through
+  double* D = jmax > 0 ? static_cast<double*>(workspace(ctx, kWsPairB, sizeof(double) * nn * batch)) : nullptr;
+  double* Ep = jmax > 0 ? static_cast<double*>(workspace(ctx, kWsPairT, sizeof(double) * nn * batch)) : nullptr;
+  if (jmax > 0 && (!D || !Ep)) return PF_ERR_CUDA;
   for (int s = 0; s < jmax; ++s) {
-    gemm(ctx, n, n, n, batch, 1.0, C, n, nn, C, n, nn, 0.0, C2, n, nn, 0.0, dJ, s, C);
-    gemm(ctx, n, n, n, batch, -1.0, S, n, nn, S, n, nn, 1.0, C2, n, nn, 0.0, dJ, s, nullptr);
+    pf::launch_sum_diff(nn * batch, C, S, D, Ep, ctx->stream);
+    ctx->launches++;
+    gemm(ctx, n, n, n, batch, 1.0, D, n, nn, Ep, n, nn, 0.0, C2, n, nn, 0.0, dJ, s, C);
     gemm(ctx, n, n, n, batch, 2.0, S, n, nn, C, n, nn, 0.0, Sp, n, nn, 0.0, dJ, s, S);
     std::swap(C, C2);
     std::swap(S, Sp);

@@ -64,6 +64,13 @@ constexpr int kB = 64;
 
 int round64(int n) { return ((n + kB - 1) / kB) * kB; }
 unsigned grid_for(int64_t elems) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((elems + 255) / 256, 1184)); }
+// blocks per matrix for an elementwise kernel over `count` matrices (grid.y): about 2 x 1184 CTAs in
+// total (one block per matrix for big batches: cfg5 forms 1024 systems, and 1024 blocks per system
+// issued 8M atomics on 1024 addresses -- 5.6 ms for a 2.5 GB pass)
+unsigned grid2(int64_t elems, int count) {
+  const int64_t per = std::max<int64_t>(1, (2368 + count - 1) / std::max(count, 1));
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((elems + 255) / 256, std::min<int64_t>(per, 1184)));
+}
 
 // A batch of nsys systems of order np (row-major, stride np^2) plus their diagonal-block inverses.
 struct Sys {
@@ -291,7 +298,7 @@ void tri_inv(pf_context* ctx, const Sys& s, bool upper, int off, int b, double* 
              double* tmp, int64_t st) {
   if (b == kB) {
     const double* src = s.inv + (int64_t)(off / kB) * 2 * kB * kB + (upper ? kB * kB : 0);
-    copy2d_kernel<<<dim3(grid_for((int64_t)kB * kB), s.nsys), 256, 0, ctx->stream>>>(kB, kB, 1.0, src, kB,
+    copy2d_kernel<<<dim3(grid2((int64_t)kB * kB, s.nsys), s.nsys), 256, 0, ctx->stream>>>(kB, kB, 1.0, src, kB,
                                                                                       s.inv_stride, dst, ldd, sd);
     ctx->launches++;
     return;
@@ -504,12 +511,12 @@ int large_eval_pairs(pf_context* ctx, const pf_method* m, int n, int batch, cons
   for (int q = 0; q < npairs; ++q) c2[q] = c[q] * c[q];
   double* d_c2 = upload(ctx, kWsSmallArrays + 1, c2);
   cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long) * nsys, ctx->stream);
-  form_shifted_kernel<<<dim3(grid_for(s.stride()), nsys), 256, 0, ctx->stream>>>(B2, n, nn, n, s.np, batch, d_c2,
+  form_shifted_kernel<<<dim3(grid2(s.stride(), nsys), nsys), 256, 0, ctx->stream>>>(B2, n, nn, n, s.np, batch, d_c2,
                                                                                  nullptr, s.M, d_mx);
   ctx->launches++;
   FactorResult fr = factor_systems(ctx, s, n, d_mx, flags, d_piv, d_piv + (size_t)n * nsys, 1e-14, true);
   if (fr.rc) return fr.rc;  // kDeclined (an I - c^2 B^2 failed the certificate) or a CUDA error
-  form_rhs_kernel<<<dim3(grid_for(s.stride()), nsys), 256, 0, ctx->stream>>>(B2, n, nn, n, s.np, s.np, n, batch, d_c2,
+  form_rhs_kernel<<<dim3(grid2(s.stride(), nsys), nsys), 256, 0, ctx->stream>>>(B2, n, nn, n, s.np, s.np, n, batch, d_c2,
                                                                              nullptr, 1, nullptr, R, s.stride());
   ctx->launches++;
   trsm_left_lower(ctx, s, 0, s.np, R, s.np, s.stride(), s.np);
@@ -529,10 +536,10 @@ int large_eval_pairs(pf_context* ctx, const pf_method* m, int n, int batch, cons
     double* d_wa = upload(ctx, kWsSmallArrays + 3 + 2 * q, wa);
     double* d_wb = upload(ctx, kWsSmallArrays + 28 + q, wb);
     // E_B into the output, E_A into T, then out = E_A B + E_B + a0 I
-    accumulate_kernel<<<dim3(grid_for(nn), batch), 256, 0, ctx->stream>>>(
+    accumulate_kernel<<<dim3(grid2(nn, batch), batch), 256, 0, ctx->stream>>>(
         R, s.np, s.stride(), n, n, batch, npairs, d_tz, d_wb, 0, 0.0, 0.0, 0.0, nullptr, 0, 0, nullptr, nullptr, 0, 0,
         outs[q], ldo, strideOut);
-    accumulate_kernel<<<dim3(grid_for(nn), batch), 256, 0, ctx->stream>>>(
+    accumulate_kernel<<<dim3(grid2(nn, batch), batch), 256, 0, ctx->stream>>>(
         R, s.np, s.stride(), n, n, batch, npairs, d_tz, d_wa, 1, consta, 0.0, 0.0, nullptr, 0, 0, nullptr, nullptr, 0,
         0, T, n, nn);
     ctx->launches += 2;
@@ -569,7 +576,7 @@ int large_eval(pf_context* ctx, const pf_method* m, int n, int batch, const doub
   bool pivoted = false;
   if (nsys > 0) {
     cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long) * nsys, ctx->stream);
-    form_shifted_kernel<<<dim3(grid_for(s.stride()), nsys), 256, 0, ctx->stream>>>(A, lda, strideA, n, s.np, batch,
+    form_shifted_kernel<<<dim3(grid2(s.stride(), nsys), nsys), 256, 0, ctx->stream>>>(A, lda, strideA, n, s.np, batch,
                                                                                    d_sh, dJ, s.M, d_mx);
     ctx->launches++;
     FactorResult fr = factor_systems(ctx, s, n, d_mx, flags, d_piv, d_perm, 1e-14);
@@ -587,7 +594,7 @@ int large_eval(pf_context* ctx, const pf_method* m, int n, int batch, const doub
       return fr.rc;
     }
     pivoted = fr.pivoted;
-    form_rhs_kernel<<<dim3(grid_for(s.stride()), nsys), 256, 0, ctx->stream>>>(
+    form_rhs_kernel<<<dim3(grid2(s.stride(), nsys), nsys), 256, 0, ctx->stream>>>(
         A, lda, strideA, n, s.np, s.np, n, batch, d_sh, dJ, residual ? 1 : 0, pivoted ? d_perm : nullptr, R,
         s.stride());
     ctx->launches++;
@@ -625,7 +632,7 @@ int large_eval(pf_context* ctx, const pf_method* m, int n, int batch, const doub
     const bool add_poly = residual || m->has_poly;
     const double constant = residual ? m->constant[q] : (m->has_poly ? m->poly[3 * q] : 0.0);
     const double d1 = m->has_poly ? m->poly[3 * q + 1] : 0.0, d2 = m->has_poly ? m->poly[3 * q + 2] : 0.0;
-    accumulate_kernel<<<dim3(grid_for((int64_t)n * n), batch), 256, 0, ctx->stream>>>(
+    accumulate_kernel<<<dim3(grid2((int64_t)n * n, batch), batch), 256, 0, ctx->stream>>>(
         R, s.np, s.stride(), n, n, batch, (int)tz.size(), d_tz, d_w, add_poly ? 1 : 0, constant, d1, d2, A, lda,
         strideA, dJ, B2, n, (int64_t)n * n, outs[q], ldo, strideOut);
     ctx->launches++;
@@ -672,7 +679,7 @@ int large_action_pairs(pf_context* ctx, const pf_method* m, int n, int k, const 
   double* d_c2 = upload(ctx, kWsSmallArrays + 1, c2);
   double* d_c = upload(ctx, kWsSmallArrays + 4, c);
   cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long) * npairs, ctx->stream);
-  form_shifted_kernel<<<dim3(grid_for(st), npairs), 256, 0, ctx->stream>>>(B2, np, 0, n, np, 1, d_c2, nullptr, s.M,
+  form_shifted_kernel<<<dim3(grid2(st, npairs), npairs), 256, 0, ctx->stream>>>(B2, np, 0, n, np, 1, d_c2, nullptr, s.M,
                                                                            d_mx);
   ctx->launches++;
   FactorResult fr = factor_systems(ctx, s, n, d_mx, flags, d_piv, d_piv + (size_t)n * npairs, 1e-14, true);
@@ -702,7 +709,7 @@ int large_action_pairs(pf_context* ctx, const pf_method* m, int n, int k, const 
   double* d_wv = upload(ctx, kWsSmallArrays + 5, wv);
   for (int step = 0; step < substeps; ++step) {
     gemm(ctx, np, k, np, 1, 1.0, Bp, np, 0, X, k, 0, 0.0, BX, k, 0, 0.0);
-    form_rhs_kernel<<<dim3(grid_for((int64_t)blk), npairs), 256, 0, ctx->stream>>>(BX, k, 0, n, np, k, k, 1, d_c, nullptr,
+    form_rhs_kernel<<<dim3(grid2((int64_t)blk, npairs), npairs), 256, 0, ctx->stream>>>(BX, k, 0, n, np, k, k, 1, d_c, nullptr,
                                                                                   1, nullptr, R, (int64_t)blk);
     ctx->launches++;
     const int rc = solve_lu(ctx, s, binv, nb, R, k, (int64_t)blk);
@@ -757,7 +764,7 @@ int large_action(pf_context* ctx, const pf_method* m, int n, int k, const double
   bool pivoted = false;
   if (P > 0) {
     cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long) * P, ctx->stream);
-    form_shifted_kernel<<<dim3(grid_for(s.stride()), P), 256, 0, ctx->stream>>>(Bp, np, 0, n, np, 1, d_sh, nullptr,
+    form_shifted_kernel<<<dim3(grid2(s.stride(), P), P), 256, 0, ctx->stream>>>(Bp, np, 0, n, np, 1, d_sh, nullptr,
                                                                                s.M, d_mx);
     ctx->launches++;
     FactorResult fr = factor_systems(ctx, s, n, d_mx, flags, d_piv, d_perm, 1e-14);
@@ -813,7 +820,7 @@ int large_action(pf_context* ctx, const pf_method* m, int n, int k, const double
     if (P > 0) {
       // R_i = c_i B X (residual, action.cpp:252-258) or X (plain), rows permuted when pivoted
       // R_i = c_i (B X) (residual) or 1 * X (plain; unit "shift" table), rows permuted when pivoted
-      form_rhs_kernel<<<dim3(grid_for((int64_t)blk), P), 256, 0, ctx->stream>>>(
+      form_rhs_kernel<<<dim3(grid2((int64_t)blk, P), P), 256, 0, ctx->stream>>>(
           residual ? BX : X, k, 0, n, np, k, k, 1, residual ? d_sh : d_one, nullptr, 1, pivoted ? d_perm : nullptr, R,
           (int64_t)blk);
       ctx->launches++;
@@ -843,7 +850,7 @@ int large_lu_factor(pf_context* ctx, int n, int batch, double* A, int64_t lda, i
   if (!d_mx || !d_piv) return PF_ERR_CUDA;
   int* d_perm = d_piv + (size_t)n * batch;
   cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long) * batch, ctx->stream);
-  load_padded_kernel<<<dim3(grid_for(s.stride()), batch), 256, 0, ctx->stream>>>(A, lda, strideA, n, s.np, s.M, d_mx);
+  load_padded_kernel<<<dim3(grid2(s.stride(), batch), batch), 256, 0, ctx->stream>>>(A, lda, strideA, n, s.np, s.M, d_mx);
   ctx->launches++;
   FactorResult fr = factor_systems(ctx, s, n, d_mx, flags, d_piv, d_perm, pivot_rel_tol);
   if (fr.rc) {
@@ -856,7 +863,7 @@ int large_lu_factor(pf_context* ctx, int n, int batch, double* A, int64_t lda, i
     }
     return fr.rc;
   }
-  copy2d_kernel<<<dim3(grid_for((int64_t)n * n), batch), 256, 0, ctx->stream>>>(n, n, 1.0, s.M, s.np, s.stride(), A, lda,
+  copy2d_kernel<<<dim3(grid2((int64_t)n * n, batch), batch), 256, 0, ctx->stream>>>(n, n, 1.0, s.M, s.np, s.stride(), A, lda,
                                                                                strideA);
   ctx->launches++;
   if (piv) {
@@ -880,20 +887,20 @@ int large_lu_solve(pf_context* ctx, int n, int k, int batch, const double* LU, i
   const size_t blk = (size_t)s.np * k;
   double* X = static_cast<double*>(workspace(ctx, kWsLargeR, sizeof(double) * blk * batch));
   if (!d_mx || !d_perm || !X) return PF_ERR_CUDA;
-  load_padded_kernel<<<dim3(grid_for(s.stride()), batch), 256, 0, ctx->stream>>>(LU, lda, strideLU, n, s.np, s.M, d_mx);
+  load_padded_kernel<<<dim3(grid2(s.stride(), batch), batch), 256, 0, ctx->stream>>>(LU, lda, strideLU, n, s.np, s.M, d_mx);
   perm_from_piv_kernel<<<batch, 32, 0, ctx->stream>>>(piv, n, d_perm, nullptr);
   ctx->launches += 2;
   diag_inverses(ctx, s);
   std::vector<double> ones(batch, 1.0);
   double* d_one = upload(ctx, kWsSmallArrays + 9, ones);
   // X = P R (padded zeros): form_rhs with c = 1, batch 1 per system via z = b (one shift slot)
-  form_rhs_kernel<<<dim3(grid_for((int64_t)blk), batch), 256, 0, ctx->stream>>>(R, ldr, strideR, n, s.np, k, k, batch,
+  form_rhs_kernel<<<dim3(grid2((int64_t)blk, batch), batch), 256, 0, ctx->stream>>>(R, ldr, strideR, n, s.np, k, k, batch,
                                                                                d_one, nullptr, 1, d_perm, X,
                                                                                (int64_t)blk);
   ctx->launches++;
   trsm_left_lower(ctx, s, 0, s.np, X, k, (int64_t)blk, k);
   trsm_left_upper(ctx, s, 0, s.np, X, k, (int64_t)blk, k);
-  copy2d_kernel<<<dim3(grid_for((int64_t)n * k), batch), 256, 0, ctx->stream>>>(n, k, 1.0, X, k, (int64_t)blk, R, ldr,
+  copy2d_kernel<<<dim3(grid2((int64_t)n * k, batch), batch), 256, 0, ctx->stream>>>(n, k, 1.0, X, k, (int64_t)blk, R, ldr,
                                                                                strideR);
   ctx->launches++;
   return cuda_fail(cudaGetLastError());
@@ -958,7 +965,7 @@ int action_op_create(pf_context* ctx, const pf_method* m, int n, const double* A
       return PF_ERR_CUDA;
     }
     cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long) * P, ctx->stream);
-    form_shifted_kernel<<<dim3(grid_for(st), P), 256, 0, ctx->stream>>>(op->B, op->np, 0, n, op->np, 1, op->d_shifts,
+    form_shifted_kernel<<<dim3(grid2(st, P), P), 256, 0, ctx->stream>>>(op->B, op->np, 0, n, op->np, 1, op->d_shifts,
                                                                        nullptr, op->M, d_mx);
     ctx->launches++;
     Sys s{op->M, op->np, P, op->inv, inv_stride};
@@ -1012,7 +1019,7 @@ int action_op_apply(pf_action_op* op, const double* V, int64_t ldv, int k, doubl
   if (op->hybrid) gemm(ctx, np, k, np, 1, 1.0, op->B, np, 0, BX, k, 0, 0.0, B2X, k, 0, 0.0);
   if (P > 0) {
     // R_i = c_i (B X) (residual, action.cpp:252-258) or X (plain), rows permuted when pivoted
-    form_rhs_kernel<<<dim3(grid_for((int64_t)blk), P), 256, 0, ctx->stream>>>(
+    form_rhs_kernel<<<dim3(grid2((int64_t)blk, P), P), 256, 0, ctx->stream>>>(
         residual ? BX : X, k, 0, n, np, k, k, 1, residual ? op->d_shifts : op->d_ones, nullptr, 1,
         op->pivoted ? op->perm : nullptr, R, (int64_t)blk);
     ctx->launches++;
