@@ -84,6 +84,7 @@ enum Slot {
   kWsPairB = 19,        // large pair mode: B = 2^-j A, B^2, E_A
   kWsPairB2 = 21,
   kWsPairT = 22,
+  kWsTriTmp = 26,       // triangular block inversion temporaries
   kWsScratch = 20,      // per-SM accumulator slots of the small kernel
   kWsSmallArrays = 64,  // small uploaded tables: kWsSmallArrays + i, i < 32
 };

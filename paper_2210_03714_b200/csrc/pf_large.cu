@@ -334,7 +334,7 @@ int64_t big_inverse_stride(int np, int nb) { return (int64_t)((np + nb - 1) / nb
 bool build_big_inverses(pf_context* ctx, const Sys& s, int nb, double* binv) {
   const int nblk = (s.np + nb - 1) / nb;
   const int64_t bstride = big_inverse_stride(s.np, nb);
-  double* tmp = static_cast<double*>(workspace(ctx, kWsT2, sizeof(double) * (size_t)(nb / 2) * (nb / 2) * s.nsys));
+  double* tmp = static_cast<double*>(workspace(ctx, kWsTriTmp, sizeof(double) * (size_t)(nb / 2) * (nb / 2) * s.nsys));
   if (!tmp) return false;
   cudaMemsetAsync(binv, 0, sizeof(double) * bstride * s.nsys, ctx->stream);
   for (int q = 0; q < nblk; ++q) {
