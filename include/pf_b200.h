@@ -162,6 +162,30 @@ int pf_action_block(pf_context* ctx, const pf_method* m, int n, int k, const dou
                     const double* dV, int64_t ldv, int substeps, double* dOut, int64_t ldo, int flags,
                     pf_status* status);
 
+/* ---- f2: banded action (proj/core/src/action.cpp). A tridiagonal matrix is three device arrays
+ * sub[d-1], diag[d], super[d-1] (TridiagMatrix, action.hpp:13-24); a block of k vectors is d x k
+ * row-major, and every column is processed with exactly the reference's single-vector operation
+ * sequence (the results are the reference's bits). ZeroPivot (|pivot| <= 1e-300) reports the row in
+ * status->column and, for the action, the 1-based shift in status->shift_index. */
+
+/* Out = A V (TridiagMatrix::matvec, action.cpp:35-44) */
+int pf_tridiag_matvec_batched(pf_context* ctx, int d, int k, const double* dSub, const double* dDiag,
+                              const double* dSuper, const double* dV, int64_t ldv, double* dOut, int64_t ldo);
+/* X = A^-1 R for k right-hand sides (thomas_solve / TridiagFactor, action.cpp:100-141) */
+int pf_thomas_solve_batched(pf_context* ctx, int d, int k, const double* dSub, const double* dDiag,
+                            const double* dSuper, const double* dRhs, int64_t ldr, double* dX, int64_t ldx,
+                            pf_status* status);
+/* X = P^-1 R, P pentadiagonal (pentadiag_solve: banded LU without pivoting, action.cpp:170-202) */
+int pf_pentadiag_solve_batched(pf_context* ctx, int d, int k, const double* dSub2, const double* dSub1,
+                               const double* dDiag, const double* dSuper1, const double* dSuper2,
+                               const double* dRhs, int64_t ldr, double* dX, int64_t ldx, pf_status* status);
+/* substep_action (action.cpp:327-339) on every column of V: A scaled by 1/substeps, every shifted
+ * system I - c_i A factored once (ActionOperator, :300-325), then substeps x (v <- action_eval(m, A,
+ * v)) with assemble_action's ascending-shift sum and polynomial part (:224-284). Weight set 0. */
+int pf_tridiag_action(pf_context* ctx, const pf_method* m, int d, int k, const double* dSub, const double* dDiag,
+                      const double* dSuper, const double* dV, int64_t ldv, int substeps, double* dOut, int64_t ldo,
+                      int flags, pf_status* status);
+
 /* DenseLu: in-place PA = LU (unit lower L below the diagonal, U on and above), LAPACK-style
  * 0-based swap sequence in dPiv (n ints per matrix). SingularShift when the best pivot
  * <= pivot_rel_tol * max(max|a|, 1e-300). */

@@ -253,3 +253,102 @@ def rel_diff_1norm(a, b) -> float:
         d = np.abs(a - b).sum(axis=0).max()
         return float(d / max(np.abs(b).sum(axis=0).max(), 1e-300))
     return one_norm(a - b) / max(one_norm(b), 1e-300)
+
+
+# ---- f2: banded action (pf_oracle_band.c, restating proj/core/src/action.cpp)
+
+class BandError(RuntimeError):
+    """ZeroPivot from the banded solvers: row (and shift index for the action)."""
+
+    def __init__(self, code: int, row: int, shift_index: int = 0):
+        super().__init__("zero pivot at row %d%s" % (row, (" (shift %d)" % shift_index) if shift_index else ""))
+        self.code, self.row, self.shift_index = code, row, shift_index
+
+
+def _cols(x):
+    x = _f64(x)
+    return (x.reshape(-1, 1), True) if x.ndim == 1 else (x, False)
+
+
+def tridiag_matvec(sub, diag, sup, v) -> np.ndarray:
+    sub, diag, sup = _f64(sub), _f64(diag), _f64(sup)
+    V, vec = _cols(v)
+    d, k = V.shape
+    out = np.empty_like(V)
+    col, res = np.empty(d), np.empty(d)
+    for c in range(k):
+        col[:] = V[:, c]
+        lib().pfo_tridiag_matvec(d, _p(sub), _p(diag), _p(sup), _p(col), _p(res))
+        out[:, c] = res
+    return out.reshape(-1) if vec else out
+
+
+def tridiag_one_norm(sub, diag, sup) -> float:
+    lib().pfo_tridiag_one_norm.restype = C.c_double
+    return float(lib().pfo_tridiag_one_norm(len(diag), _p(_f64(sub)), _p(_f64(diag)), _p(_f64(sup))))
+
+
+def thomas_solve(sub, diag, sup, rhs) -> np.ndarray:
+    sub, diag, sup = _f64(sub), _f64(diag), _f64(sup)
+    R, vec = _cols(rhs)
+    d, k = R.shape
+    out = np.empty_like(R)
+    col, x = np.empty(d), np.empty(d)
+    row = C.c_int(0)
+    for c in range(k):
+        col[:] = R[:, c]
+        rc = lib().pfo_thomas_solve(d, _p(sub), _p(diag), _p(sup), _p(col), _p(x), C.byref(row))
+        if rc:
+            raise BandError(rc, row.value)
+        out[:, c] = x
+    return out.reshape(-1) if vec else out
+
+
+def tridiag_factor(sub, diag, sup):
+    """TridiagFactor: (mult, fdiag)."""
+    sub, diag, sup = _f64(sub), _f64(diag), _f64(sup)
+    d = len(diag)
+    mult, fd = np.empty(max(d - 1, 1)), np.empty(d)
+    row = C.c_int(0)
+    rc = lib().pfo_tridiag_factor(d, _p(sub), _p(diag), _p(sup), _p(mult), _p(fd), C.byref(row))
+    if rc:
+        raise BandError(rc, row.value)
+    return mult, fd
+
+
+def tridiag_factor_solve(mult, fd, sup, rhs) -> np.ndarray:
+    rhs = _f64(rhs)
+    x = np.empty_like(rhs)
+    lib().pfo_tridiag_factor_solve(len(fd), _p(_f64(mult)), _p(_f64(fd)), _p(_f64(sup)), _p(rhs), _p(x))
+    return x
+
+
+def pentadiag_solve(sub2, sub1, diag, super1, super2, rhs) -> np.ndarray:
+    bands = [_f64(b) for b in (sub2, sub1, diag, super1, super2)]
+    R, vec = _cols(rhs)
+    d, k = R.shape
+    out = np.empty_like(R)
+    col, x = np.empty(d), np.empty(d)
+    row = C.c_int(0)
+    for c in range(k):
+        col[:] = R[:, c]
+        rc = lib().pfo_pentadiag_solve(d, *[_p(b) for b in bands], _p(col), _p(x), C.byref(row))
+        if rc:
+            raise BandError(rc, row.value)
+        out[:, c] = x
+    return out.reshape(-1) if vec else out
+
+
+def tridiag_action(sub, diag, sup, v, m: OMethod, substeps: int = 1) -> np.ndarray:
+    """substep_action (action_eval for substeps = 1) on every column of v (d x k or d)."""
+    sub, diag, sup = _f64(sub), _f64(diag), _f64(sup)
+    V, vec = _cols(v)
+    V = np.ascontiguousarray(V)
+    d, k = V.shape
+    out = np.empty_like(V)
+    st = Status()
+    rc = lib().pfo_tridiag_action(d, k, _p(sub), _p(diag), _p(sup), _p(V), C.byref(m.c), substeps, _p(out),
+                                  C.byref(st))
+    if rc:
+        raise BandError(rc, st.column, st.shift_index)
+    return out.reshape(-1) if vec else out

@@ -109,6 +109,22 @@ int pfo_cossin_batched(int n, int batch, const double* a, const pfo_pair_method*
 int pfo_action(int n, int k, const double* a, const double* v, const pfo_method* m, int substeps,
                int workers, double* out, pfo_status* st);
 
+/* f2: banded action (pf_oracle_band.c, restating proj/core/src/action.cpp). Tridiagonal matrices
+ * are (sub[d-1], diag[d], super[d-1]); V / out are d x k row-major (k independent columns). */
+void pfo_tridiag_matvec(int d, const double* sub, const double* diag, const double* super, const double* v,
+                        double* out);
+double pfo_tridiag_one_norm(int d, const double* sub, const double* diag, const double* super);
+int pfo_thomas_solve(int d, const double* sub, const double* diag, const double* super, const double* rhs,
+                     double* x, int* row);
+int pfo_tridiag_factor(int d, const double* sub, const double* diag, const double* super, double* mult,
+                       double* fdiag, int* row);
+void pfo_tridiag_factor_solve(int d, const double* mult, const double* fdiag, const double* super, const double* rhs,
+                              double* x);
+int pfo_pentadiag_solve(int d, const double* sub2, const double* sub1, const double* diag, const double* super1,
+                        const double* super2, const double* rhs, double* x, int* row);
+int pfo_tridiag_action(int d, int k, const double* sub, const double* diag, const double* super, const double* v,
+                       const pfo_method* m, int substeps, double* out, pfo_status* st);
+
 #ifdef __cplusplus
 }
 #endif

@@ -84,6 +84,13 @@ SIGNATURES = [
     ("pf_copy_to_host", C.c_int, [_VP, _VP, _VP, C.c_size_t]),
     ("pf_gemm_batched", C.c_int, [_VP, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, _VP, _I64, _I64, _VP, _I64,
                                   _I64, C.c_double, _VP, _I64, _I64, C.c_double]),
+    ("pf_tridiag_matvec_batched", C.c_int, [_VP, C.c_int, C.c_int, _VP, _VP, _VP, _VP, _I64, _VP, _I64]),
+    ("pf_thomas_solve_batched", C.c_int, [_VP, C.c_int, C.c_int, _VP, _VP, _VP, _VP, _I64, _VP, _I64,
+                                          C.POINTER(PfStatus)]),
+    ("pf_pentadiag_solve_batched", C.c_int, [_VP, C.c_int, C.c_int, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _VP, _I64,
+                                             C.POINTER(PfStatus)]),
+    ("pf_tridiag_action", C.c_int, [_VP, C.POINTER(PfMethod), C.c_int, C.c_int, _VP, _VP, _VP, _VP, _I64, C.c_int,
+                                    _VP, _I64, C.c_int, C.POINTER(PfStatus)]),
 ]
 
 

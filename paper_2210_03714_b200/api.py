@@ -154,6 +154,11 @@ def _raise(rc: int, st: N.PfStatus, batched: bool):
         if batched:
             msg = "matrix %d: %s" % (st.batch_index, msg)
         raise PfError(code, msg)
+    if code == Errc.ZeroPivot:  # thomas_solve / pentadiag_solve (action.cpp:104,113,185)
+        msg = "zero pivot at row %d" % st.column
+        if st.shift_index > 0:
+            msg = "shift %d: %s" % (st.shift_index, msg)
+        raise PfError(code, msg)
     if code == Errc.CudaError:
         raise PfError(code, "CUDA failure in the B200 engine")
     raise PfError(code, "bad argument")
@@ -612,3 +617,114 @@ def gemm(A: torch.Tensor, B: torch.Tensor, alpha: float = 1.0, beta: float = 0.0
     if rc:
         _raise(rc, N.PfStatus(), True)
     return Cm
+
+
+# ---- f2: banded action (proj/core/src/action.cpp). A tridiagonal matrix is (sub, diag, super) with
+# lengths d-1, d, d-1 (TridiagMatrix); vectors are columns of a d x k block, each processed exactly as
+# the reference processes one vector.
+
+
+class TridiagMatrix:
+    """Compact three-diagonal matrix (action.hpp:13-24), device arrays."""
+
+    def __init__(self, sub: ArrayLike, diag: ArrayLike, sup: ArrayLike):
+        self.sub = _to_device(sub)[0].reshape(-1)
+        self.diag = _to_device(diag)[0].reshape(-1)
+        self.sup = _to_device(sup)[0].reshape(-1)
+        self.d = int(self.diag.numel())
+        if self.sub.numel() != max(self.d - 1, 0) or self.sup.numel() != max(self.d - 1, 0):
+            raise PfError(Errc.LengthMismatch, "band length mismatch")
+
+    @staticmethod
+    def trid121(d: int) -> "TridiagMatrix":
+        """trid{-1, 2, -1} (action.cpp:27-33)."""
+        o = torch.full((max(d - 1, 0),), -1.0, dtype=torch.float64)
+        return TridiagMatrix(o, torch.full((d,), 2.0, dtype=torch.float64), o.clone())
+
+    def _ptrs(self):
+        # d = 1: the off-diagonal arrays are empty; hand the kernels a valid pointer
+        sp = self.sub.data_ptr() if self.sub.numel() else self.diag.data_ptr()
+        up = self.sup.data_ptr() if self.sup.numel() else self.diag.data_ptr()
+        return sp, self.diag.data_ptr(), up
+
+    def one_norm(self) -> float:
+        s, dg, u = self.sub.abs(), self.diag.abs(), self.sup.abs()
+        col = dg.clone()
+        col[1:] += u
+        col[:-1] += s
+        return float(col.max()) if self.d else 0.0
+
+
+def _block(V: ArrayLike, d: int):
+    dV, host = _to_device(V)
+    vec = dV.dim() == 1
+    V2 = (dV.reshape(d, 1) if vec else dV).contiguous()
+    if V2.shape[0] != d:
+        raise PfError(Errc.LengthMismatch, "vector length mismatch")
+    return V2, host, vec
+
+
+def _unblock(out: torch.Tensor, host: bool, vec: bool):
+    out = out.reshape(-1) if vec else out
+    return out.cpu().numpy() if host else out
+
+
+def tridiag_matvec(t: TridiagMatrix, V: ArrayLike):
+    eng = engine()
+    V2, host, vec = _block(V, t.d)
+    out = torch.empty_like(V2)
+    s, dg, u = t._ptrs()
+    rc = N.lib.pf_tridiag_matvec_batched(eng.h, t.d, V2.shape[1], s, dg, u, V2.data_ptr(), V2.shape[1],
+                                         out.data_ptr(), V2.shape[1])
+    if rc:
+        _raise(rc, N.PfStatus(), False)
+    return _unblock(out, host, vec)
+
+
+def thomas_solve(t: TridiagMatrix, rhs: ArrayLike):
+    """thomas_solve (action.cpp:100-118) for every column of rhs."""
+    eng = engine()
+    R, host, vec = _block(rhs, t.d)
+    out = torch.empty_like(R)
+    st = N.PfStatus()
+    s, dg, u = t._ptrs()
+    rc = N.lib.pf_thomas_solve_batched(eng.h, t.d, R.shape[1], s, dg, u, R.data_ptr(), R.shape[1], out.data_ptr(),
+                                       R.shape[1], C.byref(st))
+    if rc:
+        _raise(rc, st, False)
+    return _unblock(out, host, vec)
+
+
+def pentadiag_solve(sub2: ArrayLike, sub1: ArrayLike, diag: ArrayLike, super1: ArrayLike, super2: ArrayLike,
+                    rhs: ArrayLike):
+    """pentadiag_solve (action.cpp:170-202): banded LU without pivoting, every column of rhs."""
+    eng = engine()
+    bands = [_to_device(b)[0].reshape(-1) for b in (sub2, sub1, diag, super1, super2)]
+    d = int(bands[2].numel())
+    R, host, vec = _block(rhs, d)
+    out = torch.empty_like(R)
+    st = N.PfStatus()
+    ptrs = [b.data_ptr() if b.numel() else bands[2].data_ptr() for b in bands]
+    rc = N.lib.pf_pentadiag_solve_batched(eng.h, d, R.shape[1], *ptrs, R.data_ptr(), R.shape[1], out.data_ptr(),
+                                          R.shape[1], C.byref(st))
+    if rc:
+        _raise(rc, st, False)
+    return _unblock(out, host, vec)
+
+
+def tridiag_action(method, t: TridiagMatrix, V: ArrayLike, substeps: int = 1, form: Optional[int] = None,
+                   flags: int = 0):
+    """substep_action (action.cpp:327-339) -- action_eval for substeps = 1 -- on every column of V:
+    v <- r(A / N) v, N = substeps, with one factorization per shift reused (ActionOperator)."""
+    m = _resolve_method(method)
+    pk = PackedMethod(m, form)
+    eng = engine()
+    V2, host, vec = _block(V, t.d)
+    out = torch.empty_like(V2)
+    st = N.PfStatus()
+    s, dg, u = t._ptrs()
+    rc = N.lib.pf_tridiag_action(eng.h, pk.ptr(), t.d, V2.shape[1], s, dg, u, V2.data_ptr(), V2.shape[1],
+                                 int(substeps), out.data_ptr(), V2.shape[1], flags, C.byref(st))
+    if rc:
+        _raise(rc, st, False)
+    return _unblock(out, host, vec)

@@ -1,0 +1,220 @@
+// C ABI of the banded action (include/pf_b200.h, f2): host orchestration of band.cu's kernels.
+// Replaces thomas_solve / TridiagFactor / pentadiag_solve / action_eval / ActionOperator /
+// substep_action (proj/core/src/action.cpp:100-339) for blocks of vectors.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "pf_host.h"
+
+namespace pf {
+__global__ void band_scale_kernel(int d, const double* sub, const double* diag, const double* super, double s,
+                                  double* osub, double* odiag, double* osuper);
+__global__ void band_factor_kernel(int d, int nsys, const double* sub, const double* diag, const double* super,
+                                   const double* shifts, double* mult, double* fdiag, double* fsup, int* fail);
+__global__ void band_solve_kernel(int d, int k, const double* mult, const double* fdiag, const double* fsup,
+                                  const double* src, int64_t lds, const double* rhs_scale, double* X, int64_t ldx,
+                                  int64_t strideX);
+__global__ void band_matvec_kernel(int d, int k, const double* sub, const double* diag, const double* super,
+                                   const double* V, int64_t ldv, double* Out, int64_t ldo);
+__global__ void band_accumulate_kernel(int d, int k, int n_terms, const int* slot, const double* w, const double* X,
+                                       int64_t ldx, int64_t strideX, const double* V, int64_t ldv, int add_poly,
+                                       double constant, int hybrid, double d1, double d2, const double* AV,
+                                       const double* A2V, double* out, int64_t ldo);
+__global__ void penta_factor_kernel(int d, const double* sub2, const double* sub1, const double* diag,
+                                    const double* super1, const double* super2, double* W, double* F, int* fail);
+__global__ void penta_solve_kernel(int d, int k, const double* W, const double* F, const double* rhs, int64_t ldr,
+                                   double* X, int64_t ldx);
+}  // namespace pf
+
+using namespace pf::host;
+
+namespace {
+
+unsigned blocks_for(int64_t elems) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((elems + 255) / 256, 4736)); }
+
+int zero_pivot(pf_status* st, int shift_index, int row) {
+  if (st) {
+    std::memset(st, 0, sizeof(*st));
+    st->code = PF_ERR_ZERO_PIVOT;
+    st->shift_index = shift_index;
+    st->column = row;
+  }
+  return PF_ERR_ZERO_PIVOT;
+}
+
+// factor nsys systems (shifted by d_shifts when given); returns the first failing system or -1
+int factor(pf_context* ctx, int d, int nsys, const double* sub, const double* diag, const double* super,
+           const double* d_shifts, double* mult, double* fdiag, double* fsup, int* row, int* rc) {
+  int* d_fail = static_cast<int*>(workspace(ctx, kWsSmallArrays + 40, sizeof(int) * std::max(nsys, 1)));
+  if (!d_fail) {
+    *rc = PF_ERR_CUDA;
+    return -1;
+  }
+  pf::band_factor_kernel<<<(nsys + 31) / 32, 32, 0, ctx->stream>>>(d, nsys, sub, diag, super, d_shifts, mult, fdiag,
+                                                                     fsup, d_fail);
+  ctx->launches++;
+  std::vector<int> fail(nsys);
+  cudaMemcpyAsync(fail.data(), d_fail, sizeof(int) * nsys, cudaMemcpyDeviceToHost, ctx->stream);
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+    *rc = PF_ERR_CUDA;
+    return -1;
+  }
+  *rc = PF_OK;
+  for (int z = 0; z < nsys; ++z)
+    if (fail[z] >= 0) {
+      *row = fail[z];
+      return z;
+    }
+  return -1;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pf_tridiag_matvec_batched(pf_context* ctx, int d, int k, const double* dSub, const double* dDiag,
+                              const double* dSuper, const double* dV, int64_t ldv, double* dOut, int64_t ldo) {
+  if (!ctx || d < 0 || k < 0 || ldv < k || ldo < k) return PF_ERR_BAD_ARGUMENT;
+  if (d == 0 || k == 0) return PF_OK;
+  pf::band_matvec_kernel<<<blocks_for((int64_t)d * k), 256, 0, ctx->stream>>>(d, k, dSub, dDiag, dSuper, dV, ldv,
+                                                                              dOut, ldo);
+  ctx->launches++;
+  return cuda_fail(cudaGetLastError());
+}
+
+int pf_thomas_solve_batched(pf_context* ctx, int d, int k, const double* dSub, const double* dDiag,
+                            const double* dSuper, const double* dRhs, int64_t ldr, double* dX, int64_t ldx,
+                            pf_status* status) {
+  if (status) std::memset(status, 0, sizeof(*status));
+  if (!ctx || d < 1 || k < 0 || ldr < k || ldx < k) return bad(status);
+  const int64_t dm1 = std::max(d - 1, 1);
+  double* F = static_cast<double*>(workspace(ctx, kWsBandF, sizeof(double) * (size_t)(d + 2 * dm1)));
+  if (!F) return PF_ERR_CUDA;
+  double *mult = F, *fdiag = F + dm1, *fsup = F + dm1 + d;
+  int row = 0, rc = PF_OK;
+  const int z = factor(ctx, d, 1, dSub, dDiag, dSuper, nullptr, mult, fdiag, fsup, &row, &rc);
+  if (rc) return rc;
+  if (z >= 0) return zero_pivot(status, 0, row);
+  if (k == 0) return PF_OK;
+  pf::band_solve_kernel<<<dim3((k + 127) / 128, 1), 128, 0, ctx->stream>>>(d, k, mult, fdiag, fsup, dRhs, ldr,
+                                                                             nullptr, dX, ldx, 0);
+  ctx->launches++;
+  return collect_status(ctx, 0, 0, nullptr);
+}
+
+int pf_pentadiag_solve_batched(pf_context* ctx, int d, int k, const double* dSub2, const double* dSub1,
+                               const double* dDiag, const double* dSuper1, const double* dSuper2,
+                               const double* dRhs, int64_t ldr, double* dX, int64_t ldx, pf_status* status) {
+  if (status) std::memset(status, 0, sizeof(*status));
+  if (!ctx || d < 1 || k < 0 || ldr < k || ldx < k) return bad(status);
+  double* W = static_cast<double*>(workspace(ctx, kWsBandF, sizeof(double) * (size_t)d * 7));
+  int* d_fail = static_cast<int*>(workspace(ctx, kWsSmallArrays + 40, sizeof(int)));
+  if (!W || !d_fail) return PF_ERR_CUDA;
+  double* F = W + (size_t)d * 5;
+  pf::penta_factor_kernel<<<1, 32, 0, ctx->stream>>>(d, dSub2, dSub1, dDiag, dSuper1, dSuper2, W, F, d_fail);
+  ctx->launches++;
+  int fail = -1;
+  cudaMemcpyAsync(&fail, d_fail, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return PF_ERR_CUDA;
+  if (fail >= 0) return zero_pivot(status, 0, fail);
+  if (k == 0) return PF_OK;
+  pf::penta_solve_kernel<<<(k + 127) / 128, 128, 0, ctx->stream>>>(d, k, W, F, dRhs, ldr, dX, ldx);
+  ctx->launches++;
+  return collect_status(ctx, 0, 0, nullptr);
+}
+
+int pf_tridiag_action(pf_context* ctx, const pf_method* m, int d, int k, const double* dSub, const double* dDiag,
+                      const double* dSuper, const double* dV, int64_t ldv, int substeps, double* dOut, int64_t ldo,
+                      int flags, pf_status* status) {
+  if (status) std::memset(status, 0, sizeof(*status));
+  pf::SmallParams p{};
+  if (!ctx || !fill_method(m, p) || d < 1 || k < 0 || substeps < 1 || ldv < k || ldo < k) return bad(status);
+  if (k == 0) return PF_OK;
+  const bool residual = m->form == PF_FORM_RESIDUAL;
+  const bool hybrid = m->has_poly != 0;
+  const int64_t dm1 = std::max(d - 1, 1);
+  // nonzero shifts in ascending index: one factored system each
+  std::vector<double> sh;
+  std::vector<int> sh_index;
+  for (int i = 0; i < m->n_terms; ++i)
+    if (m->shifts[i] != 0.0) {
+      sh.push_back(m->shifts[i]);
+      sh_index.push_back(i);
+    }
+  const int P = (int)sh.size();
+  const size_t blk = (size_t)d * k;
+  double* A3 = static_cast<double*>(workspace(ctx, kWsBandA, sizeof(double) * (size_t)(d + 2 * dm1)));
+  double* F = static_cast<double*>(workspace(ctx, kWsBandF, sizeof(double) * (size_t)(d + 2 * dm1) * std::max(P, 1)));
+  double* Y = static_cast<double*>(workspace(ctx, kWsBandY, sizeof(double) * blk * std::max(P, 1)));
+  double* XB = static_cast<double*>(workspace(ctx, kWsBandX, sizeof(double) * blk * 4));
+  if (!A3 || !F || !Y || !XB) return PF_ERR_CUDA;
+  double *ssub = A3, *sdiag = A3 + dm1, *ssup = A3 + dm1 + d;
+  pf::band_scale_kernel<<<blocks_for(d), 256, 0, ctx->stream>>>(d, dSub, dDiag, dSuper, 1.0 / substeps, ssub, sdiag,
+                                                                 ssup);
+  ctx->launches++;
+  double *mult = F, *fdiag = F + dm1 * P, *fsup = F + dm1 * P + (int64_t)d * P;
+  double* d_sh = nullptr;
+  if (P > 0) {
+    d_sh = static_cast<double*>(workspace(ctx, kWsSmallArrays + 41, sizeof(double) * P));
+    if (!d_sh) return PF_ERR_CUDA;
+    cudaMemcpyAsync(d_sh, sh.data(), sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream);
+    int row = 0, rc = PF_OK;
+    const int z = factor(ctx, d, P, ssub, sdiag, ssup, d_sh, mult, fdiag, fsup, &row, &rc);
+    if (rc) return rc;
+    if (z >= 0) return zero_pivot(status, sh_index[z] + 1, row);  // "shift i: zero pivot at row r"
+  }
+  // terms in ascending shift index: factored slot, or -1 (plain zero shift: the term is w v)
+  std::vector<int> slot;
+  std::vector<double> w;
+  for (int i = 0, q = 0; i < m->n_terms; ++i) {
+    if (m->shifts[i] != 0.0) {
+      slot.push_back(q++);
+      w.push_back(m->weights[i]);
+    } else if (!residual) {
+      slot.push_back(-1);
+      w.push_back(m->weights[i]);
+    }
+  }
+  const int nt = (int)slot.size();
+  int* d_slot = static_cast<int*>(workspace(ctx, kWsSmallArrays + 42, sizeof(int) * std::max(nt, 1)));
+  double* d_w = static_cast<double*>(workspace(ctx, kWsSmallArrays + 43, sizeof(double) * std::max(nt, 1)));
+  if (!d_slot || !d_w) return PF_ERR_CUDA;
+  if (nt) {
+    cudaMemcpyAsync(d_slot, slot.data(), sizeof(int) * nt, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(d_w, w.data(), sizeof(double) * nt, cudaMemcpyHostToDevice, ctx->stream);
+  }
+  const bool add_poly = residual || hybrid;
+  const double constant = residual ? m->constant[0] : (hybrid ? m->poly[0] : 0.0);
+  const double d1 = hybrid ? m->poly[1] : 0.0, d2 = hybrid ? m->poly[2] : 0.0;
+  double *X = XB, *Xn = XB + blk, *AV = XB + 2 * blk, *A2V = XB + 3 * blk;
+  cudaMemcpy2DAsync(X, sizeof(double) * k, dV, sizeof(double) * ldv, sizeof(double) * k, d, cudaMemcpyDeviceToDevice,
+                    ctx->stream);
+  for (int step = 0; step < substeps; ++step) {
+    if (add_poly) {
+      pf::band_matvec_kernel<<<blocks_for((int64_t)blk), 256, 0, ctx->stream>>>(d, k, ssub, sdiag, ssup, X, k, AV, k);
+      ctx->launches++;
+    }
+    if (hybrid) {
+      pf::band_matvec_kernel<<<blocks_for((int64_t)blk), 256, 0, ctx->stream>>>(d, k, ssub, sdiag, ssup, AV, k, A2V,
+                                                                                 k);
+      ctx->launches++;
+    }
+    if (P > 0) {
+      pf::band_solve_kernel<<<dim3((k + 127) / 128, P), 128, 0, ctx->stream>>>(
+          d, k, mult, fdiag, fsup, residual ? AV : X, k, residual ? d_sh : nullptr, Y, k, (int64_t)blk);
+      ctx->launches++;
+    }
+    pf::band_accumulate_kernel<<<blocks_for((int64_t)blk), 256, 0, ctx->stream>>>(
+        d, k, nt, d_slot, d_w, Y, k, (int64_t)blk, X, k, add_poly ? 1 : 0, constant, hybrid ? 1 : 0, d1, d2, AV, A2V,
+        Xn, k);
+    ctx->launches++;
+    std::swap(X, Xn);
+  }
+  cudaMemcpy2DAsync(dOut, sizeof(double) * ldo, X, sizeof(double) * k, sizeof(double) * k, d,
+                    cudaMemcpyDeviceToDevice, ctx->stream);
+  (void)flags;
+  return collect_status(ctx, 0, flags, status);
+}
+
+}  // extern "C"

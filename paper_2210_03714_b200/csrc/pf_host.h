@@ -85,6 +85,10 @@ enum Slot {
   kWsPairB2 = 21,
   kWsPairT = 22,
   kWsTriTmp = 26,       // triangular block inversion temporaries
+  kWsBandA = 27,        // banded action: scaled band, factors, per-shift solutions, iterates
+  kWsBandF = 28,
+  kWsBandY = 29,
+  kWsBandX = 30,
   kWsScratch = 20,      // per-SM accumulator slots of the small kernel
   kWsSmallArrays = 64,  // small uploaded tables: kWsSmallArrays + i, i < 32
 };
