@@ -130,7 +130,6 @@ int pf_tridiag_action(pf_context* ctx, const pf_method* m, int d, int k, const d
   if (status) std::memset(status, 0, sizeof(*status));
   pf::SmallParams p{};
   if (!ctx || !fill_method(m, p) || d < 1 || k < 0 || substeps < 1 || ldv < k || ldo < k) return bad(status);
-  if (k == 0) return PF_OK;
   const bool residual = m->form == PF_FORM_RESIDUAL;
   const bool hybrid = m->has_poly != 0;
   const int64_t dm1 = std::max(d - 1, 1);
@@ -164,6 +163,7 @@ int pf_tridiag_action(pf_context* ctx, const pf_method* m, int d, int k, const d
     if (rc) return rc;
     if (z >= 0) return zero_pivot(status, sh_index[z] + 1, row);  // "shift i: zero pivot at row r"
   }
+  if (k == 0) return PF_OK;  // factor-only validation (ActionOperator's constructor)
   // terms in ascending shift index: factored slot, or -1 (plain zero shift: the term is w v)
   std::vector<int> slot;
   std::vector<double> w;

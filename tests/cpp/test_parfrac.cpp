@@ -7,6 +7,7 @@
 #include <string>
 #include <vector>
 
+#include "parfrac/action.hpp"
 #include "parfrac/dense.hpp"
 #include "parfrac/error.hpp"
 #include "parfrac/methods.hpp"
@@ -256,6 +257,118 @@ void test_catalog() {  // test_methods.cpp:50-110 against the generated tables
   CHECK(&catalog("R4") == &catalog("R4"));
 }
 
+// ---- banded action (proj/tests/test_action.cpp:49-188)
+
+double vec_rel(const std::vector<double>& a, const std::vector<double>& b) {
+  double n = 0, d = 0;
+  for (size_t i = 0; i < a.size(); ++i) {
+    d += (a[i] - b[i]) * (a[i] - b[i]);
+    n += b[i] * b[i];
+  }
+  return std::sqrt(d) / std::max(std::sqrt(n), 1e-300);
+}
+
+TridiagMatrix random_tridiag(int d, std::uint64_t seed, double dom) {
+  TridiagMatrix t = TridiagMatrix::zero(d);
+  NormalSampler ns(seed);
+  for (auto& x : t.sub) x = ns.next();
+  for (auto& x : t.diag) x = ns.next() + dom;
+  for (auto& x : t.super) x = ns.next();
+  return t;
+}
+
+void test_thomas() {  // test_action.cpp:49-92
+  const int d = 50;
+  TridiagMatrix eye = TridiagMatrix::zero(d);
+  std::fill(eye.diag.begin(), eye.diag.end(), 1.0);
+  std::vector<double> v(d);
+  NormalSampler ns(3);
+  for (auto& x : v) x = ns.next();
+  CHECK(thomas_solve(eye, v) == v);
+  TridiagMatrix t = random_tridiag(d, 5, 4.0);
+  std::vector<double> x = thomas_solve(t, v);
+  CHECK(vec_rel(x, DenseLu(t.to_dense()).solve(v)) <= 1e-13);
+  std::vector<double> back = t.matvec(x);
+  CHECK(vec_rel(back, v) <= 1e-12);
+  TridiagFactor factor(t);
+  for (int s = 0; s < 4; ++s) {
+    std::vector<double> r(d);
+    NormalSampler rs(100 + s);
+    for (auto& e : r) e = rs.next();
+    CHECK(factor.solve(r) == thomas_solve(t, r));
+  }
+  TridiagMatrix z = TridiagMatrix::zero(d);
+  std::fill(z.sub.begin(), z.sub.end(), 1.0);
+  bool got = false;
+  try {
+    thomas_solve(z, v);
+  } catch (const Error& e) {
+    got = e.code() == Errc::ZeroPivot && std::string(e.what()).find("zero pivot at row 0") != std::string::npos;
+  }
+  CHECK(got);
+  CHECK_THROWS(TridiagFactor(z));
+}
+
+void test_pentadiag() {  // test_action.cpp:95-121
+  const int d = 40;
+  PentadiagMatrix p;
+  p.d = d;
+  NormalSampler ns(9);
+  p.sub2.resize(d - 2);
+  p.sub1.resize(d - 1);
+  p.diag.resize(d);
+  p.super1.resize(d - 1);
+  p.super2.resize(d - 2);
+  for (auto* band : {&p.sub2, &p.sub1, &p.super1, &p.super2})
+    for (auto& e : *band) e = ns.next();
+  for (auto& e : p.diag) e = ns.next() + 6.0;
+  std::vector<double> rhs(d);
+  for (auto& e : rhs) e = ns.next();
+  CHECK(vec_rel(pentadiag_solve(p, rhs), DenseLu(p.to_dense()).solve(rhs)) <= 1e-12);
+  PentadiagMatrix zero;
+  zero.d = 2;
+  zero.sub1 = {0.0};
+  zero.diag = {0.0, 0.0};
+  zero.super1 = {0.0};
+  CHECK_THROWS(pentadiag_solve(zero, std::vector<double>{1, 1}));
+}
+
+void test_action() {  // test_action.cpp:124-188
+  const int d = 64;
+  TridiagMatrix a = TridiagMatrix::trid121(d);
+  for (auto* band : {&a.sub, &a.diag, &a.super})
+    for (auto& e : *band) e *= -0.25;
+  std::vector<double> v(d);
+  NormalSampler ns(21);
+  for (auto& x : v) x = ns.next();
+  for (const char* name : {"R4", "R8", "R10"}) {
+    const FractionMethod& m = catalog(name);
+    EvalOptions res{.form = EvalForm::Residual};
+    std::vector<double> by_action = action_eval(m, a, v, res);
+    std::vector<double> by_dense = substep_action(m, a.to_dense(), v, 1, 1, res);
+    CHECK(vec_rel(by_action, by_dense) <= 1e-11);
+    ActionOperator op(m, a);
+    CHECK(op.apply(v, res) == by_action);  // :171-188 identical results
+    std::vector<double> s4 = substep_action(m, a, v, 4, res);
+    CHECK(s4 == substep_action_block(m, a, v, 1, 4, res));
+  }
+  std::vector<double> z = action_eval(catalog("R8"), TridiagMatrix::zero(d), v, {.form = EvalForm::Residual});
+  CHECK(z == v);  // :149-157 (a0 = 1)
+  CHECK_THROWS(action_eval(catalog("R8"), a, v, {.fixed_order = false}));
+  CHECK_THROWS(action_eval(catalog("R8"), a, v, {.workers = 0}));
+  // "shift i: zero pivot at row r": 1 - c a_00 = 0 for the second shift of R4
+  const double c = to_double_nearest(catalog("R4").shifts[1]);
+  TridiagMatrix bad = TridiagMatrix::zero(4);
+  bad.diag = {1.0 / c, 1.0, 1.0, 1.0};
+  bool got = false;
+  try {
+    action_eval(catalog("R4"), bad, std::vector<double>(4, 1.0), {.form = EvalForm::Residual});
+  } catch (const Error& e) {
+    got = e.code() == Errc::ZeroPivot && std::string(e.what()).rfind("shift ", 0) == 0;
+  }
+  CHECK(got);
+}
+
 }  // namespace
 
 int main() {
@@ -268,6 +381,9 @@ int main() {
       {"residual parity vs host reference", test_residual_parity_vs_host_reference},
       {"expm / phi1 / cos-sin / action", test_expm_and_friends},
       {"catalog", test_catalog},
+      {"thomas solve and factor reuse", test_thomas},
+      {"pentadiagonal solve", test_pentadiag},
+      {"tridiagonal action, operator, substeps", test_action},
   };
   for (auto& [name, fn] : tests) {
     const int before = g_fail;
