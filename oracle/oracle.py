@@ -113,6 +113,26 @@ def mul(a, b) -> np.ndarray:
     return out
 
 
+def mul_rows(a_rows, b) -> np.ndarray:
+    """rows x n times n x n in pfo_mul's order (row i as in mul(a, b))."""
+    a_rows, b = _f64(a_rows), _f64(b)
+    out = np.empty((a_rows.shape[0], b.shape[1]))
+    lib().pfo_mul_rows(a_rows.shape[0], b.shape[0], _p(a_rows), _p(b), _p(out))
+    return out
+
+
+def phi1_doubling(E, Phi, j: int):
+    """pfo_expm_phi1's recurrence: Phi <- 0.5 ((E + I) Phi), E <- E E, j times."""
+    E, Phi = _f64(E).copy(), _f64(Phi).copy()
+    n = E.shape[0]
+    for _ in range(j):
+        T = E.copy()
+        T[np.arange(n), np.arange(n)] += 1.0
+        Phi = mul(T, Phi) * 0.5
+        E = mul(E, E)
+    return E, Phi
+
+
 def mul_rect(a, b) -> np.ndarray:
     """(n x n)(n x k), i-k-j order with the zero skip (DenseMatrix::mul generalised)."""
     a, b = _f64(a), _f64(b)

@@ -97,6 +97,20 @@ void pfo_mul(int d, const double* a, const double* o, double* out) {
     }
 }
 
+/* rows of a product: out (rows x d) = a_rows (rows x d) * o (d x d), pfo_mul's i-k-j order and
+ * zero skip per row (row i of pfo_mul depends on row i of a only) -- the f1 row-split doubling */
+void pfo_mul_rows(int rows, int d, const double* a, const double* o, double* out) {
+  memset(out, 0, sizeof(double) * (size_t)rows * (size_t)d);
+  for (int i = 0; i < rows; ++i)
+    for (int k = 0; k < d; ++k) {
+      double aik = a[(size_t)i * d + k];
+      if (aik == 0.0) continue;
+      const double* orow = &o[(size_t)k * d];
+      double* orow_out = &out[(size_t)i * d];
+      for (int j = 0; j < d; ++j) orow_out[j] += aik * orow[j];
+    }
+}
+
 void pfo_mul_rect(int d, int kc, const double* a, const double* o, double* out) {
   memset(out, 0, sizeof(double) * (size_t)d * (size_t)kc);
   for (int i = 0; i < d; ++i)

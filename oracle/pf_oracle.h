@@ -72,6 +72,7 @@ void pfo_randn_fill(uint64_t seed, int64_t count, double* out);
 /* DenseMatrix primitives, row-major n x n */
 void pfo_mul(int n, const double* a, const double* b, double* c);
 void pfo_mul_rect(int n, int k, const double* a, const double* b, double* c); /* (n x n)(n x k) */
+void pfo_mul_rows(int rows, int n, const double* a, const double* b, double* c); /* (rows x n)(n x n) */
 double pfo_one_norm(int n, const double* a);
 double pfo_max_abs(int n, const double* a);
 int pfo_squarings(double norm1, double theta);

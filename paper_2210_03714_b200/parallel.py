@@ -15,8 +15,13 @@
                    is not the deterministic mode's bit-level reference.
   Units are (c, -c) pairs when the method's nonzero shifts pair up (every frac4/frac8 set), single
   terms otherwise, so that a rank evaluates whole pairs in the fast mode.
-  The polynomial / constant part is added once, and the doubling recurrence runs on the root after
-  the reduce ("NCCL-reduce the weighted results over NVLink before squaring").
+  The polynomial / constant part is added once. The doubling recurrence runs on the root after the
+  reduce ("NCCL-reduce the weighted results over NVLink before squaring"), or, with
+  distributed_doubling=True, on every rank: each product of the recurrence is
+  split by rows (rank r computes rows [r R, (r + 1) R) of (E + I) Phi / 2 and E E) and the row
+  blocks are all-gathered after each step. A row of a product depends on that row of the left
+  factor only, so every element is computed exactly as the single-GPU product computes it: the
+  result is bit-identical to the root-only doubling for any G.
 * Batched configs (cfg2, cfg5): independent matrices, sharded by batch with no data-path collective
   (bench.py runs one batch per rank: weak scaling).
 
@@ -82,6 +87,14 @@ class CudaBackend:
 
     def phi1_doubling(self, E, Phi, j):
         return self.api.phi1_doubling(E, Phi, j)
+
+    def phi1_step_rows(self, E, Phi, r0: int, r1: int):
+        """Rows [r0, r1) of one doubling step, as pf_phi1_doubling computes them: T = E + I (the
+        diagonal by a rounded add), 0.5 (T Phi) and E E on the DMMA GEMM."""
+        T = E[r0:r1].clone()
+        idx = torch.arange(r1 - r0, device=E.device)
+        T[idx, r0 + idx] += 1.0
+        return self.api.gemm(E[r0:r1].contiguous(), E)[0], self.api.gemm(T, Phi, alpha=0.5)[0]
 
 
 def _gather_terms(local_idx: List[int], local_terms: torch.Tensor, group, world) -> Tuple[List[int], List[torch.Tensor]]:
@@ -178,16 +191,56 @@ def eval_sets_sharded(A: torch.Tensor, j, method: FractionMethod, extra_sets: Se
     return out if rank == root else None
 
 
+def _allgather_rows(block: torch.Tensor, n: int, rows: int, group, world: int) -> torch.Tensor:
+    """Every rank's row block (the last one padded to `rows`) -> the full n x n matrix."""
+    pad = block
+    if block.shape[0] < rows:
+        pad = torch.zeros((rows,) + tuple(block.shape[1:]), dtype=block.dtype, device=block.device)
+        pad[: block.shape[0]] = block
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad.contiguous(), group=group)
+    return torch.cat(parts, 0)[:n].contiguous()
+
+
+def phi1_doubling_distributed(E: torch.Tensor, Phi: torch.Tensor, j: int, group=None, backend=None):
+    """f1: Phi <- 0.5 (E + I) Phi, E <- E E, j times, every product split by rows over the ranks of
+    `group` with one all-gather of each row block per step. E and Phi must be replicated on entry;
+    they are replicated on exit, bit-identical to the single-process recurrence."""
+    backend = backend or CudaBackend()
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    n = E.shape[0]
+    rows = -(-n // world)
+    r0, r1 = min(n, rank * rows), min(n, (rank + 1) * rows)
+    for _ in range(int(j)):
+        e_r, p_r = backend.phi1_step_rows(E, Phi, r0, r1)
+        if world > 1:
+            E = _allgather_rows(e_r, n, rows, group, world)
+            Phi = _allgather_rows(p_r, n, rows, group, world)
+        else:
+            E, Phi = e_r, p_r
+    return E, Phi
+
+
 def expm_phi1_sharded(A: torch.Tensor, method="R8", deterministic: bool = True, group=None, root: int = 0,
-                      backend=None):
+                      backend=None, distributed_doubling: bool = False):
     """cfg3: exp(A) and phi1(A) with the shifts split across the ranks, one reduce before the
-    doubling recurrence (which runs on the root). Returns (E, Phi) on the root, None elsewhere."""
+    doubling recurrence -- on the root, or split by rows over all ranks (f1, distributed_doubling).
+    Returns (E, Phi) on the root, None elsewhere."""
     backend = backend or CudaBackend()
     m = catalog(method) if isinstance(method, str) else method
     phi = same_shift_method(m, FunctionId.phi(1))
     theta = min(THETA_U53[m.name], THETA_U53.get(m.name + "_phi1set", THETA_U53[m.name]))
     j = backend.squarings(A, theta)
     res = eval_sets_sharded(A, j, m, [phi], RESIDUAL, deterministic, group, backend, root)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if distributed_doubling and world > 1:
+        rank = dist.get_rank(group)
+        E, Phi = res if res is not None else (torch.empty_like(A), torch.empty_like(A))
+        dist.broadcast(E, src=root, group=group)
+        dist.broadcast(Phi, src=root, group=group)
+        E, Phi = phi1_doubling_distributed(E, Phi, int(j.max()), group, backend)
+        return (E, Phi) if rank == root else None
     if res is None:
         return None
     E, Phi = res

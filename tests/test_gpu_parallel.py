@@ -106,3 +106,25 @@ def test_action_operator_and_partition(dev, n):
     assert torch.equal(X, ref)
     for op in ops:
         op.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_emulated_distributed_doubling_is_bit_identical(dev, world):
+    """f1 on one B200: every rank's row block of each doubling step (the all-gather emulated by a
+    concatenation in rank order) reproduces pf_phi1_doubling bit for bit."""
+    from paper_2210_03714_b200 import parallel as P
+
+    n = 300
+    g = torch.Generator().manual_seed(5)
+    E0 = (torch.eye(n, dtype=torch.float64) + 0.02 * torch.randn(n, n, generator=g, dtype=torch.float64)).cuda()
+    P0 = (torch.eye(n, dtype=torch.float64) + 0.01 * torch.randn(n, n, generator=g, dtype=torch.float64)).cuda()
+    j = 4
+    E_ref, P_ref = dev.phi1_doubling(E0.clone(), P0.clone(), torch.tensor([j], dtype=torch.int32, device="cuda"))
+    be = P.CudaBackend()
+    rows = -(-n // world)
+    E, Phi = E0.clone(), P0.clone()
+    for _ in range(j):
+        blocks = [be.phi1_step_rows(E, Phi, min(n, r * rows), min(n, (r + 1) * rows)) for r in range(world)]
+        E = torch.cat([b[0] for b in blocks], 0)
+        Phi = torch.cat([b[1] for b in blocks], 0)
+    assert torch.equal(E, E_ref) and torch.equal(Phi, P_ref)

@@ -42,6 +42,13 @@ class OracleBackend:
     def phi1_doubling(self, E, Phi, j):
         return E, Phi
 
+    def phi1_step_rows(self, E, Phi, r0, r1):
+        O = self.O
+        e, ph = E.numpy(), Phi.numpy()
+        T = e[r0:r1].copy()
+        T[np.arange(r1 - r0), r0 + np.arange(r1 - r0)] += 1.0
+        return torch.from_numpy(O.mul_rows(e[r0:r1], e)), torch.from_numpy(O.mul_rows(T, ph) * 0.5)
+
 
 class OracleActionOperator:
     """Restates the oracle's block action per owned shift (oracle/pf_oracle.c pfo_action)."""
@@ -112,7 +119,14 @@ def _worker(rank, world, port, q, case):
     try:
         from paper_2210_03714_b200 import workloads as W
 
-        if case.startswith("eval"):
+        if case == "doubling":
+            rng = np.random.default_rng(11)
+            E = torch.from_numpy(np.eye(21) + 0.1 * rng.standard_normal((21, 21)))
+            Phi = torch.from_numpy(np.eye(21) + 0.05 * rng.standard_normal((21, 21)))
+            e2, p2 = P.phi1_doubling_distributed(E, Phi, 3, None, OracleBackend())
+            if rank == 0:
+                q.put([e2.numpy(), p2.numpy()])
+        elif case.startswith("eval"):
             det = case.endswith("det")
             m = M.catalog("R8")
             phi = M.same_shift_method(m, M.FunctionId.phi(1))
@@ -216,3 +230,16 @@ def test_sharded_action_fast_agrees():
     v = W.randn(41, 30 * 3).reshape(30, 3)
     ref = O.action(a, v, O.OMethod.from_method(M.catalog("R8"), M.RESIDUAL), 4)
     assert O.rel_diff_1norm(out, ref) <= 1e-13
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_doubling_is_bit_identical(world):
+    """f1: the row-split phi1 doubling (all-gather per step) equals the single-process recurrence."""
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(11)
+    E = np.eye(21) + 0.1 * rng.standard_normal((21, 21))
+    Phi = np.eye(21) + 0.05 * rng.standard_normal((21, 21))
+    e_ref, p_ref = O.phi1_doubling(E, Phi, 3)
+    e2, p2 = _run("doubling", world)
+    assert np.array_equal(e2, e_ref) and np.array_equal(p2, p_ref)
