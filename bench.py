@@ -261,16 +261,20 @@ def time_e2e(args, method_name, A_host_pinned, eng):
     pipe = api.HostPipeline(A_host_pinned.shape[1], A_host_pinned.shape[0], chunk=256, streams=4)
 
     def step():
-        pipe.expm(A_host_pinned, hO, method_name)
+        # every step: pinned H2D of the batch, the evaluation, D2H of the result (public API); the
+        # device status of all steps is checked by finish() (one synchronisation)
+        pipe.submit(A_host_pinned, hO, method_name)
 
     for _ in range(max(1, args.warmup)):
         step()
+    pipe.finish()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
         step()
     e1.record(stream)
+    pipe.finish()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
     nbytes = A_host_pinned.numel() * 8

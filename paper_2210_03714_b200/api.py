@@ -426,21 +426,27 @@ class HostPipeline:
         shape = (self.chunk, n, n)
         self.dA = [torch.empty(shape, dtype=torch.float64, device=self.device) for _ in range(streams)]
         self.dO = [torch.empty(shape, dtype=torch.float64, device=self.device) for _ in range(streams)]
+        self._pending = []
+        self._armed = False
 
     def launch_count(self) -> int:
         return sum(e.launch_count() for e in self.engines)
 
-    def expm(self, host_in: torch.Tensor, host_out: torch.Tensor, method="R4", theta: Optional[float] = None,
-             form: int = RESIDUAL):
+    def submit(self, host_in: torch.Tensor, host_out: torch.Tensor, method="R4", theta: Optional[float] = None,
+               form: int = RESIDUAL):
+        """Enqueue host_in -> expm -> host_out without synchronising: chunk c on stream c mod streams,
+        each stream ordered (its buffers are reused only after its own previous chunk), so
+        successive submissions overlap -- the next batch's first copies run under the previous
+        batch's last kernels. Device status is sticky across submissions; finish() checks it."""
         m = _resolve_method(method)
         th = _theta_for(m, theta)
         pk = PackedMethod(m, form)
+        self._pending.append((host_in, m, th, form))
         n, S = self.n, len(self.streams)
-        cur = torch.cuda.current_stream(self.device)
-        for e in self.engines:
-            N.lib.pf_context_set_sticky_status(e.h, 1)
-        for s in self.streams:
-            s.wait_stream(cur)
+        if not self._armed:
+            for e in self.engines:
+                N.lib.pf_context_set_sticky_status(e.h, 1)
+            self._armed = True
         st = N.PfStatus()
         for c, start in enumerate(range(0, self.batch, self.chunk)):
             k = c % S
@@ -452,13 +458,27 @@ class HostPipeline:
                 if rc:
                     _raise(rc, st, True)
                 host_out[start:start + mb].copy_(self.dO[k][:mb], non_blocking=True)
-        for s in self.streams:
+        cur = torch.cuda.current_stream(self.device)
+        for s in self.streams:  # the caller's stream (and its events) sees the submitted work
             cur.wait_stream(s)
+        return host_out
+
+    def finish(self):
+        """Synchronise every submission and raise the first error (recomputed synchronously on the
+        offending batch for the exact status)."""
         failed = [N.lib.pf_context_pending_error(e.h) for e in self.engines]
         for e in self.engines:
             N.lib.pf_context_set_sticky_status(e.h, 0)
-        if any(failed):  # locate and raise the precise error synchronously
-            expm(host_in.cuda(), m, th, form=form)
+        self._armed = False
+        pending, self._pending = self._pending, []
+        if any(failed):
+            for host_in, m, th, form in pending:
+                expm(host_in.cuda(), m, th, form=form)
+
+    def expm(self, host_in: torch.Tensor, host_out: torch.Tensor, method="R4", theta: Optional[float] = None,
+             form: int = RESIDUAL):
+        self.submit(host_in, host_out, method, theta, form)
+        self.finish()
         return host_out
 
 

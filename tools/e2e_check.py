@@ -1,4 +1,6 @@
-"""HostPipeline correctness (equals the device-resident call bit for bit) and timing."""
+"""HostPipeline: correctness (equals the device-resident call bit for bit), a chunk / stream sweep of
+the submit loop the bench times, and the raw PCIe ceiling (pinned H2D and D2H of the same bytes,
+alone and concurrently on two streams)."""
 import sys
 from pathlib import Path
 
@@ -15,15 +17,47 @@ pipe.expm(hA, hO, "R4")
 torch.cuda.synchronize()
 ref = api.expm(torch.from_numpy(a).cuda(), "R4").cpu()
 print("bit-identical:", torch.equal(ref, hO))
-for chunk, ns in ((512, 3), (256, 4), (1024, 2)):
-    pipe = api.HostPipeline(128, 4096, chunk=chunk, streams=ns)
-    pipe.expm(hA, hO, "R4")
+
+
+def timed(fn, reps=5):
+    fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(5):
-        pipe.expm(hA, hO, "R4")
+    for _ in range(reps):
+        fn()
     e1.record()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / 5
-    print("chunk", chunk, "streams", ns, "ms", ms, "evals/s", 4096 / ms * 1e3)
+    return e0.elapsed_time(e1) / reps
+
+
+dA = torch.empty(hA.shape, dtype=torch.float64, device="cuda")
+gb = hA.numel() * 8 / 1e9
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+h2d = timed(lambda: dA.copy_(hA, non_blocking=True))
+d2h = timed(lambda: hO.copy_(dA, non_blocking=True))
+
+
+def both():
+    with torch.cuda.stream(s1):
+        dA.copy_(hA, non_blocking=True)
+    with torch.cuda.stream(s2):
+        hO.copy_(dA, non_blocking=True)
+    torch.cuda.current_stream().wait_stream(s1)
+    torch.cuda.current_stream().wait_stream(s2)
+
+
+duplex = timed(both)
+print("PCIe: H2D %.2f ms (%.1f GB/s), D2H %.2f ms (%.1f GB/s), both at once %.2f ms" % (
+    h2d, gb / h2d * 1e3, d2h, gb / d2h * 1e3, duplex))
+kernel = timed(lambda: api.expm(dA, "R4", out=dA.new_empty(dA.shape)))
+print("device-resident expm %.2f ms" % kernel)
+for chunk, ns in ((256, 4), (128, 4), (128, 8), (512, 3), (64, 8)):
+    pipe = api.HostPipeline(128, 4096, chunk=chunk, streams=ns)
+
+    def loop():
+        for _ in range(4):
+            pipe.submit(hA, hO, "R4")
+        pipe.finish()
+    ms = timed(loop, 2) / 4
+    print("chunk", chunk, "streams", ns, "ms/batch %.2f" % ms, "evals/s %.0f" % (4096 / ms * 1e3))
