@@ -169,13 +169,8 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB) gemm_kernel(
 namespace {
 template <int BM, int BN, int BK, int WM, int WN, int MINB, bool V16>
 void launch_tile(const GemmParams& p, cudaStream_t stream) {
-  static bool configured = false;
   const int smem = (int)sizeof(GemmSmem<BM, BN, BK>);
-  if (!configured) {
-    cudaFuncSetAttribute(gemm_kernel<BM, BN, BK, WM, WN, MINB, V16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         smem);
-    configured = true;
-  }
+  set_smem_attr_once(reinterpret_cast<const void*>(gemm_kernel<BM, BN, BK, WM, WN, MINB, V16>), smem);
   const int tiles_m = (p.m + BM - 1) / BM, tiles_n = (p.n + BN - 1) / BN;
   dim3 grid(tiles_m * tiles_n, p.batch);
   gemm_kernel<BM, BN, BK, WM, WN, MINB, V16><<<grid, (BM / WM) * (BN / WN) * 32, smem, stream>>>(p, tiles_n);

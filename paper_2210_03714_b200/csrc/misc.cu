@@ -1,3 +1,6 @@
+#include <mutex>
+#include <set>
+#include <utility>
 #include <algorithm>
 // K6 and elementwise helpers: batched 1-norm, squaring-count selection, exact 2^-j scaling,
 // Y = alpha X + diag I. HBM-bound; one thread per column / element, coalesced along rows.
@@ -88,6 +91,19 @@ void launch_ldexp_batched(int n, int batch, const double* X, int64_t ldx, int64_
   if (blocks > 1184) blocks = 1184;
   dim3 grid(blocks, batch);
   ldexp_kernel<<<grid, 256, 0, stream>>>(n, X, ldx, strideX, j, Y, ldy, strideY);
+}
+
+cudaError_t set_smem_attr_once(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({fn, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({fn, dev});
+  return e;
 }
 
 // D = C - S, E = C + S (the cos/sin double-angle step as (C - S)(C + S), see pf_cossin_batched)

@@ -125,13 +125,9 @@ bool fill_method(const pf_method* m, pf::SmallParams& p) {
 }
 
 int launch_small(pf_context* ctx, pf::SmallParams& p) {
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(pf::small_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)pf::small_eval_smem_bytes());
-  });
-  if (attr_err != cudaSuccess) return PF_ERR_CUDA;
+  if (pf::set_smem_attr_once(reinterpret_cast<const void*>(pf::small_eval_kernel), (int)pf::small_eval_smem_bytes()) !=
+      cudaSuccess)
+    return PF_ERR_CUDA;
   int rc = ensure_status(ctx, p.batch);
   if (rc) return rc;
   p.status = ctx->status;

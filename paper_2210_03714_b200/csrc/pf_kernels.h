@@ -44,6 +44,10 @@ struct SmallParams {
   double pair_cp[2][PF_MAX_TERMS];
 };
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, current device): the
+// attribute is per device, and one process may drive several (api.Engine(device=...)).
+cudaError_t set_smem_attr_once(const void* fn, int bytes);
+
 __global__ void small_eval_kernel(SmallParams p);
 size_t small_eval_smem_bytes();
 int small_eval_threads();

@@ -84,11 +84,7 @@ struct Sys {
 
 void apply_inv(pf_context* ctx, const Sys& s, int blk, bool upper, bool right, double* B, int64_t ldb, int64_t sb,
                int extent) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(apply_inv64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)apply_inv64_smem_bytes());
-    configured = true;
-  }
+  set_smem_attr_once(reinterpret_cast<const void*>(apply_inv64_kernel), (int)apply_inv64_smem_bytes());
   dim3 grid((extent + kB - 1) / kB, s.nsys);
   apply_inv64_kernel<<<grid, 256, apply_inv64_smem_bytes(), ctx->stream>>>(s.inv, s.inv_stride, blk, upper ? 1 : 0, right ? 1 : 0, B, ldb, sb,
                                                     extent);
@@ -97,11 +93,7 @@ void apply_inv(pf_context* ctx, const Sys& s, int blk, bool upper, bool right, d
 
 // 64 x 64 diagonal block: LU in place (factor) and the explicit inverses of its L and U
 void lu_base(pf_context* ctx, const Sys& s, int nblocks, int off, int factor, const int* zlist) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(lu_base64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lu_base64_smem_bytes());
-    configured = true;
-  }
+  set_smem_attr_once(reinterpret_cast<const void*>(lu_base64_kernel), (int)lu_base64_smem_bytes());
   lu_base64_kernel<<<nblocks, 256, lu_base64_smem_bytes(), ctx->stream>>>(s.M, s.np, s.stride(), off, s.inv,
                                                                           s.inv_stride, factor, zlist);
   ctx->launches++;
