@@ -125,8 +125,8 @@ bool fill_method(const pf_method* m, pf::SmallParams& p) {
 }
 
 int launch_small(pf_context* ctx, pf::SmallParams& p) {
-  if (pf::set_smem_attr_once(reinterpret_cast<const void*>(pf::small_eval_kernel), (int)pf::small_eval_smem_bytes()) !=
-      cudaSuccess)
+  auto* kernel = ctx->prof ? pf::small_eval_prof_kernel : pf::small_eval_kernel;
+  if (pf::set_smem_attr_once(reinterpret_cast<const void*>(kernel), (int)pf::small_eval_smem_bytes()) != cudaSuccess)
     return PF_ERR_CUDA;
   int rc = ensure_status(ctx, p.batch);
   if (rc) return rc;
@@ -142,7 +142,7 @@ int launch_small(pf_context* ctx, pf::SmallParams& p) {
       workspace(ctx, kWsScratch, sizeof(double) * 3 * PF_SMALL_N * PF_SMALL_N * (size_t)p.scratch_slots));
   if (!p.scratch) p.scratch_slots = 0;
   if (p.batch == 0) return PF_OK;
-  pf::small_eval_kernel<<<p.batch, pf::small_eval_threads(), pf::small_eval_smem_bytes(), ctx->stream>>>(p);
+  kernel<<<p.batch, pf::small_eval_threads(), pf::small_eval_smem_bytes(), ctx->stream>>>(p);
   ctx->launches++;
   return cuda_fail(cudaGetLastError());
 }

@@ -49,6 +49,7 @@ struct SmallParams {
 cudaError_t set_smem_attr_once(const void* fn, int bytes);
 
 __global__ void small_eval_kernel(SmallParams p);
+__global__ void small_eval_prof_kernel(SmallParams p);  // with the phase profile (p.prof)
 size_t small_eval_smem_bytes();
 int small_eval_threads();
 

@@ -37,7 +37,11 @@ print(json.dumps(res, indent=1))
 # per-phase SM cycles (sum over CTAs, thread 0 clock64), R4 and R8 automatic j
 from paper_2210_03714_b200 import _native as N  # noqa: E402
 
-names = ["norm", "load_M", "lu", "certificate", "-", "solve_acc", "shift_start+E_form", "squaring", "output", "-", "lu.factor", "lu.inverse", "lu.panels", "lu.trailing"]
+# per-shift path: load_M, lu (lu.* sub-phases), certificate, solve_acc; pair path: solve_acc holds the
+# whole pair work, with pair.* sub-phases in the slots the per-shift path leaves unused
+names = ["norm", "load_M", "lu", "certificate", "pair.B2+stats", "solve_acc", "shift_start+E_form", "squaring",
+         "output", "pair.cert+M2", "lu.factor|pair.lu", "lu.inverse|pair.solve", "lu.panels|pair.UV",
+         "lu.trailing|pair.finish_AV"]
 eng = api.engine()
 for m in ("R4", "R8"):
     prof = torch.zeros(16, dtype=torch.int64, device="cuda")
