@@ -88,6 +88,17 @@ class CudaBackend:
     def phi1_doubling(self, E, Phi, j):
         return self.api.phi1_doubling(E, Phi, j)
 
+    def square_rows(self, E, r0: int, r1: int):
+        """Rows [r0, r1) of E E (pf_square_chain's product)."""
+        return self.api.gemm(E[r0:r1].contiguous(), E)[0]
+
+    def cossin_step_rows(self, Cm, S, r0: int, r1: int):
+        """Rows [r0, r1) of one cos/sin double-angle step as pf_cossin_doubling forms it:
+        (C - S)(C + S) and 2 S C."""
+        D = Cm[r0:r1] - S[r0:r1]
+        E = Cm + S
+        return self.api.gemm(D.contiguous(), E)[0], self.api.gemm(S[r0:r1].contiguous(), Cm, alpha=2.0)[0]
+
     def phi1_step_rows(self, E, Phi, r0: int, r1: int):
         """Rows [r0, r1) of one doubling step, as pf_phi1_doubling computes them: T = E + I (the
         diagonal by a rounded add), 0.5 (T Phi) and E E on the DMMA GEMM."""
@@ -220,6 +231,41 @@ def phi1_doubling_distributed(E: torch.Tensor, Phi: torch.Tensor, j: int, group=
         else:
             E, Phi = e_r, p_r
     return E, Phi
+
+
+def _row_range(n: int, group):
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    rows = -(-n // world)
+    return world, rows, min(n, rank * rows), min(n, (rank + 1) * rows)
+
+
+def square_chain_distributed(E: torch.Tensor, j: int, group=None, backend=None):
+    """f1 for expm: E <- E E, j times, each product split by rows over the ranks of `group` with an
+    all-gather per step; bit-identical to the single-process chain (pf_square_chain)."""
+    backend = backend or CudaBackend()
+    n = E.shape[0]
+    world, rows, r0, r1 = _row_range(n, group)
+    for _ in range(int(j)):
+        e_r = backend.square_rows(E, r0, r1)
+        E = _allgather_rows(e_r, n, rows, group, world) if world > 1 else e_r
+    return E
+
+
+def cossin_doubling_distributed(Cm: torch.Tensor, S: torch.Tensor, j: int, group=None, backend=None):
+    """f1 for cos/sin: C <- (C - S)(C + S), S <- 2 S C, j times, split by rows with an all-gather of
+    both per step; bit-identical to pf_cossin_doubling."""
+    backend = backend or CudaBackend()
+    n = Cm.shape[0]
+    world, rows, r0, r1 = _row_range(n, group)
+    for _ in range(int(j)):
+        c_r, s_r = backend.cossin_step_rows(Cm, S, r0, r1)
+        if world > 1:
+            Cm = _allgather_rows(c_r, n, rows, group, world)
+            S = _allgather_rows(s_r, n, rows, group, world)
+        else:
+            Cm, S = c_r, s_r
+    return Cm, S
 
 
 def expm_phi1_sharded(A: torch.Tensor, method="R8", deterministic: bool = True, group=None, root: int = 0,

@@ -128,3 +128,35 @@ def test_emulated_distributed_doubling_is_bit_identical(dev, world):
         E = torch.cat([b[0] for b in blocks], 0)
         Phi = torch.cat([b[1] for b in blocks], 0)
     assert torch.equal(E, E_ref) and torch.equal(Phi, P_ref)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_emulated_distributed_square_and_cossin(dev, world):
+    """f1 for expm's squaring chain and the cos/sin double angle: the row split reproduces
+    pf_square_chain and pf_cossin_doubling bit for bit."""
+    from paper_2210_03714_b200 import parallel as P
+
+    n = 256
+    g = torch.Generator().manual_seed(9)
+    E0 = (torch.eye(n, dtype=torch.float64) + 0.02 * torch.randn(n, n, generator=g, dtype=torch.float64)).cuda()
+    S0 = (0.05 * torch.randn(n, n, generator=g, dtype=torch.float64)).cuda()
+    j = 3
+    jt = torch.tensor([j], dtype=torch.int32, device="cuda")
+    be = P.CudaBackend()
+    rows = -(-n // world)
+    ref = dev.square_chain(E0.clone(), jt)
+    E = E0.clone()
+    for _ in range(j):
+        E = torch.cat([be.square_rows(E, min(n, r * rows), min(n, (r + 1) * rows)) for r in range(world)], 0)
+    assert torch.equal(E, ref)
+    from paper_2210_03714_b200 import _native as N
+
+    C_ref, S_ref = E0.clone(), S0.clone()
+    rc = N.lib.pf_cossin_doubling(dev.engine().h, n, 1, jt.data_ptr(), C_ref.data_ptr(), S_ref.data_ptr())
+    assert rc == 0
+    Cm, S = E0.clone(), S0.clone()
+    for _ in range(j):
+        blocks = [be.cossin_step_rows(Cm, S, min(n, r * rows), min(n, (r + 1) * rows)) for r in range(world)]
+        Cm = torch.cat([b[0] for b in blocks], 0)
+        S = torch.cat([b[1] for b in blocks], 0)
+    assert torch.equal(Cm, C_ref) and torch.equal(S, S_ref)

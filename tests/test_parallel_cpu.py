@@ -42,6 +42,10 @@ class OracleBackend:
     def phi1_doubling(self, E, Phi, j):
         return E, Phi
 
+    def square_rows(self, E, r0, r1):
+        e = E.numpy()
+        return torch.from_numpy(self.O.mul_rows(e[r0:r1], e))
+
     def phi1_step_rows(self, E, Phi, r0, r1):
         O = self.O
         e, ph = E.numpy(), Phi.numpy()
@@ -119,7 +123,13 @@ def _worker(rank, world, port, q, case):
     try:
         from paper_2210_03714_b200 import workloads as W
 
-        if case == "doubling":
+        if case == "square":
+            rng = np.random.default_rng(12)
+            E = torch.from_numpy(np.eye(19) + 0.1 * rng.standard_normal((19, 19)))
+            e2 = P.square_chain_distributed(E, 4, None, OracleBackend())
+            if rank == 0:
+                q.put([e2.numpy()])
+        elif case == "doubling":
             rng = np.random.default_rng(11)
             E = torch.from_numpy(np.eye(21) + 0.1 * rng.standard_normal((21, 21)))
             Phi = torch.from_numpy(np.eye(21) + 0.05 * rng.standard_normal((21, 21)))
@@ -243,3 +253,16 @@ def test_distributed_doubling_is_bit_identical(world):
     e_ref, p_ref = O.phi1_doubling(E, Phi, 3)
     e2, p2 = _run("doubling", world)
     assert np.array_equal(e2, e_ref) and np.array_equal(p2, p_ref)
+
+
+def test_distributed_square_chain_is_bit_identical():
+    """f1 for expm: the row-split squaring chain over gloo (world 2) equals repeated E E."""
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(12)
+    E = np.eye(19) + 0.1 * rng.standard_normal((19, 19))
+    ref = E
+    for _ in range(4):
+        ref = O.mul(ref, ref)
+    (e2,) = _run("square", 2)
+    assert np.array_equal(e2, ref)
