@@ -234,6 +234,12 @@ int pf_context_destroy(pf_context* ctx) {
   cudaFree(ctx->status);
   cudaFree(ctx->first_error);
   cudaFreeHost(ctx->h_first_error);
+  if (ctx->side) {
+    cudaStreamSynchronize(ctx->side);
+    cudaStreamDestroy(ctx->side);
+    cudaEventDestroy(ctx->ev_fork);
+    cudaEventDestroy(ctx->ev_join);
+  }
   delete ctx;
   return PF_OK;
 }

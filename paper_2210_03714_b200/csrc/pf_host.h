@@ -18,6 +18,9 @@ struct pf_context {
   std::vector<size_t> ws_bytes;
   unsigned long long* prof = nullptr;
   bool sticky = false;  // keep first_error across launches (pipelined async use)
+  // side stream for independent branches of the large LU (created on first use)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 // Dense ActionOperator (action.hpp:68-82): B = A * (1/N) and the LU factors of the owned shifts,

@@ -140,6 +140,24 @@ void trsm_right_upper(pf_context* ctx, const Sys& s, int off, int n, double* B, 
   trsm_right_upper(ctx, s, off + n1, n2, B + n1, ldb, sb, rows);
 }
 
+// Runs `branch` on the context's side stream, concurrently with what the caller enqueues next on
+// the main stream until join(): fork / join through two reused events (forks never nest: the
+// branch itself enqueues on one stream only).
+bool fork_side(pf_context* ctx) {
+  if (!ctx->side) {
+    if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      ctx->side = nullptr;
+      return false;
+    }
+  }
+  cudaEventRecord(ctx->ev_fork, ctx->stream);
+  cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
+  return true;
+}
+
 void lu_rec(pf_context* ctx, const Sys& s, int off, int n) {
   if (n == kB) {
     lu_base(ctx, s, s.nsys, off, 1, nullptr);
@@ -150,8 +168,20 @@ void lu_rec(pf_context* ctx, const Sys& s, int off, int n) {
   double* A12 = s.M + (int64_t)off * s.np + off + n1;
   double* A21 = s.M + (int64_t)(off + n1) * s.np + off;
   double* A22 = s.M + (int64_t)(off + n1) * s.np + off + n1;
-  trsm_left_lower(ctx, s, off, n1, A12, s.np, s.stride(), n2);
-  trsm_right_upper(ctx, s, off, n1, A21, s.np, s.stride(), n2);
+  // the two panel solves are independent: A21 U11^-1 on the side stream, L11^-1 A12 on the main
+  // one (their chains of small launches overlap deep in the recursion)
+  if (fork_side(ctx)) {
+    cudaStream_t main = ctx->stream;
+    ctx->stream = ctx->side;
+    trsm_right_upper(ctx, s, off, n1, A21, s.np, s.stride(), n2);
+    cudaEventRecord(ctx->ev_join, ctx->side);
+    ctx->stream = main;
+    trsm_left_lower(ctx, s, off, n1, A12, s.np, s.stride(), n2);
+    cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0);
+  } else {
+    trsm_left_lower(ctx, s, off, n1, A12, s.np, s.stride(), n2);
+    trsm_right_upper(ctx, s, off, n1, A21, s.np, s.stride(), n2);
+  }
   gemm(ctx, n2, n2, n1, s.nsys, -1.0, A21, s.np, s.stride(), A12, s.np, s.stride(), 1.0, A22, s.np, s.stride(), 0.0);
   lu_rec(ctx, s, off + n1, n2);
 }
