@@ -23,7 +23,7 @@ def _a(n, seed, norm):
     return torch.from_numpy(W.scaled_to_one_norm(W.randn_matrix(n, seed), norm)).cuda()
 
 
-@pytest.mark.parametrize("n", [100, 200])
+@pytest.mark.parametrize("n", [100, 128, 200])
 @pytest.mark.parametrize("world", [2, 3])
 def test_emulated_shift_partition_is_bit_identical(dev, n, world):
     from paper_2210_03714_b200 import methods as M, parallel as P
