@@ -275,6 +275,9 @@ int pf_context_set_profile(pf_context* ctx, unsigned long long* dev_counters) {
 
 int pf_one_norm_batched(pf_context* ctx, int n, int batch, const double* dA, int64_t lda, int64_t strideA,
                         double* dNorm) {
+  if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
+    return PF_OK;
+  }
   if (!ctx || n < 0 || batch < 0 || lda < n) return PF_ERR_BAD_ARGUMENT;
   if (batch == 0) return PF_OK;
   pf::launch_one_norm(n, batch, dA, lda, strideA, dNorm, ctx->stream);
@@ -285,6 +288,9 @@ int pf_one_norm_batched(pf_context* ctx, int n, int batch, const double* dA, int
 int pf_gemm_batched(pf_context* ctx, int m, int n, int k, int batch, double alpha, const double* dA, int64_t lda,
                     int64_t strideA, const double* dB, int64_t ldb, int64_t strideB, double beta, double* dC,
                     int64_t ldc, int64_t strideC, double gamma) {
+  if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
+    return PF_OK;
+  }
   if (!ctx || m < 0 || n < 0 || k < 0 || batch < 0) return PF_ERR_BAD_ARGUMENT;
   if (batch == 0 || m == 0 || n == 0) return PF_OK;
   gemm(ctx, m, n, k, batch, alpha, dA, lda, strideA, dB, ldb, strideB, beta, dC, ldc, strideC, gamma);
@@ -294,6 +300,10 @@ int pf_gemm_batched(pf_context* ctx, int m, int n, int k, int batch, double alph
 int pf_eval_dense_batched(pf_context* ctx, const pf_method* m, int n, int batch, const double* dB, int64_t ldb,
                           int64_t strideB, double* const* dOuts, int64_t ldo, int64_t strideOut, int flags,
                           pf_status* status) {
+  if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
+    if (status) std::memset(status, 0, sizeof(*status));
+    return PF_OK;
+  }
   pf::SmallParams p{};
   if (!ctx || n < 0 || batch < 0 || !dOuts || !fill_method(m, p) || ldb < n || ldo < n) return bad(status);
   if (n > PF_SMALL_N) {
@@ -385,6 +395,10 @@ void copy_out(pf_context* ctx, int n, int batch, const double* src, double* dst,
 int pf_eval_scaled_batched(pf_context* ctx, const pf_method* m, double theta, int n, int batch, const double* dA,
                            int64_t lda, int64_t strideA, const int* dSquaringsIn, int* dSquaringsOut,
                            double* const* dOuts, int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
+  if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
+    if (status) std::memset(status, 0, sizeof(*status));
+    return PF_OK;
+  }
   pf::SmallParams p{};
   if (!ctx || n < 0 || batch < 0 || !dOuts || !fill_method(m, p) || lda < n || ldo < n ||
       (!dSquaringsIn && !(theta > 0)))
@@ -399,6 +413,10 @@ int pf_eval_scaled_batched(pf_context* ctx, const pf_method* m, double theta, in
 int pf_expm_batched(pf_context* ctx, const pf_method* m, double theta, int n, int batch, const double* dA,
                     int64_t lda, int64_t strideA, const int* dSquaringsIn, int* dSquaringsOut, double* dOut,
                     int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
+  if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
+    if (status) std::memset(status, 0, sizeof(*status));
+    return PF_OK;
+  }
   pf::SmallParams p{};
   if (!ctx || n < 0 || batch < 0 || !dOut || !fill_method(m, p) || lda < n || ldo < n || !(theta > 0))
     return bad(status);
@@ -450,6 +468,10 @@ int pf_expm_batched(pf_context* ctx, const pf_method* m, double theta, int n, in
 
 int pf_solve_shifted_batched(pf_context* ctx, int n, int batch, const double* dB, int64_t ldb, int64_t strideB,
                              double c, double* dOut, int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
+  if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
+    if (status) std::memset(status, 0, sizeof(*status));
+    return PF_OK;
+  }
   // (I - cB)^{-1} = eval_dense of the one-term plain method {c; 1} (dense.cpp:165-171)
   const double w = 1.0, zero = 0.0;
   pf_method m{1, &c, 1, &w, 0, nullptr, &zero, PF_FORM_PLAIN};
@@ -462,6 +484,10 @@ int pf_solve_shifted_batched(pf_context* ctx, int n, int batch, const double* dB
 int pf_expm_phi1_batched(pf_context* ctx, const pf_method* m, double theta, int n, int batch, const double* dA,
                          int64_t lda, int64_t strideA, const int* dSquaringsIn, int* dSquaringsOut, double* dE,
                          double* dPhi, int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
+  if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
+    if (status) std::memset(status, 0, sizeof(*status));
+    return PF_OK;
+  }
   pf::SmallParams p{};
   if (!ctx || n < 0 || batch < 0 || !dE || !dPhi || !fill_method(m, p) || m->n_sets != 2 || lda < n || ldo < n ||
       !(theta > 0))
@@ -498,6 +524,10 @@ int pf_expm_phi1_batched(pf_context* ctx, const pf_method* m, double theta, int 
 int pf_cossin_batched(pf_context* ctx, const pf_pair_method* pm, double theta, int n, int batch, const double* dA,
                       int64_t lda, int64_t strideA, const int* dSquaringsIn, int* dSquaringsOut, double* dC,
                       double* dS, int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
+  if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
+    if (status) std::memset(status, 0, sizeof(*status));
+    return PF_OK;
+  }
   if (!ctx || !pm || pm->n_pairs < 0 || pm->n_pairs > PF_MAX_TERMS || n < 0 || batch < 0 || !dC || !dS || lda < n ||
       ldo < n || !(theta > 0))
     return bad(status);
@@ -566,6 +596,10 @@ int pf_action_block(pf_context* ctx, const pf_method* m, int n, int k, const dou
 
 int pf_lu_factor_batched(pf_context* ctx, int n, int batch, double* dA, int64_t lda, int64_t strideA, int* dPiv,
                          double pivot_rel_tol, int flags, pf_status* status) {
+  if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
+    if (status) std::memset(status, 0, sizeof(*status));
+    return PF_OK;
+  }
   if (!ctx || n < 0 || batch < 0 || lda < n || !(pivot_rel_tol >= 0)) return bad(status);
   const int rc = large_lu_factor(ctx, n, batch, dA, lda, strideA, dPiv, pivot_rel_tol, flags, status);
   if (rc) return rc;
@@ -574,6 +608,9 @@ int pf_lu_factor_batched(pf_context* ctx, int n, int batch, double* dA, int64_t 
 
 int pf_lu_solve_batched(pf_context* ctx, int n, int k, int batch, const double* dLU, int64_t lda, int64_t strideLU,
                         const int* dPiv, double* dRhs, int64_t ldr, int64_t strideR) {
+  if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
+    return PF_OK;
+  }
   if (!ctx || n < 0 || k < 0 || batch < 0 || lda < n || ldr < k || !dPiv) return PF_ERR_BAD_ARGUMENT;
   const int rc = large_lu_solve(ctx, n, k, batch, dLU, lda, strideLU, dPiv, dRhs, ldr, strideR);
   if (rc) return rc;

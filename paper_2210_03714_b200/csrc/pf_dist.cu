@@ -75,6 +75,9 @@ int pf_action_destroy(pf_action_op* op) {
 
 int pf_squarings_batched(pf_context* ctx, int n, int batch, const double* dA, int64_t lda, int64_t strideA,
                          double theta, int* dJ) {
+  if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
+    return PF_OK;
+  }
   if (!ctx || n < 0 || batch < 0 || lda < n || !(theta > 0) || !dJ) return PF_ERR_BAD_ARGUMENT;
   if (batch == 0) return PF_OK;
   double* norms = static_cast<double*>(workspace(ctx, kWsNorm, sizeof(double) * batch));
@@ -98,6 +101,9 @@ int pf_ordered_sum(pf_context* ctx, int count, const double* const* dTerms, int6
 }
 
 int pf_square_chain(pf_context* ctx, int n, int batch, const int* dJ, double* dE) {
+  if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
+    return PF_OK;
+  }
   if (!ctx || n < 0 || batch < 0 || !dJ || !dE) return PF_ERR_BAD_ARGUMENT;
   if (batch == 0 || n == 0) return PF_OK;
   double* spare = static_cast<double*>(workspace(ctx, kWsT3, sizeof(double) * (size_t)n * n * batch));
@@ -108,6 +114,9 @@ int pf_square_chain(pf_context* ctx, int n, int batch, const int* dJ, double* dE
 }
 
 int pf_phi1_doubling(pf_context* ctx, int n, int batch, const int* dJ, double* dE, double* dPhi) {
+  if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
+    return PF_OK;
+  }
   if (!ctx || n < 0 || batch < 0 || !dJ || !dE || !dPhi) return PF_ERR_BAD_ARGUMENT;
   if (batch == 0 || n == 0) return PF_OK;
   const int64_t nn = (int64_t)n * n;
@@ -137,6 +146,9 @@ int pf_phi1_doubling(pf_context* ctx, int n, int batch, const int* dJ, double* d
 }
 
 int pf_cossin_doubling(pf_context* ctx, int n, int batch, const int* dJ, double* dC, double* dS) {
+  if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
+    return PF_OK;
+  }
   if (!ctx || n < 0 || batch < 0 || !dJ || !dC || !dS) return PF_ERR_BAD_ARGUMENT;
   if (batch == 0 || n == 0) return PF_OK;
   const int64_t nn = (int64_t)n * n;
