@@ -9,7 +9,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libpfb200.so"
+_LIB_PATH = Path(os.environ.get("PF_B200_LIB") or Path(__file__).resolve().parent / "_lib" / "libpfb200.so")  # A/B builds
 
 c_double_p = C.POINTER(C.c_double)
 c_int_p = C.POINTER(C.c_int)

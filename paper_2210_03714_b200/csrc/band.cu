@@ -17,6 +17,10 @@
 //   penta_solve_kernel      (matrix only, one thread) and the per-column substitution
 #include "pf_common.cuh"
 
+#ifndef PF_BAND_KR
+#define PF_BAND_KR 6
+#endif
+
 namespace pf {
 
 namespace {
@@ -71,8 +75,8 @@ __global__ void band_factor_kernel(int d, int nsys, const double* sub, const dou
 // X[z] (d x k, ldx) = M_z^-1 R, R = c_z * src (residual; rounded product) or src; z = blockIdx.y.
 // The recurrence is sequential in the row, so memory-level parallelism comes from batching: every
 // sweep issues the loads of kR rows (RHS / band coefficients / the forward result) before the
-// dependent arithmetic on them (one outstanding 16-row batch per thread).
-constexpr int kR = 16;
+// dependent arithmetic on them (kR = 6 measured best of 4, 6, 8, 16, 32: profiles/r01_band_action.jsonl).
+constexpr int kR = PF_BAND_KR;
 
 __global__ void __launch_bounds__(128) band_solve_kernel(int d, int k, const double* __restrict__ mult,
                                                          const double* __restrict__ fdiag,
