@@ -15,7 +15,11 @@
 //   band_accumulate_kernel  assemble_action's ascending-shift sum and polynomial part (:262-283)
 //   penta_factor_kernel /   pentadiag_solve (action.cpp:170-202) split into the band elimination
 //   penta_solve_kernel      (matrix only, one thread) and the per-column substitution
+#include <algorithm>
+
 #include "pf_common.cuh"
+#include "pf_kernels.h"
+#include "band_div.cuh"
 
 #ifndef PF_BAND_KR
 #define PF_BAND_KR 6
@@ -40,10 +44,11 @@ __global__ void band_scale_kernel(int d, const double* sub, const double* diag, 
 }
 
 // System z: shifted (c = shifts[z]): diag 1 - c a, sub / super -c a; else A itself (shifts null).
-// mult[z] (d - 1), fdiag[z] (d), fsup[z] (d - 1, the system's super-diagonal). fail[z] = the
-// ZeroPivot row or -1.
+// mult[z] (d - 1), fdiag[z] (d), fsup[z] (d - 1, the system's super-diagonal), frcp[z] (d,
+// band_rcp of the pivots; optional). fail[z] = the ZeroPivot row or -1.
 __global__ void band_factor_kernel(int d, int nsys, const double* sub, const double* diag, const double* super,
-                                   const double* shifts, double* mult, double* fdiag, double* fsup, int* fail) {
+                                   const double* shifts, double* mult, double* fdiag, double* fsup, double* frcp,
+                                   int* fail) {
   const int z = blockIdx.x * blockDim.x + threadIdx.x;
   if (z >= nsys) return;
   const double c = shifts ? shifts[z] : 0.0;
@@ -51,8 +56,10 @@ __global__ void band_factor_kernel(int d, int nsys, const double* sub, const dou
   double* mu = mult + (int64_t)z * (d > 1 ? d - 1 : 1);
   double* fd = fdiag + (int64_t)z * d;
   double* fs = fsup + (int64_t)z * (d > 1 ? d - 1 : 1);
+  double* fr = frcp ? frcp + (int64_t)z * d : nullptr;
   double prev = shifted ? __dsub_rn(1.0, __dmul_rn(c, diag[0])) : diag[0];
   fd[0] = prev;
+  if (fr) fr[0] = band_rcp(prev);
   int bad = -1;
   for (int i = 1; i < d; ++i) {
     const double l = shifted ? __dmul_rn(-c, sub[i - 1]) : sub[i - 1];
@@ -67,6 +74,7 @@ __global__ void band_factor_kernel(int d, int nsys, const double* sub, const dou
     mu[i - 1] = w;
     prev = __dsub_rn(dg, __dmul_rn(w, u));
     fd[i] = prev;
+    if (fr) fr[i] = band_rcp(prev);
   }
   if (bad < 0 && fabs(prev) <= kFloor) bad = d - 1;
   fail[z] = bad;
@@ -137,6 +145,590 @@ __global__ void __launch_bounds__(128) band_solve_kernel(int d, int k, const dou
       }
     }
   }
+}
+
+// One substep of the banded action, fused (action_eval, action.cpp:224-283, on every column):
+// CTA = one 32-column strip, warp t = factored shift t. Forward: each warp forms its RHS row by
+// row (residual: c_t * (A v)_i from a 3-row sliding window of V, the matvec in
+// TridiagMatrix::matvec order; plain: v_i), eliminates, and parks the forward result in Y[t].
+// Backward: each warp back-substitutes R rows at a time into shared memory; after one barrier
+// the whole CTA sums the R x 32 outputs over the terms in ascending shift index (acc from 0,
+// every product / sum separately rounded), adds the polynomial part and writes out. HBM passes
+// per substep: V twice, Y[t] twice per shift, out once (2P + 3) -- the unfused chain
+// (matvec, P solves writing / re-reading / rewriting X_t, a P-way accumulate) moves ~5P + 5.
+//
+// The recurrences are latency chains, so the streams feeding them run ahead through a per-warp
+// cp.async queue of S stages: a stage holds R rows of the warp's 32 columns (each lane copies its
+// own column, 8 bytes) plus the R rows of band coefficients those rows need (one scalar per lane,
+// lanes < 4R). S - 1 stages are in flight while the warp works on the oldest. Interior stages
+// take a bounds-free path (pointer increments, immediate offsets); the first and last stage of
+// each sweep take the checked one. The division by the pivot uses the pivot's reciprocal
+// (band_div.cuh: bit-identical to IEEE division, checked by tools/probe_div.cu).
+namespace {
+__device__ __forceinline__ void cp8(unsigned sa, const double* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+}  // namespace
+
+template <int G, int S, int R>
+constexpr size_t band_step_smem() {
+  return sizeof(double) * ((size_t)G * S * (R * 32 + 4 * R) + (size_t)S * R * 32);
+}
+
+template <int G, int S, int R>
+__global__ void __launch_bounds__(G * 32) band_action_step_kernel(
+    int d, int k, const double* __restrict__ ssub, const double* __restrict__ sdiag, const double* __restrict__ ssup,
+    const double* __restrict__ mult, const double* __restrict__ fdiag, const double* __restrict__ fsup,
+    const double* __restrict__ frcp, BandStep st, const double* __restrict__ V, int64_t ldv, double* __restrict__ Y,
+    double* __restrict__ out, int64_t ldo) {
+  constexpr int QS = R * 32 + 4 * R;  // one queue stage: R data rows, then 4 coefficient rows of R
+  extern __shared__ double smem[];
+  const int t = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* q = smem + (size_t)t * S * QS;
+  double* vq = smem + (size_t)G * S * QS;  // [S][R][32] V rows for the backward sums
+  const unsigned q_sa = smem_u32(q), vq_sa = smem_u32(vq);
+  const int col0 = blockIdx.x * 32;
+  const int colc = min(col0 + lane, k - 1);  // dead lanes mirror the last column (Y is padded; out skips them)
+  const int64_t dm1 = d > 1 ? d - 1 : 1;
+  const double* __restrict__ mu = mult + t * dm1;
+  const double* __restrict__ fd = fdiag + (int64_t)t * d;
+  const double* __restrict__ fs = fsup + t * dm1;
+  const double* __restrict__ fr = frcp + (int64_t)t * d;
+  // Y is the kernel's own scratch, blocked per warp (row i of the warp's 32 columns at i * 32):
+  // each warp streams one contiguous region instead of 256-byte pieces 8 k bytes apart
+  double* __restrict__ y = Y + ((int64_t)blockIdx.x * G + t) * d * 32 + lane;
+  const double* __restrict__ v = V + colc;
+  const double c = st.c[t];
+  const bool residual = st.residual != 0;
+  const int nbf = (d + R - 1) / R;
+
+  // ---- forward. Stage b, slot u: row j = bR + u of V, and the coefficients of row i = j - 1
+  // (mult_{i-1}, diag_i, sub_{i-1}, super_i), the row completed when v_j arrives. Lane
+  // l < 4R copies coefficient kind l / R of slot l % R.
+  const int ckind = lane / R, cu = lane % R;
+  const int ncoef_f = (residual ? 4 : 1) * R;
+  const double* cbase_f = ckind == 0 ? mu + cu - 2 : ckind == 1 ? sdiag + cu - 1 : ckind == 2 ? ssub + cu - 2 : ssup + cu - 1;
+  auto issue_fwd = [&](int b) {
+    if (b < nbf) {
+      const unsigned sa = q_sa + (unsigned)((b % S) * QS * 8);
+      const int j0 = b * R;
+      if (b >= 1 && j0 + R <= d) {
+        const double* p = v + (int64_t)j0 * ldv;
+#pragma unroll
+        for (int u = 0; u < R; ++u, p += ldv) cp8(sa + (u * 32 + lane) * 8, p);
+        if (lane < ncoef_f) cp8(sa + (R * 32 + lane) * 8, cbase_f + j0);
+      } else {
+#pragma unroll
+        for (int u = 0; u < R; ++u)
+          if (j0 + u < d) cp8(sa + (u * 32 + lane) * 8, v + (int64_t)(j0 + u) * ldv);
+        const int i = j0 + cu - 1;
+        if (lane < ncoef_f && i >= 0 && i < d - 1 && (i >= 1 || ckind == 1 || ckind == 3))
+          cp8(sa + (R * 32 + lane) * 8, cbase_f + j0);
+      }
+    }
+    cp_commit();  // empty groups keep the wait count uniform
+  };
+  double prev = 0.0, vim1 = 0.0, vi = 0.0;
+  // row i of the forward sweep from (v_{i-1}, v_i, v_{i+1}) and its coefficients
+  auto row_fwd = [&](int i, double m, double ad, double as, double ap, double vip1) {
+    double r = vi;
+    if (residual) {
+      double acc = __dmul_rn(ad, vi);
+      if (i > 0) acc = __dadd_rn(acc, __dmul_rn(as, vim1));
+      if (i + 1 < d) acc = __dadd_rn(acc, __dmul_rn(ap, vip1));
+      r = __dmul_rn(c, acc);
+    }
+    prev = i == 0 ? r : __dsub_rn(r, __dmul_rn(m, prev));
+  };
+#pragma unroll
+  for (int b = 0; b < S - 1; ++b) issue_fwd(b);
+  for (int b = 0; b < nbf; ++b) {
+    issue_fwd(b + S - 1);
+    cp_wait<S - 1>();
+    __syncwarp();
+    const double* sq = q + (b % S) * QS;
+    const int j0 = b * R;
+    double* yb = y + (int64_t)(j0 - 1) * 32;
+    if (b >= 1 && j0 + R <= d) {
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        const double vj = sq[u * 32 + lane];
+        const double* cf = sq + R * 32 + u;
+        const double m = cf[0];
+        if (residual) {
+          const double acc = __dadd_rn(__dadd_rn(__dmul_rn(cf[R], vi), __dmul_rn(cf[2 * R], vim1)),
+                                       __dmul_rn(cf[3 * R], vj));
+          prev = __dsub_rn(__dmul_rn(c, acc), __dmul_rn(m, prev));
+        } else {
+          prev = __dsub_rn(vi, __dmul_rn(m, prev));
+        }
+        __stcg(yb + u * 32, prev);
+        vim1 = vi;
+        vi = vj;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        const int j = j0 + u;
+        if (j < d) {
+          const double vj = sq[u * 32 + lane];
+          if (j > 0) {
+            const double* cf = sq + R * 32 + u;
+            row_fwd(j - 1, cf[0], residual ? cf[R] : 0.0, residual ? cf[2 * R] : 0.0, residual ? cf[3 * R] : 0.0, vj);
+            __stcg(yb + u * 32, prev);
+          }
+          vim1 = vi;
+          vi = vj;
+        }
+      }
+    }
+    __syncwarp();  // the slot is refilled by a later issue
+  }
+  // row d - 1 (kept in the register; Y holds rows 0 .. d - 2)
+  row_fwd(d - 1, d > 1 ? mu[d - 2] : 0.0, residual ? sdiag[d - 1] : 0.0, (residual && d > 1) ? ssub[d - 2] : 0.0, 0.0,
+          0.0);
+  __threadfence_block();  // this thread's Y stores precede its own cp.async reads of them
+
+  // ---- backward. Stage b, slot u: row i = d - 1 - bR - u: Y_i (i < d - 1), super_i, fdiag_i,
+  // 1 / fdiag_i in the warp's queue; V_i (all 32 columns, row u copied by warp u % G) in the
+  // CTA's ring vq. The back-substituted x_i overwrites Y_i in the slot, where the whole CTA sums
+  // it after the barrier; a stage is therefore refilled only after the next barrier.
+  const int nbb = nbf;
+  const double* cbase_b = (ckind == 0 ? fs : ckind == 1 ? fd : fr) + (d - 1 - cu);
+  auto issue_bwd = [&](int b) {
+    if (b < nbb) {
+      const int slot = b % S;
+      const unsigned sa = q_sa + (unsigned)(slot * QS * 8);
+      const int i0 = d - 1 - b * R;
+      if (b >= 1 && i0 - (R - 1) >= 0) {
+        const double* py = y + (int64_t)i0 * 32;
+#pragma unroll
+        for (int u = 0; u < R; ++u) cp8(sa + (u * 32 + lane) * 8, py - u * 32);
+#pragma unroll
+        for (int u = 0; u < R; ++u)
+          if (u % G == t) cp8(vq_sa + ((slot * R + u) * 32 + lane) * 8, v + (int64_t)(i0 - u) * ldv);
+        if (lane < 3 * R) cp8(sa + (R * 32 + lane) * 8, cbase_b - b * R);
+      } else {
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+          const int i = i0 - u;
+          if (i >= 0 && i < d - 1) cp8(sa + (u * 32 + lane) * 8, y + (int64_t)i * 32);
+          if (u % G == t && i >= 0) cp8(vq_sa + ((slot * R + u) * 32 + lane) * 8, v + (int64_t)i * ldv);
+        }
+        const int i = i0 - cu;
+        if (lane < 3 * R && i >= 0 && (ckind != 0 || i < d - 1)) cp8(sa + (R * 32 + lane) * 8, cbase_b - b * R);
+      }
+    }
+    cp_commit();
+  };
+#pragma unroll
+  for (int b = 0; b < S - 1; ++b) issue_bwd(b);
+  const bool direct = st.direct != 0;
+  double nxt = 0.0;
+  for (int b = 0; b < nbb; ++b) {
+    cp_wait<S - 2>();  // stages <= b landed (this thread's copies)
+    __syncwarp();
+    const int slot = b % S;
+    double* sq = q + slot * QS;
+    const int i0 = d - 1 - b * R;
+    if (b >= 1 && i0 - (R - 1) >= 0) {
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        const double* cf = sq + R * 32 + u;
+        nxt = div_rcp(__dsub_rn(sq[u * 32 + lane], __dmul_rn(cf[0], nxt)), cf[R], cf[2 * R]);
+        sq[u * 32 + lane] = nxt;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        const int i = i0 - u;
+        if (i >= 0) {
+          const double* cf = sq + R * 32 + u;
+          nxt = i == d - 1 ? div_rcp(prev, cf[R], cf[2 * R])
+                           : div_rcp(__dsub_rn(sq[u * 32 + lane], __dmul_rn(cf[0], nxt)), cf[R], cf[2 * R]);
+          sq[u * 32 + lane] = nxt;
+        }
+      }
+    }
+    __syncthreads();  // every warp's x rows and the V rows of stage b visible; stage b - 1 drained
+    issue_bwd(b + S - 1);
+    const double* vs = vq + slot * R * 32;
+    for (int o = threadIdx.x; o < R * 32; o += G * 32) {
+      const int u = o >> 5, ln = o & 31, i = i0 - u, cc = col0 + ln;
+      if (i < 0 || cc >= k) continue;
+      const double vv = vs[u * 32 + ln];
+      const double* xs = smem + (size_t)slot * QS + u * 32 + ln;  // warp g's x at xs[g * S * QS]
+      double acc = 0.0;
+      if (direct) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) acc = __dadd_rn(acc, __dmul_rn(xs[(size_t)g * S * QS], st.w[g]));
+      } else {
+        for (int qq = 0; qq < st.n_terms; ++qq) {
+          const double xv = st.slot[qq] >= 0 ? xs[(size_t)st.slot[qq] * S * QS] : vv;
+          acc = __dadd_rn(acc, __dmul_rn(xv, st.w[qq]));
+        }
+      }
+      if (st.add_poly) {
+        acc = __dadd_rn(acc, __dmul_rn(st.constant, vv));
+        if (st.hybrid) {
+          // (A v)_{i-1..i+1} and (A^2 v)_i in TridiagMatrix::matvec order, from V rows i-2..i+2
+          auto av_at = [&](int r) {
+            double a = __dmul_rn(sdiag[r], V[(int64_t)r * ldv + cc]);
+            if (r > 0) a = __dadd_rn(a, __dmul_rn(ssub[r - 1], V[(int64_t)(r - 1) * ldv + cc]));
+            if (r + 1 < d) a = __dadd_rn(a, __dmul_rn(ssup[r], V[(int64_t)(r + 1) * ldv + cc]));
+            return a;
+          };
+          const double av = av_at(i);
+          double a2v = __dmul_rn(sdiag[i], av);
+          if (i > 0) a2v = __dadd_rn(a2v, __dmul_rn(ssub[i - 1], av_at(i - 1)));
+          if (i + 1 < d) a2v = __dadd_rn(a2v, __dmul_rn(ssup[i], av_at(i + 1)));
+          acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(st.d1, av), __dmul_rn(st.d2, a2v)));
+        }
+      }
+      __stcs(out + (int64_t)i * ldo + cc, acc);
+    }
+  }
+  cp_wait<0>();  // drain (empty) groups before exit
+}
+
+// Per-row coefficient records for band_action_bulk_kernel (32 bytes each, so a stage's rows are
+// one contiguous bulk copy). Forward record j of system z holds what row i = j - 1 needs when
+// v_j arrives: {mult_{i-1}, diag_i, sub_{i-1}, super_i} of the scaled A (0 where undefined).
+// Backward record i: {super_i of M_z (0 at i = d - 1), fdiag_i, band_rcp(fdiag_i), 0}.
+__global__ void band_pack_records_kernel(int d, int nsys, const double* __restrict__ ssub,
+                                         const double* __restrict__ sdiag, const double* __restrict__ ssup,
+                                         const double* __restrict__ mult, const double* __restrict__ fdiag,
+                                         const double* __restrict__ fsup, const double* __restrict__ frcp,
+                                         double4* __restrict__ frec, double4* __restrict__ brec) {
+  const int64_t dm1 = d > 1 ? d - 1 : 1;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)nsys * d;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int z = (int)(idx / d), j = (int)(idx % d), i = j - 1;
+    double4 f;
+    f.x = i >= 1 ? mult[z * dm1 + i - 1] : 0.0;
+    f.y = i >= 0 ? sdiag[i] : 0.0;
+    f.z = i >= 1 ? ssub[i - 1] : 0.0;
+    f.w = (i >= 0 && i + 1 < d) ? ssup[i] : 0.0;
+    frec[idx] = f;
+    double4 b;
+    b.x = j + 1 < d ? fsup[z * dm1 + j] : 0.0;
+    b.y = fdiag[(int64_t)z * d + j];
+    b.z = frcp[(int64_t)z * d + j];
+    b.w = 0.0;
+    brec[idx] = b;
+  }
+}
+
+void launch_band_pack_records(int d, int nsys, const double* ssub, const double* sdiag, const double* ssup,
+                              const double* mult, const double* fdiag, const double* fsup, const double* frcp,
+                              double* frec, double* brec, cudaStream_t s) {
+  const int64_t n = (int64_t)nsys * d;
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 4736));
+  band_pack_records_kernel<<<blocks, 256, 0, s>>>(d, nsys, ssub, sdiag, ssup, mult, fdiag, fsup, frcp,
+                                                  reinterpret_cast<double4*>(frec), reinterpret_cast<double4*>(brec));
+}
+
+// The same fused substep with the queue filled by the bulk-copy engine (cp.async.bulk, completion
+// on a per-warp mbarrier per stage): a stage is one copy of the warp's R Y rows (contiguous in the
+// blocked layout), one copy of the R coefficient records, and R row copies of V (one per lane,
+// 8 * (columns in the strip) bytes each) -- a handful of instructions per stage instead of one
+// per row per lane. Needs 16-byte aligned V rows (V aligned, ldv and k even); otherwise the
+// host takes band_action_step_kernel.
+namespace {
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
+}  // namespace
+
+template <int G, int S, int R>
+constexpr size_t band_bulk_smem() {
+  return sizeof(double) * ((size_t)G * S * (R * 32 + 4 * R) + (size_t)S * R * 32) + sizeof(uint64_t) * G * S;
+}
+
+template <int G, int S, int R>
+__global__ void __launch_bounds__(G * 32) band_action_bulk_kernel(
+    int d, int k, const double* __restrict__ ssub, const double* __restrict__ sdiag, const double* __restrict__ ssup,
+    const double* __restrict__ mult, const double4* __restrict__ frec, const double4* __restrict__ brec, BandStep st,
+    const double* __restrict__ V, int64_t ldv, double* __restrict__ Y, double* __restrict__ out, int64_t ldo) {
+  constexpr int QS = R * 32 + 4 * R;  // one stage: R data rows (32 columns), then R 4-double records
+  extern __shared__ __align__(128) double smem[];
+  // warp index through a shuffle: provably warp-uniform, so the bulk-copy operands derived from it
+  // live in uniform registers (no per-lane waterfall around UBLKCP)
+  const int t = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  double* q = smem + (size_t)t * S * QS;
+  double* vq = smem + (size_t)G * S * QS;  // [S][R][32] V rows for the backward sums
+  uint64_t* bars = reinterpret_cast<uint64_t*>(vq + S * R * 32);
+  const unsigned q_sa = smem_u32(q), vq_sa = smem_u32(vq), bar_sa = smem_u32(bars + t * S);
+  const int col0 = blockIdx.x * 32, ncols = min(32, k - col0);
+  const unsigned row_bytes = 8u * (unsigned)ncols;
+  const int64_t dm1 = d > 1 ? d - 1 : 1;
+  double* __restrict__ yw = Y + ((int64_t)blockIdx.x * G + t) * d * 32;  // the warp's blocked Y region
+  const double* __restrict__ vstrip = V + col0;
+  const double4* __restrict__ fr4 = frec + (int64_t)t * d;
+  const double4* __restrict__ br4 = brec + (int64_t)t * d;
+  const double c = st.c[t];
+  const bool residual = st.residual != 0;
+  const int nbf = (d + R - 1) / R;
+  if (lane < S) mbar_init(bar_sa + 8 * lane, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncwarp();
+
+  // stage n (forward b = n, backward b = n - nbf) lives in slot n % S, phase parity (n / S) & 1
+  auto issue_fwd = [&](int b) {
+    if (b >= nbf) return;
+    const int slot = b % S;
+    const unsigned sa = q_sa + (unsigned)(slot * QS * 8), bar = bar_sa + 8 * slot;
+    const int j0 = b * R, nr = min(R, d - j0);
+    if (lane == 0) {
+      mbar_expect(bar, (unsigned)nr * (row_bytes + 32u));
+      const double* src = vstrip + (int64_t)j0 * ldv;
+      for (int u = 0; u < nr; ++u, src += ldv) bulk_g2s(sa + u * 256, src, row_bytes, bar);
+      bulk_g2s(sa + R * 256, fr4 + j0, (unsigned)nr * 32u, bar);
+    }
+  };
+  auto issue_bwd = [&](int b) {
+    if (b >= nbf) return;
+    const int n = nbf + b, slot = n % S;
+    const unsigned sa = q_sa + (unsigned)(slot * QS * 8), bar = bar_sa + 8 * slot;
+    const int i0 = d - 1 - b * R, base = i0 - (R - 1);  // slot position p holds row base + p
+    const int lo = max(base, 0), hi_y = min(i0, d - 2);
+    const int ny = max(hi_y - lo + 1, 0), nrec = i0 - lo + 1;
+    const bool vrows = b % G == t;
+    if (lane == 0) {
+      mbar_expect(bar, (unsigned)ny * 256u + (unsigned)nrec * 32u + (vrows ? (unsigned)nrec * row_bytes : 0u));
+      if (ny > 0) bulk_g2s(sa + (lo - base) * 256, yw + (int64_t)lo * 32, (unsigned)ny * 256u, bar);
+      bulk_g2s(sa + R * 256 + (lo - base) * 32, br4 + lo, (unsigned)nrec * 32u, bar);
+      if (vrows) {
+        const double* src = vstrip + (int64_t)lo * ldv;
+        for (int p = lo - base; p < R; ++p, src += ldv)
+          bulk_g2s(vq_sa + (unsigned)((slot * R + p) * 256), src, row_bytes, bar);
+      }
+    }
+  };
+
+  // ---- forward (slot position u = row j0 + u; record u = the coefficients of row j0 + u - 1)
+#pragma unroll
+  for (int b = 0; b < S - 1; ++b) issue_fwd(b);
+  double prev = 0.0, vim1 = 0.0, vi = 0.0;
+  double* yl = yw + lane;
+  for (int b = 0; b < nbf; ++b) {
+    issue_fwd(b + S - 1);
+    const int slot = b % S;
+    mbar_wait(bar_sa + 8 * slot, (unsigned)(b / S) & 1u);
+    const double* sq = q + slot * QS;
+    const double4* rec = reinterpret_cast<const double4*>(sq + R * 32);
+    const int j0 = b * R;
+    double* yb = yl + (int64_t)(j0 - 1) * 32;
+    if (b >= 1 && j0 + R <= d) {
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        const double vj = sq[u * 32 + lane];
+        const double4 cf = rec[u];
+        if (residual) {
+          const double acc = __dadd_rn(__dadd_rn(__dmul_rn(cf.y, vi), __dmul_rn(cf.z, vim1)), __dmul_rn(cf.w, vj));
+          prev = __dsub_rn(__dmul_rn(c, acc), __dmul_rn(cf.x, prev));
+        } else {
+          prev = __dsub_rn(vi, __dmul_rn(cf.x, prev));
+        }
+        __stcg(yb + u * 32, prev);
+        vim1 = vi;
+        vi = vj;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        const int j = j0 + u;
+        if (j < d) {
+          const double vj = sq[u * 32 + lane];
+          if (j > 0) {
+            const int i = j - 1;
+            const double4 cf = rec[u];
+            double r = vi;
+            if (residual) {
+              double acc = __dmul_rn(cf.y, vi);
+              if (i > 0) acc = __dadd_rn(acc, __dmul_rn(cf.z, vim1));
+              acc = __dadd_rn(acc, __dmul_rn(cf.w, vj));  // i + 1 = j < d
+              r = __dmul_rn(c, acc);
+            }
+            prev = i == 0 ? r : __dsub_rn(r, __dmul_rn(cf.x, prev));
+            __stcg(yb + u * 32, prev);
+          }
+          vim1 = vi;
+          vi = vj;
+        }
+      }
+    }
+    __syncwarp();  // every lane is done with the slot before a later issue refills it
+  }
+  {  // row d - 1 (kept in the register; Y holds rows 0 .. d - 2)
+    const int i = d - 1;
+    double r = vi;
+    if (residual) {
+      double acc = __dmul_rn(sdiag[i], vi);
+      if (i > 0) acc = __dadd_rn(acc, __dmul_rn(ssub[i - 1], vim1));
+      r = __dmul_rn(c, acc);
+    }
+    prev = i == 0 ? r : __dsub_rn(r, __dmul_rn(mult[t * dm1 + i - 1], prev));
+  }
+  fence_proxy_async_global();  // the Y stores above are read back by the bulk copies below
+  __syncwarp();
+
+  // ---- backward (slot position p = row base + p, base = i0 - R + 1; the x rows overwrite Y rows
+  // in place and are summed by the whole CTA after the barrier)
+#pragma unroll
+  for (int b = 0; b < S - 1; ++b) issue_bwd(b);
+  const bool direct = st.direct != 0;
+  double nxt = 0.0;
+  for (int b = 0; b < nbf; ++b) {
+    const int n = nbf + b, slot = n % S;
+    mbar_wait(bar_sa + 8 * slot, (unsigned)(n / S) & 1u);
+    double* sq = q + slot * QS;
+    const double4* rec = reinterpret_cast<const double4*>(sq + R * 32);
+    const int i0 = d - 1 - b * R;
+    if (b >= 1 && i0 - (R - 1) >= 0) {
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        const int p = R - 1 - u;
+        const double4 cf = rec[p];
+        nxt = div_rcp(__dsub_rn(sq[p * 32 + lane], __dmul_rn(cf.x, nxt)), cf.y, cf.z);
+        sq[p * 32 + lane] = nxt;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        const int i = i0 - u, p = R - 1 - u;
+        if (i >= 0) {
+          const double4 cf = rec[p];
+          nxt = i == d - 1 ? div_rcp(prev, cf.y, cf.z)
+                           : div_rcp(__dsub_rn(sq[p * 32 + lane], __dmul_rn(cf.x, nxt)), cf.y, cf.z);
+          sq[p * 32 + lane] = nxt;
+        }
+      }
+    }
+    fence_proxy_async_smem();  // the x rows (generic stores) precede the bulk refill of this slot
+    __syncthreads();           // every warp's x rows and stage b's V rows visible; stage b - 1 drained
+    issue_bwd(b + S - 1);
+    const double* vs = vq + slot * R * 32;
+    for (int o = threadIdx.x; o < R * 32; o += G * 32) {
+      const int u = o >> 5, ln = o & 31, i = i0 - u, p = R - 1 - u, cc = col0 + ln;
+      if (i < 0 || cc >= k) continue;
+      const double vv = vs[p * 32 + ln];
+      const double* xs = smem + (size_t)slot * QS + p * 32 + ln;  // warp g's x at xs[g * S * QS]
+      double acc = 0.0;
+      if (direct) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) acc = __dadd_rn(acc, __dmul_rn(xs[(size_t)g * S * QS], st.w[g]));
+      } else {
+        for (int qq = 0; qq < st.n_terms; ++qq) {
+          const double xv = st.slot[qq] >= 0 ? xs[(size_t)st.slot[qq] * S * QS] : vv;
+          acc = __dadd_rn(acc, __dmul_rn(xv, st.w[qq]));
+        }
+      }
+      if (st.add_poly) {
+        acc = __dadd_rn(acc, __dmul_rn(st.constant, vv));
+        if (st.hybrid) {
+          auto av_at = [&](int r) {
+            double a = __dmul_rn(sdiag[r], V[(int64_t)r * ldv + cc]);
+            if (r > 0) a = __dadd_rn(a, __dmul_rn(ssub[r - 1], V[(int64_t)(r - 1) * ldv + cc]));
+            if (r + 1 < d) a = __dadd_rn(a, __dmul_rn(ssup[r], V[(int64_t)(r + 1) * ldv + cc]));
+            return a;
+          };
+          const double av = av_at(i);
+          double a2v = __dmul_rn(sdiag[i], av);
+          if (i > 0) a2v = __dadd_rn(a2v, __dmul_rn(ssub[i - 1], av_at(i - 1)));
+          if (i + 1 < d) a2v = __dadd_rn(a2v, __dmul_rn(ssup[i], av_at(i + 1)));
+          acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(st.d1, av), __dmul_rn(st.d2, a2v)));
+        }
+      }
+      __stcs(out + (int64_t)i * ldo + cc, acc);
+    }
+  }
+}
+
+
+#ifndef PF_BAND_STAGES
+#define PF_BAND_STAGES 5
+#endif
+#ifndef PF_BAND_ROWS
+#define PF_BAND_ROWS 4
+#endif
+
+cudaError_t launch_band_action_step(int P, int d, int k, const double* ssub, const double* sdiag, const double* ssup,
+                                    const double* mult, const double* fdiag, const double* fsup, const double* frcp,
+                                    const double* frec, const double* brec, const BandStep& st, const double* V,
+                                    int64_t ldv, double* Y, double* out, int64_t ldo, cudaStream_t s) {
+  constexpr int S = PF_BAND_STAGES, R = PF_BAND_ROWS;
+  const dim3 grid((k + 31) / 32);
+  // bulk copies need 16-byte aligned rows; they win once the grid is at least two CTAs per SM
+  // (k 16384: 4.7 vs 5.5 ms a substep), the per-lane queue wins on small grids where each warp's
+  // latency chain is the whole story (k 256 / 4096)
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool bulk = frec && brec && (reinterpret_cast<uintptr_t>(V) & 15) == 0 && ldv % 2 == 0 && k % 2 == 0 &&
+                    (int64_t)grid.x >= 2 * (int64_t)sms;
+  switch (P) {
+#define PF_BAND_CASE(G)                                                                                           \
+  case G:                                                                                                         \
+    if (bulk) {                                                                                                   \
+      auto fn = band_action_bulk_kernel<G, S, R>;                                                                 \
+      constexpr size_t smem = band_bulk_smem<G, S, R>();                                                          \
+      set_smem_attr_once(reinterpret_cast<const void*>(fn), (int)smem);                                           \
+      fn<<<grid, G * 32, smem, s>>>(d, k, ssub, sdiag, ssup, mult, reinterpret_cast<const double4*>(frec),        \
+                                    reinterpret_cast<const double4*>(brec), st, V, ldv, Y, out, ldo);             \
+    } else {                                                                                                      \
+      auto fn = band_action_step_kernel<G, S, R>;                                                                 \
+      constexpr size_t smem = band_step_smem<G, S, R>();                                                          \
+      set_smem_attr_once(reinterpret_cast<const void*>(fn), (int)smem);                                           \
+      fn<<<grid, G * 32, smem, s>>>(d, k, ssub, sdiag, ssup, mult, fdiag, fsup, frcp, st, V, ldv, Y, out, ldo);   \
+    }                                                                                                             \
+    break;
+    PF_BAND_CASE(1)
+    PF_BAND_CASE(2)
+    PF_BAND_CASE(3)
+    PF_BAND_CASE(4)
+    PF_BAND_CASE(5)
+    PF_BAND_CASE(6)
+    PF_BAND_CASE(7)
+    PF_BAND_CASE(8)
+    PF_BAND_CASE(9)
+    PF_BAND_CASE(10)
+    PF_BAND_CASE(11)
+    PF_BAND_CASE(12)
+#undef PF_BAND_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
 }
 
 // Out = A V (TridiagMatrix::matvec order: diag v_i, + sub v_{i-1}, + super v_{i+1})

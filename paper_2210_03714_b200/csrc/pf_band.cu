@@ -2,6 +2,7 @@
 // Replaces thomas_solve / TridiagFactor / pentadiag_solve / action_eval / ActionOperator /
 // substep_action (proj/core/src/action.cpp:100-339) for blocks of vectors.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -11,7 +12,8 @@ namespace pf {
 __global__ void band_scale_kernel(int d, const double* sub, const double* diag, const double* super, double s,
                                   double* osub, double* odiag, double* osuper);
 __global__ void band_factor_kernel(int d, int nsys, const double* sub, const double* diag, const double* super,
-                                   const double* shifts, double* mult, double* fdiag, double* fsup, int* fail);
+                                   const double* shifts, double* mult, double* fdiag, double* fsup, double* frcp,
+                                   int* fail);
 __global__ void band_solve_kernel(int d, int k, const double* mult, const double* fdiag, const double* fsup,
                                   const double* src, int64_t lds, const double* rhs_scale, double* X, int64_t ldx,
                                   int64_t strideX);
@@ -45,14 +47,14 @@ int zero_pivot(pf_status* st, int shift_index, int row) {
 
 // factor nsys systems (shifted by d_shifts when given); returns the first failing system or -1
 int factor(pf_context* ctx, int d, int nsys, const double* sub, const double* diag, const double* super,
-           const double* d_shifts, double* mult, double* fdiag, double* fsup, int* row, int* rc) {
+           const double* d_shifts, double* mult, double* fdiag, double* fsup, double* frcp, int* row, int* rc) {
   int* d_fail = static_cast<int*>(workspace(ctx, kWsSmallArrays + 40, sizeof(int) * std::max(nsys, 1)));
   if (!d_fail) {
     *rc = PF_ERR_CUDA;
     return -1;
   }
   pf::band_factor_kernel<<<(nsys + 31) / 32, 32, 0, ctx->stream>>>(d, nsys, sub, diag, super, d_shifts, mult, fdiag,
-                                                                     fsup, d_fail);
+                                                                     fsup, frcp, d_fail);
   ctx->launches++;
   std::vector<int> fail(nsys);
   cudaMemcpyAsync(fail.data(), d_fail, sizeof(int) * nsys, cudaMemcpyDeviceToHost, ctx->stream);
@@ -93,7 +95,7 @@ int pf_thomas_solve_batched(pf_context* ctx, int d, int k, const double* dSub, c
   if (!F) return PF_ERR_CUDA;
   double *mult = F, *fdiag = F + dm1, *fsup = F + dm1 + d;
   int row = 0, rc = PF_OK;
-  const int z = factor(ctx, d, 1, dSub, dDiag, dSuper, nullptr, mult, fdiag, fsup, &row, &rc);
+  const int z = factor(ctx, d, 1, dSub, dDiag, dSuper, nullptr, mult, fdiag, fsup, nullptr, &row, &rc);
   if (rc) return rc;
   if (z >= 0) return zero_pivot(status, 0, row);
   if (k == 0) return PF_OK;
@@ -144,22 +146,24 @@ int pf_tridiag_action(pf_context* ctx, const pf_method* m, int d, int k, const d
   const int P = (int)sh.size();
   const size_t blk = (size_t)d * k;
   double* A3 = static_cast<double*>(workspace(ctx, kWsBandA, sizeof(double) * (size_t)(d + 2 * dm1)));
-  double* F = static_cast<double*>(workspace(ctx, kWsBandF, sizeof(double) * (size_t)(d + 2 * dm1) * std::max(P, 1)));
-  double* Y = static_cast<double*>(workspace(ctx, kWsBandY, sizeof(double) * blk * std::max(P, 1)));
+  double* F = static_cast<double*>(workspace(ctx, kWsBandF, sizeof(double) * (size_t)(2 * d + 2 * dm1) * std::max(P, 1)));
+  // P solutions (unfused: P x d x k) or the fused kernel's per-warp forward scratch (P x d x 32 per strip)
+  const size_t kpad = (size_t)(k + 31) / 32 * 32;
+  double* Y = static_cast<double*>(workspace(ctx, kWsBandY, sizeof(double) * (size_t)d * kpad * std::max(P, 1)));
   double* XB = static_cast<double*>(workspace(ctx, kWsBandX, sizeof(double) * blk * 4));
   if (!A3 || !F || !Y || !XB) return PF_ERR_CUDA;
   double *ssub = A3, *sdiag = A3 + dm1, *ssup = A3 + dm1 + d;
   pf::band_scale_kernel<<<blocks_for(d), 256, 0, ctx->stream>>>(d, dSub, dDiag, dSuper, 1.0 / substeps, ssub, sdiag,
                                                                  ssup);
   ctx->launches++;
-  double *mult = F, *fdiag = F + dm1 * P, *fsup = F + dm1 * P + (int64_t)d * P;
+  double *mult = F, *fdiag = F + dm1 * P, *fsup = F + dm1 * P + (int64_t)d * P, *frcp = fsup + dm1 * P;
   double* d_sh = nullptr;
   if (P > 0) {
     d_sh = static_cast<double*>(workspace(ctx, kWsSmallArrays + 41, sizeof(double) * P));
     if (!d_sh) return PF_ERR_CUDA;
     cudaMemcpyAsync(d_sh, sh.data(), sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream);
     int row = 0, rc = PF_OK;
-    const int z = factor(ctx, d, P, ssub, sdiag, ssup, d_sh, mult, fdiag, fsup, &row, &rc);
+    const int z = factor(ctx, d, P, ssub, sdiag, ssup, d_sh, mult, fdiag, fsup, frcp, &row, &rc);
     if (rc) return rc;
     if (z >= 0) return zero_pivot(status, sh_index[z] + 1, row);  // "shift i: zero pivot at row r"
   }
@@ -188,6 +192,54 @@ int pf_tridiag_action(pf_context* ctx, const pf_method* m, int d, int k, const d
   const double constant = residual ? m->constant[0] : (hybrid ? m->poly[0] : 0.0);
   const double d1 = hybrid ? m->poly[1] : 0.0, d2 = hybrid ? m->poly[2] : 0.0;
   double *X = XB, *Xn = XB + blk, *AV = XB + 2 * blk, *A2V = XB + 3 * blk;
+  static const bool unfused = std::getenv("PF_BAND_UNFUSED") != nullptr;    // A/B switches
+  static const bool bulk_ok = std::getenv("PF_BAND_NO_BULK") == nullptr;
+  if (P >= 1 && P <= pf::kBandMaxShifts && nt <= pf::kBandMaxTerms && !unfused) {
+    // fused substeps (band.cu band_action_step_kernel): substep s reads its V (dV for s = 0) and
+    // writes the next one (dOut for the last, unless dOut overlaps dV's rows)
+    pf::BandStep bs{};
+    bs.n_terms = nt;
+    for (int q = 0; q < nt; ++q) {
+      bs.slot[q] = slot[q];
+      bs.w[q] = w[q];
+    }
+    for (int z = 0; z < P; ++z) bs.c[z] = sh[z];
+    bs.residual = residual;
+    bs.add_poly = add_poly;
+    bs.hybrid = hybrid;
+    bs.constant = constant;
+    bs.d1 = d1;
+    bs.d2 = d2;
+    bs.direct = nt == P;
+    for (int q = 0; q < nt; ++q) bs.direct = bs.direct && slot[q] == q;
+    double* rec = static_cast<double*>(workspace(ctx, kWsBandRec, sizeof(double) * 8 * (size_t)d * P));
+    if (!rec) return PF_ERR_CUDA;
+    double *frec = rec, *brec = rec + (size_t)4 * d * P;
+    pf::launch_band_pack_records(d, P, ssub, sdiag, ssup, mult, fdiag, fsup, frcp, frec, brec, ctx->stream);
+    ctx->launches++;
+    const char *v0 = reinterpret_cast<const char*>(dV), *v1 = v0 + sizeof(double) * ((d - 1) * ldv + k);
+    const char *o0 = reinterpret_cast<const char*>(dOut), *o1 = o0 + sizeof(double) * ((d - 1) * ldo + k);
+    const bool overlap = o0 < v1 && v0 < o1;
+    const double* src = dV;
+    int64_t lds = ldv;
+    for (int step = 0; step < substeps; ++step) {
+      const bool last = step + 1 == substeps;
+      double* dst = (last && !overlap) ? dOut : Xn;
+      const int64_t ldd = dst == dOut ? ldo : k;
+      cudaError_t e = pf::launch_band_action_step(P, d, k, ssub, sdiag, ssup, mult, fdiag, fsup, frcp,
+                                                  bulk_ok ? frec : nullptr, brec, bs, src, lds, Y, dst, ldd,
+                                                  ctx->stream);
+      ctx->launches++;
+      if (e != cudaSuccess) return cuda_fail(e);
+      src = dst;
+      lds = ldd;
+      std::swap(X, Xn);
+    }
+    if (overlap)
+      cudaMemcpy2DAsync(dOut, sizeof(double) * ldo, src, sizeof(double) * k, sizeof(double) * k, d,
+                        cudaMemcpyDeviceToDevice, ctx->stream);
+    return collect_status(ctx, 0, flags, status);
+  }
   cudaMemcpy2DAsync(X, sizeof(double) * k, dV, sizeof(double) * ldv, sizeof(double) * k, d, cudaMemcpyDeviceToDevice,
                     ctx->stream);
   for (int step = 0; step < substeps; ++step) {

@@ -92,8 +92,9 @@ enum Slot {
   kWsBandF = 28,
   kWsBandY = 29,
   kWsBandX = 30,
+  kWsBandRec = 31,      // banded action: per-row coefficient records of the bulk-copy kernel
   kWsScratch = 20,      // per-SM accumulator slots of the small kernel
-  kWsSmallArrays = 64,  // small uploaded tables: kWsSmallArrays + i, i < 32
+  kWsSmallArrays = 64,  // small uploaded tables: kWsSmallArrays + i (slots grow on demand)
 };
 
 // Large-n evaluation (pf_large.cu): outs[s] = r_s(2^-j A_b) for every weight set, any n.

@@ -88,4 +88,28 @@ void launch_sum_diff(int64_t count, const double* C, const double* S, double* D,
 // squarings from norms: j_b = smallest j >= 0 with ldexp(norm_b, -j) <= theta
 void launch_squarings(int batch, const double* norms, double theta, int* j, cudaStream_t stream);
 
+// One fused substep of the banded (tridiagonal) action, band.cu: P factored shifted systems
+// (P <= kBandMaxShifts), the ascending-index term list (slot = factored system, -1 = the plain
+// form's zero shift: w v) and the polynomial part. frcp = band_rcp(fdiag) per system. Y = the
+// forward sweep's scratch, P x d x 32 per 32-column strip.
+constexpr int kBandMaxShifts = 12;
+constexpr int kBandMaxTerms = 24;
+struct BandStep {
+  int n_terms;
+  int slot[kBandMaxTerms];
+  double w[kBandMaxTerms];
+  double c[kBandMaxShifts];
+  int residual, add_poly, hybrid;
+  int direct;  // the terms are exactly the P factored systems in order (slot[q] == q, n_terms == P)
+  double constant, d1, d2;
+};
+cudaError_t launch_band_action_step(int P, int d, int k, const double* ssub, const double* sdiag, const double* ssup,
+                                    const double* mult, const double* fdiag, const double* fsup, const double* frcp,
+                                    const double* frec, const double* brec, const BandStep& st, const double* V,
+                                    int64_t ldv, double* Y, double* out, int64_t ldo, cudaStream_t s);
+// frec / brec (nsys x d x 4 each): the bulk kernel's per-row coefficient records (band.cu)
+void launch_band_pack_records(int d, int nsys, const double* ssub, const double* sdiag, const double* ssup,
+                              const double* mult, const double* fdiag, const double* fsup, const double* frcp,
+                              double* frec, double* brec, cudaStream_t s);
+
 }  // namespace pf

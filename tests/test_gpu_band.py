@@ -74,6 +74,27 @@ def test_tridiag_action_bitwise(dev, oracle, name, form, substeps):
     assert np.array_equal(got, ref)
 
 
+@pytest.mark.parametrize("name,form", [("R8", 1), ("R8", 0), ("R10", 1), ("R4", 1), ("R5", 0)])
+@pytest.mark.parametrize("d", [1, 2, 5, 203])
+@pytest.mark.parametrize("k", [10240, 10241])
+def test_tridiag_action_wide_bitwise(dev, oracle, name, form, d, k):
+    """wide blocks: k = 10240 takes the bulk-copy kernel (>= 2 CTAs per SM, aligned rows), the odd
+    k = 10241 the per-lane queue; ragged d (203 = 50 stages of 4 + 3) and the d <= 5 edges"""
+    from paper_2210_03714_b200 import methods as M
+
+    m = M.catalog(name)
+    rng = np.random.default_rng(d + k)
+    scale = 0.25
+    sub = -scale * np.ones(max(d - 1, 0)) + 0.01 * rng.standard_normal(max(d - 1, 0))
+    diag = 2 * scale * np.ones(d) + 0.01 * rng.standard_normal(d)
+    sup = -scale * np.ones(max(d - 1, 0))
+    v = rng.standard_normal((d, k))
+    om = oracle.OMethod.from_method(m, form)
+    ref = oracle.tridiag_action(sub, diag, sup, v, om, 2)
+    got = dev.tridiag_action(m, dev.TridiagMatrix(sub, diag, sup), v, 2, form)
+    assert np.array_equal(got, ref)
+
+
 def test_tridiag_action_properties(dev, oracle):
     """the densified evaluator agrees (test_action.cpp:124-147); A = 0 gives a0 v (:149-157);
     trid121 heat step against scipy expm"""

@@ -2,9 +2,10 @@
 A (heat operator trid121 * h scaled), d rows, on the GPU (CUDA events) vs the CPU oracle on a column
 sample. Prints one JSON line.
 
-Traffic model (HBM bytes per substep): matvec X -> AV (read + write d k); per shift the solve reads
-its RHS (AV) and writes Y, then the backward sweep reads and rewrites Y (4 d k); the accumulation
-reads the P solutions + X + AV and writes X' ((P + 3) d k): 16 (2 + 4 P + P + 3) d k / 2 bytes."""
+Traffic model (HBM bytes per substep) of the fused step (band.cu band_action_*_kernel): V is read
+by the forward sweep and again by the backward sums, each shift's forward result Y_t is written
+once and read back once, the next iterate is written once: 8 (2 P + 3) d k bytes. min_traffic
+is the same less the second V read (a kernel that kept V's rows on chip): 8 (2 P + 2) d k."""
 import json
 import sys
 import time
@@ -34,7 +35,7 @@ for _ in range(reps):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / reps
-bytes_model = steps * 8.0 * d * k * (2 + 4 * P + P + 3)
+bytes_model = steps * 8.0 * d * k * (2 * P + 3)
 min_bytes = steps * 8.0 * d * k * (2 * P + 2)  # per column: write+read one sweep per shift, read/write the vector
 # CPU oracle on a column sample
 from oracle import oracle as O  # noqa: E402
