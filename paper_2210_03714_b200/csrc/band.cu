@@ -469,33 +469,44 @@ __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.p
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
 }  // namespace
 
-template <int G, int S, int R>
+// H shifts per warp (G / H warps per CTA): the warp's shifts share one V stream, one sliding-window
+// matvec and one copy schedule, and their H recurrences are independent chains the scheduler can
+// interleave. The queue slot of a warp holds [H][R][32] data rows (the forward uses the first R x 32
+// for V, the backward one block per shift for Y / x) and [H][R] 4-double records.
+template <int G, int H, int S, int R>
 constexpr size_t band_bulk_smem() {
-  return sizeof(double) * ((size_t)G * S * (R * 32 + 4 * R) + (size_t)S * R * 32) + sizeof(uint64_t) * G * S;
+  return sizeof(double) * ((size_t)(G / H) * S * (H * R * 32 + H * R * 4) + (size_t)S * R * 32) +
+         sizeof(uint64_t) * (G / H) * S;
 }
 
-template <int G, int S, int R>
-__global__ void __launch_bounds__(G * 32) band_action_bulk_kernel(
+template <int G, int H, int S, int R>
+__global__ void __launch_bounds__(G / H * 32) band_action_bulk_kernel(
     int d, int k, const double* __restrict__ ssub, const double* __restrict__ sdiag, const double* __restrict__ ssup,
     const double* __restrict__ mult, const double4* __restrict__ frec, const double4* __restrict__ brec, BandStep st,
     const double* __restrict__ V, int64_t ldv, double* __restrict__ Y, double* __restrict__ out, int64_t ldo) {
-  constexpr int QS = R * 32 + 4 * R;  // one stage: R data rows (32 columns), then R 4-double records
+  constexpr int NW = G / H;                     // warps per CTA
+  constexpr int QS = H * R * 32 + H * R * 4;    // one stage of one warp
+  constexpr int REC = H * R * 32;               // records start
   extern __shared__ __align__(128) double smem[];
   // warp index through a shuffle: provably warp-uniform, so the bulk-copy operands derived from it
   // live in uniform registers (no per-lane waterfall around UBLKCP)
-  const int t = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  double* q = smem + (size_t)t * S * QS;
-  double* vq = smem + (size_t)G * S * QS;  // [S][R][32] V rows for the backward sums
+  const int w = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  double* q = smem + (size_t)w * S * QS;
+  double* vq = smem + (size_t)NW * S * QS;  // [S][R][32] V rows for the backward sums
   uint64_t* bars = reinterpret_cast<uint64_t*>(vq + S * R * 32);
-  const unsigned q_sa = smem_u32(q), vq_sa = smem_u32(vq), bar_sa = smem_u32(bars + t * S);
+  const unsigned q_sa = smem_u32(q), vq_sa = smem_u32(vq), bar_sa = smem_u32(bars + w * S);
   const int col0 = blockIdx.x * 32, ncols = min(32, k - col0);
   const unsigned row_bytes = 8u * (unsigned)ncols;
   const int64_t dm1 = d > 1 ? d - 1 : 1;
-  double* __restrict__ yw = Y + ((int64_t)blockIdx.x * G + t) * d * 32;  // the warp's blocked Y region
+  const int t0 = w * H;  // the warp's first shift
+  // shift t's blocked Y region: ((strip * G) + t) * d * 32
+  double* __restrict__ yw = Y + ((int64_t)blockIdx.x * G + t0) * d * 32;
   const double* __restrict__ vstrip = V + col0;
-  const double4* __restrict__ fr4 = frec + (int64_t)t * d;
-  const double4* __restrict__ br4 = brec + (int64_t)t * d;
-  const double c = st.c[t];
+  const double4* __restrict__ fr4 = frec + (int64_t)t0 * d;
+  const double4* __restrict__ br4 = brec + (int64_t)t0 * d;
+  double c[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) c[h] = st.c[t0 + h];
   const bool residual = st.residual != 0;
   const int nbf = (d + R - 1) / R;
   if (lane < S) mbar_init(bar_sa + 8 * lane, 1);
@@ -509,10 +520,11 @@ __global__ void __launch_bounds__(G * 32) band_action_bulk_kernel(
     const unsigned sa = q_sa + (unsigned)(slot * QS * 8), bar = bar_sa + 8 * slot;
     const int j0 = b * R, nr = min(R, d - j0);
     if (lane == 0) {
-      mbar_expect(bar, (unsigned)nr * (row_bytes + 32u));
+      mbar_expect(bar, (unsigned)nr * (row_bytes + 32u * H));
       const double* src = vstrip + (int64_t)j0 * ldv;
       for (int u = 0; u < nr; ++u, src += ldv) bulk_g2s(sa + u * 256, src, row_bytes, bar);
-      bulk_g2s(sa + R * 256, fr4 + j0, (unsigned)nr * 32u, bar);
+#pragma unroll
+      for (int h = 0; h < H; ++h) bulk_g2s(sa + (REC + h * R * 4) * 8, fr4 + (int64_t)h * d + j0, (unsigned)nr * 32u, bar);
     }
   };
   auto issue_bwd = [&](int b) {
@@ -522,11 +534,15 @@ __global__ void __launch_bounds__(G * 32) band_action_bulk_kernel(
     const int i0 = d - 1 - b * R, base = i0 - (R - 1);  // slot position p holds row base + p
     const int lo = max(base, 0), hi_y = min(i0, d - 2);
     const int ny = max(hi_y - lo + 1, 0), nrec = i0 - lo + 1;
-    const bool vrows = b % G == t;
+    const bool vrows = b % NW == w;
     if (lane == 0) {
-      mbar_expect(bar, (unsigned)ny * 256u + (unsigned)nrec * 32u + (vrows ? (unsigned)nrec * row_bytes : 0u));
-      if (ny > 0) bulk_g2s(sa + (lo - base) * 256, yw + (int64_t)lo * 32, (unsigned)ny * 256u, bar);
-      bulk_g2s(sa + R * 256 + (lo - base) * 32, br4 + lo, (unsigned)nrec * 32u, bar);
+      mbar_expect(bar, H * ((unsigned)ny * 256u + (unsigned)nrec * 32u) + (vrows ? (unsigned)nrec * row_bytes : 0u));
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        if (ny > 0)
+          bulk_g2s(sa + (h * R * 32 + (lo - base) * 32) * 8, yw + ((int64_t)h * d + lo) * 32, (unsigned)ny * 256u, bar);
+        bulk_g2s(sa + (REC + h * R * 4 + (lo - base) * 4) * 8, br4 + (int64_t)h * d + lo, (unsigned)nrec * 32u, bar);
+      }
       if (vrows) {
         const double* src = vstrip + (int64_t)lo * ldv;
         for (int p = lo - base; p < R; ++p, src += ldv)
@@ -538,28 +554,31 @@ __global__ void __launch_bounds__(G * 32) band_action_bulk_kernel(
   // ---- forward (slot position u = row j0 + u; record u = the coefficients of row j0 + u - 1)
 #pragma unroll
   for (int b = 0; b < S - 1; ++b) issue_fwd(b);
-  double prev = 0.0, vim1 = 0.0, vi = 0.0;
+  double prev[H], vim1 = 0.0, vi = 0.0;
+#pragma unroll
+  for (int h = 0; h < H; ++h) prev[h] = 0.0;
   double* yl = yw + lane;
   for (int b = 0; b < nbf; ++b) {
     issue_fwd(b + S - 1);
     const int slot = b % S;
     mbar_wait(bar_sa + 8 * slot, (unsigned)(b / S) & 1u);
     const double* sq = q + slot * QS;
-    const double4* rec = reinterpret_cast<const double4*>(sq + R * 32);
+    const double4* rec = reinterpret_cast<const double4*>(sq + REC);  // rec[h * R + u]
     const int j0 = b * R;
     double* yb = yl + (int64_t)(j0 - 1) * 32;
     if (b >= 1 && j0 + R <= d) {
 #pragma unroll
       for (int u = 0; u < R; ++u) {
         const double vj = sq[u * 32 + lane];
-        const double4 cf = rec[u];
-        if (residual) {
-          const double acc = __dadd_rn(__dadd_rn(__dmul_rn(cf.y, vi), __dmul_rn(cf.z, vim1)), __dmul_rn(cf.w, vj));
-          prev = __dsub_rn(__dmul_rn(c, acc), __dmul_rn(cf.x, prev));
-        } else {
-          prev = __dsub_rn(vi, __dmul_rn(cf.x, prev));
+        const double4 c0 = rec[u];
+        const double acc =
+            residual ? __dadd_rn(__dadd_rn(__dmul_rn(c0.y, vi), __dmul_rn(c0.z, vim1)), __dmul_rn(c0.w, vj)) : 0.0;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const double m = h == 0 ? c0.x : rec[h * R + u].x;
+          prev[h] = residual ? __dsub_rn(__dmul_rn(c[h], acc), __dmul_rn(m, prev[h])) : __dsub_rn(vi, __dmul_rn(m, prev[h]));
+          __stcg(yb + (int64_t)h * d * 32 + u * 32, prev[h]);
         }
-        __stcg(yb + u * 32, prev);
         vim1 = vi;
         vi = vj;
       }
@@ -571,16 +590,19 @@ __global__ void __launch_bounds__(G * 32) band_action_bulk_kernel(
           const double vj = sq[u * 32 + lane];
           if (j > 0) {
             const int i = j - 1;
-            const double4 cf = rec[u];
-            double r = vi;
+            const double4 c0 = rec[u];
+            double acc = 0.0;
             if (residual) {
-              double acc = __dmul_rn(cf.y, vi);
-              if (i > 0) acc = __dadd_rn(acc, __dmul_rn(cf.z, vim1));
-              acc = __dadd_rn(acc, __dmul_rn(cf.w, vj));  // i + 1 = j < d
-              r = __dmul_rn(c, acc);
+              acc = __dmul_rn(c0.y, vi);
+              if (i > 0) acc = __dadd_rn(acc, __dmul_rn(c0.z, vim1));
+              acc = __dadd_rn(acc, __dmul_rn(c0.w, vj));  // i + 1 = j < d
             }
-            prev = i == 0 ? r : __dsub_rn(r, __dmul_rn(cf.x, prev));
-            __stcg(yb + u * 32, prev);
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+              const double r = residual ? __dmul_rn(c[h], acc) : vi;
+              prev[h] = i == 0 ? r : __dsub_rn(r, __dmul_rn(rec[h * R + u].x, prev[h]));
+              __stcg(yb + (int64_t)h * d * 32 + u * 32, prev[h]);
+            }
           }
           vim1 = vi;
           vi = vj;
@@ -591,13 +613,16 @@ __global__ void __launch_bounds__(G * 32) band_action_bulk_kernel(
   }
   {  // row d - 1 (kept in the register; Y holds rows 0 .. d - 2)
     const int i = d - 1;
-    double r = vi;
+    double acc = 0.0;
     if (residual) {
-      double acc = __dmul_rn(sdiag[i], vi);
+      acc = __dmul_rn(sdiag[i], vi);
       if (i > 0) acc = __dadd_rn(acc, __dmul_rn(ssub[i - 1], vim1));
-      r = __dmul_rn(c, acc);
     }
-    prev = i == 0 ? r : __dsub_rn(r, __dmul_rn(mult[t * dm1 + i - 1], prev));
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const double r = residual ? __dmul_rn(c[h], acc) : vi;
+      prev[h] = i == 0 ? r : __dsub_rn(r, __dmul_rn(mult[(t0 + h) * dm1 + i - 1], prev[h]));
+    }
   }
   fence_proxy_async_global();  // the Y stores above are read back by the bulk copies below
   __syncwarp();
@@ -607,30 +632,40 @@ __global__ void __launch_bounds__(G * 32) band_action_bulk_kernel(
 #pragma unroll
   for (int b = 0; b < S - 1; ++b) issue_bwd(b);
   const bool direct = st.direct != 0;
-  double nxt = 0.0;
+  double nxt[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) nxt[h] = 0.0;
   for (int b = 0; b < nbf; ++b) {
     const int n = nbf + b, slot = n % S;
     mbar_wait(bar_sa + 8 * slot, (unsigned)(n / S) & 1u);
     double* sq = q + slot * QS;
-    const double4* rec = reinterpret_cast<const double4*>(sq + R * 32);
+    const double4* rec = reinterpret_cast<const double4*>(sq + REC);
     const int i0 = d - 1 - b * R;
     if (b >= 1 && i0 - (R - 1) >= 0) {
 #pragma unroll
       for (int u = 0; u < R; ++u) {
         const int p = R - 1 - u;
-        const double4 cf = rec[p];
-        nxt = div_rcp(__dsub_rn(sq[p * 32 + lane], __dmul_rn(cf.x, nxt)), cf.y, cf.z);
-        sq[p * 32 + lane] = nxt;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const double4 cf = rec[h * R + p];
+          double* x = sq + h * R * 32 + p * 32 + lane;
+          nxt[h] = div_rcp(__dsub_rn(*x, __dmul_rn(cf.x, nxt[h])), cf.y, cf.z);
+          *x = nxt[h];
+        }
       }
     } else {
 #pragma unroll
       for (int u = 0; u < R; ++u) {
         const int i = i0 - u, p = R - 1 - u;
         if (i >= 0) {
-          const double4 cf = rec[p];
-          nxt = i == d - 1 ? div_rcp(prev, cf.y, cf.z)
-                           : div_rcp(__dsub_rn(sq[p * 32 + lane], __dmul_rn(cf.x, nxt)), cf.y, cf.z);
-          sq[p * 32 + lane] = nxt;
+#pragma unroll
+          for (int h = 0; h < H; ++h) {
+            const double4 cf = rec[h * R + p];
+            double* x = sq + h * R * 32 + p * 32 + lane;
+            nxt[h] = i == d - 1 ? div_rcp(prev[h], cf.y, cf.z)
+                                : div_rcp(__dsub_rn(*x, __dmul_rn(cf.x, nxt[h])), cf.y, cf.z);
+            *x = nxt[h];
+          }
         }
       }
     }
@@ -638,18 +673,21 @@ __global__ void __launch_bounds__(G * 32) band_action_bulk_kernel(
     __syncthreads();           // every warp's x rows and stage b's V rows visible; stage b - 1 drained
     issue_bwd(b + S - 1);
     const double* vs = vq + slot * R * 32;
-    for (int o = threadIdx.x; o < R * 32; o += G * 32) {
+    for (int o = threadIdx.x; o < R * 32; o += NW * 32) {
       const int u = o >> 5, ln = o & 31, i = i0 - u, p = R - 1 - u, cc = col0 + ln;
       if (i < 0 || cc >= k) continue;
       const double vv = vs[p * 32 + ln];
-      const double* xs = smem + (size_t)slot * QS + p * 32 + ln;  // warp g's x at xs[g * S * QS]
+      // shift g's x: warp g / H, block g % H of its slot
+      const double* xs = smem + (size_t)slot * QS + p * 32 + ln;
       double acc = 0.0;
       if (direct) {
 #pragma unroll
-        for (int g = 0; g < G; ++g) acc = __dadd_rn(acc, __dmul_rn(xs[(size_t)g * S * QS], st.w[g]));
+        for (int g = 0; g < G; ++g)
+          acc = __dadd_rn(acc, __dmul_rn(xs[(size_t)(g / H) * S * QS + (g % H) * R * 32], st.w[g]));
       } else {
         for (int qq = 0; qq < st.n_terms; ++qq) {
-          const double xv = st.slot[qq] >= 0 ? xs[(size_t)st.slot[qq] * S * QS] : vv;
+          const int g = st.slot[qq];
+          const double xv = g >= 0 ? xs[(size_t)(g / H) * S * QS + (g % H) * R * 32] : vv;
           acc = __dadd_rn(acc, __dmul_rn(xv, st.w[qq]));
         }
       }
@@ -681,6 +719,12 @@ __global__ void __launch_bounds__(G * 32) band_action_bulk_kernel(
 #ifndef PF_BAND_ROWS
 #define PF_BAND_ROWS 4
 #endif
+#ifndef PF_BAND_H
+// shifts per warp in the bulk kernel (even shift counts). H = 2 cuts instructions 30 % but halves
+// the resident warps; the kernel is latency-bound by its k / 32 x P independent chains, and
+// d 8192 k 16384 R8 measured 24.0 ms (H = 2) vs 21.7 ms (H = 1) -- profiles/r01_ncu_band_h2.txt
+#define PF_BAND_H 1
+#endif
 
 cudaError_t launch_band_action_step(int P, int d, int k, const double* ssub, const double* sdiag, const double* ssup,
                                     const double* mult, const double* fdiag, const double* fsup, const double* frcp,
@@ -700,11 +744,12 @@ cudaError_t launch_band_action_step(int P, int d, int k, const double* ssub, con
 #define PF_BAND_CASE(G)                                                                                           \
   case G:                                                                                                         \
     if (bulk) {                                                                                                   \
-      auto fn = band_action_bulk_kernel<G, S, R>;                                                                 \
-      constexpr size_t smem = band_bulk_smem<G, S, R>();                                                          \
+      constexpr int H = (G % 2 == 0 && PF_BAND_H == 2) ? 2 : 1;                                                   \
+      auto fn = band_action_bulk_kernel<G, H, S, R>;                                                              \
+      constexpr size_t smem = band_bulk_smem<G, H, S, R>();                                                       \
       set_smem_attr_once(reinterpret_cast<const void*>(fn), (int)smem);                                           \
-      fn<<<grid, G * 32, smem, s>>>(d, k, ssub, sdiag, ssup, mult, reinterpret_cast<const double4*>(frec),        \
-                                    reinterpret_cast<const double4*>(brec), st, V, ldv, Y, out, ldo);             \
+      fn<<<grid, G / H * 32, smem, s>>>(d, k, ssub, sdiag, ssup, mult, reinterpret_cast<const double4*>(frec),    \
+                                        reinterpret_cast<const double4*>(brec), st, V, ldv, Y, out, ldo);         \
     } else {                                                                                                      \
       auto fn = band_action_step_kernel<G, S, R>;                                                                 \
       constexpr size_t smem = band_step_smem<G, S, R>();                                                          \
