@@ -20,7 +20,14 @@ def _host():
     global _lib
     if _lib is None:
         if not _HOST.exists():
-            raise ImportError("libparfrac_host.so missing: run `python -m paper_2210_03714_b200.build`")
+            # the host layer is plain C++ (seconds with g++): rebuild it in-tree rather than fail when a
+            # copy of the tree arrives without it; the CUDA engine is never rebuilt implicitly
+            from . import build
+
+            try:
+                build.build_host()
+            except Exception as e:  # noqa: BLE001
+                raise ImportError("libparfrac_host.so missing and not buildable: %s" % e) from None
         _lib = C.CDLL(str(_HOST))
         _lib.pf_gen_randn.argtypes = [C.c_uint64, C.c_int64, C.c_void_p]
         _lib.pf_gen_uniform.argtypes = [C.c_uint64, C.c_int64, C.c_void_p]
