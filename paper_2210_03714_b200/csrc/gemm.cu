@@ -14,7 +14,16 @@
 namespace pf {
 namespace {
 
-constexpr int STAGES = 3;
+#ifndef PF_GEMM_STAGES
+#define PF_GEMM_STAGES 3
+#endif
+#ifndef PF_GEMM_BK
+#define PF_GEMM_BK 32
+#endif
+#ifndef PF_GEMM_WN
+#define PF_GEMM_WN 64
+#endif
+constexpr int STAGES = PF_GEMM_STAGES;
 
 template <int BM, int BN, int BK>
 struct GemmSmem {
@@ -203,7 +212,7 @@ void launch_gemm(const GemmParams& p, cudaStream_t stream) {
   } else if (p.n <= 64) {
     launch_v<128, 64, 16, 32, 32, 2>(p, v16, stream);
   } else {
-    launch_v<128, 128, 32, 32, 64, 1>(p, v16, stream);
+    launch_v<128, 128, PF_GEMM_BK, 32, PF_GEMM_WN, 1>(p, v16, stream);
   }
 }
 
