@@ -240,6 +240,12 @@ int pf_context_destroy(pf_context* ctx) {
     cudaEventDestroy(ctx->ev_fork);
     cudaEventDestroy(ctx->ev_join);
   }
+  for (size_t d = 0; d < ctx->aux.size(); ++d) {
+    cudaStreamSynchronize(ctx->aux[d]);
+    cudaStreamDestroy(ctx->aux[d]);
+    cudaEventDestroy(ctx->aux_ready[d]);
+    cudaEventDestroy(ctx->aux_done[d]);
+  }
   delete ctx;
   return PF_OK;
 }

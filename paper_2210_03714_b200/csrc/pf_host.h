@@ -21,6 +21,10 @@ struct pf_context {
   // side stream for independent branches of the large LU (created on first use)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // look-ahead streams of the large LU, one per recursion depth (created on first use): the
+  // bottom-right quadrant of each trailing update runs there while the recursion factors the rest
+  std::vector<cudaStream_t> aux;
+  std::vector<cudaEvent_t> aux_ready, aux_done;
 };
 
 // Dense ActionOperator (action.hpp:68-82): B = A * (1/N) and the LU factors of the owned shifts,

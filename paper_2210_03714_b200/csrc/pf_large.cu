@@ -158,13 +158,43 @@ bool fork_side(pf_context* ctx) {
   return true;
 }
 
-void lu_rec(pf_context* ctx, const Sys& s, int off, int n) {
+// stream and events of look-ahead depth d (created on first use); false if unavailable
+bool aux_for(pf_context* ctx, int d) {
+  while ((int)ctx->aux.size() <= d) {
+    cudaStream_t st = nullptr;
+    cudaEvent_t r = nullptr, e = nullptr;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&r, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      if (st) cudaStreamDestroy(st);
+      if (r) cudaEventDestroy(r);
+      return false;
+    }
+    ctx->aux.push_back(st);
+    ctx->aux_ready.push_back(r);
+    ctx->aux_done.push_back(e);
+  }
+  return true;
+}
+
+// LU of the diagonal block [off, off + n). `pending`: an event that must complete before this
+// call touches its own trailing block A22 = [off + n1, off + n)^2 (the caller's look-ahead GEMM
+// still updating it); everything before the trailing update (LU(A11), the panel solves) only
+// touches A11 / A12 / A21 and runs concurrently with it.
+//
+// Look-ahead: of the trailing update A22 -= A21 A12, the rows [0, h) of A22 (all columns) and the
+// block [h, n2) x [0, h) are updated on the main stream -- exactly what LU(A22)'s own A11 / A12 /
+// A21 need -- and the bottom-right quadrant [h, n2)^2, the largest piece, on the depth's aux
+// stream, where it overlaps the latency-bound recursion of LU(A22)'s first half. The child waits
+// for it right before its own trailing update.
+void lu_rec(pf_context* ctx, const Sys& s, int off, int n, cudaEvent_t pending = nullptr, int depth = 0) {
   if (n == kB) {
     lu_base(ctx, s, s.nsys, off, 1, nullptr);
     return;
   }
   const int n1 = half64(n), n2 = n - n1;
-  lu_rec(ctx, s, off, n1);
+  lu_rec(ctx, s, off, n1, nullptr, depth + 1);
   double* A12 = s.M + (int64_t)off * s.np + off + n1;
   double* A21 = s.M + (int64_t)(off + n1) * s.np + off;
   double* A22 = s.M + (int64_t)(off + n1) * s.np + off + n1;
@@ -182,8 +212,30 @@ void lu_rec(pf_context* ctx, const Sys& s, int off, int n) {
     trsm_left_lower(ctx, s, off, n1, A12, s.np, s.stride(), n2);
     trsm_right_upper(ctx, s, off, n1, A21, s.np, s.stride(), n2);
   }
+  if (pending) cudaStreamWaitEvent(ctx->stream, pending, 0);
+  // opt-in (PF_LOOKAHEAD=1): measured 1-10 % slower at n = 1024-8192 (tools/lu_timing.py) -- the
+  // quadrant GEMM's 212 KB-smem CTAs hold every SM for hundreds of microseconds, so the
+  // recursion's small launches queue behind them instead of overlapping (needs an SM-capped GEMM)
+  static const bool lookahead = std::getenv("PF_LOOKAHEAD") != nullptr;
+  if (lookahead && n2 >= 2 * kB && aux_for(ctx, depth)) {
+    const int h = half64(n2);  // = the child's own split
+    const int64_t ld = s.np, st = s.stride();
+    cudaStream_t main = ctx->stream, ax = ctx->aux[(size_t)depth];
+    cudaEventRecord(ctx->aux_ready[(size_t)depth], main);
+    cudaStreamWaitEvent(ax, ctx->aux_ready[(size_t)depth], 0);
+    ctx->stream = ax;
+    gemm(ctx, n2 - h, n2 - h, n1, s.nsys, -1.0, A21 + (int64_t)h * ld, ld, st, A12 + h, ld, st, 1.0,
+         A22 + (int64_t)h * ld + h, ld, st, 0.0);
+    cudaEventRecord(ctx->aux_done[(size_t)depth], ax);
+    ctx->stream = main;
+    gemm(ctx, h, n2, n1, s.nsys, -1.0, A21, ld, st, A12, ld, st, 1.0, A22, ld, st, 0.0);
+    gemm(ctx, n2 - h, h, n1, s.nsys, -1.0, A21 + (int64_t)h * ld, ld, st, A12, ld, st, 1.0, A22 + (int64_t)h * ld, ld,
+         st, 0.0);
+    lu_rec(ctx, s, off + n1, n2, ctx->aux_done[(size_t)depth], depth + 1);
+    return;
+  }
   gemm(ctx, n2, n2, n1, s.nsys, -1.0, A21, s.np, s.stride(), A12, s.np, s.stride(), 1.0, A22, s.np, s.stride(), 0.0);
-  lu_rec(ctx, s, off + n1, n2);
+  lu_rec(ctx, s, off + n1, n2, nullptr, depth + 1);
 }
 
 void diag_inverses(pf_context* ctx, const Sys& s) {
