@@ -150,8 +150,7 @@ int pf_tridiag_action(pf_context* ctx, const pf_method* m, int d, int k, const d
   // P solutions (unfused: P x d x k) or the fused kernel's per-warp forward scratch (P x d x 32 per strip)
   const size_t kpad = (size_t)(k + 31) / 32 * 32;
   double* Y = static_cast<double*>(workspace(ctx, kWsBandY, sizeof(double) * (size_t)d * kpad * std::max(P, 1)));
-  double* XB = static_cast<double*>(workspace(ctx, kWsBandX, sizeof(double) * blk * 4));
-  if (!A3 || !F || !Y || !XB) return PF_ERR_CUDA;
+  if (!A3 || !F || !Y) return PF_ERR_CUDA;
   double *ssub = A3, *sdiag = A3 + dm1, *ssup = A3 + dm1 + d;
   pf::band_scale_kernel<<<blocks_for(d), 256, 0, ctx->stream>>>(d, dSub, dDiag, dSuper, 1.0 / substeps, ssub, sdiag,
                                                                  ssup);
@@ -191,10 +190,14 @@ int pf_tridiag_action(pf_context* ctx, const pf_method* m, int d, int k, const d
   const bool add_poly = residual || hybrid;
   const double constant = residual ? m->constant[0] : (hybrid ? m->poly[0] : 0.0);
   const double d1 = hybrid ? m->poly[1] : 0.0, d2 = hybrid ? m->poly[2] : 0.0;
-  double *X = XB, *Xn = XB + blk, *AV = XB + 2 * blk, *A2V = XB + 3 * blk;
   static const bool unfused = std::getenv("PF_BAND_UNFUSED") != nullptr;    // A/B switches
   static const bool bulk_ok = std::getenv("PF_BAND_NO_BULK") == nullptr;
-  if (P >= 1 && P <= pf::kBandMaxShifts && nt <= pf::kBandMaxTerms && !unfused) {
+  const bool fused = P >= 1 && P <= pf::kBandMaxShifts && nt <= pf::kBandMaxTerms && !unfused;
+  // iterates: the fused path ping-pongs two d x k blocks, the unfused chain also keeps A V and A^2 V
+  double* XB = static_cast<double*>(workspace(ctx, kWsBandX, sizeof(double) * blk * (fused ? 2 : 4)));
+  if (!XB) return PF_ERR_CUDA;
+  double *X = XB, *Xn = XB + blk, *AV = fused ? nullptr : XB + 2 * blk, *A2V = fused ? nullptr : XB + 3 * blk;
+  if (fused) {
     // fused substeps (band.cu band_action_step_kernel): substep s reads its V (dV for s = 0) and
     // writes the next one (dOut for the last, unless dOut overlaps dV's rows)
     pf::BandStep bs{};

@@ -168,3 +168,34 @@ def test_large_pair_mode_and_decline(dev, oracle):
     both = dev.eval_dense(m, np.stack([good, bad]), opts)
     assert np.array_equal(np.asarray(both[0]), np.asarray(pg))
     assert np.array_equal(np.asarray(both[1]), np.asarray(pb))
+
+
+def test_lu_lookahead_option(dev, tmp_path):
+    """PF_LOOKAHEAD=1 (opt-in): the trailing update split into quadrants with the bottom-right one on
+    a per-depth stream gives the same factors as the default schedule (same GEMM per element)."""
+    import os
+    import subprocess
+    import sys
+
+    script = tmp_path / "lu.py"
+    script.write_text(
+        "import sys, numpy as np, torch\n"
+        "sys.path.insert(0, %r)\n"
+        "from paper_2210_03714_b200 import api\n"
+        "rng = np.random.default_rng(3)\n"
+        "n = 1024\n"
+        "B = rng.standard_normal((n, n)) * (1.0 / n)\n"
+        "Ms = np.stack([np.eye(n) - c * B for c in (0.5, -0.5, 1.0)])\n"
+        "lu, piv = api.DenseLu(Ms).factors()\n"
+        "np.save(sys.argv[1], lu)\n" % str(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+    outs = []
+    for flag in ("0", "1"):
+        env = dict(os.environ)
+        env.pop("PF_LOOKAHEAD", None)
+        if flag == "1":
+            env["PF_LOOKAHEAD"] = "1"
+        path = tmp_path / ("lu%s.npy" % flag)
+        subprocess.run([sys.executable, str(script), str(path)], check=True, env=env, timeout=300)
+        outs.append(np.load(path))
+    a, b = outs
+    assert np.max(np.abs(a - b)) <= 1e-13 * np.max(np.abs(a))
