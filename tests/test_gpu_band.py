@@ -139,3 +139,25 @@ def test_tridiag_action_zero_pivot_shift(dev, oracle):
         dev.tridiag_action(m, dev.TridiagMatrix(sub, diag, sup), v, 1, 1)
     assert ge.value.code == Errc.ZeroPivot
     assert str(ge.value).startswith("shift %d: zero pivot at row %d" % (oe.value.shift_index, oe.value.row))
+
+
+@pytest.mark.parametrize("form", [0, 1])
+def test_tridiag_action_many_shifts_bitwise(dev, oracle, form):
+    """a user-built method with 13 nonzero shifts (> the fused kernel's 12) and a zero shift takes
+    the unfused chain (band_matvec / band_solve / band_accumulate): still the reference's bits"""
+    from fractions import Fraction as Fr
+
+    from paper_2210_03714_b200 import methods as M
+
+    shifts = [Fr(0)] + [Fr(k + 1, 9) * (1 if k % 2 == 0 else -1) for k in range(13)]
+    m = M.build_plain(shifts, M.FunctionId.exp(), 13, "P13")
+    d, k = 257, 40
+    rng = np.random.default_rng(11)
+    sub = -0.2 * np.ones(d - 1) + 0.01 * rng.standard_normal(d - 1)
+    diag = 0.4 * np.ones(d)
+    sup = -0.2 * np.ones(d - 1)
+    v = rng.standard_normal((d, k))
+    om = oracle.OMethod.from_method(m, form)
+    ref = oracle.tridiag_action(sub, diag, sup, v, om, 3)
+    got = dev.tridiag_action(m, dev.TridiagMatrix(sub, diag, sup), v, 3, form)
+    assert np.array_equal(got, ref)
