@@ -8,6 +8,8 @@
 // rate is 250 GFLOP/s, so a single 128^3 tile takes 17 us); 3-stage cp.async pipeline, 16-byte
 // copies when the operands allow it (8-byte copies with zero fill otherwise: any shape / leading
 // dimension is legal).
+#include <algorithm>
+
 #include "pf_common.cuh"
 #include "pf_kernels.h"
 
@@ -93,18 +95,17 @@ __device__ __forceinline__ void load_stage(GemmSmem<BM, BN, BK>& sm, int stage, 
 }  // namespace
 
 // warps (BM / WM) (M) x (BN / WN) (N), each a WM x WN tile of (WM / 8) x (WN / 8) DMMA tiles.
-template <int BM, int BN, int BK, int WM, int WN, int MINB, bool V16>
-__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB) gemm_kernel(GemmParams p, int tiles_n) {
+// One BM x BN output tile (tile index `tile` of matrix bz).
+template <int BM, int BN, int BK, int WM, int WN, bool V16>
+__device__ __forceinline__ void gemm_tile(const GemmParams& p, GemmSmem<BM, BN, BK>& sm, int bz, int tile,
+                                          int tiles_n) {
   constexpr int LA = GemmSmem<BM, BN, BK>::LA;
   constexpr int LB = GemmSmem<BM, BN, BK>::LB;
   constexpr int NT = (BM / WM) * (BN / WN) * 32;
   constexpr int MI = WM / 8;      // DMMA tiles down
   constexpr int NJ = WN / 8;      // DMMA tiles across
   constexpr int WCOLS = BN / WN;  // warps across
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  GemmSmem<BM, BN, BK>& sm = *reinterpret_cast<GemmSmem<BM, BN, BK>*>(smem_raw);
-  const int bz = blockIdx.y;
-  const int m0 = (blockIdx.x / tiles_n) * BM, n0 = (blockIdx.x % tiles_n) * BN;
+  const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
   const double* A = p.A + (int64_t)bz * p.strideA;
   const double* B = p.B + (int64_t)bz * p.strideB;
   double* C = p.C + (int64_t)bz * p.strideC;
@@ -175,6 +176,23 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB) gemm_kernel(
       }
 }
 
+template <int BM, int BN, int BK, int WM, int WN, int MINB, bool V16>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB) gemm_kernel(GemmParams p, int tiles_n) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  GemmSmem<BM, BN, BK>& sm = *reinterpret_cast<GemmSmem<BM, BN, BK>*>(smem_raw);
+  if (p.max_sms <= 0) {
+    gemm_tile<BM, BN, BK, WM, WN, V16>(p, sm, blockIdx.y, blockIdx.x, tiles_n);
+    return;
+  }
+  // persistent: tiles of all matrices, strided by the grid
+  const int tiles = ((p.m + BM - 1) / BM) * tiles_n;
+  const int64_t total = (int64_t)tiles * p.batch;
+  for (int64_t L = blockIdx.x; L < total; L += gridDim.x) {
+    gemm_tile<BM, BN, BK, WM, WN, V16>(p, sm, (int)(L / tiles), (int)(L % tiles), tiles_n);
+    __syncthreads();  // the next tile's prologue refills the stage buffers
+  }
+}
+
 namespace {
 template <int BM, int BN, int BK, int WM, int WN, int MINB, bool V16>
 void launch_tile(const GemmParams& p, cudaStream_t stream) {
@@ -182,6 +200,10 @@ void launch_tile(const GemmParams& p, cudaStream_t stream) {
   set_smem_attr_once(reinterpret_cast<const void*>(gemm_kernel<BM, BN, BK, WM, WN, MINB, V16>), smem);
   const int tiles_m = (p.m + BM - 1) / BM, tiles_n = (p.n + BN - 1) / BN;
   dim3 grid(tiles_m * tiles_n, p.batch);
+  if (p.max_sms > 0) {
+    const int64_t total = (int64_t)tiles_m * tiles_n * p.batch;
+    grid = dim3((unsigned)std::min<int64_t>(total, (int64_t)p.max_sms * MINB), 1);
+  }
   gemm_kernel<BM, BN, BK, WM, WN, MINB, V16><<<grid, (BM / WM) * (BN / WN) * 32, smem, stream>>>(p, tiles_n);
 }
 

@@ -170,6 +170,7 @@ void gemm(pf_context* ctx, int m, int n, int k, int batch, double alpha, const d
   g.jmask = jmask;
   g.step = step;
   g.pass = pass;
+  g.max_sms = ctx->gemm_cap;
   pf::launch_gemm(g, ctx->stream);
   ctx->launches++;
 }

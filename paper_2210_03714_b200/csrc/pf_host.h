@@ -25,6 +25,7 @@ struct pf_context {
   // bottom-right quadrant of each trailing update runs there while the recursion factors the rest
   std::vector<cudaStream_t> aux;
   std::vector<cudaEvent_t> aux_ready, aux_done;
+  int gemm_cap = 0;  // > 0: host gemm() launches persistent GEMMs on at most this many SMs
 };
 
 // Dense ActionOperator (action.hpp:68-82): B = A * (1/N) and the LU factors of the owned shifts,

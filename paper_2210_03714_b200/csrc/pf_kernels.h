@@ -69,6 +69,9 @@ struct GemmParams {
   const int* jmask;
   int step;
   const double* pass;
+  // > 0: persistent launch on at most max_sms SMs' worth of CTAs, each looping over tiles (leaves
+  // SMs free for concurrent work on other streams)
+  int max_sms;
 };
 void launch_gemm(const GemmParams& p, cudaStream_t stream);
 

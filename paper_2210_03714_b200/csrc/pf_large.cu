@@ -224,8 +224,14 @@ void lu_rec(pf_context* ctx, const Sys& s, int off, int n, cudaEvent_t pending =
     cudaEventRecord(ctx->aux_ready[(size_t)depth], main);
     cudaStreamWaitEvent(ax, ctx->aux_ready[(size_t)depth], 0);
     ctx->stream = ax;
+    // capped: the quadrant leaves SMs to the recursion it overlaps (PF_LOOKAHEAD_RESERVE SMs, 24)
+    static const int reserve = std::getenv("PF_LOOKAHEAD_RESERVE") ? std::atoi(std::getenv("PF_LOOKAHEAD_RESERVE")) : 24;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    ctx->gemm_cap = std::max(1, sms - reserve);
     gemm(ctx, n2 - h, n2 - h, n1, s.nsys, -1.0, A21 + (int64_t)h * ld, ld, st, A12 + h, ld, st, 1.0,
          A22 + (int64_t)h * ld + h, ld, st, 0.0);
+    ctx->gemm_cap = 0;
     cudaEventRecord(ctx->aux_done[(size_t)depth], ax);
     ctx->stream = main;
     gemm(ctx, h, n2, n1, s.nsys, -1.0, A21, ld, st, A12, ld, st, 1.0, A22, ld, st, 0.0);
