@@ -540,7 +540,7 @@ __global__ void load_padded_kernel(const double* A, int64_t lda, int64_t strideA
                                    unsigned long long* mx) {
   const int z = blockIdx.y;
   const double* a = A + (int64_t)z * strideA;
-  double* m = M + (int64_t)z * np * np;
+  double* m = M ? M + (int64_t)z * np * np : nullptr;  // M null: max |a| only (in-place factorisation)
   double loc = 0.0;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)np * np;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -552,7 +552,7 @@ __global__ void load_padded_kernel(const double* A, int64_t lda, int64_t strideA
     } else {
       v = (r == c) ? 1.0 : 0.0;
     }
-    m[idx] = v;
+    if (m) m[idx] = v;
   }
   for (int o = 16; o > 0; o >>= 1) loc = fmax(loc, __shfl_xor_sync(0xffffffffu, loc, o));
   if ((threadIdx.x & 31) == 0) atomicMax(mx + z, (unsigned long long)__double_as_longlong(loc));

@@ -930,8 +930,12 @@ int large_lu_factor(pf_context* ctx, int n, int batch, double* A, int64_t lda, i
   if (!d_mx || !d_piv) return PF_ERR_CUDA;
   int* d_perm = d_piv + (size_t)n * batch;
   cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long) * batch, ctx->stream);
-  load_padded_kernel<<<dim3(grid2(s.stride(), batch), batch), 256, 0, ctx->stream>>>(A, lda, strideA, n, s.np, s.M, d_mx);
+  // n a multiple of 64 and a packed batch: factor in the caller's buffer (no padded copy in and out)
+  const bool in_place = s.np == n && lda == n && strideA == (int64_t)n * n;
+  load_padded_kernel<<<dim3(grid2(s.stride(), batch), batch), 256, 0, ctx->stream>>>(A, lda, strideA, n, s.np,
+                                                                                      in_place ? nullptr : s.M, d_mx);
   ctx->launches++;
+  if (in_place) s.M = A;
   FactorResult fr = factor_systems(ctx, s, n, d_mx, flags, d_piv, d_perm, pivot_rel_tol);
   if (fr.rc) {
     if (status) {
@@ -943,9 +947,11 @@ int large_lu_factor(pf_context* ctx, int n, int batch, double* A, int64_t lda, i
     }
     return fr.rc;
   }
-  copy2d_kernel<<<dim3(grid2((int64_t)n * n, batch), batch), 256, 0, ctx->stream>>>(n, n, 1.0, s.M, s.np, s.stride(), A, lda,
-                                                                               strideA);
-  ctx->launches++;
+  if (!in_place) {
+    copy2d_kernel<<<dim3(grid2((int64_t)n * n, batch), batch), 256, 0, ctx->stream>>>(n, n, 1.0, s.M, s.np, s.stride(),
+                                                                                 A, lda, strideA);
+    ctx->launches++;
+  }
   if (piv) {
     if (fr.pivoted) {  // every system's swap sequence (identity for the certified ones)
       cudaMemcpyAsync(piv, d_piv, sizeof(int) * (size_t)n * batch, cudaMemcpyDeviceToDevice, ctx->stream);
