@@ -241,6 +241,14 @@ int pf_context_destroy(pf_context* ctx) {
     cudaEventDestroy(ctx->ev_fork);
     cudaEventDestroy(ctx->ev_join);
   }
+  for (auto& g : ctx->lu_graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (ctx->gstream) {
+    cudaStreamSynchronize(ctx->gstream);
+    cudaStreamDestroy(ctx->gstream);
+    cudaEventDestroy(ctx->ev_g0);
+    cudaEventDestroy(ctx->ev_g1);
+  }
   for (size_t d = 0; d < ctx->aux.size(); ++d) {
     cudaStreamSynchronize(ctx->aux[d]);
     cudaStreamDestroy(ctx->aux[d]);

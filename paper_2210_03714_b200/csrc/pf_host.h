@@ -26,6 +26,18 @@ struct pf_context {
   std::vector<cudaStream_t> aux;
   std::vector<cudaEvent_t> aux_ready, aux_done;
   int gemm_cap = 0;  // > 0: host gemm() launches persistent GEMMs on at most this many SMs
+  // replayable launch graphs of the large LU recursion, keyed by its buffers and shape
+  struct LuGraph {
+    const double* M = nullptr;
+    const double* inv = nullptr;
+    int64_t inv_stride = 0;
+    int np = 0, nsys = 0;
+    cudaGraphExec_t exec = nullptr;  // nullptr: seen once (the next call captures)
+    int64_t launches = 0;
+  };
+  std::vector<LuGraph> lu_graphs;
+  cudaStream_t gstream = nullptr;  // private capture / replay stream (the caller's may be the legacy one)
+  cudaEvent_t ev_g0 = nullptr, ev_g1 = nullptr;
 };
 
 // Dense ActionOperator (action.hpp:68-82): B = A * (1/N) and the LU factors of the owned shifts,

@@ -244,6 +244,89 @@ void lu_rec(pf_context* ctx, const Sys& s, int off, int n, cudaEvent_t pending =
   lu_rec(ctx, s, off + n1, n2, nullptr, depth + 1);
 }
 
+// lu_rec(0, np) through a CUDA graph: the recursion is a fixed chain of several hundred small
+// launches on the same buffers, so it is captured once (on the second call with a given
+// (M, inv, np, nsys); the first runs directly) and replayed, which removes the per-launch gaps.
+// Capture and replay run on the context's private stream, fenced to the caller's stream by two
+// events (the caller's may be the legacy default stream, which cannot be captured).
+// PF_NO_LU_GRAPH disables (as does the opt-in look-ahead, whose aux streams are not captured).
+bool graph_stream(pf_context* ctx) {
+  if (ctx->gstream) return true;
+  if (cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_g0, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_g1, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    ctx->gstream = nullptr;
+    return false;
+  }
+  return true;
+}
+
+void run_lu_graph(pf_context* ctx, const Sys& s) {  // on ctx->stream == ctx->gstream
+  pf_context::LuGraph* hit = nullptr;
+  for (auto& g : ctx->lu_graphs)
+    if (g.M == s.M && g.inv == s.inv && g.inv_stride == s.inv_stride && g.np == s.np && g.nsys == s.nsys) hit = &g;
+  if (hit && hit->exec) {
+    if (cudaGraphLaunch(hit->exec, ctx->stream) == cudaSuccess) {
+      ctx->launches += hit->launches;
+      return;
+    }
+    cudaGetLastError();
+  }
+  if (!hit) {  // first sighting: run directly, capture next time
+    if (ctx->lu_graphs.size() >= 8) {
+      if (ctx->lu_graphs.front().exec) cudaGraphExecDestroy(ctx->lu_graphs.front().exec);
+      ctx->lu_graphs.erase(ctx->lu_graphs.begin());
+    }
+    pf_context::LuGraph g;
+    g.M = s.M;
+    g.inv = s.inv;
+    g.inv_stride = s.inv_stride;
+    g.np = s.np;
+    g.nsys = s.nsys;
+    ctx->lu_graphs.push_back(g);
+    lu_rec(ctx, s, 0, s.np);
+    return;
+  }
+  const int64_t l0 = ctx->launches;
+  cudaGraph_t graph = nullptr;
+  if (cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    lu_rec(ctx, s, 0, s.np);
+    return;
+  }
+  lu_rec(ctx, s, 0, s.np);
+  const cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+  cudaGraphExec_t exec = nullptr;
+  if (e != cudaSuccess || !graph || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+    cudaGetLastError();
+    if (graph) cudaGraphDestroy(graph);
+    ctx->launches = l0;
+    lu_rec(ctx, s, 0, s.np);  // the captured launches never ran
+    return;
+  }
+  cudaGraphDestroy(graph);
+  hit->exec = exec;
+  hit->launches = ctx->launches - l0;
+  cudaGraphLaunch(exec, ctx->stream);
+}
+
+void run_lu(pf_context* ctx, const Sys& s) {
+  static const bool graphs = std::getenv("PF_NO_LU_GRAPH") == nullptr && std::getenv("PF_LOOKAHEAD") == nullptr;
+  if (!graphs || !graph_stream(ctx) || !fork_side(ctx)) {  // fork_side: the side stream exists
+    lu_rec(ctx, s, 0, s.np);
+    return;
+  }
+  cudaStream_t main = ctx->stream;
+  cudaEventRecord(ctx->ev_g0, main);
+  cudaStreamWaitEvent(ctx->gstream, ctx->ev_g0, 0);
+  ctx->stream = ctx->gstream;
+  run_lu_graph(ctx, s);
+  ctx->stream = main;
+  cudaEventRecord(ctx->ev_g1, ctx->gstream);
+  cudaStreamWaitEvent(main, ctx->ev_g1, 0);
+}
+
 void diag_inverses(pf_context* ctx, const Sys& s) {
   for (int off = 0; off < s.np; off += kB) {
     lu_base(ctx, s, s.nsys, off, 0, nullptr);
@@ -311,7 +394,7 @@ FactorResult factor_systems(pf_context* ctx, const Sys& s, int n, unsigned long 
     return fr;
   }
   if (nf == 0) {
-    lu_rec(ctx, s, 0, s.np);
+    run_lu(ctx, s);
     return fr;
   }
   fr.pivoted = true;
@@ -326,7 +409,7 @@ FactorResult factor_systems(pf_context* ctx, const Sys& s, int n, unsigned long 
     for (int q = 0; q < nf; ++q)
       cudaMemcpyAsync(side + q * s.stride(), s.M + fails[q] * s.stride(), sizeof(double) * s.stride(),
                       cudaMemcpyDeviceToDevice, ctx->stream);
-    lu_rec(ctx, s, 0, s.np);
+    run_lu(ctx, s);
     for (int q = 0; q < nf; ++q)
       cudaMemcpyAsync(s.M + fails[q] * s.stride(), side + q * s.stride(), sizeof(double) * s.stride(),
                       cudaMemcpyDeviceToDevice, ctx->stream);
