@@ -199,3 +199,33 @@ def test_lu_lookahead_option(dev, tmp_path):
         outs.append(np.load(path))
     a, b = outs
     assert np.max(np.abs(a - b)) <= 1e-13 * np.max(np.abs(a))
+
+
+def test_lu_graph_replay_is_bitwise(dev):
+    """run_lu: the first factorisation with given buffers runs directly, the second captures the
+    recursion into a CUDA graph, the third replays it -- all three bit-identical (same launches)."""
+    import ctypes as C
+
+    from paper_2210_03714_b200 import _native as N
+
+    eng = dev.engine()
+    n, nsys = 1024, 4
+    g = torch.Generator(device="cuda").manual_seed(5)
+    B = torch.randn(nsys, n, n, dtype=torch.float64, device="cuda", generator=g) * (1.0 / n)
+    src = torch.eye(n, dtype=torch.float64, device="cuda") - 0.5 * B
+    work = torch.empty_like(src)
+    piv = torch.empty(nsys, n, dtype=torch.int32, device="cuda")
+    outs = []
+    for _ in range(3):
+        work.copy_(src)
+        st = N.PfStatus()
+        rc = N.lib.pf_lu_factor_batched(eng.h, n, nsys, work.data_ptr(), n, n * n, piv.data_ptr(), 1e-14, 0,
+                                        C.byref(st))
+        assert rc == 0
+        torch.cuda.synchronize()
+        outs.append(work.clone())
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+    # and it is an LU of src: L U == src to rounding
+    L = torch.tril(outs[2], -1) + torch.eye(n, dtype=torch.float64, device="cuda")
+    U = torch.triu(outs[2])
+    assert float((L @ U - src).abs().max()) < 1e-12
