@@ -13,6 +13,11 @@
 //                           (system, column)
 //   band_matvec_kernel      TridiagMatrix::matvec (action.cpp:35-44)
 //   band_accumulate_kernel  assemble_action's ascending-shift sum and polynomial part (:262-283)
+//   band_action_bulk_kernel / band_action_step_kernel
+//                           one whole substep (action_eval on every column) fused: forward sweep,
+//                           back-substitution and the ordered sum in one launch (the three kernels
+//                           above remain the path for methods with more than 12 factored shifts)
+//   band_pack_records_kernel per-row coefficient records for the bulk kernel's copies
 //   penta_factor_kernel /   pentadiag_solve (action.cpp:170-202) split into the band elimination
 //   penta_solve_kernel      (matrix only, one thread) and the per-column substitution
 #include <algorithm>
