@@ -220,12 +220,9 @@ void launch_gemm(const GemmParams& p, cudaStream_t stream) {
   // 16-byte copies need even leading dimensions / batch strides and 16-byte aligned bases
   const bool v16 = ((p.lda | p.ldb | p.strideA | p.strideB) & 1) == 0 &&
                    ((reinterpret_cast<uintptr_t>(p.A) | reinterpret_cast<uintptr_t>(p.B)) & 15) == 0;
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  int dev = 0, sms = 148;  // per call: contexts on different devices / host threads share this code
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t big_tiles = (int64_t)((p.m + 127) / 128) * ((p.n + (p.n <= 64 ? 63 : 127)) / (p.n <= 64 ? 64 : 128)) * p.batch;
   // measured on B200 (tools/large_timing.py gemm): 128 x 128 x 32 tiles 31.6 / 31.9 TF/s at 4096^3 /
   // 8192^3 vs 30.6 / 30.9 with BK = 16; 4 warps of 64 x 64 spill at 255 registers (18.5 TF/s)

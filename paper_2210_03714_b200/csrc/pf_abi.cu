@@ -135,8 +135,8 @@ int launch_small(pf_context* ctx, pf::SmallParams& p) {
   p.prof = ctx->prof;
   // per-SM accumulator slots: one CTA per SM (smem-bound), so %smid indexes a private slot that
   // stays in L2 across the shifts; slots beyond the guard fall back to the output buffer
-  static int sms = 0;
-  if (sms == 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  int sms = 148;  // per call (cheap attribute query): no shared mutable state across host threads
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
   p.scratch_slots = 2 * sms;
   p.scratch = static_cast<double*>(
       workspace(ctx, kWsScratch, sizeof(double) * 3 * PF_SMALL_N * PF_SMALL_N * (size_t)p.scratch_slots));
