@@ -56,6 +56,8 @@ __global__ void lincomb2_kernel(int n, int k, double d1, const double* X, double
                                 double* out, int64_t ldo);
 size_t apply_inv64_smem_bytes();
 size_t lu_base64_smem_bytes();
+__global__ void lu_base128_kernel(double* M, int64_t ld, int64_t strideM, int off, double* inv, int64_t inv_stride);
+size_t lu_base128_smem_bytes();
 
 namespace host {
 namespace {
@@ -193,6 +195,16 @@ void lu_rec(pf_context* ctx, const Sys& s, int off, int n, cudaEvent_t pending =
     lu_base(ctx, s, s.nsys, off, 1, nullptr);
     return;
   }
+  // a 128 block in one launch (LU of both halves, the panels and the update between them) instead
+  // of five dependent ones; PF_NO_LEAF128 keeps the 64 leaves
+  static const bool leaf128 = std::getenv("PF_NO_LEAF128") == nullptr;
+  if (n == 2 * kB && leaf128 && pending == nullptr) {
+    set_smem_attr_once(reinterpret_cast<const void*>(lu_base128_kernel), (int)lu_base128_smem_bytes());
+    lu_base128_kernel<<<s.nsys, 256, lu_base128_smem_bytes(), ctx->stream>>>(s.M, s.np, s.stride(), off, s.inv,
+                                                                             s.inv_stride);
+    ctx->launches++;
+    return;
+  }
   const int n1 = half64(n), n2 = n - n1;
   lu_rec(ctx, s, off, n1, nullptr, depth + 1);
   double* A12 = s.M + (int64_t)off * s.np + off + n1;
@@ -249,7 +261,7 @@ void lu_rec(pf_context* ctx, const Sys& s, int off, int n, cudaEvent_t pending =
 // (M, inv, np, nsys); the first runs directly) and replayed, which removes the per-launch gaps.
 // Capture and replay run on the context's private stream, fenced to the caller's stream by two
 // events (the caller's may be the legacy default stream, which cannot be captured).
-// PF_NO_LU_GRAPH disables (as does the opt-in look-ahead, whose aux streams are not captured).
+// Opt-in (PF_LU_GRAPH=1; not with the opt-in look-ahead, whose aux streams are not captured).
 bool graph_stream(pf_context* ctx) {
   if (ctx->gstream) return true;
   if (cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -312,7 +324,10 @@ void run_lu_graph(pf_context* ctx, const Sys& s) {  // on ctx->stream == ctx->gs
 }
 
 void run_lu(pf_context* ctx, const Sys& s) {
-  static const bool graphs = std::getenv("PF_NO_LU_GRAPH") == nullptr && std::getenv("PF_LOOKAHEAD") == nullptr;
+  // opt-in (PF_LU_GRAPH=1): instantiating the captured recursion costs ~6 ms (128 leaves) to
+  // ~40 ms (64 leaves) once per buffer set, so it pays off only over many repeated factorisations
+  // of the same shape and buffers (-3 % per call at n = 4096); one-shot calls lose (cfg3 +5 ms)
+  static const bool graphs = std::getenv("PF_LU_GRAPH") != nullptr && std::getenv("PF_LOOKAHEAD") == nullptr;
   if (!graphs || !graph_stream(ctx) || !fork_side(ctx)) {  // fork_side: the side stream exists
     lu_rec(ctx, s, 0, s.np);
     return;

@@ -201,9 +201,20 @@ def test_lu_lookahead_option(dev, tmp_path):
     assert np.max(np.abs(a - b)) <= 1e-13 * np.max(np.abs(a))
 
 
-def test_lu_graph_replay_is_bitwise(dev):
-    """run_lu: the first factorisation with given buffers runs directly, the second captures the
-    recursion into a CUDA graph, the third replays it -- all three bit-identical (same launches)."""
+def test_lu_graph_replay_is_bitwise(dev, tmp_path):
+    """run_lu with PF_LU_GRAPH=1 (opt-in): the first factorisation with given buffers runs directly,
+    the second captures the recursion into a CUDA graph, the third replays it -- all three
+    bit-identical (same launches). Runs in a subprocess (the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+
+    if os.environ.get("PF_LU_GRAPH") != "1":
+        env = dict(os.environ, PF_LU_GRAPH="1")
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__ + "::test_lu_graph_replay_is_bitwise"],
+                           env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+        return
     import ctypes as C
 
     from paper_2210_03714_b200 import _native as N
