@@ -288,6 +288,138 @@ __global__ void __launch_bounds__(256) lu_base128_kernel(double* M, int64_t ld, 
 }
 
 // ---------------------------------------------------------------------------------------------
+// Triangular solve with a 128 x 128 diagonal block [off, off + 128) in one launch (the three
+// launches of the host recursion at that level -- inverse, update, inverse -- fused per chunk):
+//   mode 0 (left, L unit lower):  B1 <- L11^-1 B1;            B2 <- L22^-1 (B2 - L21 B1)
+//   mode 1 (left, U upper):       B2 <- U22^-1 B2;            B1 <- U11^-1 (B1 - U12 B2)
+//   mode 2 (right, U upper):      B1 <- B1 U11^-1;            B2 <- (B2 - B1 U12) U22^-1
+// Left modes: CTA = 64 columns of the 128-row panel B; right mode: CTA = 64 rows of the 128-column
+// panel. Explicit 64-block inverses from `inv` (as apply_inv64), the coupling block from M.
+size_t trsm128_smem_bytes() { return sizeof(double) * (5 * B64 * L64); }
+
+namespace {
+// D (64 x 64, smem, stride L64) = X Y (both smem 64 x 64), into registers: two 16 x 16 tiles per warp
+__device__ __forceinline__ void mm64_regs(const double* X, const double* Y, double (&acc)[2][2][2][2]) {
+  const int warp = warp_id();
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int tile = warp * 2 + u, i = tile >> 2, j = tile & 3;
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj) acc[u][mi][nj][0] = acc[u][mi][nj][1] = 0.0;
+    mm16(X + 16 * i * L64, L64, Y + 16 * j, L64, B64, acc[u]);
+  }
+}
+// D = base - acc (base == nullptr: D = acc), D smem 64 x 64
+__device__ __forceinline__ void store64(double* D, const double* base, const double (&acc)[2][2][2][2]) {
+  const int warp = warp_id(), lane = lane_id();
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int tile = warp * 2 + u, i = tile >> 2, j = tile & 3;
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int idx = (16 * i + 8 * mi + g) * L64 + 16 * j + 8 * nj + 2 * t + e;
+          D[idx] = base ? base[idx] - acc[u][mi][nj][e] : acc[u][mi][nj][e];
+        }
+  }
+}
+}  // namespace
+
+__global__ void __launch_bounds__(256) trsm128_kernel(const double* M, int64_t ld, int64_t strideM, int off,
+                                                      const double* inv, int64_t inv_stride, int mode, double* Bm,
+                                                      int64_t ldb, int64_t strideB, int extent) {
+  extern __shared__ __align__(16) double t_smem[];
+  double* t1 = t_smem;             // first inverse to apply
+  double* t2 = t1 + B64 * L64;     // second inverse
+  double* cpl = t2 + B64 * L64;    // coupling block (L21 or U12)
+  double* b1 = cpl + B64 * L64;    // the chunk's first 64 (rows, or columns in mode 2)
+  double* b2 = b1 + B64 * L64;     // ... and second 64
+  const int z = blockIdx.y, tile = blockIdx.x;
+  const double* blkinv = inv + (int64_t)z * inv_stride + (int64_t)(off / B64) * 2 * B64 * B64;
+  const double* m = M + (int64_t)z * strideM + (int64_t)off * ld + off;
+  const bool right = mode == 2;
+  double* b = Bm + (int64_t)z * strideB + (right ? (int64_t)tile * B64 * ldb : (int64_t)tile * B64);
+  const int live = min(B64, extent - tile * B64);  // columns (left) or rows (right) in range
+  // mode 0: t1 = L11^-1, t2 = L22^-1, cpl = L21; modes 1, 2: t1 = U11^-1, t2 = U22^-1, cpl = U12
+  const double* i1 = blkinv + (mode == 0 ? 0 : B64 * B64);
+  const double* i2 = blkinv + 2 * B64 * B64 + (mode == 0 ? 0 : B64 * B64);
+  const double* c0 = mode == 0 ? m + (int64_t)B64 * ld : m + B64;
+  for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
+    const int r = idx >> 6, c = idx & 63;
+    t1[r * L64 + c] = i1[idx];
+    t2[r * L64 + c] = i2[idx];
+    cpl[r * L64 + c] = c0[(int64_t)r * ld + c];
+    if (!right) {  // B rows r and 64 + r, chunk column c
+      const bool ok = c < live;
+      b1[r * L64 + c] = ok ? b[(int64_t)r * ldb + c] : 0.0;
+      b2[r * L64 + c] = ok ? b[(int64_t)(B64 + r) * ldb + c] : 0.0;
+    } else {  // B row r of the chunk, columns c and 64 + c
+      const bool ok = r < live;
+      b1[r * L64 + c] = ok ? b[(int64_t)r * ldb + c] : 0.0;
+      b2[r * L64 + c] = ok ? b[(int64_t)r * ldb + B64 + c] : 0.0;
+    }
+  }
+  __syncthreads();
+  double acc[2][2][2][2];
+  if (mode == 0) {
+    mm64_regs(t1, b1, acc);  // B1' = L11^-1 B1
+    __syncthreads();
+    store64(b1, nullptr, acc);
+    __syncthreads();
+    mm64_regs(cpl, b1, acc);  // B2 - L21 B1'
+    __syncthreads();
+    store64(b2, b2, acc);
+    __syncthreads();
+    mm64_regs(t2, b2, acc);  // L22^-1 (...)
+    __syncthreads();
+    store64(b2, nullptr, acc);
+  } else if (mode == 1) {
+    mm64_regs(t2, b2, acc);  // B2' = U22^-1 B2
+    __syncthreads();
+    store64(b2, nullptr, acc);
+    __syncthreads();
+    mm64_regs(cpl, b2, acc);  // B1 - U12 B2'
+    __syncthreads();
+    store64(b1, b1, acc);
+    __syncthreads();
+    mm64_regs(t1, b1, acc);  // U11^-1 (...)
+    __syncthreads();
+    store64(b1, nullptr, acc);
+  } else {
+    mm64_regs(b1, t1, acc);  // B1' = B1 U11^-1
+    __syncthreads();
+    store64(b1, nullptr, acc);
+    __syncthreads();
+    mm64_regs(b1, cpl, acc);  // B2 - B1' U12
+    __syncthreads();
+    store64(b2, b2, acc);
+    __syncthreads();
+    mm64_regs(b2, t2, acc);  // (...) U22^-1
+    __syncthreads();
+    store64(b2, nullptr, acc);
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
+    const int r = idx >> 6, c = idx & 63;
+    if (!right) {
+      if (c < live) {
+        b[(int64_t)r * ldb + c] = b1[r * L64 + c];
+        b[(int64_t)(B64 + r) * ldb + c] = b2[r * L64 + c];
+      }
+    } else if (r < live) {
+      b[(int64_t)r * ldb + c] = b1[r * L64 + c];
+      b[(int64_t)r * ldb + B64 + c] = b2[r * L64 + c];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // In-place block solve with an explicit 64 x 64 inverse T (T = Linv or Uinv of diagonal block blk):
 //   left : B[64 x cols] <- T B     (CTA = 64 columns)
 //   right: B[rows x 64] <- B T     (CTA = 64 rows)

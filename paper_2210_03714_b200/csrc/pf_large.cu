@@ -58,6 +58,9 @@ size_t apply_inv64_smem_bytes();
 size_t lu_base64_smem_bytes();
 __global__ void lu_base128_kernel(double* M, int64_t ld, int64_t strideM, int off, double* inv, int64_t inv_stride);
 size_t lu_base128_smem_bytes();
+__global__ void trsm128_kernel(const double* M, int64_t ld, int64_t strideM, int off, const double* inv,
+                               int64_t inv_stride, int mode, double* Bm, int64_t ldb, int64_t strideB, int extent);
+size_t trsm128_smem_bytes();
 
 namespace host {
 namespace {
@@ -103,8 +106,27 @@ void lu_base(pf_context* ctx, const Sys& s, int nblocks, int off, int factor, co
 
 int half64(int n) { return std::max(kB, ((n / kB) / 2) * kB); }
 
+// the three solve levels of a 128 diagonal block in one launch (large.cu trsm128_kernel); mode 0
+// L^-1 B, 1 U^-1 B, 2 B U^-1. PF_NO_LEAF128 keeps the 64-block recursion.
+bool trsm128(pf_context* ctx, const Sys& s, int off, int mode, double* B, int64_t ldb, int64_t sb, int extent) {
+  static const bool leaf128 = std::getenv("PF_NO_LEAF128") == nullptr;
+  if (!leaf128) return false;
+  dim3 grid((extent + kB - 1) / kB, s.nsys);
+  // only where the three separate launches are latency-bound: the fused kernel runs one CTA per SM
+  // (174 KB smem), the separate ones overlap better on big grids (cfg5's 256 systems: +3 ms fused)
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  if ((int64_t)grid.x * grid.y > 2 * (int64_t)sms) return false;
+  set_smem_attr_once(reinterpret_cast<const void*>(trsm128_kernel), (int)trsm128_smem_bytes());
+  trsm128_kernel<<<grid, 256, trsm128_smem_bytes(), ctx->stream>>>(s.M, s.np, s.stride(), off, s.inv, s.inv_stride,
+                                                                   mode, B, ldb, sb, extent);
+  ctx->launches++;
+  return true;
+}
+
 // B (n x cols) <- L^-1 B, L = unit-lower diagonal block [off, off + n) of s.M
 void trsm_left_lower(pf_context* ctx, const Sys& s, int off, int n, double* B, int64_t ldb, int64_t sb, int cols) {
+  if (n == 2 * kB && trsm128(ctx, s, off, 0, B, ldb, sb, cols)) return;
   if (n == kB) {
     apply_inv(ctx, s, off / kB, false, false, B, ldb, sb, cols);
     return;
@@ -118,6 +140,7 @@ void trsm_left_lower(pf_context* ctx, const Sys& s, int off, int n, double* B, i
 
 // B (n x cols) <- U^-1 B
 void trsm_left_upper(pf_context* ctx, const Sys& s, int off, int n, double* B, int64_t ldb, int64_t sb, int cols) {
+  if (n == 2 * kB && trsm128(ctx, s, off, 1, B, ldb, sb, cols)) return;
   if (n == kB) {
     apply_inv(ctx, s, off / kB, true, false, B, ldb, sb, cols);
     return;
@@ -131,6 +154,7 @@ void trsm_left_upper(pf_context* ctx, const Sys& s, int off, int n, double* B, i
 
 // B (rows x n) <- B U^-1
 void trsm_right_upper(pf_context* ctx, const Sys& s, int off, int n, double* B, int64_t ldb, int64_t sb, int rows) {
+  if (n == 2 * kB && trsm128(ctx, s, off, 2, B, ldb, sb, rows)) return;
   if (n == kB) {
     apply_inv(ctx, s, off / kB, true, true, B, ldb, sb, rows);
     return;
