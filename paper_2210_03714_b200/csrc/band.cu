@@ -51,35 +51,62 @@ __global__ void band_scale_kernel(int d, const double* sub, const double* diag, 
 // System z: shifted (c = shifts[z]): diag 1 - c a, sub / super -c a; else A itself (shifts null).
 // mult[z] (d - 1), fdiag[z] (d), fsup[z] (d - 1, the system's super-diagonal), frcp[z] (d,
 // band_rcp of the pivots; optional). fail[z] = the ZeroPivot row or -1.
-__global__ void band_factor_kernel(int d, int nsys, const double* sub, const double* diag, const double* super,
-                                   const double* shifts, double* mult, double* fdiag, double* fsup, double* frcp,
+__global__ void band_factor_kernel(int d, int nsys, const double* __restrict__ sub, const double* __restrict__ diag,
+                                   const double* __restrict__ super, const double* shifts, double* __restrict__ mult,
+                                   double* __restrict__ fdiag, double* __restrict__ fsup, double* __restrict__ frcp,
                                    int* fail) {
   const int z = blockIdx.x * blockDim.x + threadIdx.x;
   if (z >= nsys) return;
   const double c = shifts ? shifts[z] : 0.0;
   const bool shifted = shifts != nullptr;
-  double* mu = mult + (int64_t)z * (d > 1 ? d - 1 : 1);
-  double* fd = fdiag + (int64_t)z * d;
-  double* fs = fsup + (int64_t)z * (d > 1 ? d - 1 : 1);
-  double* fr = frcp ? frcp + (int64_t)z * d : nullptr;
+  double* __restrict__ mu = mult + (int64_t)z * (d > 1 ? d - 1 : 1);
+  double* __restrict__ fd = fdiag + (int64_t)z * d;
+  double* __restrict__ fs = fsup + (int64_t)z * (d > 1 ? d - 1 : 1);
+  double* __restrict__ fr = frcp ? frcp + (int64_t)z * d : nullptr;
   double prev = shifted ? __dsub_rn(1.0, __dmul_rn(c, diag[0])) : diag[0];
   fd[0] = prev;
   if (fr) fr[0] = band_rcp(prev);
   int bad = -1;
-  for (int i = 1; i < d; ++i) {
-    const double l = shifted ? __dmul_rn(-c, sub[i - 1]) : sub[i - 1];
-    const double u = shifted ? __dmul_rn(-c, super[i - 1]) : super[i - 1];
-    const double dg = shifted ? __dsub_rn(1.0, __dmul_rn(c, diag[i])) : diag[i];
-    fs[i - 1] = u;
-    if (fabs(prev) <= kFloor) {
-      bad = i - 1;
-      break;
+  // the recurrence is sequential: the coefficient loads of the next 8 rows are issued while the
+  // current 8 are eliminated, so global latency stays off the chain (same operations, same bits)
+  constexpr int kF = 8;
+  double la[kF], ua[kF], da[kF], lb[kF], ub[kF], db[kF];
+  auto fetch = [&](double (&ls)[kF], double (&us)[kF], double (&ds)[kF], int i0) {
+#pragma unroll
+    for (int u = 0; u < kF; ++u) {
+      const int i = i0 + u;
+      ls[u] = i < d ? __ldg(sub + i - 1) : 0.0;
+      us[u] = i < d ? __ldg(super + i - 1) : 0.0;
+      ds[u] = i < d ? __ldg(diag + i) : 1.0;
     }
-    const double w = __ddiv_rn(l, prev);
-    mu[i - 1] = w;
-    prev = __dsub_rn(dg, __dmul_rn(w, u));
-    fd[i] = prev;
-    if (fr) fr[i] = band_rcp(prev);
+  };
+  auto eliminate = [&](const double (&ls)[kF], const double (&us)[kF], const double (&ds)[kF], int i0) {
+#pragma unroll
+    for (int u = 0; u < kF; ++u) {
+      const int i = i0 + u;
+      if (i >= d || bad >= 0) break;
+      const double l = shifted ? __dmul_rn(-c, ls[u]) : ls[u];
+      const double uu = shifted ? __dmul_rn(-c, us[u]) : us[u];
+      const double dg = shifted ? __dsub_rn(1.0, __dmul_rn(c, ds[u])) : ds[u];
+      fs[i - 1] = uu;
+      if (fabs(prev) <= kFloor) {
+        bad = i - 1;
+        break;
+      }
+      const double w = __ddiv_rn(l, prev);
+      mu[i - 1] = w;
+      prev = __dsub_rn(dg, __dmul_rn(w, uu));
+      fd[i] = prev;
+      if (fr) fr[i] = band_rcp(prev);
+    }
+  };
+  if (d > 1) fetch(la, ua, da, 1);
+  for (int i0 = 1; i0 < d && bad < 0; i0 += 2 * kF) {  // two batches per trip: static buffers
+    if (i0 + kF < d) fetch(lb, ub, db, i0 + kF);
+    eliminate(la, ua, da, i0);
+    if (i0 + kF >= d || bad >= 0) break;
+    if (i0 + 2 * kF < d) fetch(la, ua, da, i0 + 2 * kF);
+    eliminate(lb, ub, db, i0 + kF);
   }
   if (bad < 0 && fabs(prev) <= kFloor) bad = d - 1;
   fail[z] = bad;
