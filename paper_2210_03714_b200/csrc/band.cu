@@ -121,6 +121,7 @@ constexpr int kR = PF_BAND_KR;
 __global__ void __launch_bounds__(128) band_solve_kernel(int d, int k, const double* __restrict__ mult,
                                                          const double* __restrict__ fdiag,
                                                          const double* __restrict__ fsup,
+                                                         const double* __restrict__ frcp,
                                                          const double* __restrict__ src, int64_t lds,
                                                          const double* __restrict__ rhs_scale, double* __restrict__ X,
                                                          int64_t ldx, int64_t strideX) {
@@ -131,6 +132,7 @@ __global__ void __launch_bounds__(128) band_solve_kernel(int d, int k, const dou
   const double* __restrict__ mu = mult + (int64_t)z * dm1;
   const double* __restrict__ fd = fdiag + (int64_t)z * d;
   const double* __restrict__ fs = fsup + (int64_t)z * dm1;
+  const double* __restrict__ fr = frcp + (int64_t)z * d;  // band_rcp of the pivots (div_rcp)
   double* __restrict__ x = X + (int64_t)z * strideX + col;
   const double* __restrict__ s = src + col;
   const bool scaled = rhs_scale != nullptr;
@@ -157,22 +159,23 @@ __global__ void __launch_bounds__(128) band_solve_kernel(int d, int k, const dou
     }
   }
   // backward: x_{d-1} /= fdiag_{d-1}; x_i = (x_i - super_i x_{i+1}) / fdiag_i
-  double nxt = __ddiv_rn(prev, fd[d - 1]);
+  double nxt = div_rcp(prev, fd[d - 1], fr[d - 1]);
   x[(int64_t)(d - 1) * ldx] = nxt;
   for (int i0 = d - 2; i0 >= 0; i0 -= kR) {
-    double y[kR], f[kR], g[kR];
+    double y[kR], f[kR], g[kR], gr[kR];
 #pragma unroll
     for (int u = 0; u < kR; ++u) {
       const int i = i0 - u;
       y[u] = i >= 0 ? x[(int64_t)i * ldx] : 0.0;
       f[u] = i >= 0 ? __ldg(fs + i) : 0.0;
       g[u] = i >= 0 ? __ldg(fd + i) : 1.0;
+      gr[u] = i >= 0 ? __ldg(fr + i) : 1.0;
     }
 #pragma unroll
     for (int u = 0; u < kR; ++u) {
       const int i = i0 - u;
       if (i >= 0) {
-        nxt = __ddiv_rn(__dsub_rn(y[u], __dmul_rn(f[u], nxt)), g[u]);
+        nxt = div_rcp(__dsub_rn(y[u], __dmul_rn(f[u], nxt)), g[u], gr[u]);
         x[(int64_t)i * ldx] = nxt;
       }
     }

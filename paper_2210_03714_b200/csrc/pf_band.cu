@@ -15,8 +15,8 @@ __global__ void band_factor_kernel(int d, int nsys, const double* sub, const dou
                                    const double* shifts, double* mult, double* fdiag, double* fsup, double* frcp,
                                    int* fail);
 __global__ void band_solve_kernel(int d, int k, const double* mult, const double* fdiag, const double* fsup,
-                                  const double* src, int64_t lds, const double* rhs_scale, double* X, int64_t ldx,
-                                  int64_t strideX);
+                                  const double* frcp, const double* src, int64_t lds, const double* rhs_scale,
+                                  double* X, int64_t ldx, int64_t strideX);
 __global__ void band_matvec_kernel(int d, int k, const double* sub, const double* diag, const double* super,
                                    const double* V, int64_t ldv, double* Out, int64_t ldo);
 __global__ void band_accumulate_kernel(int d, int k, int n_terms, const int* slot, const double* w, const double* X,
@@ -91,16 +91,16 @@ int pf_thomas_solve_batched(pf_context* ctx, int d, int k, const double* dSub, c
   if (status) std::memset(status, 0, sizeof(*status));
   if (!ctx || d < 1 || k < 0 || ldr < k || ldx < k) return bad(status);
   const int64_t dm1 = std::max(d - 1, 1);
-  double* F = static_cast<double*>(workspace(ctx, kWsBandF, sizeof(double) * (size_t)(d + 2 * dm1)));
+  double* F = static_cast<double*>(workspace(ctx, kWsBandF, sizeof(double) * (size_t)(2 * d + 2 * dm1)));
   if (!F) return PF_ERR_CUDA;
-  double *mult = F, *fdiag = F + dm1, *fsup = F + dm1 + d;
+  double *mult = F, *fdiag = F + dm1, *fsup = F + dm1 + d, *frcp = fsup + dm1;
   int row = 0, rc = PF_OK;
-  const int z = factor(ctx, d, 1, dSub, dDiag, dSuper, nullptr, mult, fdiag, fsup, nullptr, &row, &rc);
+  const int z = factor(ctx, d, 1, dSub, dDiag, dSuper, nullptr, mult, fdiag, fsup, frcp, &row, &rc);
   if (rc) return rc;
   if (z >= 0) return zero_pivot(status, 0, row);
   if (k == 0) return PF_OK;
-  pf::band_solve_kernel<<<dim3((k + 127) / 128, 1), 128, 0, ctx->stream>>>(d, k, mult, fdiag, fsup, dRhs, ldr,
-                                                                             nullptr, dX, ldx, 0);
+  pf::band_solve_kernel<<<dim3((k + 127) / 128, 1), 128, 0, ctx->stream>>>(d, k, mult, fdiag, fsup, frcp, dRhs,
+                                                                             ldr, nullptr, dX, ldx, 0);
   ctx->launches++;
   return collect_status(ctx, 0, 0, nullptr);
 }
@@ -257,7 +257,7 @@ int pf_tridiag_action(pf_context* ctx, const pf_method* m, int d, int k, const d
     }
     if (P > 0) {
       pf::band_solve_kernel<<<dim3((k + 127) / 128, P), 128, 0, ctx->stream>>>(
-          d, k, mult, fdiag, fsup, residual ? AV : X, k, residual ? d_sh : nullptr, Y, k, (int64_t)blk);
+          d, k, mult, fdiag, fsup, frcp, residual ? AV : X, k, residual ? d_sh : nullptr, Y, k, (int64_t)blk);
       ctx->launches++;
     }
     pf::band_accumulate_kernel<<<blocks_for((int64_t)blk), 256, 0, ctx->stream>>>(
