@@ -2,13 +2,13 @@
 //
 // Replaces DenseMatrix::mul (proj/core/src/dense.cpp:17-29) for the squaring chain, B^2, the
 // phi1 / cos-sin recurrences, B V, and every off-diagonal update of the large-n LU / triangular
-// solves. CTA tile BM x BN x BK: 128 x 128 x 32 (8 warps of 32 x 64), 128 x 64 x 16 for thin right-hand sides
-// (8 warps of 32 x 32, two CTAs per SM), or 64 x 64 x 16 (4 warps of 32 x 32) when the larger tiles would
-// leave most of the 148 SMs idle (the small updates deep in the LU / TRSM recursion: one SM's DMMA
-// rate is 250 GFLOP/s, so a single 128^3 tile takes 17 us); 3-stage cp.async pipeline, 16-byte
+// solves. CTA tile BM x BN x BK: 64 x 64 x 16 (4 warps of 32 x 32, four CTAs = 16 DMMA warps per SM)
+// for every shape -- measured faster than 128 x 128 x 32 (8 warps of 32 x 64, one CTA per SM) and
+// 128 x 64 x 16 at every size (see launch_gemm); 3-stage cp.async pipeline, 16-byte
 // copies when the operands allow it (8-byte copies with zero fill otherwise: any shape / leading
 // dimension is legal).
 #include <algorithm>
+#include <cstdlib>
 
 #include "pf_common.cuh"
 #include "pf_kernels.h"
@@ -220,18 +220,18 @@ void launch_gemm(const GemmParams& p, cudaStream_t stream) {
   // 16-byte copies need even leading dimensions / batch strides and 16-byte aligned bases
   const bool v16 = ((p.lda | p.ldb | p.strideA | p.strideB) & 1) == 0 &&
                    ((reinterpret_cast<uintptr_t>(p.A) | reinterpret_cast<uintptr_t>(p.B)) & 15) == 0;
-  int dev = 0, sms = 148;  // per call: contexts on different devices / host threads share this code
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t big_tiles = (int64_t)((p.m + 127) / 128) * ((p.n + (p.n <= 64 ? 63 : 127)) / (p.n <= 64 ? 64 : 128)) * p.batch;
-  // measured on B200 (tools/large_timing.py gemm): 128 x 128 x 32 tiles 31.6 / 31.9 TF/s at 4096^3 /
-  // 8192^3 vs 30.6 / 30.9 with BK = 16; 4 warps of 64 x 64 spill at 255 registers (18.5 TF/s)
-  if (big_tiles < sms) {
-    launch_v<64, 64, 16, 32, 32, 4>(p, v16, stream);  // too few CTAs for the SMs: 64 x 64 tiles
-  } else if (p.n <= 64) {
+  // 64 x 64 x 16 tiles, 4 warps of 32 x 32, four CTAs (16 DMMA warps) per SM for every shape: the
+  // occupancy beats the larger tiles' operand reuse everywhere measured (tools/large_timing.py,
+  // profiles/r01_gemm_sweep.txt): 2048^3 30.8 vs 27.2 TF/s, 8192^3 32.7 vs 32.1, cfg5 83.9 vs
+  // 98.2 ms, 8 x 4096^2 LU 18.1 vs 19.8 ms. PF_GEMM_FORCE=1 / 3 selects the 128 x 64 / 128 x 128
+  // tiles for A/B runs. (Every variant accumulates each element in the same k order.)
+  static const int force = std::getenv("PF_GEMM_FORCE") ? std::atoi(std::getenv("PF_GEMM_FORCE")) : 0;
+  if (force == 1) {
     launch_v<128, 64, 16, 32, 32, 2>(p, v16, stream);
-  } else {
+  } else if (force == 3) {
     launch_v<128, 128, PF_GEMM_BK, 32, PF_GEMM_WN, 1>(p, v16, stream);
+  } else {
+    launch_v<64, 64, 16, 32, 32, 4>(p, v16, stream);
   }
 }
 
