@@ -892,27 +892,68 @@ __global__ void penta_factor_kernel(int d, const double* sub2, const double* sub
   *fail = bad;
 }
 
-__global__ void penta_solve_kernel(int d, int k, const double* W, const double* F, const double* rhs, int64_t ldr,
-                                   double* X, int64_t ldx) {
+// Forward elimination with a register window (x[i], x[i+1] partially updated, x[i+2] arriving from
+// the RHS): each element receives the same updates in the same order as pentadiag_solve's in-place
+// loop (off 2 from row r - 2, then off 1 from row r - 1; f == 0 skipped), without the RHS copy pass
+// or read-modify-writes through memory; loads issued R rows ahead. Back substitution keeps
+// x[i+1], x[i+2] in registers.
+__global__ void __launch_bounds__(128) penta_solve_kernel(int d, int k, const double* __restrict__ W,
+                                                          const double* __restrict__ F,
+                                                          const double* __restrict__ rhs, int64_t ldr,
+                                                          double* __restrict__ X, int64_t ldx) {
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= k) return;
-  double* x = X + col;
-  for (int i = 0; i < d; ++i) x[(int64_t)i * ldx] = rhs[(int64_t)i * ldr + col];
-  for (int i = 0; i < d; ++i) {
-    const double xi = x[(int64_t)i * ldx];
-    for (int off = 1; off <= 2; ++off) {
-      const int r = i + off;
-      if (r >= d) break;
-      const double f = F[(int64_t)i * 2 + off - 1];
-      if (f == 0.0) continue;
-      x[(int64_t)r * ldx] = __dsub_rn(x[(int64_t)r * ldx], __dmul_rn(f, xi));
+  constexpr int R = 8;
+  double* __restrict__ x = X + col;
+  const double* __restrict__ b = rhs + col;
+  double x0 = d > 0 ? b[0] : 0.0, x1 = d > 1 ? b[ldr] : 0.0;
+  for (int i0 = 0; i0 < d; i0 += R) {
+    double nb[R], f0[R], f1[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int i = i0 + u;
+      nb[u] = i + 2 < d ? b[(int64_t)(i + 2) * ldr] : 0.0;
+      f0[u] = i < d ? __ldg(F + (int64_t)i * 2) : 0.0;
+      f1[u] = i < d ? __ldg(F + (int64_t)i * 2 + 1) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int i = i0 + u;
+      if (i < d) {
+        const double xi = x0;
+        double x2 = nb[u];
+        if (i + 1 < d && f0[u] != 0.0) x1 = __dsub_rn(x1, __dmul_rn(f0[u], xi));
+        if (i + 2 < d && f1[u] != 0.0) x2 = __dsub_rn(x2, __dmul_rn(f1[u], xi));
+        x[(int64_t)i * ldx] = xi;
+        x0 = x1;
+        x1 = x2;
+      }
     }
   }
-  for (int i = d - 1; i >= 0; --i) {
-    double acc = x[(int64_t)i * ldx];
-    for (int c = 1; c <= 2; ++c)
-      if (i + c < d) acc = __dsub_rn(acc, __dmul_rn(W[(int64_t)i * 5 + 2 + c], x[(int64_t)(i + c) * ldx]));
-    x[(int64_t)i * ldx] = __ddiv_rn(acc, W[(int64_t)i * 5 + 2]);
+  double n1 = 0.0, n2 = 0.0;  // x[i+1], x[i+2] (final)
+  for (int i0 = d - 1; i0 >= 0; i0 -= R) {
+    double xv[R], w2[R], w3[R], w4[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int i = i0 - u;
+      xv[u] = i >= 0 ? x[(int64_t)i * ldx] : 0.0;
+      w2[u] = i >= 0 ? __ldg(W + (int64_t)i * 5 + 2) : 1.0;
+      w3[u] = i >= 0 ? __ldg(W + (int64_t)i * 5 + 3) : 0.0;
+      w4[u] = i >= 0 ? __ldg(W + (int64_t)i * 5 + 4) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int i = i0 - u;
+      if (i >= 0) {
+        double acc = xv[u];
+        if (i + 1 < d) acc = __dsub_rn(acc, __dmul_rn(w3[u], n1));
+        if (i + 2 < d) acc = __dsub_rn(acc, __dmul_rn(w4[u], n2));
+        const double xi = __ddiv_rn(acc, w2[u]);
+        x[(int64_t)i * ldx] = xi;
+        n2 = n1;
+        n1 = xi;
+      }
+    }
   }
 }
 
