@@ -21,12 +21,13 @@
  *   factor-once substepping (assemble_action / ActionOperator / substep_action,
  *   action.cpp:224-339).
  *
- * Parity pinning: PARITY UNPINNED against reference outputs. The reference cannot be compiled
- * here (gmpxx.h / libgmpxx and vendor/ are absent) and ships no golden output matrices, so this
- * restatement is pinned instead by the reference's own known-answer tests and properties
- * (tests/test_oracle.py: test_dense.cpp:34-156, test_action.cpp:124-188, the published
- * SplitMix64 sequence) and by independent referees (scipy expm, eigh); golden fixtures in
- * tests/golden/ freeze its output so drift is caught.
+ * Parity pinning: PINNED against the reference itself. oracle/Makefile compiles
+ * /root/reference/proj/core/src/*.cpp unmodified (GMP/gmpxx shims in oracle/shim/) into
+ * oracle/_ref/libparfrac_ref.so; the reference's own doctest suites and acceptance checklist pass
+ * on that build, and tests/test_ref_pin.py requires this restatement to equal it bit for bit
+ * (LU factors and pivots, solve_shifted, mul, eval_dense for every catalog method and both forms,
+ * cfg1/cfg2 expm, exp+phi1, dense block action, the banded solvers and actions, generators).
+ * tests/golden/ holds reference outputs (make_golden.py) that this library must reproduce.
  */
 #ifndef PF_ORACLE_H
 #define PF_ORACLE_H

@@ -103,7 +103,7 @@ def build_cpp_tests(verbose: bool = False) -> Path:
 
 def build_oracle() -> Path:
     """The CPU checker (test infrastructure; never loaded by the product path)."""
-    _run(["make", "-s", "-C", str(ROOT / "oracle")])
+    _run(["make", "-s", "-j8", "-C", str(ROOT / "oracle")])
     return ROOT / "oracle" / "libpforacle.so"
 
 

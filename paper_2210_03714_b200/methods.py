@@ -65,6 +65,18 @@ class FunctionId:
     def name(self) -> str:
         return "phi%d" % self.phi_order if self.tag == "phi" else self.tag
 
+    @staticmethod
+    def parse(name: str) -> "FunctionId":
+        """Inverse of name(); "phi" means phi1 and phi0 is exp (series.cpp:27-46)."""
+        fixed = {"exp": FunctionId.exp(), "log1m": FunctionId.log_one_minus(), "cos": FunctionId.cosine(),
+                 "sin": FunctionId.sine(), "phi": FunctionId.phi(1)}
+        if name in fixed:
+            return fixed[name]
+        if name.startswith("phi") and len(name) > 3 and name[3:].isdigit():
+            m = int(name[3:])
+            return FunctionId.exp() if m == 0 else FunctionId.phi(m)
+        raise_error(Errc.BadArgument, "unknown function: " + name)
+
 
 @functools.lru_cache(maxsize=None)
 def _factorial(k: int) -> int:

@@ -206,11 +206,11 @@ def test_action_determinism_and_substepping(oracle):
 
 
 def test_golden_fixtures_reproduce_bitwise(oracle):
-    """The oracle reproduces the committed fixtures exactly (tests/golden/make_golden.py)."""
+    """The oracle reproduces the committed reference fixtures exactly (tests/golden/make_golden.py)."""
     meta = json.loads((GOLD / "golden.json").read_text())
     from tests.golden.make_golden import compute
 
-    fresh = compute()
+    fresh = compute("oracle")
     for key, entry in meta["cases"].items():
         arr = np.load(GOLD / entry["file"])
         assert hashlib.sha256(arr.tobytes()).hexdigest() == entry["sha256"], key
