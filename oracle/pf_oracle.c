@@ -85,42 +85,41 @@ static void parallel_for_index(int n, int workers, pfo_task fn, void* ctx) {
 
 /* ---------------------------------------------------------------- DenseMatrix (dense.cpp:17-68) */
 
-void pfo_mul(int d, const double* a, const double* o, double* out) {
-  memset(out, 0, sizeof(double) * (size_t)d * (size_t)d);
-  for (int i = 0; i < d; ++i)
-    for (int k = 0; k < d; ++k) {
-      double aik = a[(size_t)i * d + k];
-      if (aik == 0.0) continue;
-      const double* orow = &o[(size_t)k * d];
-      double* orow_out = &out[(size_t)i * d];
-      for (int j = 0; j < d; ++j) orow_out[j] += aik * orow[j];
+/* Products in dense.cpp:17-29's i-k-j order with the a_ik == 0 skip. Every output element
+ * receives its products in ascending k exactly as in the reference loop; the loops are only
+ * tiled (row blocks of MB, column blocks of JB) so B streams through cache once per row block
+ * instead of once per row -- the same operations, in the same per-element order, bit for bit. */
+#define PFO_MB 16
+#define PFO_JB 256
+static void mul_block_rows(int rows, int d, int kc, const double* a, const double* o, double* out) {
+  memset(out, 0, sizeof(double) * (size_t)rows * (size_t)kc);
+  for (int j0 = 0; j0 < kc; j0 += PFO_JB) {
+    const int j1 = j0 + PFO_JB < kc ? j0 + PFO_JB : kc;
+    for (int i0 = 0; i0 < rows; i0 += PFO_MB) {
+      const int i1 = i0 + PFO_MB < rows ? i0 + PFO_MB : rows;
+      for (int k = 0; k < d; ++k) {
+        const double* orow = &o[(size_t)k * kc];
+        for (int i = i0; i < i1; ++i) {
+          const double aik = a[(size_t)i * d + k];
+          if (aik == 0.0) continue;
+          double* orow_out = &out[(size_t)i * kc];
+          for (int j = j0; j < j1; ++j) orow_out[j] += aik * orow[j];
+        }
+      }
     }
+  }
 }
+
+void pfo_mul(int d, const double* a, const double* o, double* out) { mul_block_rows(d, d, d, a, o, out); }
 
 /* rows of a product: out (rows x d) = a_rows (rows x d) * o (d x d), pfo_mul's i-k-j order and
  * zero skip per row (row i of pfo_mul depends on row i of a only) -- the f1 row-split doubling */
 void pfo_mul_rows(int rows, int d, const double* a, const double* o, double* out) {
-  memset(out, 0, sizeof(double) * (size_t)rows * (size_t)d);
-  for (int i = 0; i < rows; ++i)
-    for (int k = 0; k < d; ++k) {
-      double aik = a[(size_t)i * d + k];
-      if (aik == 0.0) continue;
-      const double* orow = &o[(size_t)k * d];
-      double* orow_out = &out[(size_t)i * d];
-      for (int j = 0; j < d; ++j) orow_out[j] += aik * orow[j];
-    }
+  mul_block_rows(rows, d, d, a, o, out);
 }
 
 void pfo_mul_rect(int d, int kc, const double* a, const double* o, double* out) {
-  memset(out, 0, sizeof(double) * (size_t)d * (size_t)kc);
-  for (int i = 0; i < d; ++i)
-    for (int k = 0; k < d; ++k) {
-      double aik = a[(size_t)i * d + k];
-      if (aik == 0.0) continue;
-      const double* orow = &o[(size_t)k * kc];
-      double* orow_out = &out[(size_t)i * kc];
-      for (int j = 0; j < kc; ++j) orow_out[j] += aik * orow[j];
-    }
+  mul_block_rows(d, d, kc, a, o, out);
 }
 
 double pfo_one_norm(int d, const double* a) {
@@ -166,42 +165,73 @@ int pfo_substeps(double norm1, double theta) { /* action.cpp:398 */
 
 /* ---------------------------------------------------------------- DenseLu (dense.cpp:102-163) */
 
+/* DenseLu (dense.cpp:102-133). The reference applies, to every element (r, j), the updates
+ * a_rj -= f_r,col * u_col,j for col = 0, 1, ... in ascending order, each with the final
+ * multiplier f (skipped when f == 0) and the final U row entry, and swaps whole rows at each
+ * pivot. Here the same updates are applied panel by panel (width PFO_NB): within a panel
+ * right-looking on the panel's columns (pivot search, full-row swaps, multipliers exactly as in the
+ * reference), then the U rows of the panel and the trailing block receive the panel's updates in
+ * ascending col. Per element the operation sequence is unchanged, so factors and pivots are
+ * bit-identical to the unblocked loop (tests/test_ref_pin.py); the trailing matrix streams through
+ * cache once per panel instead of once per column. */
+#define PFO_NB 32
 int pfo_lu(int d, double* lu, int* piv, double pivot_rel_tol, pfo_status* st) {
   double ma = pfo_max_abs(d, lu);
   const double sc = ma > 1e-300 ? ma : 1e-300;
   const double tol = pivot_rel_tol * sc;
-  for (int col = 0; col < d; ++col) {
-    int p = col;
-    double best = fabs(lu[(size_t)col * d + col]);
-    for (int r = col + 1; r < d; ++r) {
-      double v = fabs(lu[(size_t)r * d + col]);
-      if (v > best) {
-        best = v;
-        p = r;
+  for (int c0 = 0; c0 < d; c0 += PFO_NB) {
+    const int c1 = c0 + PFO_NB < d ? c0 + PFO_NB : d;
+    for (int col = c0; col < c1; ++col) {
+      int p = col;
+      double best = fabs(lu[(size_t)col * d + col]);
+      for (int r = col + 1; r < d; ++r) {
+        double v = fabs(lu[(size_t)r * d + col]);
+        if (v > best) {
+          best = v;
+          p = r;
+        }
+      }
+      if (best <= tol) {
+        if (st) {
+          st->code = CODE(ERRC_SINGULAR_SHIFT);
+          st->column = col;
+          st->pivot_magnitude = best;
+          st->scale = sc;
+        }
+        return CODE(ERRC_SINGULAR_SHIFT);
+      }
+      if (p != col)
+        for (int j = 0; j < d; ++j) {
+          double t = lu[(size_t)p * d + j];
+          lu[(size_t)p * d + j] = lu[(size_t)col * d + j];
+          lu[(size_t)col * d + j] = t;
+        }
+      piv[col] = p;
+      const double inv_piv = 1.0 / lu[(size_t)col * d + col];
+      for (int r = col + 1; r < d; ++r) {
+        double f = lu[(size_t)r * d + col] * inv_piv;
+        lu[(size_t)r * d + col] = f;
+        if (f == 0.0) continue;
+        for (int j = col + 1; j < c1; ++j) lu[(size_t)r * d + j] -= f * lu[(size_t)col * d + j];
       }
     }
-    if (best <= tol) {
-      if (st) {
-        st->code = CODE(ERRC_SINGULAR_SHIFT);
-        st->column = col;
-        st->pivot_magnitude = best;
-        st->scale = sc;
+    if (c1 == d) break;
+    /* U rows of the panel, trailing columns: row t gets cols c0..t-1 in order (rows < t final) */
+    for (int t = c0 + 1; t < c1; ++t)
+      for (int s = c0; s < t; ++s) {
+        const double f = lu[(size_t)t * d + s];
+        if (f == 0.0) continue;
+        for (int j = c1; j < d; ++j) lu[(size_t)t * d + j] -= f * lu[(size_t)s * d + j];
       }
-      return CODE(ERRC_SINGULAR_SHIFT);
-    }
-    if (p != col)
-      for (int j = 0; j < d; ++j) {
-        double t = lu[(size_t)p * d + j];
-        lu[(size_t)p * d + j] = lu[(size_t)col * d + j];
-        lu[(size_t)col * d + j] = t;
-      }
-    piv[col] = p;
-    const double inv_piv = 1.0 / lu[(size_t)col * d + col];
-    for (int r = col + 1; r < d; ++r) {
-      double f = lu[(size_t)r * d + col] * inv_piv;
-      lu[(size_t)r * d + col] = f;
-      if (f == 0.0) continue;
-      for (int j = col + 1; j < d; ++j) lu[(size_t)r * d + j] -= f * lu[(size_t)col * d + j];
+    /* trailing block: every row gets the panel's cols c0..c1-1 in order */
+    for (int j0 = c1; j0 < d; j0 += PFO_JB) {
+      const int j1 = j0 + PFO_JB < d ? j0 + PFO_JB : d;
+      for (int r = c1; r < d; ++r)
+        for (int s = c0; s < c1; ++s) {
+          const double f = lu[(size_t)r * d + s];
+          if (f == 0.0) continue;
+          for (int j = j0; j < j1; ++j) lu[(size_t)r * d + j] -= f * lu[(size_t)s * d + j];
+        }
     }
   }
   return 0;
@@ -226,14 +256,103 @@ void pfo_lu_solve(int d, const double* lu, const int* piv, double* x) {
   }
 }
 
-void pfo_lu_solve_matrix(int d, int kc, const double* lu, const int* piv, const double* rhs, double* out) {
-  double* col = (double*)malloc(sizeof(double) * (size_t)d);
-  for (int j = 0; j < kc; ++j) {
-    for (int i = 0; i < d; ++i) col[i] = rhs[(size_t)i * kc + j];
-    pfo_lu_solve(d, lu, piv, col);
-    for (int i = 0; i < d; ++i) out[(size_t)i * kc + j] = col[i];
+/* solve_matrix (dense.cpp:153-163): every RHS column runs DenseLu::solve (swaps, then the
+ * dot-product forward and back substitutions with ascending j). PFO_CB columns are carried side by
+ * side -- per column the same operations in the same order -- so each row of the factors is read
+ * once per column block instead of once per column. */
+#define PFO_CB 16
+static void solve_cols(int d, int kc, const double* lu, const int* piv, const double* rhs, double* out, int cb,
+                       int ce) {
+  double* x = (double*)malloc(sizeof(double) * (size_t)d * PFO_CB);
+  double acc[PFO_CB];
+  for (int c0 = cb; c0 < ce; c0 += PFO_CB) {
+    const int w = c0 + PFO_CB < ce ? PFO_CB : ce - c0;
+    for (int i = 0; i < d; ++i)
+      for (int c = 0; c < w; ++c) x[(size_t)i * PFO_CB + c] = rhs[(size_t)i * kc + c0 + c];
+    for (int i = 0; i < d; ++i)
+      if (piv[i] != i)
+        for (int c = 0; c < w; ++c) {
+          double t = x[(size_t)i * PFO_CB + c];
+          x[(size_t)i * PFO_CB + c] = x[(size_t)piv[i] * PFO_CB + c];
+          x[(size_t)piv[i] * PFO_CB + c] = t;
+        }
+    for (int i = 1; i < d; ++i) {
+      const double* row = &lu[(size_t)i * d];
+      for (int c = 0; c < w; ++c) acc[c] = x[(size_t)i * PFO_CB + c];
+      for (int j = 0; j < i; ++j) {
+        const double l = row[j];
+        const double* xj = &x[(size_t)j * PFO_CB];
+        for (int c = 0; c < w; ++c) acc[c] -= l * xj[c];
+      }
+      for (int c = 0; c < w; ++c) x[(size_t)i * PFO_CB + c] = acc[c];
+    }
+    for (int i = d - 1; i >= 0; --i) {
+      const double* row = &lu[(size_t)i * d];
+      for (int c = 0; c < w; ++c) acc[c] = x[(size_t)i * PFO_CB + c];
+      for (int j = i + 1; j < d; ++j) {
+        const double u = row[j];
+        const double* xj = &x[(size_t)j * PFO_CB];
+        for (int c = 0; c < w; ++c) acc[c] -= u * xj[c];
+      }
+      const double piv_ii = row[i];
+      for (int c = 0; c < w; ++c) x[(size_t)i * PFO_CB + c] = acc[c] / piv_ii;
+    }
+    for (int i = 0; i < d; ++i)
+      for (int c = 0; c < w; ++c) out[(size_t)i * kc + c0 + c] = x[(size_t)i * PFO_CB + c];
   }
-  free(col);
+  free(x);
+}
+
+void pfo_lu_solve_matrix(int d, int kc, const double* lu, const int* piv, const double* rhs, double* out) {
+  solve_cols(d, kc, lu, piv, rhs, out, 0, kc);
+}
+
+/* Threaded variants for the big checks (cfg3/cfg4 at full size): columns of a solve and rows of a
+ * product are independent, so splitting them over threads changes no element's operations. */
+typedef struct {
+  int d, kc, chunk;
+  const double *lu, *rhs, *a, *o;
+  const int* piv;
+  double* out;
+} mt_ctx;
+
+static void solve_chunk(int t, void* p) {
+  mt_ctx* c = (mt_ctx*)p;
+  const int cb = t * c->chunk, ce = cb + c->chunk < c->kc ? cb + c->chunk : c->kc;
+  solve_cols(c->d, c->kc, c->lu, c->piv, c->rhs, c->out, cb, ce);
+}
+
+static void solve_mt(int d, int kc, const double* lu, const int* piv, const double* rhs, double* out, int threads) {
+  if (threads <= 1 || kc <= PFO_CB) {
+    solve_cols(d, kc, lu, piv, rhs, out, 0, kc);
+    return;
+  }
+  int chunk = (kc + threads - 1) / threads;
+  chunk = (chunk + PFO_CB - 1) / PFO_CB * PFO_CB;
+  mt_ctx c = {d, kc, chunk, lu, rhs, NULL, NULL, piv, out};
+  parallel_for_index((kc + chunk - 1) / chunk, threads, solve_chunk, &c);
+}
+
+static void mul_chunk(int t, void* p) {
+  mt_ctx* c = (mt_ctx*)p;
+  const int r0 = t * c->chunk, r1 = r0 + c->chunk < c->d ? r0 + c->chunk : c->d;
+  mul_block_rows(r1 - r0, c->d, c->kc, c->a + (size_t)r0 * c->d, c->o, c->out + (size_t)r0 * c->kc);
+}
+
+/* (d x d)(d x kc) split by rows over threads */
+static void mul_mt(int d, int kc, const double* a, const double* o, double* out, int threads) {
+  if (threads <= 1 || d < 2 * PFO_MB) {
+    mul_block_rows(d, d, kc, a, o, out);
+    return;
+  }
+  int chunk = (d + threads - 1) / threads;
+  chunk = (chunk + PFO_MB - 1) / PFO_MB * PFO_MB;
+  mt_ctx c = {d, kc, chunk, NULL, NULL, a, o, NULL, out};
+  parallel_for_index((d + chunk - 1) / chunk, threads, mul_chunk, &c);
+}
+
+void pfo_mul_mt(int d, const double* a, const double* o, double* out, int threads) {
+  mul_mt(d, d, a, o, out, threads);
 }
 
 int pfo_solve_shifted(int d, const double* b, double c, double* out, pfo_status* st) {
@@ -263,6 +382,7 @@ typedef struct {
   const pfo_method* m;
   double** x;        /* per shift: solved X_i (unweighted), NULL for zero shifts */
   pfo_status* stats; /* per shift */
+  int inner;         /* threads per shift's solve (workers beyond one per shift) */
 } eval_ctx;
 
 static void eval_shift(int i, void* p) {
@@ -290,7 +410,7 @@ static void eval_shift(int i, void* p) {
     c->stats[i].shift_index = i + 1;
   } else {
     double* x = (double*)malloc(sizeof(double) * nn);
-    pfo_lu_solve_matrix(d, d, mm, piv, rhs, x);
+    solve_mt(d, d, mm, piv, rhs, x, c->inner);
     c->x[i] = x;
   }
   free(rhs);
@@ -311,6 +431,9 @@ int pfo_eval_dense(int d, const double* b, const pfo_method* m, int workers, dou
   c.m = m;
   c.x = (double**)calloc((size_t)(n > 0 ? n : 1), sizeof(double*));
   c.stats = (pfo_status*)calloc((size_t)(n > 0 ? n : 1), sizeof(pfo_status));
+  int nz = 0;
+  for (int i = 0; i < n; ++i) nz += m->shifts[i] != 0.0;
+  c.inner = nz > 0 && workers > nz ? workers / nz : 1;
   parallel_for_index(n, workers, eval_shift, &c);
   int rc = 0;
   for (int i = 0; i < n; ++i)
@@ -350,7 +473,7 @@ int pfo_eval_dense(int d, const double* b, const pfo_method* m, int workers, dou
           if (d2 != 0.0) {
             if (!b2) {
               b2 = (double*)malloc(sizeof(double) * nn);
-              pfo_mul(d, b, b, b2);
+              mul_mt(d, d, b, b, b2, workers);
             }
             axpy(nn, poly, d2, b2);
           }
@@ -391,7 +514,7 @@ int pfo_expm(int d, const double* a, const pfo_method* m, double theta, int j_fi
   if (!rc) {
     double* t = (double*)malloc(sizeof(double) * nn);
     for (int s = 0; s < j; ++s) {
-      pfo_mul(d, out, out, t);
+      mul_mt(d, d, out, out, t, workers);
       memcpy(out, t, sizeof(double) * nn);
     }
     free(t);
@@ -464,10 +587,10 @@ int pfo_expm_phi1(int d, const double* a, const pfo_method* m, double theta, int
     for (int s = 0; s < j; ++s) {
       memcpy(t, out_e, sizeof(double) * nn); /* T = E + I */
       add_scaled_identity(d, t, 1.0);
-      pfo_mul(d, t, out_phi, u); /* Phi = 0.5 (T Phi) */
+      mul_mt(d, d, t, out_phi, u, workers); /* Phi = 0.5 (T Phi) */
       scale(nn, u, 0.5);
       memcpy(out_phi, u, sizeof(double) * nn);
-      pfo_mul(d, out_e, out_e, t); /* E = E E */
+      mul_mt(d, d, out_e, out_e, t, workers); /* E = E E */
       memcpy(out_e, t, sizeof(double) * nn);
     }
     free(t);
@@ -523,7 +646,7 @@ int pfo_cossin(int d, const double* a, const pfo_pair_method* pm, double theta, 
   double* b = (double*)malloc(sizeof(double) * nn);
   double* b2 = (double*)malloc(sizeof(double) * nn);
   scaled_copy(nn, a, j, b);
-  pfo_mul(d, b, b, b2);
+  mul_mt(d, d, b, b, b2, workers);
   pair_ctx c = {d, b2, pm, (double**)calloc((size_t)pm->n_pairs + 1, sizeof(double*)),
                 (pfo_status*)calloc((size_t)pm->n_pairs + 1, sizeof(pfo_status))};
   parallel_for_index(pm->n_pairs, workers, pair_shift, &c);
@@ -550,13 +673,13 @@ int pfo_cossin(int d, const double* a, const pfo_pair_method* pm, double theta, 
       out_c[(size_t)i * d + i] = pm->a0 - accc[(size_t)i * d + i];
       t[(size_t)i * d + i] = pm->a1 - accs[(size_t)i * d + i];
     }
-    pfo_mul(d, b, t, out_s);
+    mul_mt(d, d, b, t, out_s, workers);
     double* c2m = accc; /* reuse */
     double* s2m = accs;
     for (int s = 0; s < j; ++s) {
-      pfo_mul(d, out_c, out_c, c2m);
-      pfo_mul(d, out_s, out_s, s2m);
-      pfo_mul(d, out_s, out_c, t);
+      mul_mt(d, d, out_c, out_c, c2m, workers);
+      mul_mt(d, d, out_s, out_s, s2m, workers);
+      mul_mt(d, d, out_s, out_c, t, workers);
       for (size_t i = 0; i < nn; ++i) {
         out_c[i] = c2m[i] - s2m[i];
         out_s[i] = 2.0 * t[i];
@@ -697,7 +820,7 @@ int pfo_action(int d, int k, const double* a, const double* v, const pfo_method*
     for (int i = 0; i < n; ++i) terms[i] = (double*)malloc(sizeof(double) * cnt);
     memcpy(x, v, sizeof(double) * cnt);
     for (int step = 0; step < substeps; ++step) {
-      if (m->form == 1 || m->has_poly) pfo_mul_rect(d, k, b, x, bv);
+      if (m->form == 1 || m->has_poly) mul_mt(d, k, b, x, bv, workers);
       solve_ctx sc = {d, k, m, fc.lu, fc.piv, x, bv, terms};
       parallel_for_index(n, workers, solve_shift, &sc);
       memset(out, 0, sizeof(double) * cnt);
@@ -707,7 +830,7 @@ int pfo_action(int d, int k, const double* a, const double* v, const pfo_method*
         for (size_t j = 0; j < cnt; ++j) out[j] += constant * x[j];
         if (m->has_poly) {
           const double d1 = m->poly[1], d2 = m->poly[2];
-          pfo_mul_rect(d, k, b, bv, b2v);
+          mul_mt(d, k, b, bv, b2v, workers);
           for (size_t j = 0; j < cnt; ++j) out[j] += d1 * bv[j] + d2 * b2v[j];
         }
       }

@@ -22,7 +22,7 @@
  *   action.cpp:224-339).
  *
  * Parity pinning: PINNED against the reference itself. oracle/Makefile compiles
- * /root/reference/proj/core/src/*.cpp unmodified (GMP/gmpxx shims in oracle/shim/) into
+ * /root/reference/proj/core/src/(*).cpp unmodified (GMP/gmpxx shims in oracle/shim/) into
  * oracle/_ref/libparfrac_ref.so; the reference's own doctest suites and acceptance checklist pass
  * on that build, and tests/test_ref_pin.py requires this restatement to equal it bit for bit
  * (LU factors and pivots, solve_shifted, mul, eval_dense for every catalog method and both forms,
@@ -74,6 +74,7 @@ void pfo_randn_fill(uint64_t seed, int64_t count, double* out);
 void pfo_mul(int n, const double* a, const double* b, double* c);
 void pfo_mul_rect(int n, int k, const double* a, const double* b, double* c); /* (n x n)(n x k) */
 void pfo_mul_rows(int rows, int n, const double* a, const double* b, double* c); /* (rows x n)(n x n) */
+void pfo_mul_mt(int n, const double* a, const double* b, double* c, int threads); /* rows split over threads */
 double pfo_one_norm(int n, const double* a);
 double pfo_max_abs(int n, const double* a);
 int pfo_squarings(double norm1, double theta);

@@ -110,6 +110,23 @@ def test_lu_pivots_and_factors_bitwise(ref, oracle, n):
         assert np.array_equal(lu_r, lu_o)
 
 
+@pytest.mark.parametrize("n", [300, 533])
+def test_blocked_oracle_kernels_bitwise_multi_panel(ref, oracle, n):
+    """pf_oracle.c tiles the LU (32-column panels), the multi-RHS solve (32-column blocks) and the
+    products (32 x 512 tiles) without changing any element's operation order; sizes that span
+    several ragged panels and tiles, with pivoting and exact zeros, must still match the reference."""
+    b = rand(n, 7 + n, 50.0)
+    a = np.eye(n) - 0.9 * b
+    a[::7, ::5] = 0.0
+    lu_r, piv_r = ref.lu(a)
+    lu_o, piv_o = oracle.lu(a)
+    assert np.array_equal(piv_r, piv_o) and np.array_equal(lu_r, lu_o)
+    assert (piv_o != np.arange(n)).sum() > n // 2  # genuinely pivoting
+    rhs = rand(n, 8 + n, 3.0)
+    assert np.array_equal(ref.lu_solve_matrix(a, rhs), oracle.lu_solve_matrix(lu_o, piv_o, rhs))
+    assert np.array_equal(ref.mul(a, rhs), oracle.mul(a, rhs))
+
+
 def test_singular_detection_same_column(ref, oracle):
     a = np.array([[1.0, 2.0, 3.0], [2.0, 4.0, 6.0], [1.0, 0.0, 1.0]])
     with pytest.raises(ref.RefError) as er:
@@ -144,6 +161,7 @@ def test_eval_dense_bitwise(ref, oracle, name, form):
             continue
         assert np.array_equal(want, oracle.eval_dense(om(name, form), b, workers=3))
         assert np.array_equal(want, ref.eval_dense(rm, b, form, workers=4))  # worker count is invisible
+        assert np.array_equal(want, oracle.eval_dense(om(name, form), b, workers=20))  # threaded solves
 
 
 @pytest.mark.parametrize("name", ["R4", "R8"])
@@ -169,7 +187,7 @@ def test_expm_phi1_bitwise(ref, oracle):
     th = M.THETA_U53["R8_phi1set"]
     e_r, p_r, j_r = ref.expm_phi1(ref.RefMethod.catalog("R8"), ref.RefMethod.build_plain(8, "5", "phi1", 8), a, th,
                                   M.RESIDUAL)
-    e_o, p_o, j_o = oracle.expm_phi1(a, O.OMethod.from_method(r8, M.RESIDUAL, extra=(phi,)), th)
+    e_o, p_o, j_o = oracle.expm_phi1(a, O.OMethod.from_method(r8, M.RESIDUAL, extra=(phi,)), th, workers=19)
     assert j_r == j_o and np.array_equal(e_r, e_o) and np.array_equal(p_r, p_o)
 
 
