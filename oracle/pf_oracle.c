@@ -770,6 +770,7 @@ typedef struct {
   const double* x;  /* current V */
   const double* bv; /* B V */
   double** terms;
+  int inner;        /* threads per shift's solve */
 } solve_ctx;
 
 static void solve_shift(int i, void* p) { /* assemble_action per-shift body, action.cpp:240-263 */
@@ -781,7 +782,7 @@ static void solve_shift(int i, void* p) { /* assemble_action per-shift body, act
     if (sh == 0.0)
       memcpy(term, c->x, sizeof(double) * cnt);
     else
-      pfo_lu_solve_matrix(c->d, c->k, c->lu[i], c->piv[i], c->x, term);
+      solve_mt(c->d, c->k, c->lu[i], c->piv[i], c->x, term, c->inner);
     scale(cnt, term, w);
   } else {
     if (sh == 0.0) {
@@ -790,7 +791,7 @@ static void solve_shift(int i, void* p) { /* assemble_action per-shift body, act
     }
     double* rhs = (double*)malloc(sizeof(double) * cnt);
     for (size_t j = 0; j < cnt; ++j) rhs[j] = sh * c->bv[j];
-    pfo_lu_solve_matrix(c->d, c->k, c->lu[i], c->piv[i], rhs, term);
+    solve_mt(c->d, c->k, c->lu[i], c->piv[i], rhs, term, c->inner);
     scale(cnt, term, w);
     free(rhs);
   }
@@ -821,7 +822,9 @@ int pfo_action(int d, int k, const double* a, const double* v, const pfo_method*
     memcpy(x, v, sizeof(double) * cnt);
     for (int step = 0; step < substeps; ++step) {
       if (m->form == 1 || m->has_poly) mul_mt(d, k, b, x, bv, workers);
-      solve_ctx sc = {d, k, m, fc.lu, fc.piv, x, bv, terms};
+      int nz = 0;
+      for (int i = 0; i < n; ++i) nz += m->shifts[i] != 0.0;
+      solve_ctx sc = {d, k, m, fc.lu, fc.piv, x, bv, terms, nz > 0 && workers > nz ? workers / nz : 1};
       parallel_for_index(n, workers, solve_shift, &sc);
       memset(out, 0, sizeof(double) * cnt);
       for (int i = 0; i < n; ++i) axpy(cnt, out, 1.0, terms[i]);

@@ -1,7 +1,7 @@
 """GPU parity of the large-n path (n > 128: recursive LU / triangular solves on the DMMA GEMM),
 the dense block action, DenseLu, and the phi1 / cos-sin compositions at mid sizes, against the
-CPU oracle on identical seeded inputs. Full BASELINE sizes are covered by size-independent
-properties in test_gpu_configs.py."""
+CPU oracle on identical seeded inputs. Full BASELINE sizes are compared with the oracle in
+test_gpu_configs.py."""
 import numpy as np
 import pytest
 
@@ -129,7 +129,7 @@ def test_action_block(dev, oracle, n, k, name, form):
     ref = oracle.action(a, v, oracle.OMethod.from_method(m, form), nsub)
     amp = float(sum(abs(w) for w in m.weights) + sum(abs(d) for d in m.poly))
     tol = max(TOL, 100 * amp * 2.23e-16) if name.startswith("R10") else TOL
-    assert oracle.rel_diff_1norm(got, ref) <= tol * nsub
+    assert oracle.rel_diff_1norm(got, ref) <= tol  # flat bar, independent of the substep count
 
 
 def test_dense_lu_api(dev, oracle):

@@ -285,7 +285,7 @@ def test_native_library_is_loaded(dev):
 
 
 def test_golden_fixtures_on_device(dev, oracle):
-    """Device path against the frozen oracle outputs (tests/golden/)."""
+    """Device path against the frozen reference outputs (tests/golden/, made by oracle/_ref)."""
     import json
     from pathlib import Path
 
@@ -305,3 +305,11 @@ def test_golden_fixtures_on_device(dev, oracle):
     assert oracle.rel_diff_1norm(dev.eval_dense("R8", x["eval24_B"], dev.EvalOptions(form=1)),
                                  g("eval24_R8_residual")) <= TOL
     assert oracle.rel_diff_1norm(dev.solve_shifted(x["pivot24_B"], 0.2), g("pivot24_solve_shifted_0.2")) <= 1e-13
+    e, p = dev.expm_phi1(x["phi48_A"], "R8")
+    assert oracle.rel_diff_1norm(e, g("phi48_R8_exp")) <= TOL
+    assert oracle.rel_diff_1norm(p, g("phi48_R8_phi1")) <= TOL
+    act = dev.action(x["action40_A"], x["action40_V"], "R8", substeps=3)
+    assert oracle.rel_diff_1norm(act, g("action40_R8_residual_N3")) <= TOL
+    t = dev.TridiagMatrix(*x["trid200"])
+    band = dev.tridiag_action("R8", t, x["trid200_v"], substeps=4, form=1)
+    assert np.array_equal(np.asarray(band), g("trid200_R8_residual_N4"))  # banded path is bit-exact

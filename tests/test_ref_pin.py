@@ -199,6 +199,9 @@ def test_dense_action_bitwise(ref, oracle, name, form):
     want = ref.dense_action(ref.RefMethod.catalog(name), a, v, 3, form, workers=2)
     got = oracle.action(a, v, om(name, form), 3, workers=3)
     assert np.array_equal(want, got)
+    v2 = W.randn(43, n * 40).reshape(n, 40)  # several 16-column solve blocks over threads
+    assert np.array_equal(ref.dense_action(ref.RefMethod.catalog(name), a, v2, 2, form),
+                          oracle.action(a, v2, om(name, form), 2, workers=29))
 
 
 def test_golden_fixtures_are_reference_outputs(ref):
