@@ -8,11 +8,18 @@ weighted sum -> j_b squarings, all inside one fused kernel per matrix).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--method R4|R8]
 
-Multi-GPU (torchrun, one process per GPU): batch-sharded weak scaling, every rank evaluates its own
-4096-matrix batch; no collective on the data path (the matrices are independent).
-`--impl reference` times the reference algorithm on the host cores: the reference C++ cannot be
-built here (no gmpxx / vendor), so this is the oracle restatement (kind "port") of
-proj/core/src/dense.cpp, run with parallel_for_index over the batch (cli.cpp:314,228).
+--gpus N > 1 without a torchrun environment re-launches this script under torch.distributed.run
+with N ranks (one per GPU); batch-sharded weak scaling: every rank evaluates its own 4096-matrix
+batch, no collective on the data path (the matrices are independent); time = max over ranks.
+
+Parity: the timed run's outputs are compared, matrix by matrix, with THE REFERENCE BUILD
+(oracle/_ref: /root/reference/proj/core/src compiled unmodified; eval_dense + DenseMatrix::mul)
+over the whole batch; the same run is the cpu_baseline (kind "reference").
+`--impl reference` times that reference build on the host cores over the whole batch per step
+(all host threads, parallel over the batch as cli.cpp:314), on rank 0 only.
+Secondary lines (N = 1): the R8 variant of the headline, and clocked single-GPU lines for
+configs[2..4] (cfg3 exp+phi1 4096^2, cfg4 action 16384^2 x 64, cfg5 cos/sin 256 x 512^2) with a
+reduced-unit reference CPU timing extrapolated by the SURVEY §8(d) FLOP model.
 """
 from __future__ import annotations
 
@@ -42,8 +49,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--method", default="R4")
     ap.add_argument("--batch", type=int, default=BATCH)
-    ap.add_argument("--no-secondary", action="store_true", help="skip the R8 secondary measurement")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the R8 and cfg3/4/5 secondary lines")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU reference legs (cpu_baseline, parity)")
     return ap.parse_args()
 
 
@@ -54,9 +61,90 @@ def dist_env():
     return rank, world, local
 
 
+def relaunch_under_torchrun(args) -> int:
+    """--gpus N > 1 outside torchrun: start N ranks on this node (one per GPU) and wait."""
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def host_cpu():
+    """(threads usable by this process, CPU model string)."""
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count() or 1
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return cores, model
+
+
+def reference_backend():
+    """THE REFERENCE BUILD (oracle/_ref) when present, else the restatement pinned to it bit for bit."""
+    from oracle import ref as R
+
+    if R.available():
+        try:
+            R.lib()
+            return "reference"
+        except Exception:
+            pass
+    return "port"
+
+
+def cpu_expm_batched(a, method_name, threads):
+    """expm over a batch on the host: reference build (eval_dense + DenseMatrix::mul) or the port."""
+    from paper_2210_03714_b200 import methods as M
+
+    th = M.THETA_U53[method_name]
+    if reference_backend() == "reference":
+        from oracle import ref as R
+
+        return R.expm_batched(R.RefMethod.catalog(method_name), a, th, M.RESIDUAL, threads=threads)
+    from oracle import oracle as O
+
+    return O.expm_batched(a, O.OMethod.from_method(M.catalog(method_name), M.RESIDUAL), th, threads=threads)
+
+
+def parity_vs_reference(got, js_got, a, method_name, threads):
+    """Whole-batch comparison with the reference build; returns (parity dict, cpu seconds, kind)."""
+    t0 = time.perf_counter()
+    want, js = cpu_expm_batched(a, method_name, threads)
+    dt = time.perf_counter() - t0
+    num = np.abs(got - want).sum(axis=1).max(axis=1)
+    den = np.abs(want).sum(axis=1).max(axis=1)
+    rel = num / den
+    kind = reference_backend()
+    return ({"vs": "oracle/_ref (reference build)" if kind == "reference" else "oracle restatement (pinned)",
+             "max_rel_1norm": float(rel.max()), "mean_rel_1norm": float(rel.mean()),
+             "squarings_equal": bool(np.array_equal(np.asarray(js_got), js)), "n_compared": int(len(rel)),
+             "tol": 1e-11, "pass": bool(rel.max() <= 1e-11 and np.array_equal(np.asarray(js_got), js))},
+            dt, kind)
+
+
 def algorithmic_flops(js: np.ndarray, n_shifts: int, n: int = N_MAT) -> float:
     """per matrix (P * 8/3 + 2 j_b) n^3 (residual LU+TRSM per shift, one GEMM per squaring)."""
     return float(np.sum(n_shifts * (8.0 / 3.0) + 2.0 * js.astype(np.float64)) * n ** 3)
+
+
+def executed_flops(js: np.ndarray, n_shifts: int, n: int = N_MAT) -> float:
+    """What the kernel performs in pair mode (every cfg2 matrix is certified, since
+    ||2^-j A||_1 <= theta): B^2 (2n^3), per (c, -c) pair one LU of I - c^2 B^2 and one TRSM with a
+    dense RHS (8/3 n^3), the final A.V product (2n^3), then 2 j_b n^3 of squaring."""
+    pairs = n_shifts // 2
+    return float(np.sum(2.0 + pairs * (8.0 / 3.0) + 2.0 + 2.0 * js.astype(np.float64)) * n ** 3)
 
 
 class ClockSampler:
@@ -127,64 +215,36 @@ def load_profile_traffic():
     return None, None
 
 
-def cpu_baseline(method_name: str, budget_s: float = 12.0):
-    """Oracle restatement of dense.cpp on the host cores, bounded sample of the cfg2 workload."""
-    from oracle import oracle as O
-    from paper_2210_03714_b200 import methods as M, workloads as W
-
-    cores = os.cpu_count() or 1
-    m = M.catalog(method_name)
-    om = O.OMethod.from_method(m, 1)
-    th = M.THETA_U53[method_name]
-    chunk = max(cores * 2, 16)
-    done = 0
-    t_work = 0.0
-    t0 = time.perf_counter()
-    seed0 = 1000
-    while time.perf_counter() - t0 < budget_s and done < BATCH:
-        a = W.cfg2(batch=chunk, seed0=seed0 + done)
-        ts = time.perf_counter()
-        O.expm_batched(a, om, th, threads=cores)
-        t_work += time.perf_counter() - ts
-        done += chunk
-    rate = done / t_work
-    return {"value": rate, "unit": "evals/s", "cores": cores, "kind": "port",
-            "sample": "%d of the 4096 cfg2 matrices (%s, residual, scaling+squaring), %d host threads, "
-                      "oracle restatement of proj/core/src/dense.cpp compiled -O3 (reference not buildable: "
-                      "no gmpxx/vendor)" % (done, method_name, cores)}
-
-
 def run_reference(args):
+    """The reference's own CPU implementation (oracle/_ref) of the headline workload on the host
+    cores: every step evaluates the whole batch (all host threads, parallel over the batch)."""
     rank, world, local = dist_env()
     if rank != 0:
         return
-    from oracle import oracle as O
-    from paper_2210_03714_b200 import methods as M, workloads as W
+    from paper_2210_03714_b200 import workloads as W
 
-    cores = os.cpu_count() or 1
-    m = M.catalog(args.method)
-    om = O.OMethod.from_method(m, 1)
-    th = M.THETA_U53[args.method]
-    sample = max(cores * 4, 32)
-    a = W.cfg2(batch=sample)
+    cores, model = host_cpu()
+    kind = reference_backend()
+    a = W.cfg2(batch=args.batch)
     for _ in range(args.warmup):
-        O.expm_batched(a[: cores], om, th, threads=cores)
+        cpu_expm_batched(a, args.method, cores)
     times = []
     for _ in range(args.steps):
         t = time.perf_counter()
-        O.expm_batched(a, om, th, threads=cores)
+        cpu_expm_batched(a, args.method, cores)
         times.append(time.perf_counter() - t)
     per = float(np.mean(times))
-    value = sample / per
+    value = args.batch / per
+    what = ("reference build oracle/_ref (/root/reference/proj/core/src compiled unmodified, -O3 -DNDEBUG): "
+            "eval_dense + DenseMatrix::mul" if kind == "reference" else "oracle restatement of dense.cpp (pinned)")
     line = {"impl": "reference", "metric": "f(A) evals/sec (FP64)", "value": value, "unit": "evals/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": per * 1e3 * (args.batch / sample), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "cfg2_batched_expm_%dx128x128_%s" % (args.batch, args.method), "batch": args.batch,
                        "n": N_MAT, "method": args.method, "form": "residual"},
-            "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "port",
-                             "sample": "%d cfg2 matrices per step (of %d), %d threads; oracle restatement of "
-                                       "dense.cpp (reference not buildable here)" % (sample, args.batch, cores)},
+            "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": kind, "cpu_model": model,
+                             "sample": "the whole %d-matrix batch per step, %d host threads (affinity), %s" % (
+                                 args.batch, cores, what)},
             "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -213,6 +273,7 @@ def time_ours(args, method_name, A, rank, world, local, dist, eng):
     torch.cuda.synchronize()
     js = j_out.cpu().numpy()
     flops = algorithmic_flops(js, m.processors())
+    exe_flops = executed_flops(js, m.processors())
 
     # --- timed region: K steps, barrier + sync both sides, CUDA events on the context stream
     stream = torch.cuda.current_stream()
@@ -246,8 +307,8 @@ def time_ours(args, method_name, A, rank, world, local, dist, eng):
         torch.cuda.synchronize()
         kt.append(k0.elapsed_time(k1))
     kernel_ms = float(np.median(kt))  # median of the individually timed launches (robust to one slow launch)
-    return {"ms": ms, "flops": flops, "kernel_ms": kernel_ms, "launches": launches, "clocks": clk.summary(),
-            "js": js, "out": out}
+    return {"ms": ms, "flops": flops, "exe_flops": exe_flops, "kernel_ms": kernel_ms, "launches": launches,
+            "clocks": clk.summary(), "js": js, "out": out}
 
 
 def time_e2e(args, method_name, A_host_pinned, eng):
@@ -281,10 +342,163 @@ def time_e2e(args, method_name, A_host_pinned, eng):
     return ms, nbytes, nbytes
 
 
+def timed_region(fn, steps, local, stream):
+    """K calls bracketed by synchronisation, CUDA events on the launching stream, clocks sampled."""
+    import torch
+
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps, clk.summary()
+
+
+def large_config_lines(peak, local, cores):
+    """Clocked single-GPU lines for BASELINE configs[2..4] plus a reduced-unit reference CPU timing
+    extrapolated by the SURVEY §8(d) FLOP model (the full CPU runs take hours)."""
+    import torch
+    from paper_2210_03714_b200 import api, methods as M, workloads as W
+
+    stream = torch.cuda.current_stream()
+    eng = api.engine()
+    lines = []
+    kind = reference_backend()
+
+    def ref_unit(n, fn, reps=1):
+        t = time.perf_counter()
+        for _ in range(reps):
+            fn(n)
+        return (time.perf_counter() - t) / reps
+
+    def mk(name, workload, unit_s, ms, clocks, alg, exe, launches, cpu, extra):
+        tf = alg / (ms * 1e-3) / 1e12
+        te = exe / (ms * 1e-3) / 1e12
+        d = {"config": name, "workload": workload, "value": 1e3 / ms * unit_s, "unit": "evals/s",
+             "ms_per_eval": ms / unit_s if unit_s > 1 else ms, "ms_per_step": ms, "clocks": clocks,
+             "algorithmic_tflops": tf, "frac_algorithmic": tf / peak, "executed_tflops": te,
+             "frac_executed": te / peak, "flops_algorithmic": alg, "flops_executed": exe,
+             "gpu_launches_per_step": launches, "cpu_baseline": cpu}
+        d.update(extra)
+        return d
+
+    # ---- cfg3: exp and phi1 of one 4096^2, R8 shifts, j = 8
+    from oracle import ref as R
+
+    A = torch.from_numpy(W.cfg3()).cuda()
+    n = 4096
+    fn = lambda: api.expm_phi1(A, "R8")  # noqa: E731
+    fn()
+    l0 = eng.launch_count()
+    fn()
+    torch.cuda.synchronize()
+    launches = eng.launch_count() - l0
+    ms, clk = timed_region(fn, 3, local, stream)
+    alg = 8 * (8 / 3) * n ** 3 + 8 * 2 * 2 * n ** 3
+    exe = (2 + 4 * (8 / 3) + 2 * 2 + 8 * 2 * 2) * n ** 3
+    cpu = None
+    if kind == "reference":
+        nu = 1024
+        b = W.scaled_to_one_norm(W.randn_matrix(nu, 3), 0.2)
+        mm = np.eye(nu) - 0.2 * b
+        t_shift = ref_unit(nu, lambda _: R.lu_solve_matrix(mm, b))
+        t_mul = ref_unit(nu, lambda _: R.mul(b, b))
+        scale = (n / nu) ** 3
+        waves = math.ceil(8 / min(8, cores))
+        est = waves * t_shift * scale + 16 * t_mul * scale
+        cpu = {"value": 1.0 / est, "unit": "evals/s", "cores": min(8, cores), "kind": "reference",
+               "sample": "reduced unit, extrapolated: reference DenseLu + solve_matrix (one residual shift) and "
+                         "DenseMatrix::mul at n = 1024 (%.2f s, %.2f s), x (4096/1024)^3; 8 shifts over "
+                         "workers = min(8, cores) (dense.cpp:202), 16 single-threaded products" % (t_shift, t_mul)}
+    lines.append(mk("cfg3", "exp+phi1 of one 4096^2, R8 shifts, j = 8, residual", 1, ms, clk, alg, exe, launches, cpu,
+                    {"executed_basis": "pair mode: B^2, 4 pair LU+TRSM, 2 combine products, 16 doubling GEMMs"}))
+    del A
+
+    # ---- cfg5: cos/sin of 256 x 512^2, R8 pairs, j = 12
+    A = torch.from_numpy(W.cfg5()).cuda()
+    n, bsz = 512, 256
+    fn = lambda: api.cossin(A, "R8")  # noqa: E731
+    fn()
+    l0 = eng.launch_count()
+    fn()
+    torch.cuda.synchronize()
+    launches = eng.launch_count() - l0
+    ms, clk = timed_region(fn, 3, local, stream)
+    _, _, js = api.cossin(A, "R8", return_squarings=True)
+    jm = float(js.double().mean())
+    alg = bsz * (1 + 4 * 4 / 3 + 1 + 3 * jm) * 2 * n ** 3
+    exe = bsz * (1 + 4 * 4 / 3 + 1 + 2 * jm) * 2 * n ** 3
+    cpu = None
+    if kind == "reference":
+        from oracle import oracle as O
+
+        nu = 256
+        a1 = W.cfg5(batch=1, n=nu)
+        pm = O.OPair.from_pair(M.pair_method(M.catalog("R8")))
+        t_unit = ref_unit(nu, lambda _: O.cossin(a1[0], pm, M.THETA_U53["R8"], j_fixed=int(jm + 0.5)))
+        per_mat = t_unit * (n / nu) ** 3
+        est = per_mat * math.ceil(bsz / cores)
+        cpu = {"value": bsz / est, "unit": "evals/s", "cores": cores, "kind": "port",
+               "sample": "reduced unit, extrapolated: one cos/sin evaluation at n = 256 with j = %d on the "
+                         "restatement (the reference has no cos/sin composition; its LU/solve/mul are pinned bit for "
+                         "bit), x (512/256)^3, batch of 256 over %d threads" % (int(jm + 0.5), cores)}
+    lines.append(mk("cfg5", "cos/sin of 256 x 512^2 symmetric, R8 pairs, C^2-S^2 / 2SC", bsz, ms, clk, alg, exe,
+                    launches, cpu, {"mean_squarings": jm,
+                                    "executed_basis": "C^2 - S^2 formed as (C - S)(C + S): 2 GEMMs per doubling"}))
+    del A
+
+    # ---- cfg4: exp(tA) V, 16384^2, k = 64, N = 42
+    a, v = W.cfg4()
+    nsub = M.substeps_for(W.one_norm(a), M.THETA_U53["R8"])
+    A = torch.from_numpy(a).cuda()
+    V = torch.from_numpy(v).cuda()
+    del a
+    n, k = 16384, 64
+    fn = lambda: api.action(A, V, "R8", substeps=nsub)  # noqa: E731
+    fn()
+    l0 = eng.launch_count()
+    fn()
+    torch.cuda.synchronize()
+    launches = eng.launch_count() - l0
+    ms, clk = timed_region(fn, 2, local, stream)
+    alg = 8 * (2 / 3) * n ** 3 + nsub * 8 * 2 * n * n * k + nsub * 2 * n * n * k
+    exe = 2 * n ** 3 + 4 * (2 / 3) * n ** 3 + nsub * 6 * 2 * n * n * k
+    cpu = None
+    if kind == "reference":
+        nu = 1024
+        au = W.randn_matrix(nu, 4) / np.sqrt(nu) - 2.0 * np.eye(nu)
+        au *= 4.0 / W.one_norm(au) / nsub
+        vu = W.randn(5, nu * k).reshape(nu, k)
+        rm = R.RefMethod.catalog("R8")
+        w = min(8, cores)
+        t1 = ref_unit(nu, lambda _: R.dense_action(rm, au, vu, 1, M.RESIDUAL, workers=w))
+        t2 = ref_unit(nu, lambda _: R.dense_action(rm, au, vu, 2, M.RESIDUAL, workers=w))
+        t_step = max(t2 - t1, 1e-9)
+        t_fac = max(t1 - t_step, 1e-9)
+        est = t_fac * (n / nu) ** 3 + nsub * t_step * (n / nu) ** 2
+        cpu = {"value": 1.0 / est, "unit": "evals/s", "cores": w, "kind": "reference",
+               "sample": "reduced unit, extrapolated: the dense block action (reference DenseLu per shift factored "
+                         "once, assemble_action order per column) at n = 1024, k = 64 with 1 and 2 substeps "
+                         "(factor %.2f s, substep %.3f s), x (16384/1024)^3 for the LUs and ^2 per substep, "
+                         "%d substeps, workers = %d" % (t_fac, t_step, nsub, w)}
+    lines.append(mk("cfg4", "exp(tA)V, 16384^2 x 64, R8, N = %d substeps, factor once" % nsub, 1, ms, clk, alg, exe,
+                    launches, cpu, {"substeps": nsub,
+                                    "executed_basis": "pair mode: B^2, 4 pair LUs, per substep BX + 4 pair solves "
+                                                      "+ B.V (6 x 2n^2k)"}))
+    del A, V
+    torch.cuda.empty_cache()
+    return lines
+
+
 def run_ours(args):
     import torch
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit("bench.py: WORLD_SIZE=%d but --gpus %d" % (world, args.gpus))
     dist = None
     if world > 1:
         import torch.distributed as tdist
@@ -296,6 +510,7 @@ def run_ours(args):
 
     eng = api.engine()
     peak_probe = float(N.lib.pf_probe_dmma_tflops(local))
+    cores, model = host_cpu()
     # inputs: each rank evaluates its own cfg2-distributed batch (weak scaling; seeds offset by rank)
     a_np = W.cfg2(batch=args.batch, seed0=1000 + rank * args.batch)
     A = torch.from_numpy(a_np).cuda()
@@ -311,9 +526,32 @@ def run_ours(args):
         t = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args.method)
+    # parity of the timed outputs against the reference build, whole batch (rank 0's shard at N > 1);
+    # at N = 1 the same reference run is the cpu_baseline
+    cpu, parity, parity2 = None, None, None
+    if rank == 0 and not args.no_cpu:
+        parity, dt, kind = parity_vs_reference(main["out"].cpu().numpy(), main["js"], a_np, args.method, cores)
+        if world == 1:
+            cpu = {"value": args.batch / dt, "unit": "evals/s", "cores": cores, "kind": kind, "cpu_model": model,
+                   "sample": "the whole %d-matrix batch (%s, residual, scaling+squaring) once, %d host threads "
+                             "(affinity), parallel over the batch (cli.cpp:314); %s" % (
+                                 args.batch, args.method, cores,
+                                 "reference build oracle/_ref: eval_dense + DenseMatrix::mul from "
+                                 "/root/reference compiled unmodified" if kind == "reference"
+                                 else "restatement pinned bit for bit to the reference")}
+        if secondary is not None:
+            parity2, _, _ = parity_vs_reference(secondary["out"].cpu().numpy(), secondary["js"], a_np,
+                                                secondary["name"], cores)
+    del main["out"]
+    if secondary is not None:
+        del secondary["out"]
+    large = None
+    if rank == 0 and world == 1 and not args.no_secondary:
+        del A
+        torch.cuda.empty_cache()
+        large = large_config_lines(peak_probe, local, cores)
+    if dist:
+        dist.barrier()
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -322,8 +560,13 @@ def run_ours(args):
 
     def roof(res):
         achieved = res["flops"] / (res["kernel_ms"] * 1e-3) / 1e12
+        executed = res["exe_flops"] / (res["kernel_ms"] * 1e-3) / 1e12
         return {"bound": "tensor", "achieved": achieved, "peak": peak_probe, "unit": "TFLOP/s",
                 "frac": achieved / peak_probe, "traffic": traffic,
+                "flops_basis": "algorithmic (SURVEY §8(d): per matrix P*8/3 n^3 + 2 j_b n^3); pair mode executes "
+                               "fewer -- see executed_*",
+                "executed_achieved": executed, "executed_frac": executed / peak_probe,
+                "executed_flops_per_launch": res["exe_flops"],
                 "kernel": "small_eval_kernel (fused norm+LU+solve+accumulate+squaring)",
                 "kernel_ms": res["kernel_ms"],
                 "flops_per_launch": res["flops"],
@@ -349,17 +592,22 @@ def run_ours(args):
                    "mean_squarings": float(main["js"].mean()),
                    "l2": "inputs %d MiB per rank > 126 MB L2" % (args.batch * N_MAT * N_MAT * 8 >> 20)},
         "roofline": roof(main),
+        "parity": parity,
         "cpu_baseline": cpu,
         "e2e": {"value": args.batch * world / (e2e_ms * 1e-3), "unit": "evals/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "gpu_launches": main["launches"],
         "clocks": main["clocks"],
         "fp64_peak_tflops_probe": peak_probe,
+        "host": {"cpu_model": model, "threads": cores},
     }
     if secondary is not None:
         line["secondary"] = {"method": secondary["name"], "value": args.batch * world / (secondary["ms"] * 1e-3),
                              "unit": "evals/s", "ms_per_step": secondary["ms"], "roofline": roof(secondary),
-                             "mean_squarings": float(secondary["js"].mean())}
+                             "mean_squarings": float(secondary["js"].mean()), "parity": parity2,
+                             "clocks": secondary["clocks"]}
+    if large is not None:
+        line["large_configs"] = large
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
@@ -367,6 +615,8 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
     if args.impl == "reference":
         run_reference(args)
     else:
