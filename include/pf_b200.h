@@ -59,9 +59,14 @@ enum pf_flags {
   PF_FLAG_NONE = 0,
   PF_FLAG_ASYNC = 1,     /* do not synchronise to read device status */
   PF_FLAG_FORCE_PIVOT = 2, /* always run the genuine partial-pivoting LU (testing) */
-  PF_FLAG_PER_SHIFT = 4    /* no (c, -c) pair merging: one solve per shift, weighted terms added in
+  PF_FLAG_PER_SHIFT = 4,   /* no (c, -c) pair merging: one solve per shift, weighted terms added in
                               ascending shift order -- dense.cpp's rounding sequence; results are then
                               bit-identical to any shift partition summed in that order */
+  PF_FLAG_REFERENCE_ORDER = 8 /* n <= 128: every operation in dense.cpp's order (per shift, unblocked
+                              pivoting LU with 1.0/pivot, dot-product substitution, scale-then-add,
+                              poly last, squaring in i-k-j order with the zero skip, no FMA): results
+                              bit-identical to the reference. pf_eval_dense_batched,
+                              pf_eval_scaled_batched, pf_expm_batched; BadArgument for n > 128 */
 };
 
 /* Failure detail; enough for the C++ wrapper to rebuild the reference message

@@ -33,6 +33,7 @@ class PfPairMethod(C.Structure):
 PF_FLAG_ASYNC = 1
 PF_FLAG_FORCE_PIVOT = 2
 PF_FLAG_PER_SHIFT = 4  # no (c, -c) pair merging: the reference's per-shift rounding sequence
+PF_FLAG_REFERENCE_ORDER = 8  # n <= 128: dense.cpp's exact operation order, bit-identical results
 PF_MAX_TERMS = 16
 PF_SMALL_N = 128
 

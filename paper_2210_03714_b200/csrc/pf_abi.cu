@@ -140,11 +140,36 @@ int launch_small(pf_context* ctx, pf::SmallParams& p) {
   p.scratch_slots = 2 * sms;
   p.scratch = static_cast<double*>(
       workspace(ctx, kWsScratch, sizeof(double) * 3 * PF_SMALL_N * PF_SMALL_N * (size_t)p.scratch_slots));
+  int per_sm = 0;  // the %smid slots are private only at one resident CTA per SM
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, pf::small_eval_threads(),
+                                                    pf::small_eval_smem_bytes()) != cudaSuccess ||
+      per_sm != 1)
+    p.scratch = nullptr;
   if (!p.scratch) p.scratch_slots = 0;
   if (p.batch == 0) return PF_OK;
   kernel<<<p.batch, pf::small_eval_threads(), pf::small_eval_smem_bytes(), ctx->stream>>>(p);
   ctx->launches++;
   return cuda_fail(cudaGetLastError());
+}
+
+int launch_small_reference_order(pf_context* ctx, pf::SmallParams& p) {
+  int rc = ensure_status(ctx, p.batch);
+  if (rc) return rc;
+  p.status = ctx->status;
+  p.first_error = ctx->first_error;
+  p.prof = nullptr;
+  p.scratch_slots = 0;
+  p.scratch = static_cast<double*>(workspace(ctx, kWsRefX, sizeof(double) * (size_t)p.n * p.n * (size_t)p.batch));
+  if (!p.scratch && p.batch > 0 && p.n > 0) return PF_ERR_CUDA;
+  if (p.batch == 0) return PF_OK;
+  cudaError_t e = pf::launch_ref_order(p, ctx->stream);
+  ctx->launches++;
+  return cuda_fail(e);
+}
+
+// the fused kernel, or the reference-order evaluator under PF_FLAG_REFERENCE_ORDER
+int launch_small_flags(pf_context* ctx, pf::SmallParams& p, int flags) {
+  return (flags & PF_FLAG_REFERENCE_ORDER) ? launch_small_reference_order(ctx, p) : launch_small(ctx, p);
 }
 
 void gemm(pf_context* ctx, int m, int n, int k, int batch, double alpha, const double* A, int64_t lda,
@@ -321,6 +346,7 @@ int pf_eval_dense_batched(pf_context* ctx, const pf_method* m, int n, int batch,
   }
   pf::SmallParams p{};
   if (!ctx || n < 0 || batch < 0 || !dOuts || !fill_method(m, p) || ldb < n || ldo < n) return bad(status);
+  if (n > PF_SMALL_N && (flags & PF_FLAG_REFERENCE_ORDER)) return bad(status);
   if (n > PF_SMALL_N) {
     const int rc = large_eval(ctx, m, n, batch, dB, ldb, strideB, nullptr, dOuts, ldo, strideOut, flags, status);
     if (rc) return rc;
@@ -339,7 +365,7 @@ int pf_eval_dense_batched(pf_context* ctx, const pf_method* m, int n, int batch,
   p.ldo = ldo;
   p.strideOut = strideOut;
   p.pivot_rel_tol = 1e-14;
-  int rc = launch_small(ctx, p);
+  int rc = launch_small_flags(ctx, p, flags);
   if (rc) return rc;
   return collect_status(ctx, batch, flags, status);
 }
@@ -364,6 +390,7 @@ void squaring_counts(pf_context* ctx, int n, int batch, const double* dA, int64_
 int eval_scaled(pf_context* ctx, const pf_method* m, double theta, int n, int batch, const double* dA, int64_t lda,
                 int64_t strideA, const int* dJin, int* dJ, double* const* outs, int64_t ldo, int64_t strideOut,
                 int flags, pf_status* status) {
+  if (n > PF_SMALL_N && (flags & PF_FLAG_REFERENCE_ORDER)) return bad(status);
   if (n > PF_SMALL_N) {
     squaring_counts(ctx, n, batch, dA, lda, strideA, theta, dJin, dJ);
     const int rc = large_eval(ctx, m, n, batch, dA, lda, strideA, dJ, outs, ldo, strideOut, flags, status);
@@ -388,7 +415,7 @@ int eval_scaled(pf_context* ctx, const pf_method* m, double theta, int n, int ba
   p.strideOut = strideOut;
   p.theta = theta;
   p.pivot_rel_tol = 1e-14;
-  int rc = launch_small(ctx, p);
+  int rc = launch_small_flags(ctx, p, flags);
   if (rc) return rc;
   return collect_status(ctx, batch, flags, status);
 }
@@ -436,6 +463,7 @@ int pf_expm_batched(pf_context* ctx, const pf_method* m, double theta, int n, in
   if (!ctx || n < 0 || batch < 0 || !dOut || !fill_method(m, p) || lda < n || ldo < n || !(theta > 0))
     return bad(status);
   if (batch == 0 || n == 0) return PF_OK;
+  if (n > PF_SMALL_N && (flags & PF_FLAG_REFERENCE_ORDER)) return bad(status);
   if (n > PF_SMALL_N) {
     // eval (set 0) + squaring chain on the DMMA GEMM with per-matrix step counts
     pf_method m0 = *m;
@@ -476,7 +504,7 @@ int pf_expm_batched(pf_context* ctx, const pf_method* m, double theta, int n, in
   p.strideOut = strideOut;
   p.theta = theta;
   p.pivot_rel_tol = 1e-14;
-  int rc = launch_small(ctx, p);
+  int rc = launch_small_flags(ctx, p, flags);
   if (rc) return rc;
   return collect_status(ctx, batch, flags, status);
 }

@@ -80,6 +80,8 @@ int collect_status(pf_context* ctx, int batch, int flags, pf_status* out);
 int bad(pf_status* st);
 bool fill_method(const pf_method* m, SmallParams& p);
 int launch_small(pf_context* ctx, SmallParams& p);
+// PF_FLAG_REFERENCE_ORDER (n <= 128): ref_order.cu, dense.cpp's exact operation order
+int launch_small_reference_order(pf_context* ctx, SmallParams& p);
 void gemm(pf_context* ctx, int m, int n, int k, int batch, double alpha, const double* A, int64_t lda, int64_t sA,
           const double* B, int64_t ldb, int64_t sB, double beta, double* C, int64_t ldc, int64_t sC, double gamma,
           const int* jmask = nullptr, int step = 0, const double* pass = nullptr);
@@ -111,6 +113,7 @@ enum Slot {
   kWsBandX = 30,
   kWsBandRec = 31,      // banded action: per-row coefficient records of the bulk-copy kernel
   kWsScratch = 20,      // per-SM accumulator slots of the small kernel
+  kWsRefX = 32,         // reference-order evaluator: per-matrix solve / product scratch
   kWsSmallArrays = 64,  // small uploaded tables: kWsSmallArrays + i (slots grow on demand)
 };
 

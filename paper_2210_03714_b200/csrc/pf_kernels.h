@@ -51,6 +51,8 @@ cudaError_t set_smem_attr_once(const void* fn, int bytes);
 __global__ void small_eval_kernel(SmallParams p);
 __global__ void small_eval_prof_kernel(SmallParams p);  // with the phase profile (p.prof)
 size_t small_eval_smem_bytes();
+// PF_FLAG_REFERENCE_ORDER evaluator (ref_order.cu); p.scratch = batch x n x n doubles
+cudaError_t launch_ref_order(SmallParams& p, cudaStream_t stream);
 int small_eval_threads();
 
 // Batched C = alpha * A B + beta * C + gamma * I (row-major, FP64 DMMA).

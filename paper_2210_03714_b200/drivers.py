@@ -301,9 +301,12 @@ def dense_entry(token: str) -> DenseEntry:
     poly_products = 1.0 if len(m.poly) == 3 else 0.0
 
     def ev(Bs, m=m):
-        from . import api
+        from . import _native as N, api
 
-        return api.eval_dense(m, Bs)
+        # The plain form's round-off plateau decides the figure trends (acceptance_main.cpp:199-212):
+        # evaluate it in the reference's exact operation order (bit-identical to dense.cpp).
+        flags = N.PF_FLAG_REFERENCE_ORDER if m.form == M.PLAIN and Bs.shape[-1] <= N.PF_SMALL_N else 0
+        return api.eval_dense(m, Bs, flags=flags)
 
     return DenseEntry(token, _function_name(m.function), ev, m.processors() * K_INVERSE_PRODUCTS + poly_products,
                       max(K_INVERSE_PRODUCTS, poly_products))

@@ -53,37 +53,26 @@ def test_bench_action_csv(D):
 
 
 def test_acceptance_figure_trends(D, oracle):
-    """acceptance_main.cpp:176-252 at its own sizes (d = 100 dense, d = 1000 action). Three trends
-    hold as the reference asserts them. "R8 <= taylor8 on >= 90% of the window" is decided by
-    round-off: at the window's low end the plain-form R8 sits on its ~4e-12 plateau, next to
-    taylor8's truncation error (5e-13 at h = 0.3, 3.5e-12 at h = 0.37). The CPU restatement of the
-    reference's eval_dense wins 11/12; the GPU's R8 (equal to it within the 1e-11 parity bound, not
-    bitwise) lands 4.2e-12 at h = 0.37 and wins 10/12. The test pins exactly that: any point where
-    the two disagree has both R8 errors on the round-off plateau and within 2x of each other."""
-    from paper_2210_03714_b200 import api, methods as M
+    """acceptance_main.cpp:176-252 at its own sizes (d = 100 dense, d = 1000 action): all four
+    trends hold exactly as the reference asserts them, incl. "R8 <= taylor8 on >= 90% of the
+    window" (:205-212), which round-off decides at the window's low end. The drivers evaluate the
+    plain-form methods with PF_FLAG_REFERENCE_ORDER, so the GPU's R8 values are the reference's
+    bits (checked here against the restatement, itself bit-identical to oracle/_ref)."""
+    from paper_2210_03714_b200 import _native as N, api, methods as M
 
     res = D.figure_trends()
-    assert res[0][0], res[0][1]
-    for ok, msg in res[2:]:
+    for ok, msg in res:
         assert ok, msg
     a = D.make_dense_matrix(D.MatrixSpec("randn", 100, 1))
     scale = D.two_norm_est(a)
     window = D.log_grid(0.3, 3.0, 12)
     Bs = np.stack([a * (h / scale) for h in window])
-    dB = torch.from_numpy(Bs).cuda()
-    t8 = D.taylor8(dB).cpu().numpy()
-    m = M.catalog("R8")
-    g8 = api.eval_dense(m, dB).cpu().numpy()
-    om = oracle.OMethod.from_method(m, m.form)
-    gpu_wins = cpu_wins = 0
+    g8 = api.eval_dense(M.catalog("R8"), torch.from_numpy(Bs).cuda(), flags=N.PF_FLAG_REFERENCE_ORDER).cpu().numpy()
+    om = oracle.OMethod.from_method(M.catalog("R8"), M.PLAIN)
     for gi in range(len(window)):
-        e_gpu, e_cpu, e_t8 = D.dense_errors("exp", Bs[gi], [g8[gi], oracle.eval_dense(om, Bs[gi]), t8[gi]])
-        gpu_wins += e_gpu <= e_t8
-        cpu_wins += e_cpu <= e_t8
-        if (e_gpu <= e_t8) != (e_cpu <= e_t8):
-            assert max(e_gpu, e_cpu) < 1e-11 and max(e_gpu, e_cpu) < 2 * min(e_gpu, e_cpu), (window[gi], e_gpu, e_cpu)
-    assert res[1][1] == "R8 <= taylor8 on %d/12 grid points" % gpu_wins
-    assert cpu_wins * 10 >= 12 * 9 and abs(gpu_wins - cpu_wins) <= 1, (gpu_wins, cpu_wins)
+        assert np.array_equal(g8[gi], oracle.eval_dense(om, Bs[gi])), window[gi]
+    wins = int(res[1][1].split(" on ")[1].split("/")[0])
+    assert wins * 10 >= 12 * 9
 
 
 def test_acceptance_bound_compliance(D):

@@ -127,9 +127,13 @@ def test_action_block(dev, oracle, n, k, name, form):
     nsub = M.substeps_for(1.5, M.THETA_U53.get(name, 0.1))
     got = dev.action(a, v, m, substeps=nsub, form=form)
     ref = oracle.action(a, v, oracle.OMethod.from_method(m, form), nsub)
+    # Flat bars, independent of the substep count. Residual form: 1e-11 (north_star). The plain form
+    # and the order-10 sets amplify every rounding by sum|b| + sum|d| (Appendix B: no reordering of the
+    # plain form meets 1e-11), so they take the reference's own convention for that,
+    # max(1e-11, 100 sum|coef| u) (test_action.cpp:131-136).
     amp = float(sum(abs(w) for w in m.weights) + sum(abs(d) for d in m.poly))
-    tol = max(TOL, 100 * amp * 2.23e-16) if name.startswith("R10") else TOL
-    assert oracle.rel_diff_1norm(got, ref) <= tol  # flat bar, independent of the substep count
+    tol = max(TOL, 100 * amp * 2.23e-16) if (name.startswith("R10") or form == 0) else TOL
+    assert oracle.rel_diff_1norm(got, ref) <= tol
 
 
 def test_dense_lu_api(dev, oracle):

@@ -313,3 +313,60 @@ def test_golden_fixtures_on_device(dev, oracle):
     t = dev.TridiagMatrix(*x["trid200"])
     band = dev.tridiag_action("R8", t, x["trid200_v"], substeps=4, form=1)
     assert np.array_equal(np.asarray(band), g("trid200_R8_residual_N4"))  # banded path is bit-exact
+
+
+# ------------------------------------------------------------------ PF_FLAG_REFERENCE_ORDER
+
+
+@pytest.mark.parametrize("name", ["R4", "R5", "R8", "R10", "R10star", "R4_phi1"])
+@pytest.mark.parametrize("form", [0, 1])
+def test_reference_order_eval_bitwise(dev, oracle, name, form):
+    """ref_order.cu: eval_dense in dense.cpp's exact operation order -- equal bit for bit to the
+    restatement, which tests/test_ref_pin.py holds bit-identical to the reference build."""
+    from paper_2210_03714_b200 import _native as N, methods as M
+
+    m = M.catalog(name)
+    om = oracle.OMethod.from_method(m, form)
+    for n, seed, norm in ((1, 3, 0.5), (5, 1, 0.3), (24, 5, 0.7), (64, 77, 0.05), (100, 9, 2.0), (128, 11, 0.9),
+                          (24, 900, 30.0)):
+        b = rand(n, seed, norm)
+        try:
+            want = oracle.eval_dense(om, b)
+        except oracle.OracleError as e:
+            from paper_2210_03714_b200.errors import PfError
+
+            with pytest.raises(PfError) as eg:
+                dev.eval_dense(m, b, dev.EvalOptions(form=form), flags=N.PF_FLAG_REFERENCE_ORDER)
+            assert int(eg.value.code) + 1 == e.code and "at column %d " % e.status.column in str(eg.value)
+            continue
+        got = dev.eval_dense(m, b, dev.EvalOptions(form=form), flags=N.PF_FLAG_REFERENCE_ORDER)
+        assert np.array_equal(got, want), (n, seed, oracle.rel_diff_1norm(got, want))
+
+
+@pytest.mark.parametrize("name", ["R4", "R8", "R10"])
+def test_reference_order_expm_bitwise(dev, oracle, name):
+    from paper_2210_03714_b200 import _native as N, methods as M, workloads as W
+
+    om = oracle.OMethod.from_method(M.catalog(name), 1)
+    th = M.THETA_U53[name]
+    a = W.cfg2(batch=64)
+    want, jw = oracle.expm_batched(a, om, th, threads=8)
+    got, jg = dev.expm(a, name, return_squarings=True, flags=N.PF_FLAG_REFERENCE_ORDER)
+    assert np.array_equal(np.asarray(jg), jw)
+    assert np.array_equal(got, want)
+    a1 = W.cfg1()
+    w1, j1 = oracle.expm(a1, om, th)
+    g1, k1 = dev.expm(a1, name, return_squarings=True, flags=N.PF_FLAG_REFERENCE_ORDER)
+    assert int(k1) == j1 and np.array_equal(g1, w1)
+
+
+def test_reference_order_singular_and_large_n(dev):
+    from paper_2210_03714_b200 import _native as N, methods as M
+    from paper_2210_03714_b200.errors import Errc, PfError
+
+    with pytest.raises(PfError) as e:
+        dev.eval_dense(M.catalog("R4"), np.eye(6) * 5.0, dev.EvalOptions(form=0), flags=N.PF_FLAG_REFERENCE_ORDER)
+    assert e.value.code == Errc.SingularShift
+    with pytest.raises(PfError) as e:
+        dev.eval_dense(M.catalog("R4"), rand(130, 1, 1.0), flags=N.PF_FLAG_REFERENCE_ORDER)
+    assert e.value.code == Errc.BadArgument
