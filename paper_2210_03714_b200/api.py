@@ -130,15 +130,19 @@ class Engine:
         return int(N.lib.pf_context_launch_count(self.h))
 
 
-_engine: Optional[Engine] = None
+_engines: dict = {}
 
 
-def engine() -> Engine:
-    global _engine
-    if _engine is None:
-        _engine = Engine(torch.cuda.current_device() if torch.cuda.is_available() else 0)
-    _engine.bind_stream()
-    return _engine
+def engine(device: Optional[int] = None) -> Engine:
+    """The context of `device` (default: torch's current CUDA device), one per device per process,
+    bound to torch's current stream on that device."""
+    if device is None:
+        device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+    eng = _engines.get(device)
+    if eng is None:
+        eng = _engines[device] = Engine(device)
+    eng.bind_stream()
+    return eng
 
 
 # ------------------------------------------------------------------------------------------ helpers
@@ -174,6 +178,9 @@ def _to_device(x: ArrayLike) -> Tuple[torch.Tensor, bool]:
     if x.dtype != torch.float64:
         raise PfError(Errc.BadArgument, "FP64 only")
     if x.is_cuda:
+        if torch.cuda.is_available() and x.device.index != torch.cuda.current_device():
+            raise PfError(Errc.BadArgument, "tensor on cuda:%d but the current device (engine) is cuda:%d; use "
+                                            "torch.cuda.device(...)" % (x.device.index, torch.cuda.current_device()))
         return x.contiguous(), False
     return x.contiguous().cuda(), True
 

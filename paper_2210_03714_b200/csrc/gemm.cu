@@ -216,7 +216,29 @@ void launch_v(const GemmParams& p, bool v16, cudaStream_t stream) {
 }
 }  // namespace
 
+void launch_gemm_chunk(const GemmParams& p, cudaStream_t stream);
+
+// grid.y carries the batch (at most 65535 per launch): larger batches run as several launches on
+// consecutive slices of the matrices and of the per-matrix step masks.
 void launch_gemm(const GemmParams& p, cudaStream_t stream) {
+  constexpr int kMaxGridY = 65535;
+  if (p.max_sms > 0 || p.batch <= kMaxGridY) {
+    launch_gemm_chunk(p, stream);
+    return;
+  }
+  for (int b0 = 0; b0 < p.batch; b0 += kMaxGridY) {
+    GemmParams q = p;
+    q.batch = std::min(kMaxGridY, p.batch - b0);
+    q.A = p.A + (int64_t)b0 * p.strideA;
+    q.B = p.B + (int64_t)b0 * p.strideB;
+    q.C = p.C + (int64_t)b0 * p.strideC;
+    if (p.jmask) q.jmask = p.jmask + b0;
+    if (p.pass) q.pass = p.pass + (int64_t)b0 * p.strideC;
+    launch_gemm_chunk(q, stream);
+  }
+}
+
+void launch_gemm_chunk(const GemmParams& p, cudaStream_t stream) {
   // 16-byte copies need even leading dimensions / batch strides and 16-byte aligned bases
   const bool v16 = ((p.lda | p.ldb | p.strideA | p.strideB) & 1) == 0 &&
                    ((reinterpret_cast<uintptr_t>(p.A) | reinterpret_cast<uintptr_t>(p.B)) & 15) == 0;

@@ -241,7 +241,11 @@ const char* pf_error_string(int code) {
 int pf_context_create(int device, pf_context** out) {
   if (!out) return PF_ERR_BAD_ARGUMENT;
   *out = nullptr;
-  if (cudaSetDevice(device) != cudaSuccess) return PF_ERR_CUDA;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return PF_ERR_CUDA;
+  pf_context probe;
+  probe.device = device;
+  DeviceGuard device_guard(&probe);  // allocate on `device`, leave the caller's current device alone
   auto* ctx = new pf_context();
   ctx->device = device;
   if (cudaMalloc(&ctx->first_error, sizeof(int)) != cudaSuccess ||
@@ -255,6 +259,7 @@ int pf_context_create(int device, pf_context** out) {
 
 int pf_context_destroy(pf_context* ctx) {
   if (!ctx) return PF_OK;
+  DeviceGuard device_guard(ctx);
   cudaStreamSynchronize(ctx->stream);
   for (void* p : ctx->ws) cudaFree(p);
   cudaFree(ctx->status);
@@ -285,6 +290,7 @@ int pf_context_destroy(pf_context* ctx) {
 }
 
 int pf_context_set_stream(pf_context* ctx, void* stream) {
+  DeviceGuard device_guard(ctx);
   if (!ctx) return PF_ERR_BAD_ARGUMENT;
   ctx->stream = static_cast<cudaStream_t>(stream);
   return PF_OK;
@@ -293,12 +299,14 @@ int pf_context_set_stream(pf_context* ctx, void* stream) {
 int64_t pf_context_launch_count(pf_context* ctx) { return ctx ? ctx->launches : 0; }
 
 int pf_context_set_sticky_status(pf_context* ctx, int sticky) {
+  DeviceGuard device_guard(ctx);
   if (!ctx) return PF_ERR_BAD_ARGUMENT;
   ctx->sticky = sticky != 0;
   return cuda_fail(cudaMemsetAsync(ctx->first_error, 0x7f, sizeof(int), ctx->stream));
 }
 
 int pf_context_pending_error(pf_context* ctx) {
+  DeviceGuard device_guard(ctx);
   if (!ctx) return PF_ERR_BAD_ARGUMENT;
   if (cudaMemcpyAsync(ctx->h_first_error, ctx->first_error, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream) !=
           cudaSuccess ||
@@ -308,6 +316,7 @@ int pf_context_pending_error(pf_context* ctx) {
 }
 
 int pf_context_set_profile(pf_context* ctx, unsigned long long* dev_counters) {
+  DeviceGuard device_guard(ctx);
   if (!ctx) return PF_ERR_BAD_ARGUMENT;
   ctx->prof = dev_counters;
   return PF_OK;
@@ -315,6 +324,7 @@ int pf_context_set_profile(pf_context* ctx, unsigned long long* dev_counters) {
 
 int pf_one_norm_batched(pf_context* ctx, int n, int batch, const double* dA, int64_t lda, int64_t strideA,
                         double* dNorm) {
+  DeviceGuard device_guard(ctx);
   if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
     return PF_OK;
   }
@@ -328,6 +338,7 @@ int pf_one_norm_batched(pf_context* ctx, int n, int batch, const double* dA, int
 int pf_gemm_batched(pf_context* ctx, int m, int n, int k, int batch, double alpha, const double* dA, int64_t lda,
                     int64_t strideA, const double* dB, int64_t ldb, int64_t strideB, double beta, double* dC,
                     int64_t ldc, int64_t strideC, double gamma) {
+  DeviceGuard device_guard(ctx);
   if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
     return PF_OK;
   }
@@ -340,6 +351,7 @@ int pf_gemm_batched(pf_context* ctx, int m, int n, int k, int batch, double alph
 int pf_eval_dense_batched(pf_context* ctx, const pf_method* m, int n, int batch, const double* dB, int64_t ldb,
                           int64_t strideB, double* const* dOuts, int64_t ldo, int64_t strideOut, int flags,
                           pf_status* status) {
+  DeviceGuard device_guard(ctx);
   if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
     if (status) std::memset(status, 0, sizeof(*status));
     return PF_OK;
@@ -437,6 +449,7 @@ void copy_out(pf_context* ctx, int n, int batch, const double* src, double* dst,
 int pf_eval_scaled_batched(pf_context* ctx, const pf_method* m, double theta, int n, int batch, const double* dA,
                            int64_t lda, int64_t strideA, const int* dSquaringsIn, int* dSquaringsOut,
                            double* const* dOuts, int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
+  DeviceGuard device_guard(ctx);
   if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
     if (status) std::memset(status, 0, sizeof(*status));
     return PF_OK;
@@ -455,6 +468,7 @@ int pf_eval_scaled_batched(pf_context* ctx, const pf_method* m, double theta, in
 int pf_expm_batched(pf_context* ctx, const pf_method* m, double theta, int n, int batch, const double* dA,
                     int64_t lda, int64_t strideA, const int* dSquaringsIn, int* dSquaringsOut, double* dOut,
                     int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
+  DeviceGuard device_guard(ctx);
   if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
     if (status) std::memset(status, 0, sizeof(*status));
     return PF_OK;
@@ -511,6 +525,7 @@ int pf_expm_batched(pf_context* ctx, const pf_method* m, double theta, int n, in
 
 int pf_solve_shifted_batched(pf_context* ctx, int n, int batch, const double* dB, int64_t ldb, int64_t strideB,
                              double c, double* dOut, int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
+  DeviceGuard device_guard(ctx);
   if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
     if (status) std::memset(status, 0, sizeof(*status));
     return PF_OK;
@@ -527,6 +542,7 @@ int pf_solve_shifted_batched(pf_context* ctx, int n, int batch, const double* dB
 int pf_expm_phi1_batched(pf_context* ctx, const pf_method* m, double theta, int n, int batch, const double* dA,
                          int64_t lda, int64_t strideA, const int* dSquaringsIn, int* dSquaringsOut, double* dE,
                          double* dPhi, int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
+  DeviceGuard device_guard(ctx);
   if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
     if (status) std::memset(status, 0, sizeof(*status));
     return PF_OK;
@@ -567,6 +583,7 @@ int pf_expm_phi1_batched(pf_context* ctx, const pf_method* m, double theta, int 
 int pf_cossin_batched(pf_context* ctx, const pf_pair_method* pm, double theta, int n, int batch, const double* dA,
                       int64_t lda, int64_t strideA, const int* dSquaringsIn, int* dSquaringsOut, double* dC,
                       double* dS, int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
+  DeviceGuard device_guard(ctx);
   if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
     if (status) std::memset(status, 0, sizeof(*status));
     return PF_OK;
@@ -627,6 +644,7 @@ int pf_cossin_batched(pf_context* ctx, const pf_pair_method* pm, double theta, i
 int pf_action_block(pf_context* ctx, const pf_method* m, int n, int k, const double* dA, int64_t lda,
                     const double* dV, int64_t ldv, int substeps, double* dOut, int64_t ldo, int flags,
                     pf_status* status) {
+  DeviceGuard device_guard(ctx);
   pf::SmallParams p{};
   if (!ctx || !fill_method(m, p) || n < 0 || k < 0 || substeps < 1 || lda < n || ldv < k || ldo < k || !dA || !dV ||
       !dOut)
@@ -639,6 +657,7 @@ int pf_action_block(pf_context* ctx, const pf_method* m, int n, int k, const dou
 
 int pf_lu_factor_batched(pf_context* ctx, int n, int batch, double* dA, int64_t lda, int64_t strideA, int* dPiv,
                          double pivot_rel_tol, int flags, pf_status* status) {
+  DeviceGuard device_guard(ctx);
   if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
     if (status) std::memset(status, 0, sizeof(*status));
     return PF_OK;
@@ -651,6 +670,7 @@ int pf_lu_factor_batched(pf_context* ctx, int n, int batch, double* dA, int64_t 
 
 int pf_lu_solve_batched(pf_context* ctx, int n, int k, int batch, const double* dLU, int64_t lda, int64_t strideLU,
                         const int* dPiv, double* dRhs, int64_t ldr, int64_t strideR) {
+  DeviceGuard device_guard(ctx);
   if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
     return PF_OK;
   }
@@ -661,6 +681,7 @@ int pf_lu_solve_batched(pf_context* ctx, int n, int k, int batch, const double* 
 }
 
 int pf_device_alloc(pf_context* ctx, size_t bytes, void** out) {
+  DeviceGuard device_guard(ctx);
   if (!ctx || !out) return PF_ERR_BAD_ARGUMENT;
   *out = nullptr;
   if (bytes == 0) return PF_OK;
@@ -668,6 +689,7 @@ int pf_device_alloc(pf_context* ctx, size_t bytes, void** out) {
 }
 
 int pf_device_free(pf_context* ctx, void* p) {
+  DeviceGuard device_guard(ctx);
   if (!ctx) return PF_ERR_BAD_ARGUMENT;
   if (!p) return PF_OK;
   cudaStreamSynchronize(ctx->stream);
@@ -675,6 +697,7 @@ int pf_device_free(pf_context* ctx, void* p) {
 }
 
 int pf_copy_to_device(pf_context* ctx, void* dst, const void* src, size_t bytes) {
+  DeviceGuard device_guard(ctx);
   if (!ctx) return PF_ERR_BAD_ARGUMENT;
   if (bytes == 0) return PF_OK;
   if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess) return PF_ERR_CUDA;
@@ -682,6 +705,7 @@ int pf_copy_to_device(pf_context* ctx, void* dst, const void* src, size_t bytes)
 }
 
 int pf_copy_to_host(pf_context* ctx, void* dst, const void* src, size_t bytes) {
+  DeviceGuard device_guard(ctx);
   if (!ctx) return PF_ERR_BAD_ARGUMENT;
   if (bytes == 0) return PF_OK;
   if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess) return PF_ERR_CUDA;

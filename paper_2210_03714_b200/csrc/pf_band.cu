@@ -77,6 +77,7 @@ extern "C" {
 
 int pf_tridiag_matvec_batched(pf_context* ctx, int d, int k, const double* dSub, const double* dDiag,
                               const double* dSuper, const double* dV, int64_t ldv, double* dOut, int64_t ldo) {
+  DeviceGuard device_guard(ctx);
   if (!ctx || d < 0 || k < 0 || ldv < k || ldo < k) return PF_ERR_BAD_ARGUMENT;
   if (d == 0 || k == 0) return PF_OK;
   pf::band_matvec_kernel<<<blocks_for((int64_t)d * k), 256, 0, ctx->stream>>>(d, k, dSub, dDiag, dSuper, dV, ldv,
@@ -88,6 +89,7 @@ int pf_tridiag_matvec_batched(pf_context* ctx, int d, int k, const double* dSub,
 int pf_thomas_solve_batched(pf_context* ctx, int d, int k, const double* dSub, const double* dDiag,
                             const double* dSuper, const double* dRhs, int64_t ldr, double* dX, int64_t ldx,
                             pf_status* status) {
+  DeviceGuard device_guard(ctx);
   if (status) std::memset(status, 0, sizeof(*status));
   if (!ctx || d < 1 || k < 0 || ldr < k || ldx < k) return bad(status);
   const int64_t dm1 = std::max(d - 1, 1);
@@ -108,6 +110,7 @@ int pf_thomas_solve_batched(pf_context* ctx, int d, int k, const double* dSub, c
 int pf_pentadiag_solve_batched(pf_context* ctx, int d, int k, const double* dSub2, const double* dSub1,
                                const double* dDiag, const double* dSuper1, const double* dSuper2,
                                const double* dRhs, int64_t ldr, double* dX, int64_t ldx, pf_status* status) {
+  DeviceGuard device_guard(ctx);
   if (status) std::memset(status, 0, sizeof(*status));
   if (!ctx || d < 1 || k < 0 || ldr < k || ldx < k) return bad(status);
   double* W = static_cast<double*>(workspace(ctx, kWsBandF, sizeof(double) * (size_t)d * 7));
@@ -129,6 +132,7 @@ int pf_pentadiag_solve_batched(pf_context* ctx, int d, int k, const double* dSub
 int pf_tridiag_action(pf_context* ctx, const pf_method* m, int d, int k, const double* dSub, const double* dDiag,
                       const double* dSuper, const double* dV, int64_t ldv, int substeps, double* dOut, int64_t ldo,
                       int flags, pf_status* status) {
+  DeviceGuard device_guard(ctx);
   if (status) std::memset(status, 0, sizeof(*status));
   pf::SmallParams p{};
   if (!ctx || !fill_method(m, p) || d < 1 || k < 0 || substeps < 1 || ldv < k || ldo < k) return bad(status);

@@ -49,6 +49,7 @@ extern "C" {
 
 int pf_action_create(pf_context* ctx, const pf_method* m, int n, const double* dA, int64_t lda, int substeps,
                      const int* owned, int flags, pf_status* status, pf_action_op** out) {
+  DeviceGuard device_guard(ctx);
   pf::SmallParams p{};
   if (!ctx || !out || !fill_method(m, p) || n < 1 || lda < n || substeps < 1 || !dA) return bad(status);
   *out = nullptr;
@@ -60,6 +61,7 @@ int pf_action_create(pf_context* ctx, const pf_method* m, int n, const double* d
 int pf_action_apply(pf_action_op* op, const double* dV, int64_t ldv, int k, double* dOut, int64_t ldo,
                     int include_poly, double* dTerms, pf_status* status) {
   if (!op || !dV || k < 1 || ldv < k || ldo < k || !dOut) return bad(status);
+  DeviceGuard device_guard(op->ctx);
   const int rc = action_op_apply(op, dV, ldv, k, dOut, ldo, include_poly, dTerms);
   if (rc) return rc;
   return collect_status(op->ctx, 0, 0, status);
@@ -69,12 +71,14 @@ int pf_action_term_count(pf_action_op* op) { return op ? (int)op->term_index.siz
 
 int pf_action_destroy(pf_action_op* op) {
   if (!op) return PF_OK;
+  DeviceGuard device_guard(op->ctx);
   action_op_destroy(op);
   return PF_OK;
 }
 
 int pf_squarings_batched(pf_context* ctx, int n, int batch, const double* dA, int64_t lda, int64_t strideA,
                          double theta, int* dJ) {
+  DeviceGuard device_guard(ctx);
   if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
     return PF_OK;
   }
@@ -89,6 +93,7 @@ int pf_squarings_batched(pf_context* ctx, int n, int batch, const double* dA, in
 }
 
 int pf_ordered_sum(pf_context* ctx, int count, const double* const* dTerms, int64_t n_elems, double* dOut) {
+  DeviceGuard device_guard(ctx);
   if (!ctx || count < 1 || !dTerms || n_elems < 0 || !dOut) return PF_ERR_BAD_ARGUMENT;
   if (n_elems == 0) return PF_OK;
   auto** dptrs = static_cast<const double**>(workspace(ctx, kWsSmallArrays + 30, sizeof(double*) * count));
@@ -101,6 +106,7 @@ int pf_ordered_sum(pf_context* ctx, int count, const double* const* dTerms, int6
 }
 
 int pf_square_chain(pf_context* ctx, int n, int batch, const int* dJ, double* dE) {
+  DeviceGuard device_guard(ctx);
   if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
     return PF_OK;
   }
@@ -114,6 +120,7 @@ int pf_square_chain(pf_context* ctx, int n, int batch, const int* dJ, double* dE
 }
 
 int pf_phi1_doubling(pf_context* ctx, int n, int batch, const int* dJ, double* dE, double* dPhi) {
+  DeviceGuard device_guard(ctx);
   if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
     return PF_OK;
   }
@@ -146,6 +153,7 @@ int pf_phi1_doubling(pf_context* ctx, int n, int batch, const int* dJ, double* d
 }
 
 int pf_cossin_doubling(pf_context* ctx, int n, int batch, const int* dJ, double* dC, double* dS) {
+  DeviceGuard device_guard(ctx);
   if (ctx && batch == 0) {  // nothing to evaluate (null buffers of empty tensors are fine)
     return PF_OK;
   }

@@ -67,6 +67,28 @@ struct pf_action_op {
 namespace pf {
 namespace host {
 
+// Every ABI entry point runs on its context's device and restores the caller's current device
+// afterwards: one process may drive several GPUs through several contexts, and the caller's
+// current device may be any of them.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(const pf_context* ctx) {
+    if (!ctx || cudaGetDevice(&prev) != cudaSuccess) {
+      prev = -1;
+      return;
+    }
+    if (prev == ctx->device)
+      prev = -1;
+    else
+      cudaSetDevice(ctx->device);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 int action_op_create(pf_context* ctx, const pf_method* m, int n, const double* A, int64_t lda, int substeps,
                      const int* owned, int flags, pf_status* status, pf_action_op** out);
 int action_op_apply(pf_action_op* op, const double* V, int64_t ldv, int k, double* out, int64_t ldo,

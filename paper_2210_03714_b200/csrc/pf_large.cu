@@ -308,6 +308,11 @@ void run_lu_graph(pf_context* ctx, const Sys& s) {  // on ctx->stream == ctx->gs
       return;
     }
     cudaGetLastError();
+    cudaGraphExecDestroy(hit->exec);  // stale: drop it and run directly from now on
+    hit->exec = nullptr;
+    hit->M = nullptr;
+    lu_rec(ctx, s, 0, s.np);
+    return;
   }
   if (!hit) {  // first sighting: run directly, capture next time
     if (ctx->lu_graphs.size() >= 8) {
@@ -344,7 +349,11 @@ void run_lu_graph(pf_context* ctx, const Sys& s) {  // on ctx->stream == ctx->gs
   cudaGraphDestroy(graph);
   hit->exec = exec;
   hit->launches = ctx->launches - l0;
-  cudaGraphLaunch(exec, ctx->stream);
+  if (cudaGraphLaunch(exec, ctx->stream) != cudaSuccess) {
+    cudaGetLastError();
+    ctx->launches = l0;
+    lu_rec(ctx, s, 0, s.np);
+  }
 }
 
 void run_lu(pf_context* ctx, const Sys& s) {
@@ -410,6 +419,10 @@ FactorResult factor_systems(pf_context* ctx, const Sys& s, int n, unsigned long 
   certificate_kernel<<<dim3((n + 255) / 256, s.nsys), 256, 0, ctx->stream>>>(s.M, s.np, n, nchunks, d_part, d_mx,
                                                                              pivot_rel_tol, d_ok);
   ctx->launches += 3;
+  if (cudaGetLastError() != cudaSuccess) {  // a certificate that never ran must not read as "certified"
+    fr.rc = PF_ERR_CUDA;
+    return fr;
+  }
   std::vector<int> ok(s.nsys);
   std::vector<unsigned long long> mxbits(s.nsys);
   cudaMemcpyAsync(ok.data(), d_ok, sizeof(int) * s.nsys, cudaMemcpyDeviceToHost, ctx->stream);
@@ -750,8 +763,9 @@ int large_eval_pairs(pf_context* ctx, const pf_method* m, int n, int batch, cons
   return cuda_fail(cudaGetLastError());
 }
 
-int large_eval(pf_context* ctx, const pf_method* m, int n, int batch, const double* A, int64_t lda, int64_t strideA,
-               const int* dJ, double* const* outs, int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
+static int large_eval_chunk(pf_context* ctx, const pf_method* m, int n, int batch, const double* A, int64_t lda,
+                            int64_t strideA, const int* dJ, double* const* outs, int64_t ldo, int64_t strideOut,
+                            int flags, pf_status* status) {
   if (status) std::memset(status, 0, sizeof(*status));
   if (batch == 0 || n == 0) return PF_OK;
   {
@@ -1041,8 +1055,8 @@ int large_action(pf_context* ctx, const pf_method* m, int n, int k, const double
 }
 
 // ---------------------------------------------------------------------------------------------
-int large_lu_factor(pf_context* ctx, int n, int batch, double* A, int64_t lda, int64_t strideA, int* piv,
-                    double pivot_rel_tol, int flags, pf_status* status) {
+static int large_lu_factor_chunk(pf_context* ctx, int n, int batch, double* A, int64_t lda, int64_t strideA,
+                                 int* piv, double pivot_rel_tol, int flags, pf_status* status) {
   if (status) std::memset(status, 0, sizeof(*status));
   if (batch == 0 || n == 0) return PF_OK;
   Sys s;
@@ -1279,6 +1293,50 @@ void action_op_destroy(pf_action_op* op) {
   cudaFree(op->d_ones);
   cudaFree(op->binv);
   delete op;
+}
+
+}  // namespace host
+}  // namespace pf
+
+namespace pf {
+namespace host {
+
+// The large-path kernels put the system index (shift x matrix) in gridDim.y / gridDim.z, at most
+// 65535: batches are processed in slices of at most 65535 / PF_MAX_TERMS matrices (status batch
+// indices are rebased to the caller's batch).
+constexpr int kLargeBatchChunk = 65535 / PF_MAX_TERMS;
+
+int large_eval(pf_context* ctx, const pf_method* m, int n, int batch, const double* A, int64_t lda, int64_t strideA,
+               const int* dJ, double* const* outs, int64_t ldo, int64_t strideOut, int flags, pf_status* status) {
+  if (batch <= kLargeBatchChunk)
+    return large_eval_chunk(ctx, m, n, batch, A, lda, strideA, dJ, outs, ldo, strideOut, flags, status);
+  for (int b0 = 0; b0 < batch; b0 += kLargeBatchChunk) {
+    const int nb = std::min(kLargeBatchChunk, batch - b0);
+    double* o[2] = {outs[0] + (int64_t)b0 * strideOut, m->n_sets > 1 ? outs[1] + (int64_t)b0 * strideOut : nullptr};
+    const int rc = large_eval_chunk(ctx, m, n, nb, A + (int64_t)b0 * strideA, lda, strideA, dJ ? dJ + b0 : nullptr, o,
+                                    ldo, strideOut, flags, status);
+    if (rc) {
+      if (status) status->batch_index += b0;
+      return rc;
+    }
+  }
+  return PF_OK;
+}
+
+int large_lu_factor(pf_context* ctx, int n, int batch, double* A, int64_t lda, int64_t strideA, int* piv,
+                    double pivot_rel_tol, int flags, pf_status* status) {
+  if (batch <= kLargeBatchChunk)
+    return large_lu_factor_chunk(ctx, n, batch, A, lda, strideA, piv, pivot_rel_tol, flags, status);
+  for (int b0 = 0; b0 < batch; b0 += kLargeBatchChunk) {
+    const int nb = std::min(kLargeBatchChunk, batch - b0);
+    const int rc = large_lu_factor_chunk(ctx, n, nb, A + (int64_t)b0 * strideA, lda, strideA,
+                                         piv ? piv + (int64_t)b0 * n : nullptr, pivot_rel_tol, flags, status);
+    if (rc) {
+      if (status) status->batch_index += b0;
+      return rc;
+    }
+  }
+  return PF_OK;
 }
 
 }  // namespace host
