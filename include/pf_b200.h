@@ -21,6 +21,10 @@
  * pf_solve_shifted            solve_shifted(b, c) (dense.hpp:62)
  * pf_one_norm_batched         DenseMatrix::one_norm (dense.hpp:32, dense.cpp:54-62)
  * pf_gemm_batched             DenseMatrix::mul (dense.hpp:26, dense.cpp:17-29)
+ * pf_context_create_multi     new: the worker pool of eval_dense (EvalOptions.workers, dense.hpp:64-68;
+ *   + pf_eval_multi_gpu       dense.cpp:202 parallel_for_index, worker_pool.hpp:16-44) as devices: the
+ *                             shifts of ONE matrix partitioned over GPUs, one NCCL exchange, results
+ *                             bit-identical for any device count in deterministic mode
  *
  * Conventions: matrices are row-major doubles (DenseMatrix layout, dense.hpp:36-37), device
  * pointers, leading dimension `ld*` in elements, batch stride `stride*` in elements. Calls are
@@ -191,6 +195,25 @@ int pf_tridiag_action(pf_context* ctx, const pf_method* m, int d, int k, const d
                       const double* dSuper, const double* dV, int64_t ldv, int substeps, double* dOut, int64_t ldo,
                       int flags, pf_status* status);
 
+/* Device-resident ActionOperator (action.hpp:73-82, action.cpp:300-325) for a tridiagonal A: the bands
+ * scaled by 1/substeps and every nonzero shift's system factored ONCE at creation (ZeroPivot
+ * reported then, "shift i: zero pivot at row r"); each apply runs `substeps` steps v <- r(A/N) v on
+ * k columns with method m's weights and form (its nonzero shifts must be the creation method's;
+ * ActionOperator::apply's opts.form may differ per apply). Same bits as pf_tridiag_action. */
+typedef struct pf_tridiag_op pf_tridiag_op;
+int pf_tridiag_op_create(pf_context* ctx, const pf_method* m, int d, const double* dSub, const double* dDiag,
+                         const double* dSuper, int substeps, pf_status* status, pf_tridiag_op** out);
+int pf_tridiag_op_apply(pf_tridiag_op* op, const pf_method* m, const double* dV, int64_t ldv, int k, double* dOut,
+                        int64_t ldo, pf_status* status);
+int pf_tridiag_op_destroy(pf_tridiag_op* op);
+/* Device-resident TridiagFactor (action.hpp:35-44): factored once (ZeroPivot at creation), solves
+ * with the reference's operation sequence (same bits as thomas_solve). */
+typedef struct pf_tridiag_factor pf_tridiag_factor;
+int pf_tridiag_factor_create(pf_context* ctx, int d, const double* dSub, const double* dDiag, const double* dSuper,
+                             pf_status* status, pf_tridiag_factor** out);
+int pf_tridiag_factor_solve(pf_tridiag_factor* f, int k, const double* dRhs, int64_t ldr, double* dX, int64_t ldx);
+int pf_tridiag_factor_destroy(pf_tridiag_factor* f);
+
 /* DenseLu: in-place PA = LU (unit lower L below the diagonal, U on and above), LAPACK-style
  * 0-based swap sequence in dPiv (n ints per matrix). SingularShift when the best pivot
  * <= pivot_rel_tol * max(max|a|, 1e-300). */
@@ -238,6 +261,35 @@ int pf_action_apply(pf_action_op* op, const double* dV, int64_t ldv, int k, doub
                     int include_poly, double* dTerms, pf_status* status);
 int pf_action_term_count(pf_action_op* op);
 int pf_action_destroy(pf_action_op* op);
+
+/* ---- multi-GPU evaluation of one matrix ----
+ * A multi-device context: one sub-context (own stream) per entry of device_ids plus an NCCL
+ * communicator over them (ncclCommInitAll; libnccl.so.2 is loaded at run time). The returned
+ * context is the root (device_ids[0]) and works with every other entry point on that device.
+ * Repeated ids are allowed (several shares on one GPU, for tests): the exchange then uses peer
+ * copies with the same partition and reduction order. */
+int pf_context_create_multi(int n_devices, const int* device_ids, pf_context** out);
+int pf_context_device_count(pf_context* ctx);
+int pf_context_uses_nccl(pf_context* ctx);
+
+enum pf_recurrence {
+  PF_REC_NONE = 0,     /* r(A) for every weight set (eval_dense, no scaling) */
+  PF_REC_EXP = 1,      /* exp: r(2^-j A) (set 0), then j squarings on the root */
+  PF_REC_EXP_PHI1 = 2  /* exp and phi1 (sets 0 and 1), then j phi1 doublings on the root */
+};
+/* f(A) of ONE n x n matrix (device pointers on the root device) with the nonzero shifts partitioned
+ * over the context's devices: (c, -c) pairs per device when there are at least as many pairs as
+ * devices, else single shifts (R8 on 8 GPUs: one shift each); zero shifts and a_0 / poly on the root.
+ * Every device evaluates its share concurrently; ONE exchange brings the result to the root before
+ * the recurrence: deterministic = 0 -> ncclReduce(sum) of per-device partial sums (agrees to
+ * rounding for any device count); deterministic = 1 -> every weighted term is sent to the root
+ * (ncclSend/ncclRecv, root only), summed in ascending shift index and completed with the
+ * polynomial part exactly as eval_dense does (dense.cpp:244-250): bit-identical for any device
+ * count. j_out (host, may be NULL) receives the squaring count. SingularShift reports the global
+ * 1-based shift index. */
+int pf_eval_multi_gpu(pf_context* ctx, const pf_method* m, double theta, int recurrence, int n, const double* dA,
+                      int64_t lda, double* dOut0, double* dOut1, int64_t ldo, int deterministic, int flags,
+                      int* j_out, pf_status* status);
 
 /* Device memory helpers for hosts without their own CUDA runtime (the C++ host layer): allocation
  * on the context's device, synchronous copies ordered on the context's stream. */

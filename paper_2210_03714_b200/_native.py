@@ -92,7 +92,22 @@ SIGNATURES = [
                                              C.POINTER(PfStatus)]),
     ("pf_tridiag_action", C.c_int, [_VP, C.POINTER(PfMethod), C.c_int, C.c_int, _VP, _VP, _VP, _VP, _I64, C.c_int,
                                     _VP, _I64, C.c_int, C.POINTER(PfStatus)]),
+    ("pf_context_create_multi", C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(_VP)]),
+    ("pf_context_device_count", C.c_int, [_VP]),
+    ("pf_context_uses_nccl", C.c_int, [_VP]),
+    ("pf_eval_multi_gpu", C.c_int, [_VP, C.POINTER(PfMethod), C.c_double, C.c_int, C.c_int, _VP, _I64, _VP, _VP, _I64,
+                                    C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(PfStatus)]),
 ]
+SIGNATURES += [
+    ("pf_tridiag_op_create", C.c_int, [_VP, C.POINTER(PfMethod), C.c_int, _VP, _VP, _VP, C.c_int,
+                                       C.POINTER(PfStatus), C.POINTER(_VP)]),
+    ("pf_tridiag_op_apply", C.c_int, [_VP, C.POINTER(PfMethod), _VP, _I64, C.c_int, _VP, _I64, C.POINTER(PfStatus)]),
+    ("pf_tridiag_op_destroy", C.c_int, [_VP]),
+    ("pf_tridiag_factor_create", C.c_int, [_VP, C.c_int, _VP, _VP, _VP, C.POINTER(PfStatus), C.POINTER(_VP)]),
+    ("pf_tridiag_factor_solve", C.c_int, [_VP, C.c_int, _VP, _I64, _VP, _I64]),
+    ("pf_tridiag_factor_destroy", C.c_int, [_VP]),
+]
+PF_REC_NONE, PF_REC_EXP, PF_REC_EXP_PHI1 = 0, 1, 2
 
 
 def load(path: os.PathLike | str | None = None) -> C.CDLL:

@@ -415,6 +415,79 @@ def expm(A: ArrayLike, method="R4", theta: Optional[float] = None, squarings: Op
     return res
 
 
+class MultiDevice:
+    """pf_context_create_multi + pf_eval_multi_gpu: ONE matrix with its shifts partitioned over
+    several GPUs of this process (the C ABI's own NCCL communicator), the single-process counterpart
+    of parallel.py's one-process-per-GPU path. ``deterministic=True`` gives results bit-identical
+    for any device count (the reference's workers contract, dense.cpp:202/245-246); repeated device
+    ids emulate several shares on one GPU (tests)."""
+
+    def __init__(self, device_ids: Sequence[int]):
+        ids = (C.c_int * len(device_ids))(*device_ids)
+        h = C.c_void_p()
+        rc = N.lib.pf_context_create_multi(len(device_ids), ids, C.byref(h))
+        if rc:
+            raise PfError(Errc.CudaError, "pf_context_create_multi failed (%d)" % rc)
+        self.h = h
+        self.device_ids = list(device_ids)
+        self.root = device_ids[0]
+
+    @property
+    def uses_nccl(self) -> bool:
+        return bool(N.lib.pf_context_uses_nccl(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            N.lib.pf_context_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _run(self, method, A: ArrayLike, recurrence: int, theta: Optional[float], form: int, deterministic: bool,
+             extra: Sequence[FractionMethod] = (), flags: int = 0):
+        m = _resolve_method(method)
+        pk = PackedMethod(m, form, extra)
+        with torch.cuda.device(self.root):
+            dA, host = _to_device(A)
+            n = dA.shape[0]
+            if dA.dim() != 2 or dA.shape[1] != n:
+                raise PfError(Errc.BadArgument, "expected one square matrix")
+            outs = [torch.empty_like(dA) for _ in range(1 + len(extra))]
+            torch.cuda.synchronize()
+            st = N.PfStatus()
+            j = C.c_int(0)
+            rc = N.lib.pf_eval_multi_gpu(self.h, pk.ptr(), float(theta or 0.0), recurrence, n, dA.data_ptr(), n,
+                                         outs[0].data_ptr(), outs[1].data_ptr() if len(outs) > 1 else None, n,
+                                         1 if deterministic else 0, flags, C.byref(j), C.byref(st))
+            if rc:
+                _raise(rc, st, False)
+            torch.cuda.synchronize()
+        res = [_back(o.unsqueeze(0), host, True, A) for o in outs]
+        return res, j.value
+
+    def eval_dense(self, method, B: ArrayLike, form: int = RESIDUAL, deterministic: bool = True):
+        return self._run(method, B, N.PF_REC_NONE, None, form, deterministic)[0][0]
+
+    def expm(self, method, A: ArrayLike, theta: Optional[float] = None, form: int = RESIDUAL,
+             deterministic: bool = True, return_squarings: bool = False):
+        m = _resolve_method(method)
+        (e,), j = self._run(m, A, N.PF_REC_EXP, _theta_for(m, theta), form, deterministic)
+        return (e, j) if return_squarings else e
+
+    def expm_phi1(self, method, A: ArrayLike, theta: Optional[float] = None, deterministic: bool = True,
+                  return_squarings: bool = False):
+        m = _resolve_method(method)
+        phi = same_shift_method(m, FunctionId.phi(1))
+        th = theta if theta is not None else min(_theta_for(m, None), THETA_U53.get(m.name + "_phi1set")
+                                                 or _theta_for(phi, None))
+        (e, p), j = self._run(m, A, N.PF_REC_EXP_PHI1, th, RESIDUAL, deterministic, extra=[phi])
+        return (e, p, j) if return_squarings else (e, p)
+
+
 class HostPipeline:
     """Batched expm of HOST matrices with the host->device copy, the evaluation and the
     device->host copy overlapped across chunks: `streams` CUDA streams, one pf_context each (so

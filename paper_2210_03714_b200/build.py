@@ -2,6 +2,8 @@
 
 * ``_lib/libpfb200.so``  -- the CUDA engine behind include/pf_b200.h (nvcc, sm_100a only)
 * ``_lib/libparfrac_host.so`` -- the C++ host layer (namespace parfrac, the reference's API)
+* ``_lib/libparfrac_gen.so``  -- host-only input generators and binary128 error oracles (no CUDA:
+  the CPU reference arm loads it without touching the engine)
 
 ``python -m paper_2210_03714_b200.build`` or ``__graft_entry__.build()``.
 """
@@ -87,6 +89,21 @@ def build_host(verbose: bool = False) -> Path:
     return out
 
 
+GEN_SOURCES = ("generators.cpp", "hp_oracle.cpp")
+
+
+def build_gen(verbose: bool = False) -> Path:
+    """Seeded generators + binary128 oracles, host only (not linked to the CUDA engine)."""
+    LIB.mkdir(exist_ok=True)
+    out = LIB / "libparfrac_gen.so"
+    srcs = [CPP / "src" / f for f in GEN_SOURCES]
+    hdrs = list((CPP / "include").rglob("*.hpp"))
+    if _stale(out, srcs + hdrs):
+        cxx = shutil.which("g++") or "g++"
+        _run([cxx, *CXX_FLAGS, "-shared", "-o", str(out), *map(str, srcs), "-lpthread"])
+    return out
+
+
 def build_cpp_tests(verbose: bool = False) -> Path:
     """The C++ parity test binary over the host layer (tests/cpp/test_parfrac.cpp)."""
     src = ROOT / "tests" / "cpp" / "test_parfrac.cpp"
@@ -109,6 +126,7 @@ def build_oracle() -> Path:
 
 def build_all(verbose: bool = False):
     eng = build_engine(verbose)
+    build_gen(verbose)
     host = build_host(verbose)
     tst = build_cpp_tests(verbose)
     orc = build_oracle()

@@ -4,6 +4,7 @@
 // vector with exactly the reference's operation sequence. New: block variants over k vectors
 // (d x k row-major), the shape the GPU is built for.
 
+#include <memory>
 #include <span>
 #include <vector>
 
@@ -29,15 +30,20 @@ struct TridiagMatrix {
 /// Thomas algorithm (action.hpp:29-31); ZeroPivot "zero pivot at row r" below 1e-300.
 std::vector<double> thomas_solve(const TridiagMatrix& t, std::span<const double> rhs);
 
-/// Thomas factorization reused across vectors (action.hpp:35-44): validated (ZeroPivot) at
-/// construction; solve() performs the same floating-point operations as thomas_solve.
+struct TridiagFactorDevice;
+struct ActionOperatorDevice;
+
+/// Thomas factorization reused across vectors (action.hpp:35-44): factored ONCE on the device at
+/// construction (ZeroPivot there) and kept resident; solve() moves only the right-hand side and
+/// performs the same floating-point operations as thomas_solve.
 class TridiagFactor {
  public:
   explicit TridiagFactor(const TridiagMatrix& t);
   std::vector<double> solve(std::span<const double> rhs) const;
 
  private:
-  TridiagMatrix t_;
+  int d_ = 0;
+  std::shared_ptr<const TridiagFactorDevice> dev_;
 };
 
 /// Compact five-diagonal matrix (action.hpp:48-55).
@@ -61,14 +67,19 @@ std::vector<double> substep_action(const FractionMethod& method, const TridiagMa
                                    int substeps, const EvalOptions& opts = {});
 
 /// One method bound to one tridiagonal matrix (action.hpp:73-82); results identical to action_eval.
+/// The factored shifted systems live on the device from construction to destruction (factored
+/// once, action.cpp:300-312); apply() moves only the vectors.
 class ActionOperator {
  public:
   ActionOperator(const FractionMethod& method, const TridiagMatrix& a);
   std::vector<double> apply(std::span<const double> v, const EvalOptions& opts = {}) const;
+  /// New: apply to each of the k columns of V (d x k row-major) in one device call.
+  std::vector<double> apply_block(std::span<const double> v, int k, const EvalOptions& opts = {}) const;
 
  private:
   FractionMethod method_;
   TridiagMatrix a_;
+  std::shared_ptr<ActionOperatorDevice> dev_;
 };
 
 /// New: substep_action on each of the k columns of V (d x k row-major), one device call.

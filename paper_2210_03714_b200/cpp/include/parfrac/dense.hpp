@@ -4,6 +4,7 @@
 // New entry points: expm / expm_phi1 / cossin with scaling and squaring, batched
 // evaluation, and the dense block action.
 
+#include <memory>
 #include <optional>
 #include <span>
 #include <vector>
@@ -40,7 +41,11 @@ class DenseMatrix {
   std::vector<double> a_;
 };
 
-/// LU factors with partial pivoting (dense.hpp:44-59); factored on the device.
+struct DenseLuDevice;  // the factors and pivots kept in device memory (dense.cpp)
+
+/// LU factors with partial pivoting (dense.hpp:44-59); factored on the device, and the factors STAY
+/// there: every solve / solve_matrix reuses them (only the right-hand sides move). Copies share
+/// the immutable device factors.
 class DenseLu {
  public:
   DenseLu(const DenseMatrix& a, double pivot_rel_tol = 1e-14);
@@ -55,6 +60,7 @@ class DenseLu {
   int d_ = 0;
   std::vector<double> lu_;
   std::vector<int> piv_;
+  std::shared_ptr<const DenseLuDevice> dev_;
 };
 
 /// (I - cB)^{-1} (dense.hpp:62)
@@ -64,6 +70,12 @@ struct EvalOptions {
   int workers = 1;
   bool fixed_order = true;
   std::optional<EvalForm> form;
+  /// New (B200): the reference's worker pool over shifts (dense.cpp:202) as GPUs. devices > 1 or a
+  /// device_ids list partitions the shifts of ONE matrix over those GPUs (pf_eval_multi_gpu, one
+  /// NCCL exchange); with fixed_order (always, as in the reference) the result is bit-identical
+  /// for any device count. device_ids overrides devices (ids 0..devices-1).
+  int devices = 1;
+  std::vector<int> device_ids;
 };
 
 /// r(B) (dense.hpp:70-75)
@@ -79,8 +91,13 @@ DenseMatrix expm(const FractionMethod& method, const DenseMatrix& a, EvalForm fo
 std::vector<DenseMatrix> expm_batched(const FractionMethod& method, const std::vector<DenseMatrix>& as,
                                       EvalForm form = EvalForm::Residual);
 
-/// (exp(A), phi1(A)) from one solve per shift, then phi1 doubling.
-std::pair<DenseMatrix, DenseMatrix> expm_phi1(const FractionMethod& method, const DenseMatrix& a);
+/// exp(A) with EvalOptions: form override, and devices / device_ids for the shift-partitioned
+/// multi-GPU evaluation (one exchange, then the squaring on the first device).
+DenseMatrix expm(const FractionMethod& method, const DenseMatrix& a, const EvalOptions& opts, int* squarings = nullptr);
+
+/// (exp(A), phi1(A)) from one solve per shift, then phi1 doubling (multi-GPU with opts.devices).
+std::pair<DenseMatrix, DenseMatrix> expm_phi1(const FractionMethod& method, const DenseMatrix& a,
+                                              const EvalOptions& opts = {});
 
 /// (cos(A), sin(A)) through merged conjugate shift pairs and C^2 - S^2 / 2SC.
 std::pair<DenseMatrix, DenseMatrix> cossin(const FractionMethod& method, const DenseMatrix& a);

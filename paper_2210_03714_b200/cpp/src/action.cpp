@@ -19,9 +19,9 @@ namespace {
 // device copy of the three bands (the off-diagonals of a 1 x 1 matrix are empty: point at diag)
 struct DevBand {
   Buf sub, diag, sup;
-  DevBand(pf_context* ctx, const TridiagMatrix& t)
-      : sub(ctx, size_t(std::max(t.d - 1, 1))), diag(ctx, size_t(std::max(t.d, 1))),
-        sup(ctx, size_t(std::max(t.d - 1, 1))) {
+  DevBand(Device& dev, const TridiagMatrix& t)
+      : sub(dev, size_t(std::max(t.d - 1, 1))), diag(dev, size_t(std::max(t.d, 1))),
+        sup(dev, size_t(std::max(t.d - 1, 1))) {
     if (int(t.diag.size()) != t.d || int(t.sub.size()) != std::max(t.d - 1, 0) ||
         int(t.super.size()) != std::max(t.d - 1, 0))
       raise(Errc::LengthMismatch, "band length mismatch");
@@ -42,9 +42,9 @@ std::vector<double> tridiag_action_block(const FractionMethod& method, const Tri
   Packed pk({&method}, opts.form.value_or(method.form));
   Device& dev = device();
   std::lock_guard<std::mutex> lock(dev.mu);
-  DevBand band(dev.ctx, a);
+  DevBand band(dev, a);
   const size_t n = std::max<size_t>(v.size(), 1);
-  Buf in(dev.ctx, n), out(dev.ctx, n);
+  Buf in(dev, n), out(dev, n);
   if (!v.empty()) in.put(v.data(), v.size());
   pf_status st{};
   const int rc = pf_tridiag_action(dev.ctx, &pk.m, a.d, k, band.sub.d(), band.diag.d(), band.sup.d(), in.d(), k,
@@ -79,8 +79,8 @@ std::vector<double> TridiagMatrix::matvec(std::span<const double> v) const {
   if (d == 0) return {};
   Device& dev = device();
   std::lock_guard<std::mutex> lock(dev.mu);
-  DevBand band(dev.ctx, *this);
-  Buf in(dev.ctx, size_t(d)), out(dev.ctx, size_t(d));
+  DevBand band(dev, *this);
+  Buf in(dev, size_t(d)), out(dev, size_t(d));
   in.put(v.data(), size_t(d));
   const int rc = pf_tridiag_matvec_batched(dev.ctx, d, 1, band.sub.d(), band.diag.d(), band.sup.d(), in.d(), 1,
                                            out.d(), 1);
@@ -116,8 +116,8 @@ std::vector<double> thomas_solve(const TridiagMatrix& t, std::span<const double>
   if (t.d == 0) return {};
   Device& dev = device();
   std::lock_guard<std::mutex> lock(dev.mu);
-  DevBand band(dev.ctx, t);
-  Buf in(dev.ctx, size_t(t.d)), out(dev.ctx, size_t(t.d));
+  DevBand band(dev, t);
+  Buf in(dev, size_t(t.d)), out(dev, size_t(t.d));
   in.put(rhs.data(), size_t(t.d));
   pf_status st{};
   const int rc = pf_thomas_solve_batched(dev.ctx, t.d, 1, band.sub.d(), band.diag.d(), band.sup.d(), in.d(), 1,
@@ -128,19 +128,42 @@ std::vector<double> thomas_solve(const TridiagMatrix& t, std::span<const double>
   return r;
 }
 
-TridiagFactor::TridiagFactor(const TridiagMatrix& t) : t_(t) {
+struct TridiagFactorDevice {
+  pf_tridiag_factor* f = nullptr;
+  ~TridiagFactorDevice() { pf_tridiag_factor_destroy(f); }
+};
+
+struct ActionOperatorDevice {
+  pf_tridiag_op* op = nullptr;
+  ~ActionOperatorDevice() { pf_tridiag_op_destroy(op); }
+};
+
+TridiagFactor::TridiagFactor(const TridiagMatrix& t) : d_(t.d) {
   if (t.d == 0) return;
   Device& dev = device();
   std::lock_guard<std::mutex> lock(dev.mu);
-  DevBand band(dev.ctx, t);
+  DevBand band(dev, t);
+  auto f = std::make_shared<TridiagFactorDevice>();
   pf_status st{};
-  // k = 0: factor only (ZeroPivot at construction, action.cpp:120-133)
-  const int rc = pf_thomas_solve_batched(dev.ctx, t.d, 0, band.sub.d(), band.diag.d(), band.sup.d(), band.diag.d(),
-                                         0, band.diag.d(), 0, &st);
+  // factored once; ZeroPivot at construction (action.cpp:120-133)
+  const int rc = pf_tridiag_factor_create(dev.ctx, t.d, band.sub.d(), band.diag.d(), band.sup.d(), &st, &f->f);
   if (rc) rethrow(rc, st, false);
+  dev_ = std::move(f);
 }
 
-std::vector<double> TridiagFactor::solve(std::span<const double> rhs) const { return thomas_solve(t_, rhs); }
+std::vector<double> TridiagFactor::solve(std::span<const double> rhs) const {
+  if (int(rhs.size()) != d_) raise(Errc::LengthMismatch, "rhs length mismatch");
+  if (d_ == 0) return {};
+  Device& dev = device();
+  std::lock_guard<std::mutex> lock(dev.mu);
+  Buf in(dev, size_t(d_)), out(dev, size_t(d_));
+  in.put(rhs.data(), size_t(d_));
+  const int rc = pf_tridiag_factor_solve(dev_->f, 1, in.d(), 1, out.d(), 1);
+  if (rc) rethrow(rc, pf_status{}, false);
+  std::vector<double> r(static_cast<size_t>(d_));
+  out.get(r.data(), size_t(d_));
+  return r;
+}
 
 std::vector<double> PentadiagMatrix::matvec(std::span<const double> v) const {
   std::vector<double> out(size_t(d), 0.0);
@@ -173,9 +196,9 @@ std::vector<double> pentadiag_solve(const PentadiagMatrix& p, std::span<const do
   if (d == 0) return {};
   Device& dev = device();
   std::lock_guard<std::mutex> lock(dev.mu);
-  Buf s2(dev.ctx, std::max<size_t>(p.sub2.size(), 1)), s1(dev.ctx, std::max<size_t>(p.sub1.size(), 1)),
-      dg(dev.ctx, size_t(d)), u1(dev.ctx, std::max<size_t>(p.super1.size(), 1)),
-      u2(dev.ctx, std::max<size_t>(p.super2.size(), 1)), in(dev.ctx, size_t(d)), out(dev.ctx, size_t(d));
+  Buf s2(dev, std::max<size_t>(p.sub2.size(), 1)), s1(dev, std::max<size_t>(p.sub1.size(), 1)),
+      dg(dev, size_t(d)), u1(dev, std::max<size_t>(p.super1.size(), 1)),
+      u2(dev, std::max<size_t>(p.super2.size(), 1)), in(dev, size_t(d)), out(dev, size_t(d));
   if (!p.sub2.empty()) s2.put(p.sub2.data(), p.sub2.size());
   if (!p.sub1.empty()) s1.put(p.sub1.data(), p.sub1.size());
   dg.put(p.diag.data(), size_t(d));
@@ -208,12 +231,39 @@ std::vector<double> substep_action_block(const FractionMethod& method, const Tri
 }
 
 ActionOperator::ActionOperator(const FractionMethod& method, const TridiagMatrix& a) : method_(method), a_(a) {
-  // every shifted system factored once up front: ZeroPivot at construction (action.cpp:300-312)
-  tridiag_action_block(method_, a_, {}, 0, 1, {});
+  // every shifted system factored once, kept on the device: ZeroPivot at construction (action.cpp:300-312)
+  if (a.d == 0) return;
+  Packed pk({&method_}, method_.form);
+  Device& dev = device();
+  std::lock_guard<std::mutex> lock(dev.mu);
+  DevBand band(dev, a);
+  auto op = std::make_shared<ActionOperatorDevice>();
+  pf_status st{};
+  const int rc = pf_tridiag_op_create(dev.ctx, &pk.m, a.d, band.sub.d(), band.diag.d(), band.sup.d(), 1, &st, &op->op);
+  if (rc) rethrow(rc, st, true);
+  dev_ = std::move(op);
+}
+
+std::vector<double> ActionOperator::apply_block(std::span<const double> v, int k, const EvalOptions& opts) const {
+  if (opts.workers < 1) raise(Errc::BadArgument, "workers must be >= 1");
+  if (!opts.fixed_order) raise(Errc::BadArgument, "only fixed-order reduction is supported");
+  if (k < 0 || v.size() != size_t(a_.d) * size_t(k)) raise(Errc::LengthMismatch, "vector length mismatch");
+  std::vector<double> r(v.size());
+  if (v.empty()) return r;
+  Packed pk({&method_}, opts.form.value_or(method_.form));
+  Device& dev = device();
+  std::lock_guard<std::mutex> lock(dev.mu);
+  Buf in(dev, v.size()), out(dev, v.size());
+  in.put(v.data(), v.size());
+  pf_status st{};
+  const int rc = pf_tridiag_op_apply(dev_->op, &pk.m, in.d(), k, k, out.d(), k, &st);
+  if (rc) rethrow(rc, st, true);
+  out.get(r.data(), r.size());
+  return r;
 }
 
 std::vector<double> ActionOperator::apply(std::span<const double> v, const EvalOptions& opts) const {
-  return tridiag_action_block(method_, a_, v, 1, 1, opts);
+  return apply_block(v, 1, opts);
 }
 
 }  // namespace parfrac

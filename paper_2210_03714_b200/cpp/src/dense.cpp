@@ -13,6 +13,11 @@
 
 namespace parfrac {
 
+struct DenseLuDevice {
+  engine::Buf lu, piv;
+  DenseLuDevice(pf_context* ctx, int d) : lu(ctx, size_t(d) * d), piv(ctx, (size_t(d) + 1) / 2) {}
+};
+
 namespace {
 
 using namespace engine;
@@ -21,6 +26,41 @@ DenseMatrix from_flat(int d, const double* p) {
   DenseMatrix m(d);
   std::copy(p, p + size_t(d) * d, m.data().begin());
   return m;
+}
+
+std::vector<int> device_list(const EvalOptions& opts) {
+  if (!opts.device_ids.empty()) return opts.device_ids;
+  if (opts.devices < 1) raise(Errc::BadArgument, "devices must be >= 1");
+  std::vector<int> ids(size_t(opts.devices));
+  for (int i = 0; i < opts.devices; ++i) ids[size_t(i)] = i;
+  return ids;
+}
+
+bool multi_gpu(const EvalOptions& opts) { return opts.devices > 1 || !opts.device_ids.empty(); }
+
+// ONE matrix over the devices `ids` (pf_eval_multi_gpu, deterministic: the reference's fixed-order
+// contract); returns the output of every weight set of `sets`
+std::vector<DenseMatrix> eval_multi(const std::vector<const FractionMethod*>& sets, EvalForm form, const DenseMatrix& a,
+                                    int recurrence, double theta, const std::vector<int>& ids, int* squarings) {
+  Packed pk(sets, form);
+  MultiDevices& md = multi_devices();
+  std::lock_guard<std::mutex> lock(md.mu);
+  pf_context* ctx = md.get(ids);
+  const int d = a.dim();
+  const size_t nn = size_t(d) * d;
+  std::vector<DenseMatrix> res(sets.size(), DenseMatrix(d));
+  if (nn == 0) return res;
+  Buf in(ctx, nn), o0(ctx, nn), o1(ctx, sets.size() > 1 ? nn : 1);
+  in.put(a.data().data(), nn);
+  pf_status st{};
+  int j = 0;
+  const int rc = pf_eval_multi_gpu(ctx, &pk.m, theta, recurrence, d, in.d(), d, o0.d(), sets.size() > 1 ? o1.d() : nullptr,
+                                   d, 1, 0, &j, &st);
+  if (rc) rethrow(rc, st, true);
+  o0.get(res[0].data().data(), nn);
+  if (sets.size() > 1) o1.get(res[1].data().data(), nn);
+  if (squarings) *squarings = j;
+  return res;
 }
 
 }  // namespace
@@ -38,7 +78,7 @@ DenseMatrix DenseMatrix::mul(const DenseMatrix& o) const {
   const size_t nn = size_t(d_) * d_;
   DenseMatrix out(d_);
   if (nn == 0) return out;
-  Buf a(dev.ctx, nn), b(dev.ctx, nn), c(dev.ctx, nn);
+  Buf a(dev, nn), b(dev, nn), c(dev, nn);
   a.put(a_.data(), nn);
   b.put(o.a_.data(), nn);
   const int rc = pf_gemm_batched(dev.ctx, d_, d_, d_, 1, 1.0, a.d(), d_, 0, b.d(), d_, 0, 0.0, c.d(), d_, 0, 0.0);
@@ -92,13 +132,14 @@ DenseLu::DenseLu(const DenseMatrix& a, double pivot_rel_tol) : d_(a.dim()), lu_(
   const size_t nn = size_t(d_) * d_;
   piv_.resize(size_t(d_));
   if (nn == 0) return;
-  Buf m(dev.ctx, nn), piv(dev.ctx, (size_t(d_) + 1) / 2);
-  m.put(lu_.data(), nn);
+  auto f = std::make_shared<DenseLuDevice>(dev.ctx, d_);
+  f->lu.put(lu_.data(), nn);
   pf_status st{};
-  const int rc = pf_lu_factor_batched(dev.ctx, d_, 1, m.d(), d_, 0, piv.i(), pivot_rel_tol, 0, &st);
+  const int rc = pf_lu_factor_batched(dev.ctx, d_, 1, f->lu.d(), d_, 0, f->piv.i(), pivot_rel_tol, 0, &st);
   if (rc) rethrow(rc, st, false);
-  m.get(lu_.data(), nn);
-  Buf::check(pf_copy_to_host(dev.ctx, piv_.data(), piv.d(), sizeof(int) * size_t(d_)));
+  f->lu.get(lu_.data(), nn);  // host copies for factors() / pivots(); the device keeps its own
+  Buf::check(pf_copy_to_host(dev.ctx, piv_.data(), f->piv.d(), sizeof(int) * size_t(d_)));
+  dev_ = std::move(f);
 }
 
 DenseMatrix DenseLu::solve_matrix(const DenseMatrix& rhs) const {
@@ -108,11 +149,9 @@ DenseMatrix DenseLu::solve_matrix(const DenseMatrix& rhs) const {
   const size_t nn = size_t(d_) * d_;
   DenseMatrix out = rhs;
   if (nn == 0) return out;
-  Buf lu(dev.ctx, nn), piv(dev.ctx, (size_t(d_) + 1) / 2), r(dev.ctx, nn);
-  lu.put(lu_.data(), nn);
-  Buf::check(pf_copy_to_device(dev.ctx, piv.d(), piv_.data(), sizeof(int) * size_t(d_)));
+  Buf r(dev, nn);
   r.put(rhs.data().data(), nn);
-  const int rc = pf_lu_solve_batched(dev.ctx, d_, d_, 1, lu.d(), d_, 0, piv.i(), r.d(), d_, 0);
+  const int rc = pf_lu_solve_batched(dev.ctx, d_, d_, 1, dev_->lu.d(), d_, 0, dev_->piv.i(), r.d(), d_, 0);
   if (rc) rethrow(rc, pf_status{}, false);
   r.get(out.data().data(), nn);
   return out;
@@ -124,12 +163,9 @@ std::vector<double> DenseLu::solve(std::span<const double> rhs) const {
   std::lock_guard<std::mutex> lock(dev.mu);
   std::vector<double> x(rhs.begin(), rhs.end());
   if (d_ == 0) return x;
-  const size_t nn = size_t(d_) * d_;
-  Buf lu(dev.ctx, nn), piv(dev.ctx, (size_t(d_) + 1) / 2), r(dev.ctx, size_t(d_));
-  lu.put(lu_.data(), nn);
-  Buf::check(pf_copy_to_device(dev.ctx, piv.d(), piv_.data(), sizeof(int) * size_t(d_)));
+  Buf r(dev, size_t(d_));
   r.put(x.data(), size_t(d_));
-  const int rc = pf_lu_solve_batched(dev.ctx, d_, 1, 1, lu.d(), d_, 0, piv.i(), r.d(), 1, 0);
+  const int rc = pf_lu_solve_batched(dev.ctx, d_, 1, 1, dev_->lu.d(), d_, 0, dev_->piv.i(), r.d(), 1, 0);
   if (rc) rethrow(rc, pf_status{}, false);
   r.get(x.data(), size_t(d_));
   return x;
@@ -141,7 +177,7 @@ DenseMatrix solve_shifted(const DenseMatrix& b, double c) {
   const int d = b.dim();
   const size_t nn = size_t(d) * d;
   if (nn == 0) return DenseMatrix(d);
-  Buf in(dev.ctx, nn), out(dev.ctx, nn);
+  Buf in(dev, nn), out(dev, nn);
   in.put(b.data().data(), nn);
   pf_status st{};
   const int rc = pf_solve_shifted_batched(dev.ctx, d, 1, in.d(), d, 0, c, out.d(), d, 0, 0, &st);
@@ -166,7 +202,7 @@ std::vector<DenseMatrix> eval_dense_batched(const FractionMethod& method, const 
   std::lock_guard<std::mutex> lock(dev.mu);
   const size_t nn = size_t(d) * d, batch = bs.size();
   if (nn == 0) return std::vector<DenseMatrix>(batch, DenseMatrix(d));
-  Buf in(dev.ctx, nn * batch), out(dev.ctx, nn * batch);
+  Buf in(dev, nn * batch), out(dev, nn * batch);
   std::vector<double> host(nn * batch);
   for (size_t k = 0; k < batch; ++k) std::copy(bs[k].data().begin(), bs[k].data().end(), host.begin() + k * nn);
   in.put(host.data(), nn * batch);
@@ -180,6 +216,11 @@ std::vector<DenseMatrix> eval_dense_batched(const FractionMethod& method, const 
 }
 
 DenseMatrix eval_dense(const FractionMethod& method, const DenseMatrix& b, const EvalOptions& opts) {
+  if (multi_gpu(opts)) {
+    if (opts.workers < 1) raise(Errc::BadArgument, "workers must be >= 1");
+    if (!opts.fixed_order) raise(Errc::BadArgument, "only fixed-order reduction is supported");
+    return eval_multi({&method}, opts.form.value_or(method.form), b, PF_REC_NONE, 0.0, device_list(opts), nullptr)[0];
+  }
   return eval_dense_batched(method, {b}, opts)[0];
 }
 
@@ -192,7 +233,7 @@ std::vector<DenseMatrix> expm_batched(const FractionMethod& method, const std::v
   Device& dev = device();
   std::lock_guard<std::mutex> lock(dev.mu);
   const size_t nn = size_t(d) * d, batch = as.size();
-  Buf in(dev.ctx, nn * batch), out(dev.ctx, nn * batch);
+  Buf in(dev, nn * batch), out(dev, nn * batch);
   std::vector<double> host(nn * batch);
   for (size_t k = 0; k < batch; ++k) std::copy(as[k].data().begin(), as[k].data().end(), host.begin() + k * nn);
   in.put(host.data(), nn * batch);
@@ -217,15 +258,28 @@ DenseMatrix expm(const FractionMethod& method, const DenseMatrix& a, EvalForm fo
   return e;
 }
 
-std::pair<DenseMatrix, DenseMatrix> expm_phi1(const FractionMethod& method, const DenseMatrix& a) {
+DenseMatrix expm(const FractionMethod& method, const DenseMatrix& a, const EvalOptions& opts, int* squarings) {
+  if (opts.workers < 1) raise(Errc::BadArgument, "workers must be >= 1");
+  if (!opts.fixed_order) raise(Errc::BadArgument, "only fixed-order reduction is supported");
+  const EvalForm form = opts.form.value_or(EvalForm::Residual);
+  if (!multi_gpu(opts)) return expm(method, a, form, squarings);
+  return eval_multi({&method}, form, a, PF_REC_EXP, theta_u53(method), device_list(opts), squarings)[0];
+}
+
+std::pair<DenseMatrix, DenseMatrix> expm_phi1(const FractionMethod& method, const DenseMatrix& a,
+                                              const EvalOptions& opts) {
   const FractionMethod& phi = derived_set(method.name + "_phi1set");
-  Packed pk({&method, &phi}, EvalForm::Residual);
   const double th = std::min(theta_u53(method), phi.theta_u53);
+  if (multi_gpu(opts)) {
+    auto r = eval_multi({&method, &phi}, EvalForm::Residual, a, PF_REC_EXP_PHI1, th, device_list(opts), nullptr);
+    return {r[0], r[1]};
+  }
+  Packed pk({&method, &phi}, EvalForm::Residual);
   const int d = a.dim();
   const size_t nn = size_t(d) * d;
   Device& dev = device();
   std::lock_guard<std::mutex> lock(dev.mu);
-  Buf in(dev.ctx, nn), e(dev.ctx, nn), p(dev.ctx, nn);
+  Buf in(dev, nn), e(dev, nn), p(dev, nn);
   in.put(a.data().data(), nn);
   pf_status st{};
   const int rc = pf_expm_phi1_batched(dev.ctx, &pk.m, th, d, 1, in.d(), d, 0, nullptr, nullptr, e.d(), p.d(), d, 0, 0, &st);
@@ -249,7 +303,7 @@ std::pair<DenseMatrix, DenseMatrix> cossin(const FractionMethod& method, const D
   const size_t nn = size_t(d) * d;
   Device& dev = device();
   std::lock_guard<std::mutex> lock(dev.mu);
-  Buf in(dev.ctx, nn), c(dev.ctx, nn), s(dev.ctx, nn);
+  Buf in(dev, nn), c(dev, nn), s(dev, nn);
   in.put(a.data().data(), nn);
   pf_status st{};
   const int rc = pf_cossin_batched(dev.ctx, &p, theta_u53(method), d, 1, in.d(), d, 0, nullptr, nullptr, c.d(), s.d(),
@@ -276,7 +330,7 @@ std::vector<double> substep_action(const FractionMethod& method, const DenseMatr
   Device& dev = device();
   std::lock_guard<std::mutex> lock(dev.mu);
   const size_t nn = size_t(d) * d, nk = size_t(d) * k;
-  Buf ad(dev.ctx, nn), vd(dev.ctx, nk), od(dev.ctx, nk);
+  Buf ad(dev, nn), vd(dev, nk), od(dev, nk);
   ad.put(a.data().data(), nn);
   vd.put(v.data(), nk);
   pf_status st{};

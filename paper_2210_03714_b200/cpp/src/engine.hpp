@@ -1,6 +1,8 @@
 #pragma once
 // Internal to the C++ host layer (not installed): the process-wide B200 context, device buffers,
 // and the mapping of ABI status codes back to parfrac::Error with the reference's messages.
+#include <algorithm>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -16,11 +18,16 @@ namespace engine {
 struct Device {
   std::mutex mu;
   pf_context* ctx = nullptr;
+  // device buffers are recycled (size classes of powers of two): a call does not pay cudaMalloc
+  std::multimap<size_t, void*> pool;
   Device() {
     if (pf_context_create(0, &ctx) != PF_OK)
       raise(Errc::BadArgument, "parfrac: no CUDA device (the B200 engine has no CPU fallback)");
   }
-  ~Device() { pf_context_destroy(ctx); }
+  ~Device() {
+    for (auto& kv : pool) pf_device_free(ctx, kv.second);
+    pf_context_destroy(ctx);
+  }
 };
 
 inline Device& device() {
@@ -28,12 +35,58 @@ inline Device& device() {
   return d;
 }
 
+// Multi-device contexts for EvalOptions::devices / device_ids, one per device list, process-wide.
+struct MultiDevices {
+  std::mutex mu;
+  std::map<std::vector<int>, pf_context*> ctxs;
+  ~MultiDevices() {
+    for (auto& kv : ctxs) pf_context_destroy(kv.second);
+  }
+  pf_context* get(const std::vector<int>& ids) {
+    auto it = ctxs.find(ids);
+    if (it != ctxs.end()) return it->second;
+    pf_context* c = nullptr;
+    if (pf_context_create_multi(int(ids.size()), ids.data(), &c) != PF_OK)
+      raise(Errc::BadArgument, "parfrac: cannot create a context over the requested devices");
+    ctxs[ids] = c;
+    return c;
+  }
+};
+
+inline MultiDevices& multi_devices() {
+  static MultiDevices m;
+  return m;
+}
+
+// A device buffer of `count` doubles from the pool of `dev` (caller holds dev.mu for its lifetime).
 class Buf {
  public:
-  Buf(pf_context* ctx, size_t count) : ctx_(ctx) {
-    if (pf_device_alloc(ctx, count * sizeof(double), &p_) != PF_OK) raise(Errc::BadArgument, "device allocation failed");
+  Buf(Device& dev, size_t count) : dev_(&dev), ctx_(dev.ctx) {
+    size_t bytes = 256;
+    while (bytes < count * sizeof(double)) bytes <<= 1;
+    bytes_ = bytes;
+    auto it = dev.pool.find(bytes);
+    if (it != dev.pool.end()) {
+      p_ = it->second;
+      dev.pool.erase(it);
+    } else if (pf_device_alloc(ctx_, bytes, &p_) != PF_OK) {
+      raise(Errc::BadArgument, "device allocation failed");
+    }
   }
-  ~Buf() { pf_device_free(ctx_, p_); }
+  // a buffer owned outside the pool (long-lived objects: DenseLu factors, operators)
+  Buf(pf_context* ctx, size_t count) : ctx_(ctx) {
+    if (pf_device_alloc(ctx, std::max<size_t>(count, 1) * sizeof(double), &p_) != PF_OK)
+      raise(Errc::BadArgument, "device allocation failed");
+  }
+  ~Buf() {
+    if (!p_) return;
+    if (dev_)
+      dev_->pool.emplace(bytes_, p_);
+    else
+      pf_device_free(ctx_, p_);
+  }
+  Buf(const Buf&) = delete;
+  Buf& operator=(const Buf&) = delete;
   double* d() const { return static_cast<double*>(p_); }
   int* i() const { return static_cast<int*>(p_); }
   void put(const double* h, size_t count) { check(pf_copy_to_device(ctx_, p_, h, count * sizeof(double))); }
@@ -43,8 +96,10 @@ class Buf {
   }
 
  private:
+  Device* dev_ = nullptr;
   pf_context* ctx_;
   void* p_ = nullptr;
+  size_t bytes_ = 0;
 };
 
 inline Errc errc_of(int rc) { return rc >= 1 && rc <= 10 ? static_cast<Errc>(rc - 1) : Errc::BadArgument; }

@@ -260,6 +260,7 @@ int pf_context_create(int device, pf_context** out) {
 int pf_context_destroy(pf_context* ctx) {
   if (!ctx) return PF_OK;
   DeviceGuard device_guard(ctx);
+  group_destroy(ctx);
   cudaStreamSynchronize(ctx->stream);
   for (void* p : ctx->ws) cudaFree(p);
   cudaFree(ctx->status);

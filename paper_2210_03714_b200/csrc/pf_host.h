@@ -6,8 +6,11 @@
 #include "pf_common.cuh"
 #include "pf_kernels.h"
 
+struct pf_group;  // multi-device contexts (pf_multi.cu)
+
 struct pf_context {
   int device = 0;
+  pf_group* group = nullptr;  // set on the root of pf_context_create_multi
   cudaStream_t stream = nullptr;
   int64_t launches = 0;
   pf::DevStatus* status = nullptr;
@@ -88,6 +91,8 @@ struct DeviceGuard {
   DeviceGuard(const DeviceGuard&) = delete;
   DeviceGuard& operator=(const DeviceGuard&) = delete;
 };
+
+void group_destroy(pf_context* root);  // members, streams and NCCL communicators of a multi context
 
 int action_op_create(pf_context* ctx, const pf_method* m, int n, const double* A, int64_t lda, int substeps,
                      const int* owned, int flags, pf_status* status, pf_action_op** out);

@@ -12,7 +12,7 @@ from pathlib import Path
 
 import numpy as np
 
-_HOST = Path(__file__).resolve().parent / "_lib" / "libparfrac_host.so"
+_HOST = Path(__file__).resolve().parent / "_lib" / "libparfrac_gen.so"  # host only: no CUDA engine
 _lib = None
 
 
@@ -20,14 +20,14 @@ def _host():
     global _lib
     if _lib is None:
         if not _HOST.exists():
-            # the host layer is plain C++ (seconds with g++): rebuild it in-tree rather than fail when a
-            # copy of the tree arrives without it; the CUDA engine is never rebuilt implicitly
+            # plain C++ (seconds with g++): rebuild it in-tree rather than fail when a copy of the tree
+            # arrives without it; the CUDA engine is never rebuilt implicitly
             from . import build
 
             try:
-                build.build_host()
+                build.build_gen()
             except Exception as e:  # noqa: BLE001
-                raise ImportError("libparfrac_host.so missing and not buildable: %s" % e) from None
+                raise ImportError("libparfrac_gen.so missing and not buildable: %s" % e) from None
         _lib = C.CDLL(str(_HOST))
         _lib.pf_gen_randn.argtypes = [C.c_uint64, C.c_int64, C.c_void_p]
         _lib.pf_gen_uniform.argtypes = [C.c_uint64, C.c_int64, C.c_void_p]

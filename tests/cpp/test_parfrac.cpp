@@ -369,6 +369,79 @@ void test_action() {  // test_action.cpp:124-188
   CHECK(got);
 }
 
+// ---- multi-GPU through EvalOptions (pf_context_create_multi / pf_eval_multi_gpu). One GPU here:
+// {0} is a one-rank NCCL communicator; {0, 0, ...} runs the same partition with peer copies.
+// fixed_order => bit-identical for any device count (test_dense.cpp:108-119's contract).
+void test_multi_device() {
+  DenseMatrix b = scaled_to_one_norm(random_matrix(96, 41), 0.6);
+  for (const char* name : {"R4", "R8", "R10"}) {
+    const FractionMethod& m = catalog(name);
+    EvalOptions one{.form = EvalForm::Residual, .device_ids = {0}};
+    DenseMatrix ref = eval_dense(m, b, one);
+    for (int g : {2, 3, 8}) {
+      EvalOptions opts{.form = EvalForm::Residual, .device_ids = std::vector<int>(size_t(g), 0)};
+      CHECK(rel_diff_1norm(eval_dense(m, b, opts), ref) == 0.0);
+    }
+    CHECK(rel_diff_1norm(ref, eval_dense(m, b, {.form = EvalForm::Residual})) <= 1e-12);
+  }
+  DenseMatrix a = scaled_to_one_norm(random_matrix(160, 42), 4.0);
+  int j1 = -1, j4 = -1;
+  DenseMatrix e1 = expm(catalog("R8"), a, EvalOptions{.devices = 1, .device_ids = {0}}, &j1);
+  DenseMatrix e4 = expm(catalog("R8"), a, EvalOptions{.device_ids = {0, 0, 0, 0}}, &j4);
+  CHECK(j1 == j4 && j1 > 0);
+  CHECK(rel_diff_1norm(e1, e4) == 0.0);
+  CHECK(rel_diff_1norm(e1, expm(catalog("R8"), a)) <= 1e-12);
+  auto [pe, pp] = expm_phi1(catalog("R8"), a, EvalOptions{.device_ids = {0, 0}});
+  auto [qe, qp] = expm_phi1(catalog("R8"), a);
+  CHECK(rel_diff_1norm(pe, qe) <= 1e-12 && rel_diff_1norm(pp, qp) <= 1e-12);
+  // SingularShift keeps the reference message with the global shift index
+  bool got = false;
+  try {
+    DenseMatrix five = DenseMatrix::identity(6);
+    five.scale(5.0);
+    eval_dense(catalog("R4"), five, {.form = EvalForm::Plain, .device_ids = {0, 0, 0}});
+  } catch (const Error& e) {
+    got = e.code() == Errc::SingularShift && std::string(e.what()).rfind("shift 2: singular system", 0) == 0;
+  }
+  CHECK(got);
+}
+
+// ---- device-resident factors: DenseLu, TridiagFactor, ActionOperator reuse them across calls
+void test_resident_factors() {
+  DenseMatrix m = random_matrix(70, 7);
+  m.add_scaled_identity(12.0);
+  DenseLu lu(m);
+  DenseLu copy = lu;  // shares the device factors
+  DenseMatrix r1 = scaled_to_one_norm(random_matrix(70, 8), 1.0);
+  DenseMatrix x1 = lu.solve_matrix(r1), x2 = copy.solve_matrix(r1);
+  CHECK(rel_diff_1norm(x1, x2) == 0.0);
+  DenseMatrix back = m.mul(x1);
+  CHECK(rel_diff_1norm(back, r1) <= 1e-12);
+  std::vector<double> col(70);
+  for (int i = 0; i < 70; ++i) col[size_t(i)] = r1.at(i, 3);
+  std::vector<double> xc = lu.solve(col);
+  for (int i = 0; i < 70; ++i) CHECK(std::abs(xc[size_t(i)] - x1.at(i, 3)) <= 1e-13 * (1.0 + std::abs(x1.at(i, 3))));
+  TridiagMatrix t = random_tridiag(300, 9, 4.0);
+  TridiagFactor f(t);
+  std::vector<double> rhs(300);
+  NormalSampler ns(10);
+  for (auto& e : rhs) e = ns.next();
+  CHECK(f.solve(rhs) == thomas_solve(t, rhs));
+  CHECK(f.solve(rhs) == f.solve(rhs));
+  TridiagMatrix a = TridiagMatrix::trid121(300);
+  for (auto* band : {&a.sub, &a.diag, &a.super})
+    for (auto& e : *band) e *= -0.3;
+  ActionOperator op(catalog("R8"), a);
+  for (EvalForm form : {EvalForm::Residual, EvalForm::Plain}) {  // apply's opts.form may change per call
+    EvalOptions o{.form = form};
+    CHECK(op.apply(rhs, o) == action_eval(catalog("R8"), a, rhs, o));
+  }
+  std::vector<double> block(300 * 5);
+  for (auto& e : block) e = ns.next();
+  std::vector<double> ob = op.apply_block(block, 5, {.form = EvalForm::Residual});
+  CHECK(ob == substep_action_block(catalog("R8"), a, block, 5, 1, {.form = EvalForm::Residual}));
+}
+
 }  // namespace
 
 int main() {
@@ -384,6 +457,8 @@ int main() {
       {"thomas solve and factor reuse", test_thomas},
       {"pentadiagonal solve", test_pentadiag},
       {"tridiagonal action, operator, substeps", test_action},
+      {"multi-device evaluation (EvalOptions::devices / device_ids)", test_multi_device},
+      {"device-resident DenseLu / TridiagFactor / ActionOperator", test_resident_factors},
   };
   for (auto& [name, fn] : tests) {
     const int before = g_fail;

@@ -51,10 +51,18 @@ def test_context_create_fails_cleanly_without_gpu():
     assert rc == 11 and not h.value  # PF_ERR_CUDA, nothing allocated
 
 
-def test_host_library_exports_generators():
-    lib = C.CDLL(str(ROOT / "paper_2210_03714_b200" / "_lib" / "libparfrac_host.so"))
-    for name in ("pf_gen_randn", "pf_gen_uniform", "pf_gen_randn_batch"):
-        assert hasattr(lib, name)
+def test_generator_library_is_host_only():
+    """The input generators (used by the CPU reference arm) live in libparfrac_gen.so, which does not
+    link the CUDA engine; libparfrac_host.so (the C++ drop-in layer) exports them too."""
+    import subprocess
+
+    lib_dir = ROOT / "paper_2210_03714_b200" / "_lib"
+    for so in ("libparfrac_gen.so", "libparfrac_host.so"):
+        lib = C.CDLL(str(lib_dir / so))
+        for name in ("pf_gen_randn", "pf_gen_uniform", "pf_gen_randn_batch"):
+            assert hasattr(lib, name)
+    deps = subprocess.run(["ldd", str(lib_dir / "libparfrac_gen.so")], capture_output=True, text=True).stdout
+    assert "libpfb200" not in deps and "libcuda" not in deps and "libcudart" not in deps
 
 
 def test_api_fails_loudly_without_device():
