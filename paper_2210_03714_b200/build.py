@@ -26,6 +26,9 @@ INCLUDE = ROOT / "include"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills",
               "--expt-relaxed-constexpr", "-I" + str(INCLUDE), "-I" + str(CSRC)]
+# the exact method layer (Rational, moment solve, theta) runs on the GMP runtime, as the reference's
+# does; the image has libgmp.so.10 but no development symlink, so link it by soname
+GMP_LINK = "-l:libgmp.so.10"
 CXX_FLAGS = ["-O3", "-std=c++20", "-fPIC", "-ffp-contract=off", "-Wall", "-I" + str(INCLUDE), "-I" + str(CPP / "include")]
 
 
@@ -79,13 +82,15 @@ def build_host(verbose: bool = False) -> Path:
     LIB.mkdir(exist_ok=True)
     out = LIB / "libparfrac_host.so"
     srcs = sorted((CPP / "src").glob("*.cpp")) if (CPP / "src").exists() else []
+    srcs = [p for p in srcs if p.name not in GEN_SOURCES or p.name == "generators.cpp"]
     if not srcs:
         return out
-    hdrs = list((CPP / "include").rglob("*.hpp")) + [INCLUDE / "pf_b200.h"]
+    hdrs = list((CPP / "include").rglob("*.hpp")) + list((CPP / "src").glob("*.h*")) + \
+        list((CPP / "src").glob("*.inc")) + [INCLUDE / "pf_b200.h"]
     if _stale(out, srcs + hdrs + [LIB / "libpfb200.so"]):
         cxx = shutil.which("g++") or "g++"
         _run([cxx, *CXX_FLAGS, "-shared", "-o", str(out), *map(str, srcs), "-L" + str(LIB), "-lpfb200",
-              "-Wl,-rpath,$ORIGIN", "-lpthread"])
+              "-Wl,-rpath,$ORIGIN", GMP_LINK, "-lpthread"])
     return out
 
 
@@ -114,7 +119,7 @@ def build_cpp_tests(verbose: bool = False) -> Path:
     if _stale(out, deps):
         cxx = shutil.which("g++") or "g++"
         _run([cxx, *CXX_FLAGS, "-o", str(out), str(src), "-L" + str(LIB), "-lparfrac_host", "-lpfb200",
-              "-Wl,-rpath,$ORIGIN", "-lpthread"])
+              "-Wl,-rpath,$ORIGIN", GMP_LINK, "-lpthread"])
     return out
 
 

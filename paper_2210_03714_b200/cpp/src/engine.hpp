@@ -133,7 +133,7 @@ struct Packed {
     }
     for (auto* s : sets) {
       for (int k = 0; k < 3; ++k) poly.push_back(s->poly.size() == 3 ? to_double_nearest(s->poly[k]) : 0.0);
-      constant.push_back(to_double_nearest(s->constant));
+      constant.push_back(to_double_nearest(s->constant_term()));
     }
     m.n_terms = int(shifts.size());
     m.shifts = shifts.data();

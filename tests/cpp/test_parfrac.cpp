@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdio>
 #include <functional>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -16,6 +17,7 @@
 using namespace parfrac;
 
 static int g_fail = 0, g_checks = 0;
+static bool g_host_only = false;  // --host-only: the method layer only (no GPU needed)
 #define CHECK(cond)                                                         \
   do {                                                                      \
     ++g_checks;                                                             \
@@ -103,7 +105,7 @@ DenseMatrix host_eval(const FractionMethod& m, const DenseMatrix& b, EvalForm fo
       for (int j = 0; j < d; ++j) rhs.at(r, j) = rhs.at(r, j) / mm.at(r, r) * w;
     acc.axpy(1.0, rhs);
   }
-  if (form == EvalForm::Residual) acc.add_scaled_identity(to_double_nearest(m.constant));
+  if (form == EvalForm::Residual) acc.add_scaled_identity(to_double_nearest(m.constant_term()));
   return acc;
 }
 
@@ -247,14 +249,77 @@ void test_expm_and_friends() {
   CHECK(err <= 1e-11 * nrm);
 }
 
-void test_catalog() {  // test_methods.cpp:50-110 against the generated tables
-  CHECK(catalog("R4").weights[3].text == "-515/9");
-  CHECK(catalog("R8").weights[0].text == "-9979069/32256");
-  CHECK(catalog("R10star").poly[0].text == "-34244933704346617/14676708556800");
+void test_catalog() {  // test_methods.cpp:50-110: exact rationals, correctly rounded doubles
+  CHECK(to_fraction_string(catalog("R4").weights[3]) == "-515/9");
+  CHECK(to_fraction_string(catalog("R8").weights[0]) == "-9979069/32256");
+  CHECK(to_fraction_string(catalog("R10star").poly[0]) == "-34244933704346617/14676708556800");
   CHECK(catalog("R4").processors() == 4);
-  CHECK(catalog("R4").constant.text == "1");
+  CHECK(catalog("R4").constant_term() == Rational(1));
+  CHECK(to_double_nearest(catalog("R4").shifts[1]) == 0.2);
+  CHECK(to_double_nearest(catalog("R8").weights[5]) == -0x1.182875d1dc706p+11);  // SURVEY Appendix A hex
   CHECK_THROWS(catalog("R99"));
   CHECK(&catalog("R4") == &catalog("R4"));
+  // rational_from_string / to_double_nearest (test_rational.cpp:30-46)
+  CHECK(rational_from_string(" 6/4 ") == Rational(3, 2));
+  CHECK(rational_from_string("-2.5") == Rational(-5, 2));
+  CHECK_THROWS(rational_from_string("1/0"));
+  CHECK_THROWS(rational_from_string("abc"));
+  CHECK(to_double_nearest(Rational(1, 3)) == 1.0 / 3.0);
+  CHECK(to_double_nearest(Rational(-2, 3)) == -2.0 / 3.0);
+}
+
+// ---- f3: methods from any shift set, exactly (methods.cpp:95-186), and theta (bounds.cpp:97-254)
+void test_method_construction_and_theta() {
+  // the catalog sets rebuilt from their shifts by the moment solve (test_methods.cpp:50-110)
+  for (const char* name : {"R4", "R5", "R8", "R4_phi1"}) {
+    const FractionMethod& m = catalog(name);
+    FractionMethod b = build_plain(m.shifts, CoeffSeries(m.function), m.order, name);
+    bool same = b.weights.size() == m.weights.size();
+    for (size_t i = 0; same && i < b.weights.size(); ++i) same = b.weights[i] == m.weights[i];
+    CHECK(same);
+  }
+  // R10 / R10star: hybrids from their free weights
+  for (const char* name : {"R10", "R10star"}) {
+    const FractionMethod& m = catalog(name);
+    std::map<int, Rational> free;
+    free[9] = m.weights[8];
+    free[10] = m.weights[9];
+    FractionMethod h = build_hybrid(m.shifts, free, CoeffSeries(FunctionId::exp()), 10, name);
+    bool same = true;
+    for (size_t i = 0; i < m.weights.size(); ++i) same = same && h.weights[i] == m.weights[i];
+    for (size_t k = 0; k < 3; ++k) same = same && h.poly[k] == m.poly[k];
+    CHECK(same);
+  }
+  // phi1 weights on the R8 shifts = the derived table (frac8_template(5))
+  FractionMethod phi = build_plain(frac8_template().shift_pattern(Rational(5)), CoeffSeries(FunctionId::phi(1)), 8,
+                                   "R8_phi1");
+  const FractionMethod& tab = derived_set("R8_phi1set");
+  bool same = true;
+  for (size_t i = 0; i < tab.weights.size(); ++i) same = same && phi.weights[i] == tab.weights[i];
+  CHECK(same);
+  CHECK(phi.constant_term() == Rational(1));
+  // errors: duplicate shifts, wrong counts
+  std::vector<Rational> dup{Rational(0), Rational(1, 5), Rational(1, 5)};
+  CHECK_THROWS(build_plain(dup, CoeffSeries(FunctionId::exp()), 2, "dup"));
+  CHECK_THROWS(solve_weights(dup, CoeffSeries(FunctionId::exp()), 3));
+  // theta KATs (test_bounds.cpp:59-71) and the 2^-53 table
+  const double u24 = std::ldexp(1.0, -24), u53 = std::ldexp(1.0, -53);
+  CHECK(std::abs(theta_taylor(5, u24) - 0.186) <= 0.002);
+  CHECK(std::abs(theta_taylor(10, u24) - 1.073) <= 0.005);
+  CHECK(std::abs(theta(catalog("R5"), CoeffSeries(FunctionId::exp()), u24).theta - 0.298) <= 0.002);
+  CHECK(std::abs(theta(catalog("R10star"), CoeffSeries(FunctionId::exp()), u24).theta - 1.734) <= 0.005);
+  for (const char* name : {"R4", "R8", "R10"}) {
+    const double t = theta(catalog(name), CoeffSeries(FunctionId::exp()), u53).theta;
+    CHECK(std::abs(t - catalog(name).theta_u53) <= 2e-6 * t);
+  }
+  const double tp = theta(phi, CoeffSeries(FunctionId::phi(1)), u53).theta;
+  CHECK(std::abs(tp - tab.theta_u53) <= 2e-6 * tp);
+  // a method built here drives the evaluator like a catalog one (theta computed on demand)
+  FractionMethod r4b = build_plain(frac4_template().shift_pattern(Rational(5)), CoeffSeries(FunctionId::exp()), 4, "R4b");
+  CHECK(std::abs(theta_u53(r4b) - catalog("R4").theta_u53) <= 2e-6 * catalog("R4").theta_u53);
+  if (g_host_only) return;
+  DenseMatrix a = scaled_to_one_norm(random_matrix(40, 3), 1.5);
+  CHECK(rel_diff_1norm(expm(r4b, a), expm(catalog("R4"), a)) <= 1e-13);
 }
 
 // ---- banded action (proj/tests/test_action.cpp:49-188)
@@ -444,8 +509,13 @@ void test_resident_factors() {
 
 }  // namespace
 
-int main() {
-  const std::vector<std::pair<const char*, std::function<void()>>> tests = {
+int main(int argc, char** argv) {
+  g_host_only = argc > 1 && std::string(argv[1]) == "--host-only";
+  const std::vector<std::pair<const char*, std::function<void()>>> host_tests = {
+      {"catalog", test_catalog},
+      {"method construction (f3) and theta", test_method_construction_and_theta},
+  };
+  const std::vector<std::pair<const char*, std::function<void()>>> all_tests = {
       {"lu solve and singularity detection", test_lu_solve_and_singular},
       {"solve_shifted", test_solve_shifted},
       {"eval_dense on trivial and diagonal inputs", test_eval_dense_trivial_and_diagonal},
@@ -454,13 +524,14 @@ int main() {
       {"residual parity vs host reference", test_residual_parity_vs_host_reference},
       {"expm / phi1 / cos-sin / action", test_expm_and_friends},
       {"catalog", test_catalog},
+      {"method construction (f3) and theta", test_method_construction_and_theta},
       {"thomas solve and factor reuse", test_thomas},
       {"pentadiagonal solve", test_pentadiag},
       {"tridiagonal action, operator, substeps", test_action},
       {"multi-device evaluation (EvalOptions::devices / device_ids)", test_multi_device},
       {"device-resident DenseLu / TridiagFactor / ActionOperator", test_resident_factors},
   };
-  for (auto& [name, fn] : tests) {
+  for (auto& [name, fn] : g_host_only ? host_tests : all_tests) {
     const int before = g_fail;
     try {
       fn();

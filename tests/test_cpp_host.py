@@ -16,3 +16,17 @@ def test_cpp_parity_suite():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failures" in r.stdout
+
+
+def test_cpp_method_layer_on_host():
+    """The exact method layer of the C++ host (f3: Rational on GMP, solve_weights / build_plain /
+    build_hybrid, theta) needs no GPU: the same binary with --host-only."""
+    if not BIN.exists():  # g++ only (the CUDA engine library is already in the tree)
+        from paper_2210_03714_b200 import build
+
+        build.build_host()
+        build.build_cpp_tests()
+    r = subprocess.run([str(BIN), "--host-only"], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failures" in r.stdout and "PASS method construction (f3) and theta" in r.stdout
