@@ -493,6 +493,34 @@ def large_config_lines(peak, local, cores):
     return lines
 
 
+def time_cfg3_sharded(local, dist, steps: int = 3):
+    """cfg3 (exp + phi1 of one 4096^2, R8 shifts) with the s resolvents partitioned over the ranks
+    (parallel.expm_phi1_sharded: one NCCL reduce before the doubling, the doubling split by rows
+    with an all-gather per step -- f1). Every rank times the same evaluation; max over ranks."""
+    import torch
+    from paper_2210_03714_b200 import parallel as P, workloads as W
+
+    A = torch.from_numpy(W.cfg3()).cuda()
+    fn = lambda: P.expm_phi1_sharded(A, "R8", deterministic=False, distributed_doubling=True)  # noqa: E731
+    fn()
+    if dist:
+        dist.barrier()
+    stream = torch.cuda.current_stream()
+    ms, clk = timed_region(fn, steps, local, stream)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    del A
+    n = 4096
+    flops = 8 * (8 / 3) * n ** 3 + 8 * 2 * 2 * n ** 3
+    return {"config": "cfg3", "workload": "exp+phi1 of one 4096^2, R8 shifts partitioned over the ranks "
+                                          "(pairs, or single shifts when ranks > pairs), NCCL reduce, row-split "
+                                          "doubling with all-gathers", "value": 1e3 / ms, "unit": "evals/s",
+            "ms_per_eval": ms, "algorithmic_tflops": flops / (ms * 1e-3) / 1e12, "steps": steps, "clocks": clk,
+            "scaling": "strong"}
+
+
 def run_ours(args):
     import torch
 
@@ -545,6 +573,9 @@ def run_ours(args):
     del main["out"]
     if secondary is not None:
         del secondary["out"]
+    sharded = None
+    if not args.no_secondary:
+        sharded = time_cfg3_sharded(local, dist)
     large = None
     if rank == 0 and world == 1 and not args.no_secondary:
         del A
@@ -608,6 +639,8 @@ def run_ours(args):
                              "clocks": secondary["clocks"]}
     if large is not None:
         line["large_configs"] = large
+    if sharded is not None:
+        line["cfg3_shift_partitioned"] = sharded
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

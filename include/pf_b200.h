@@ -240,6 +240,12 @@ int pf_squarings_batched(pf_context* ctx, int n, int batch, const double* dA, in
 /* dOut = ((t_0 + t_1) + t_2) + ... elementwise, each add rounded: the ascending-shift reduction of
  * eval_dense (dense.cpp:245-246). dTerms is a HOST array of `count` device pointers. */
 int pf_ordered_sum(pf_context* ctx, int count, const double* const* dTerms, int64_t n_elems, double* dOut);
+/* Row block [r0, r0 + rows) of X + I (Y = X, plus 1 where r0 + i == j): E + I of a row-split phi1
+ * doubling step, rounded as pf_phi1_doubling forms it. */
+int pf_add_identity_rows(pf_context* ctx, int rows, int n, int r0, const double* dX, int64_t ldx, double* dY,
+                         int64_t ldy);
+/* dDiff = C - S and/or dSum = C + S over `count` doubles (the cos/sin step's (C - S)(C + S)). */
+int pf_sum_diff(pf_context* ctx, int64_t count, const double* dC, const double* dS, double* dDiff, double* dSum);
 /* E <- E^(2^j_b) per matrix (contiguous n x n batch). */
 int pf_square_chain(pf_context* ctx, int n, int batch, const int* dJ, double* dE);
 /* j_b steps of Phi <- 0.5 (E + I) Phi, E <- E E. */

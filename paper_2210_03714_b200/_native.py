@@ -106,6 +106,8 @@ SIGNATURES += [
     ("pf_tridiag_factor_create", C.c_int, [_VP, C.c_int, _VP, _VP, _VP, C.POINTER(PfStatus), C.POINTER(_VP)]),
     ("pf_tridiag_factor_solve", C.c_int, [_VP, C.c_int, _VP, _I64, _VP, _I64]),
     ("pf_tridiag_factor_destroy", C.c_int, [_VP]),
+    ("pf_add_identity_rows", C.c_int, [_VP, C.c_int, C.c_int, C.c_int, _VP, _I64, _VP, _I64]),
+    ("pf_sum_diff", C.c_int, [_VP, _I64, _VP, _VP, _VP, _VP]),
 ]
 PF_REC_NONE, PF_REC_EXP, PF_REC_EXP_PHI1 = 0, 1, 2
 

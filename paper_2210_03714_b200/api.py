@@ -709,14 +709,36 @@ def gemm(A: torch.Tensor, B: torch.Tensor, alpha: float = 1.0, beta: float = 0.0
     b3 = B if B.dim() == 3 else B.unsqueeze(0)
     bsz, m, k = a3.shape
     n = b3.shape[2]
-    if Cm is None:
-        Cm = torch.zeros(bsz, m, n, dtype=torch.float64, device=a3.device)
+    if Cm is None:  # beta == 0: the output is not read
+        Cm = (torch.empty if beta == 0.0 else torch.zeros)(bsz, m, n, dtype=torch.float64, device=a3.device)
     c3 = Cm if Cm.dim() == 3 else Cm.unsqueeze(0)
     rc = N.lib.pf_gemm_batched(eng.h, m, n, k, bsz, alpha, a3.data_ptr(), k, m * k, b3.data_ptr(), n, k * n, beta,
                                c3.data_ptr(), n, m * n, gamma)
     if rc:
         _raise(rc, N.PfStatus(), True)
     return Cm
+
+
+def add_identity_rows(X_rows: torch.Tensor, r0: int, out: torch.Tensor) -> torch.Tensor:
+    """out = rows [r0, r0 + R) of X + I, given those rows of X (pf_add_identity_rows)."""
+    eng = engine()
+    rows, n = X_rows.shape
+    rc = N.lib.pf_add_identity_rows(eng.h, rows, n, r0, X_rows.data_ptr(), X_rows.stride(0), out.data_ptr(),
+                                    out.stride(0))
+    if rc:
+        _raise(rc, N.PfStatus(), False)
+    return out
+
+
+def sum_diff(Cm: torch.Tensor, S: torch.Tensor, diff: Optional[torch.Tensor] = None,
+             total: Optional[torch.Tensor] = None):
+    """diff = C - S and/or total = C + S elementwise on the device (pf_sum_diff)."""
+    eng = engine()
+    rc = N.lib.pf_sum_diff(eng.h, Cm.numel(), Cm.data_ptr(), S.data_ptr(), diff.data_ptr() if diff is not None else None,
+                           total.data_ptr() if total is not None else None)
+    if rc:
+        _raise(rc, N.PfStatus(), False)
+    return diff, total
 
 
 # ---- f2: banded action (proj/core/src/action.cpp). A tridiagonal matrix is (sub, diag, super) with

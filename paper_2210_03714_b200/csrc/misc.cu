@@ -110,9 +110,28 @@ cudaError_t set_smem_attr_once(const void* fn, int bytes) {
 __global__ void sum_diff_kernel(int64_t count, const double* C, const double* S, double* D, double* E) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
     const double c = C[i], s = S[i];
-    D[i] = c - s;
-    E[i] = c + s;
+    if (D) D[i] = c - s;
+    if (E) E[i] = c + s;
   }
+}
+
+// rows [r0, r0 + rows) of X + I: y_ij = x_ij, plus 1.0 where r0 + i == j (scale_add_identity's
+// rounding for alpha = 1, diag = 1): one row block of the phi1 doubling's E + I
+__global__ void add_identity_rows_kernel(int rows, int n, int r0, const double* X, int64_t ldx, double* Y,
+                                         int64_t ldy) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)rows * n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / n), c = (int)(idx % n);
+    double v = X[(int64_t)r * ldx + c];
+    if (r0 + r == c) v = __dadd_rn(v, 1.0);
+    Y[(int64_t)r * ldy + c] = v;
+  }
+}
+
+void launch_add_identity_rows(int rows, int n, int r0, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                              cudaStream_t stream) {
+  const int64_t blocks = std::min<int64_t>(((int64_t)rows * n + 255) / 256, 4736);
+  add_identity_rows_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, stream>>>(rows, n, r0, X, ldx, Y, ldy);
 }
 
 void launch_sum_diff(int64_t count, const double* C, const double* S, double* D, double* E, cudaStream_t stream) {

@@ -92,6 +92,25 @@ int pf_squarings_batched(pf_context* ctx, int n, int batch, const double* dA, in
   return cuda_fail(cudaGetLastError());
 }
 
+int pf_add_identity_rows(pf_context* ctx, int rows, int n, int r0, const double* dX, int64_t ldx, double* dY,
+                         int64_t ldy) {
+  DeviceGuard device_guard(ctx);
+  if (!ctx || rows < 0 || n < 0 || r0 < 0 || ldx < n || ldy < n) return PF_ERR_BAD_ARGUMENT;
+  if (rows == 0 || n == 0) return PF_OK;
+  pf::launch_add_identity_rows(rows, n, r0, dX, ldx, dY, ldy, ctx->stream);
+  ctx->launches++;
+  return cuda_fail(cudaGetLastError());
+}
+
+int pf_sum_diff(pf_context* ctx, int64_t count, const double* dC, const double* dS, double* dDiff, double* dSum) {
+  DeviceGuard device_guard(ctx);
+  if (!ctx || count < 0 || (!dDiff && !dSum)) return PF_ERR_BAD_ARGUMENT;
+  if (count == 0) return PF_OK;
+  pf::launch_sum_diff(count, dC, dS, dDiff, dSum, ctx->stream);
+  ctx->launches++;
+  return cuda_fail(cudaGetLastError());
+}
+
 int pf_ordered_sum(pf_context* ctx, int count, const double* const* dTerms, int64_t n_elems, double* dOut) {
   DeviceGuard device_guard(ctx);
   if (!ctx || count < 1 || !dTerms || n_elems < 0 || !dOut) return PF_ERR_BAD_ARGUMENT;

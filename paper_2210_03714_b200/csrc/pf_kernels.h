@@ -88,7 +88,10 @@ void launch_scale_add_identity(int n, int batch, double alpha, const double* X, 
 // Y = ldexp(X, -j_b) per matrix (j from device array)
 void launch_ldexp_batched(int n, int batch, const double* X, int64_t ldx, int64_t strideX, const int* j, double* Y,
                           int64_t ldy, int64_t strideY, cudaStream_t stream);
-// D = C - S, E = C + S over `count` contiguous doubles
+// rows [r0, r0 + rows) of X + I (row block of the phi1 doubling's E + I)
+void launch_add_identity_rows(int rows, int n, int r0, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                              cudaStream_t stream);
+// D = C - S, E = C + S over `count` contiguous doubles (either output may be null)
 void launch_sum_diff(int64_t count, const double* C, const double* S, double* D, double* E, cudaStream_t stream);
 // squarings from norms: j_b = smallest j >= 0 with ldexp(norm_b, -j) <= theta
 void launch_squarings(int batch, const double* norms, double theta, int* j, cudaStream_t stream);

@@ -44,8 +44,10 @@ def term_indices(method: FractionMethod, form: int) -> List[int]:
     return [i for i, c in enumerate(method.shifts) if c != 0 or form == PLAIN]
 
 
-def term_units(method: FractionMethod, form: int) -> List[List[int]]:
-    """Partition units: (c, -c) shift pairs (residual form, every nonzero shift paired), else terms."""
+def term_units(method: FractionMethod, form: int, world: int = 1) -> List[List[int]]:
+    """Partition units: (c, -c) shift pairs (residual form, every nonzero shift paired) while there
+    are at least as many pairs as ranks, else single terms -- R8 (4 pairs) keeps 8 GPUs busy with one
+    shift each, the north_star's "one shift per GPU"."""
     terms = term_indices(method, form)
     sh = method.shift_doubles()
     if form == RESIDUAL and terms:
@@ -59,12 +61,14 @@ def term_units(method: FractionMethod, form: int) -> List[List[int]]:
             used.update((i, j))
             units.append([i, j])
         else:
-            return units
+            if len(units) >= world:
+                return units
     return [[i] for i in terms]
 
 
-def owned_terms(method: FractionMethod, form: int, rank: int, world: int) -> List[int]:
-    return sorted(i for u, unit in enumerate(term_units(method, form)) if u % world == rank for i in unit)
+def owned_terms(method: FractionMethod, form: int, rank: int, world: int, per_shift: bool = False) -> List[int]:
+    units = [[i] for i in term_indices(method, form)] if per_shift else term_units(method, form, world)
+    return sorted(i for u, unit in enumerate(units) if u % world == rank for i in unit)
 
 
 class CudaBackend:
@@ -88,51 +92,45 @@ class CudaBackend:
     def phi1_doubling(self, E, Phi, j):
         return self.api.phi1_doubling(E, Phi, j)
 
-    def square_rows(self, E, r0: int, r1: int):
-        """Rows [r0, r1) of E E (pf_square_chain's product)."""
-        return self.api.gemm(E[r0:r1].contiguous(), E)[0]
+    def square_rows(self, E, r0: int, r1: int, out=None):
+        """Rows [r0, r1) of E E (pf_square_chain's product), into `out` when given."""
+        return self.api.gemm(E[r0:r1], E, Cm=out)[0]
 
-    def cossin_step_rows(self, Cm, S, r0: int, r1: int):
+    def cossin_step_rows(self, Cm, S, r0: int, r1: int, out_c=None, out_s=None, scratch=None):
         """Rows [r0, r1) of one cos/sin double-angle step as pf_cossin_doubling forms it:
-        (C - S)(C + S) and 2 S C."""
-        D = Cm[r0:r1] - S[r0:r1]
-        E = Cm + S
-        return self.api.gemm(D.contiguous(), E)[0], self.api.gemm(S[r0:r1].contiguous(), Cm, alpha=2.0)[0]
+        (C - S)(C + S) and 2 S C, the differences / sums by pf_sum_diff (no eager tensor math)."""
+        if scratch is None:
+            scratch = (torch.empty_like(Cm[r0:r1]), torch.empty_like(Cm))
+        D, E = scratch
+        self.api.sum_diff(Cm[r0:r1], S[r0:r1], diff=D)
+        self.api.sum_diff(Cm, S, total=E)
+        return self.api.gemm(D, E, Cm=out_c)[0], self.api.gemm(S[r0:r1], Cm, alpha=2.0, Cm=out_s)[0]
 
-    def phi1_step_rows(self, E, Phi, r0: int, r1: int):
+    def phi1_step_rows(self, E, Phi, r0: int, r1: int, out_e=None, out_p=None, scratch=None):
         """Rows [r0, r1) of one doubling step, as pf_phi1_doubling computes them: T = E + I (the
-        diagonal by a rounded add), 0.5 (T Phi) and E E on the DMMA GEMM."""
-        T = E[r0:r1].clone()
-        idx = torch.arange(r1 - r0, device=E.device)
-        T[idx, r0 + idx] += 1.0
-        return self.api.gemm(E[r0:r1].contiguous(), E)[0], self.api.gemm(T, Phi, alpha=0.5)[0]
+        diagonal by a rounded add, pf_add_identity_rows), 0.5 (T Phi) and E E on the DMMA GEMM."""
+        T = scratch if scratch is not None else torch.empty_like(E[r0:r1])
+        self.api.add_identity_rows(E[r0:r1], r0, T)
+        return self.api.gemm(E[r0:r1], E, Cm=out_e)[0], self.api.gemm(T, Phi, alpha=0.5, Cm=out_p)[0]
 
 
-def _gather_terms(local_idx: List[int], local_terms: torch.Tensor, group, world) -> Tuple[List[int], List[torch.Tensor]]:
-    """all_gather of variable-count term stacks (padded to the largest count with index -1);
-    returns every rank's terms sorted by shift index."""
-    dev = local_terms.device
-    cnt = torch.tensor([len(local_idx)], dtype=torch.int64, device=dev)
-    cnts = [torch.zeros_like(cnt) for _ in range(world)]
-    dist.all_gather(cnts, cnt, group=group)
-    mx = max(int(c.item()) for c in cnts)
+def _gather_terms_to_root(method: FractionMethod, form: int, local_terms: torch.Tensor, group, world: int, rank: int,
+                          root: int, per_shift: bool = True) -> Tuple[List[int], List[torch.Tensor]]:
+    """Every rank's weighted terms to `root` only (torch.distributed.gather: NCCL send/recv on GPUs):
+    the partition is known on every rank, so the root knows whose stack holds which shift index.
+    Returns (shift indices, terms) in ascending index on the root, ([], []) elsewhere."""
+    owners = [owned_terms(method, form, r, world, per_shift) for r in range(world)]
+    mx = max(len(o) for o in owners)
     shape = tuple(local_terms.shape[1:])
-    pad_t = torch.zeros((mx,) + shape, dtype=local_terms.dtype, device=dev)
-    if local_idx:
-        pad_t[: len(local_idx)] = local_terms
-    pad_i = torch.full((mx,), -1, dtype=torch.int64, device=dev)
-    if local_idx:
-        pad_i[: len(local_idx)] = torch.tensor(local_idx, dtype=torch.int64, device=dev)
-    all_t = [torch.empty_like(pad_t) for _ in range(world)]
-    all_i = [torch.empty_like(pad_i) for _ in range(world)]
-    dist.all_gather(all_t, pad_t, group=group)
-    dist.all_gather(all_i, pad_i, group=group)
-    pairs = []
-    for ti, tt in zip(all_i, all_t):
-        for q in range(mx):
-            k = int(ti[q].item())
-            if k >= 0:
-                pairs.append((k, tt[q]))
+    pad = local_terms
+    if local_terms.shape[0] < mx:
+        pad = torch.empty((mx,) + shape, dtype=local_terms.dtype, device=local_terms.device)
+        pad[: local_terms.shape[0]] = local_terms
+    gathered = [torch.empty_like(pad) for _ in range(world)] if rank == root else None
+    dist.gather(pad.contiguous(), gathered, dst=root, group=group)
+    if rank != root:
+        return [], []
+    pairs = [(owners[r][q], gathered[r][q]) for r in range(world) for q in range(len(owners[r]))]
     pairs.sort(key=lambda p: p[0])
     return [p[0] for p in pairs], [p[1] for p in pairs]
 
@@ -157,7 +155,7 @@ def eval_sets_sharded(A: torch.Tensor, j, method: FractionMethod, extra_sets: Se
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     sets = [method] + list(extra_sets)
-    mine = owned_terms(method, form, rank, world)
+    mine = owned_terms(method, form, rank, world, per_shift=deterministic)
     sh = method.shift_doubles()
     constants = _constants(sets, form)
     poly = _poly(sets)
@@ -176,7 +174,7 @@ def eval_sets_sharded(A: torch.Tensor, j, method: FractionMethod, extra_sets: Se
             lt = torch.stack(local[s_i]) if local[s_i] else torch.zeros((0,) + tuple(A.shape), dtype=A.dtype,
                                                                          device=A.device)
             if world > 1:
-                idx, terms = _gather_terms(mine, lt, group, world)
+                idx, terms = _gather_terms_to_root(method, form, lt, group, world, rank, root)
             else:
                 idx, terms = mine, list(lt)
             if rank != root:
@@ -202,35 +200,15 @@ def eval_sets_sharded(A: torch.Tensor, j, method: FractionMethod, extra_sets: Se
     return out if rank == root else None
 
 
-def _allgather_rows(block: torch.Tensor, n: int, rows: int, group, world: int) -> torch.Tensor:
-    """Every rank's row block (the last one padded to `rows`) -> the full n x n matrix."""
-    pad = block
+def _allgather_rows(block: torch.Tensor, n: int, rows: int, group, world: int, buf: torch.Tensor) -> torch.Tensor:
+    """Every rank's row block (the last one padded to `rows`) gathered into the preallocated
+    (world * rows) x n buffer `buf` (one all_gather_into_tensor); returns its first n rows."""
     if block.shape[0] < rows:
         pad = torch.zeros((rows,) + tuple(block.shape[1:]), dtype=block.dtype, device=block.device)
         pad[: block.shape[0]] = block
-    parts = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(parts, pad.contiguous(), group=group)
-    return torch.cat(parts, 0)[:n].contiguous()
-
-
-def phi1_doubling_distributed(E: torch.Tensor, Phi: torch.Tensor, j: int, group=None, backend=None):
-    """f1: Phi <- 0.5 (E + I) Phi, E <- E E, j times, every product split by rows over the ranks of
-    `group` with one all-gather of each row block per step. E and Phi must be replicated on entry;
-    they are replicated on exit, bit-identical to the single-process recurrence."""
-    backend = backend or CudaBackend()
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
-    n = E.shape[0]
-    rows = -(-n // world)
-    r0, r1 = min(n, rank * rows), min(n, (rank + 1) * rows)
-    for _ in range(int(j)):
-        e_r, p_r = backend.phi1_step_rows(E, Phi, r0, r1)
-        if world > 1:
-            E = _allgather_rows(e_r, n, rows, group, world)
-            Phi = _allgather_rows(p_r, n, rows, group, world)
-        else:
-            E, Phi = e_r, p_r
-    return E, Phi
+        block = pad
+    dist.all_gather_into_tensor(buf, block.contiguous(), group=group)
+    return buf[:n]
 
 
 def _row_range(n: int, group):
@@ -240,16 +218,44 @@ def _row_range(n: int, group):
     return world, rows, min(n, rank * rows), min(n, (rank + 1) * rows)
 
 
+def phi1_doubling_distributed(E: torch.Tensor, Phi: torch.Tensor, j: int, group=None, backend=None):
+    """f1: Phi <- 0.5 (E + I) Phi, E <- E E, j times, every product split by rows over the ranks of
+    `group` with one all-gather of each row block per step into preallocated buffers. E and Phi must
+    be replicated on entry; they are replicated on exit, bit-identical to the single-process recurrence."""
+    backend = backend or CudaBackend()
+    n = E.shape[0]
+    world, rows, r0, r1 = _row_range(n, group)
+    if world == 1:
+        for _ in range(int(j)):
+            E, Phi = backend.phi1_step_rows(E, Phi, 0, n)
+        return E, Phi
+    # double-buffered full matrices and the local row blocks, allocated once
+    bufs_e = [torch.empty((world * rows, n), dtype=E.dtype, device=E.device) for _ in range(2)]
+    bufs_p = [torch.empty_like(bufs_e[0]) for _ in range(2)]
+    e_r, p_r, t_r = (torch.empty((r1 - r0, n), dtype=E.dtype, device=E.device) for _ in range(3))
+    for s in range(int(j)):
+        e_b, p_b = backend.phi1_step_rows(E, Phi, r0, r1, out_e=e_r, out_p=p_r, scratch=t_r)
+        E = _allgather_rows(e_b, n, rows, group, world, bufs_e[s % 2])
+        Phi = _allgather_rows(p_b, n, rows, group, world, bufs_p[s % 2])
+    return E.contiguous(), Phi.contiguous()
+
+
 def square_chain_distributed(E: torch.Tensor, j: int, group=None, backend=None):
     """f1 for expm: E <- E E, j times, each product split by rows over the ranks of `group` with an
     all-gather per step; bit-identical to the single-process chain (pf_square_chain)."""
     backend = backend or CudaBackend()
     n = E.shape[0]
     world, rows, r0, r1 = _row_range(n, group)
-    for _ in range(int(j)):
-        e_r = backend.square_rows(E, r0, r1)
-        E = _allgather_rows(e_r, n, rows, group, world) if world > 1 else e_r
-    return E
+    if world == 1:
+        for _ in range(int(j)):
+            E = backend.square_rows(E, 0, n)
+        return E
+    bufs = [torch.empty((world * rows, n), dtype=E.dtype, device=E.device) for _ in range(2)]
+    e_r = torch.empty((r1 - r0, n), dtype=E.dtype, device=E.device)
+    for s in range(int(j)):
+        e_b = backend.square_rows(E, r0, r1, out=e_r)
+        E = _allgather_rows(e_b, n, rows, group, world, bufs[s % 2])
+    return E.contiguous()
 
 
 def cossin_doubling_distributed(Cm: torch.Tensor, S: torch.Tensor, j: int, group=None, backend=None):
@@ -258,14 +264,19 @@ def cossin_doubling_distributed(Cm: torch.Tensor, S: torch.Tensor, j: int, group
     backend = backend or CudaBackend()
     n = Cm.shape[0]
     world, rows, r0, r1 = _row_range(n, group)
-    for _ in range(int(j)):
-        c_r, s_r = backend.cossin_step_rows(Cm, S, r0, r1)
-        if world > 1:
-            Cm = _allgather_rows(c_r, n, rows, group, world)
-            S = _allgather_rows(s_r, n, rows, group, world)
-        else:
-            Cm, S = c_r, s_r
-    return Cm, S
+    if world == 1:
+        for _ in range(int(j)):
+            Cm, S = backend.cossin_step_rows(Cm, S, 0, n)
+        return Cm, S
+    bufs_c = [torch.empty((world * rows, n), dtype=Cm.dtype, device=Cm.device) for _ in range(2)]
+    bufs_s = [torch.empty_like(bufs_c[0]) for _ in range(2)]
+    c_r, s_r, d_r = (torch.empty((r1 - r0, n), dtype=Cm.dtype, device=Cm.device) for _ in range(3))
+    e_full = torch.empty_like(Cm)
+    for s in range(int(j)):
+        c_b, s_b = backend.cossin_step_rows(Cm, S, r0, r1, out_c=c_r, out_s=s_r, scratch=(d_r, e_full))
+        Cm = _allgather_rows(c_b, n, rows, group, world, bufs_c[s % 2])
+        S = _allgather_rows(s_b, n, rows, group, world, bufs_s[s % 2])
+    return Cm.contiguous(), S.contiguous()
 
 
 def expm_phi1_sharded(A: torch.Tensor, method="R8", deterministic: bool = True, group=None, root: int = 0,
@@ -306,20 +317,24 @@ def action_sharded(A: torch.Tensor, V: torch.Tensor, method="R8", substeps: int 
     m = catalog(method) if isinstance(method, str) else method
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    mine = owned_terms(m, form, rank, world)
+    mine = owned_terms(m, form, rank, world, per_shift=deterministic)
     op = operator_factory(A, m, substeps, form, owned=mine)
     X = V.reshape(V.shape[0], -1).contiguous()
     for _ in range(substeps):
         if deterministic:
+            # every weighted term to rank 0 only, the ascending-shift sum there, the next iterate to all
             _, terms = op.apply(X, include_poly=True, with_terms=True)
             nloc = op.terms
             local = terms[:nloc]
             if world > 1:
-                _, gathered = _gather_terms(mine, local, group, world)
+                _, gathered = _gather_terms_to_root(m, form, local, group, world, rank, 0)
             else:
                 gathered = list(local)
-            ts = list(gathered) + [terms[nloc + q] for q in range(op.poly_terms)]
-            X = ordered_sum(ts) if len(ts) > 1 else ts[0].clone()
+            if rank == 0:
+                ts = list(gathered) + [terms[nloc + q] for q in range(op.poly_terms)]
+                X = ordered_sum(ts) if len(ts) > 1 else ts[0].clone()
+            if world > 1:
+                dist.broadcast(X, src=0, group=group)
         else:
             part = op.apply(X, include_poly=(rank == 0))
             if world > 1:

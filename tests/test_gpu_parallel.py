@@ -24,7 +24,7 @@ def _a(n, seed, norm):
 
 
 @pytest.mark.parametrize("n", [100, 128, 200])
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_emulated_shift_partition_is_bit_identical(dev, n, world):
     from paper_2210_03714_b200 import methods as M, parallel as P
 

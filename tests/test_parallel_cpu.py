@@ -42,11 +42,11 @@ class OracleBackend:
     def phi1_doubling(self, E, Phi, j):
         return E, Phi
 
-    def square_rows(self, E, r0, r1):
+    def square_rows(self, E, r0, r1, **kw):
         e = E.numpy()
         return torch.from_numpy(self.O.mul_rows(e[r0:r1], e))
 
-    def phi1_step_rows(self, E, Phi, r0, r1):
+    def phi1_step_rows(self, E, Phi, r0, r1, **kw):
         O = self.O
         e, ph = E.numpy(), Phi.numpy()
         T = e[r0:r1].copy()
@@ -187,13 +187,22 @@ def test_term_partition():
     # plain form: single terms (the zero shift is a term)
     assert P.term_units(m, M.PLAIN) == [[i] for i in range(9)]
     assert P.owned_terms(m, M.PLAIN, 0, 3) == [0, 3, 6]
+    # more ranks than pairs: single shifts, so R8 keeps 8 GPUs busy (one shift each); 4 ranks: pairs
+    assert P.term_units(m, M.RESIDUAL, 8) == [[i] for i in range(1, 9)]
+    assert [P.owned_terms(m, M.RESIDUAL, r, 8) for r in range(8)] == [[i] for i in range(1, 9)]
+    assert [P.owned_terms(m, M.RESIDUAL, r, 4) for r in range(4)] == [[1, 2], [3, 4], [5, 6], [7, 8]]
+    # deterministic mode: one shift per unit regardless of the pairing
+    assert P.owned_terms(m, M.RESIDUAL, 0, 3, per_shift=True) == [1, 4, 7]
 
 
-def test_sharded_eval_deterministic_is_bit_identical():
+@pytest.mark.parametrize("world", [2, 5])
+def test_sharded_eval_deterministic_is_bit_identical(world):
+    """world 5 > 4 pairs: single shifts per rank; the root-only gather + ascending sum still equals
+    the single-process evaluation bit for bit."""
     from oracle import oracle as O
     from paper_2210_03714_b200 import workloads as W
 
-    e2 = _run("eval_det", 2)
+    e2 = _run("eval_det", world)
     m = M.catalog("R8")
     phi = M.same_shift_method(m, M.FunctionId.phi(1))
     a = W.scaled_to_one_norm(W.randn_matrix(24, 3), 3.0)
@@ -202,11 +211,12 @@ def test_sharded_eval_deterministic_is_bit_identical():
     assert np.array_equal(e2[0], ref[0]) and np.array_equal(e2[1], ref[1])
 
 
-def test_sharded_eval_fast_agrees():
+@pytest.mark.parametrize("world", [2, 5])
+def test_sharded_eval_fast_agrees(world):
     from oracle import oracle as O
     from paper_2210_03714_b200 import workloads as W
 
-    e2 = _run("eval_fast", 2)
+    e2 = _run("eval_fast", world)
     m = M.catalog("R8")
     phi = M.same_shift_method(m, M.FunctionId.phi(1))
     a = W.scaled_to_one_norm(W.randn_matrix(24, 3), 3.0)
