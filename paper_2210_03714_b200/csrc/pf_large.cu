@@ -402,6 +402,66 @@ struct FactorResult {
 
 constexpr int kDeclined = -1000;  // pair mode declined: the caller takes the per-shift path
 
+// ---- blocked partial pivoting (DenseLu, dense.cpp:102-133) for the systems the certificate rejects
+// Recursive column split (rows always to the bottom): LU(left half) with pivoting over all rows below,
+// its swaps applied to the right half (laswp), U12 = L11^-1 A12 (DMMA TRSM with 64-block inverses),
+// A22 -= A21 U12 (DMMA GEMM), LU(right half), its swaps applied back to the left half. 64-wide leaves
+// are factored by pivot_lu.cu's cluster kernel (pivot search, exchanges and rank-1 updates in
+// distributed shared memory). Pivots follow the reference's rule on the blocked values: bit-identical
+// to dense.cpp's wherever pivots are well separated (the blocked update rounds differently).
+void rlu_pivot(pf_context* ctx, const Sys& sp, int off, int w, int* piv, const double* d_tol, const int* zorig,
+               int* failed) {
+  if (w <= kB) {
+    pf::launch_panel_lu(sp.M, sp.np, sp.stride(), sp.np, off, w, sp.nsys, piv, sp.np, d_tol, zorig, failed,
+                        ctx->status, ctx->first_error, ctx->stream);
+    ctx->launches++;
+    lu_base(ctx, sp, sp.nsys, off, 0, nullptr);  // the leaf's L and U block inverses (for the TRSMs)
+    return;
+  }
+  const int w1 = half64(w), w2 = w - w1;
+  const int64_t ld = sp.np, st = sp.stride();
+  rlu_pivot(ctx, sp, off, w1, piv, d_tol, zorig, failed);
+  pf::launch_laswp(sp.M, ld, st, piv, sp.np, off, off + w1, off + w1, off + w, sp.nsys, failed, ctx->stream);
+  ctx->launches++;
+  double* A12 = sp.M + (int64_t)off * ld + off + w1;
+  double* A21 = sp.M + (int64_t)(off + w1) * ld + off;
+  double* A22 = sp.M + (int64_t)(off + w1) * ld + off + w1;
+  trsm_left_lower(ctx, sp, off, w1, A12, ld, st, w2);
+  gemm(ctx, sp.np - off - w1, w2, w1, sp.nsys, -1.0, A21, ld, st, A12, ld, st, 1.0, A22, ld, st, 0.0);
+  rlu_pivot(ctx, sp, off + w1, w2, piv, d_tol, zorig, failed);
+  pf::launch_laswp(sp.M, ld, st, piv, sp.np, off + w1, off + w, off, off + w1, sp.nsys, failed, ctx->stream);
+  ctx->launches++;
+}
+
+// the nf = fails.size() failing systems: gathered into `side` when they are a subset (the caller
+// already parked their matrices there), factored, scattered back with their swap sequences
+int pivoted_blocked_lu(pf_context* ctx, const Sys& s, int n, const std::vector<int>& fails, double* side,
+                       const std::vector<double>& tol_all, const int* d_fail, int* d_piv) {
+  const int nf = (int)fails.size();
+  Sys sp = s;
+  sp.nsys = nf;
+  if (side) sp.M = side;
+  double* inv_g = side ? static_cast<double*>(workspace(ctx, kWsLargeX2 + 2, sizeof(double) * s.inv_stride * nf))
+                       : s.inv;
+  int* piv_g = static_cast<int*>(workspace(ctx, kWsSmallArrays + 24, sizeof(int) * (size_t)s.np * nf * 2));
+  if (!inv_g || !piv_g) return PF_ERR_CUDA;
+  sp.inv = inv_g;
+  int* failed = piv_g + (size_t)s.np * nf;
+  cudaMemsetAsync(failed, 0, sizeof(int) * nf, ctx->stream);
+  std::vector<double> tol(nf);
+  for (int q = 0; q < nf; ++q) tol[q] = tol_all[fails[q]];
+  double* d_tol = upload(ctx, kWsSmallArrays + 25, tol);
+  rlu_pivot(ctx, sp, 0, s.np, piv_g, d_tol, d_fail, failed);
+  for (int q = 0; q < nf; ++q) {
+    if (side)
+      cudaMemcpyAsync(s.M + fails[q] * s.stride(), side + q * s.stride(), sizeof(double) * s.stride(),
+                      cudaMemcpyDeviceToDevice, ctx->stream);
+    cudaMemcpyAsync(d_piv + (size_t)fails[q] * n, piv_g + (size_t)q * s.np, sizeof(int) * n, cudaMemcpyDeviceToDevice,
+                    ctx->stream);
+  }
+  return cuda_fail(cudaGetLastError());
+}
+
 FactorResult factor_systems(pf_context* ctx, const Sys& s, int n, unsigned long long* d_mx, int flags,
                             int* d_piv, int* d_perm, double pivot_rel_tol, bool decline = false) {
   FactorResult fr;
@@ -479,9 +539,18 @@ FactorResult factor_systems(pf_context* ctx, const Sys& s, int n, unsigned long 
     fr.rc = rc;
     return fr;
   }
-  lu_pivot_kernel<<<nf, 1024, 0, ctx->stream>>>(s.M, s.np, s.stride(), n, d_piv, d_tol, ctx->status,
-                                                ctx->first_error, d_fail);
-  ctx->launches++;
+  static const bool unblocked = std::getenv("PF_PIVOT_UNBLOCKED") != nullptr;  // A/B: the old fallback
+  if (unblocked) {
+    lu_pivot_kernel<<<nf, 1024, 0, ctx->stream>>>(s.M, s.np, s.stride(), n, d_piv, d_tol, ctx->status,
+                                                  ctx->first_error, d_fail);
+    ctx->launches++;
+  } else {
+    rc = pivoted_blocked_lu(ctx, s, n, fails, side, tol, d_fail, d_piv);
+    if (rc) {
+      fr.rc = rc;
+      return fr;
+    }
+  }
   pf_status ps;
   rc = collect_status(ctx, s.nsys, 0, &ps);
   if (rc) {

@@ -244,3 +244,47 @@ def test_lu_graph_replay_is_bitwise(dev, tmp_path):
     L = torch.tril(outs[2], -1) + torch.eye(n, dtype=torch.float64, device="cuda")
     U = torch.triu(outs[2])
     assert float((L @ U - src).abs().max()) < 1e-12
+
+
+# ------------------------------------------------------------------ blocked partial pivoting (a3, n > 128)
+
+
+@pytest.mark.parametrize("n", [200, 333, 512, 2048])
+def test_blocked_pivoting_lu_pivots_match_reference(dev, oracle, n):
+    """Non-dominant systems (the certificate rejects them) run the blocked partial-pivoting LU:
+    64-wide panels factored in a thread-block cluster's shared memory, DMMA TRSM / GEMM for the
+    rest. Pivots equal the reference's (dense.cpp:105-115 rule) on these inputs, whose pivots are
+    well separated; factors and solves agree to rounding."""
+    from paper_2210_03714_b200 import workloads as W
+
+    b = W.randn_matrix(n, 7000 + n) / np.sqrt(n)
+    mm = np.eye(n) - 3.0 * b  # far from diagonally dominant: genuine row exchanges
+    LU, piv = dev.DenseLu(mm).factors()
+    rlu, rpiv = oracle.lu(mm)
+    assert np.array_equal(piv, rpiv)
+    assert (rpiv != np.arange(n)).sum() > n // 2
+    assert oracle.rel_diff_1norm(LU, rlu) <= 1e-11
+    rhs = W.randn(7, n * 5).reshape(n, 5)
+    x = dev.DenseLu(mm).solve_matrix(rhs)
+    want = np.linalg.solve(mm, rhs)
+    assert np.abs(x - want).max() <= 1e-10 * np.abs(want).max()
+
+
+def test_blocked_pivoting_batch_and_singular_column(dev):
+    """A batch mixing a certified system, pivoting systems and a singular one: the singular system
+    reports SingularShift at the reference's column; the others factor."""
+    from paper_2210_03714_b200 import workloads as W
+    from paper_2210_03714_b200.errors import Errc, PfError
+
+    n = 400
+    good = np.eye(n) + 0.01 * W.randn_matrix(n, 1) / np.sqrt(n)
+    piv1 = np.eye(n) - 3.0 * W.randn_matrix(n, 2) / np.sqrt(n)
+    sing = np.eye(n) - 3.0 * W.randn_matrix(n, 3) / np.sqrt(n)
+    sing[:, 257] = 0.0  # column 257 vanishes: best pivot 0 there
+    for mm in (good, piv1):
+        LU, piv = dev.DenseLu(mm).factors()
+        assert np.isfinite(LU).all()
+    with pytest.raises(PfError) as e:
+        dev.DenseLu(np.stack([good, piv1, sing]))
+    assert e.value.code == Errc.SingularShift
+    assert "at column 257 " in str(e.value) and "matrix 2" in str(e.value)
