@@ -78,14 +78,12 @@ struct GemmParams {
 void launch_gemm(const GemmParams& p, cudaStream_t stream);
 
 // Partial-pivoting panel of the blocked large LU (pivot_lu.cu): rows [off, np) x columns [off, off+w)
-// of each of nsys systems, pivots into piv[z * npiv + col]; SingularShift below tol[z] is recorded for
+// of each of nsys systems, pivots into piv[z * npiv + col]; the panel's row exchanges are then applied
+// to every other column (moves: 2 * 64 int2 per system). SingularShift below tol[z] is recorded for
 // system zorig[z] and marks failed[z] (later panels skip it).
 cudaError_t launch_panel_lu(double* M, int64_t ld, int64_t strideM, int np, int off, int w, int nsys, int* piv,
                             int npiv, const double* tol, const int* zorig, int* failed, DevStatus* status,
-                            int* first_error, cudaStream_t stream);
-// swaps k0..k1-1 of every system's sequence applied to columns [c0, c1) (LAPACK laswp)
-void launch_laswp(double* M, int64_t ld, int64_t strideM, const int* piv, int npiv, int k0, int k1, int c0, int c1,
-                  int nsys, const int* failed, cudaStream_t stream);
+                            int* first_error, int2* moves, int* moves_n, cudaStream_t stream);
 
 // Batched 1-norm (column sums in ascending row order, then max).
 void launch_one_norm(int n, int batch, const double* A, int64_t lda, int64_t strideA, double* out,

@@ -404,33 +404,37 @@ constexpr int kDeclined = -1000;  // pair mode declined: the caller takes the pe
 
 // ---- blocked partial pivoting (DenseLu, dense.cpp:102-133) for the systems the certificate rejects
 // Recursive column split (rows always to the bottom): LU(left half) with pivoting over all rows below,
-// its swaps applied to the right half (laswp), U12 = L11^-1 A12 (DMMA TRSM with 64-block inverses),
-// A22 -= A21 U12 (DMMA GEMM), LU(right half), its swaps applied back to the left half. 64-wide leaves
-// are factored by pivot_lu.cu's cluster kernel (pivot search, exchanges and rank-1 updates in
-// distributed shared memory). Pivots follow the reference's rule on the blocked values: bit-identical
-// to dense.cpp's wherever pivots are well separated (the blocked update rounds differently).
-void rlu_pivot(pf_context* ctx, const Sys& sp, int off, int w, int* piv, const double* d_tol, const int* zorig,
-               int* failed) {
+// U12 = L11^-1 A12 (DMMA TRSM with 64-block inverses), A22 -= A21 U12 (DMMA GEMM), LU(right half).
+// Each 64-wide leaf is factored by pivot_lu.cu's cluster kernel (pivot search and rank-1 updates in
+// distributed shared memory) and its row exchanges are applied to the whole rows right after, so the
+// matrix always has the reference's row order. Pivots follow the reference's rule on the blocked
+// values: equal to dense.cpp's wherever pivots are well separated (the blocked updates round differently).
+struct PivotScratch {
+  int* piv;
+  const double* tol;
+  const int* zorig;
+  int* failed;
+  int2* moves;
+  int* moves_n;
+};
+
+void rlu_pivot(pf_context* ctx, const Sys& sp, int off, int w, const PivotScratch& ps) {
   if (w <= kB) {
-    pf::launch_panel_lu(sp.M, sp.np, sp.stride(), sp.np, off, w, sp.nsys, piv, sp.np, d_tol, zorig, failed,
-                        ctx->status, ctx->first_error, ctx->stream);
-    ctx->launches++;
+    pf::launch_panel_lu(sp.M, sp.np, sp.stride(), sp.np, off, w, sp.nsys, ps.piv, sp.np, ps.tol, ps.zorig, ps.failed,
+                        ctx->status, ctx->first_error, ps.moves, ps.moves_n, ctx->stream);
+    ctx->launches += 2;
     lu_base(ctx, sp, sp.nsys, off, 0, nullptr);  // the leaf's L and U block inverses (for the TRSMs)
     return;
   }
   const int w1 = half64(w), w2 = w - w1;
   const int64_t ld = sp.np, st = sp.stride();
-  rlu_pivot(ctx, sp, off, w1, piv, d_tol, zorig, failed);
-  pf::launch_laswp(sp.M, ld, st, piv, sp.np, off, off + w1, off + w1, off + w, sp.nsys, failed, ctx->stream);
-  ctx->launches++;
+  rlu_pivot(ctx, sp, off, w1, ps);
   double* A12 = sp.M + (int64_t)off * ld + off + w1;
   double* A21 = sp.M + (int64_t)(off + w1) * ld + off;
   double* A22 = sp.M + (int64_t)(off + w1) * ld + off + w1;
   trsm_left_lower(ctx, sp, off, w1, A12, ld, st, w2);
   gemm(ctx, sp.np - off - w1, w2, w1, sp.nsys, -1.0, A21, ld, st, A12, ld, st, 1.0, A22, ld, st, 0.0);
-  rlu_pivot(ctx, sp, off + w1, w2, piv, d_tol, zorig, failed);
-  pf::launch_laswp(sp.M, ld, st, piv, sp.np, off + w1, off + w, off, off + w1, sp.nsys, failed, ctx->stream);
-  ctx->launches++;
+  rlu_pivot(ctx, sp, off + w1, w2, ps);
 }
 
 // the nf = fails.size() failing systems: gathered into `side` when they are a subset (the caller
@@ -443,15 +447,18 @@ int pivoted_blocked_lu(pf_context* ctx, const Sys& s, int n, const std::vector<i
   if (side) sp.M = side;
   double* inv_g = side ? static_cast<double*>(workspace(ctx, kWsLargeX2 + 2, sizeof(double) * s.inv_stride * nf))
                        : s.inv;
-  int* piv_g = static_cast<int*>(workspace(ctx, kWsSmallArrays + 24, sizeof(int) * (size_t)s.np * nf * 2));
-  if (!inv_g || !piv_g) return PF_ERR_CUDA;
+  int* piv_g = static_cast<int*>(workspace(ctx, kWsSmallArrays + 24, sizeof(int) * ((size_t)s.np + 1) * nf));
+  int2* moves = static_cast<int2*>(workspace(ctx, kWsSmallArrays + 26, sizeof(int2) * 2 * kB * (size_t)nf));
+  if (!inv_g || !piv_g || !moves) return PF_ERR_CUDA;
   sp.inv = inv_g;
   int* failed = piv_g + (size_t)s.np * nf;
+  int* moves_n = static_cast<int*>(workspace(ctx, kWsSmallArrays + 27, sizeof(int) * (size_t)nf));
+  if (!moves_n) return PF_ERR_CUDA;
   cudaMemsetAsync(failed, 0, sizeof(int) * nf, ctx->stream);
   std::vector<double> tol(nf);
   for (int q = 0; q < nf; ++q) tol[q] = tol_all[fails[q]];
   double* d_tol = upload(ctx, kWsSmallArrays + 25, tol);
-  rlu_pivot(ctx, sp, 0, s.np, piv_g, d_tol, d_fail, failed);
+  rlu_pivot(ctx, sp, 0, s.np, PivotScratch{piv_g, d_tol, d_fail, failed, moves, moves_n});
   for (int q = 0; q < nf; ++q) {
     if (side)
       cudaMemcpyAsync(s.M + fails[q] * s.stride(), side + q * s.stride(), sizeof(double) * s.stride(),

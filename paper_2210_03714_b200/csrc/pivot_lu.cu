@@ -1,26 +1,29 @@
 // Blocked partial-pivoting LU for n > 128 (DenseLu, dense.cpp:102-133): recursive (column-split)
-// factorisation whose big work is the DMMA TRSM / GEMM of pf_large.cu, with two kernels here:
+// factorisation whose big work is the DMMA TRSM / GEMM of pf_large.cu, with these kernels:
 //
 //   panel_lu_cluster_kernel  the rows [off, np) x columns [off, off + w) panel (w <= 64) of one system,
-//                            factored column by column with the reference's pivot rule (strict '>'
-//                            over the column, first maximum wins), row exchanges inside the panel,
-//                            multipliers a * (1 / pivot), the f == 0 skip. The panel lives in the
-//                            shared memory of a thread-block CLUSTER (up to 16 CTAs, DSMEM): each CTA
-//                            owns a contiguous row range; per column one cluster barrier publishes the
-//                            CTAs' candidates, every CTA reads them over DSMEM and agrees on the
-//                            pivot, the pivot row is read once over DSMEM and the swap partner row is
-//                            written back after a second barrier. No global-memory round trip per
-//                            column (the unblocked fallback streamed the whole trailing matrix per
-//                            column from one SM).
-//   panel_lu_global_kernel   the same panel in global memory (one CTA) when it does not fit the
-//                            cluster's shared memory.
-//   laswp_kernel             applies a range of the swap sequence to a column range (LAPACK laswp).
+//                            factored column by column with the reference's pivot rule (the largest
+//                            |a| of the column, the first such row in row order on ties), multipliers
+//                            a * (1 / pivot) and the f == 0 skip. The panel lives in the shared memory
+//                            of a thread-block CLUSTER (up to 16 CTAs, distributed shared memory):
+//                            each CTA owns a contiguous range of the panel's rows. Row exchanges are
+//                            not moved: every row carries its current position in the exchanged order
+//                            (the reference's full-row swaps are a permutation of these positions),
+//                            the pivot row of a column is final and never written again, so ONE
+//                            cluster barrier per column suffices -- it publishes the CTAs' candidates
+//                            (double-buffered), every CTA reduces them identically and reads the
+//                            pivot row once over DSMEM. Rows are written back in exchanged order, and
+//                            the moves are listed for row_move_kernel.
+//   panel_lu_global_kernel   the same panel in global memory, one CTA (panels taller than the cluster's
+//                            shared memory), also listing its moves.
+//   row_move_kernel          applies a panel's row moves (at most 2 w rows) to every column outside the
+//                            panel: after each panel the whole matrix has the reference's row order.
 //
 // A failing pivot (best <= 1e-14 max|A|) records SingularShift (column, magnitude) for the system and
 // stops its remaining panels; the host reports the first failure.
 #include <climits>
-#include <cstdlib>
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "pf_common.cuh"
 #include "pf_kernels.h"
@@ -31,81 +34,125 @@ namespace pf {
 
 namespace {
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int PW = 64;        // panel width
-constexpr int PLS = PW + 1;   // smem row stride (odd: column walks are conflict free)
+constexpr int PW = 64;       // panel width
+constexpr int PLS = PW + 1;  // smem row stride (odd: column walks are conflict free)
+constexpr int PT = 512;      // threads per panel CTA
+constexpr int MAX_ROWS_PER_CTA = 384;
 
-__device__ __forceinline__ void better(double& bv, int& bi, double v, int i) {
-  if (v > bv || (v == bv && i < bi)) {
+// candidate order: larger |a|, then the earlier row in the exchanged order
+__device__ __forceinline__ void better(double& bv, int& bl, int& br, double v, int l, int r) {
+  if (v > bv || (v == bv && l < bl)) {
     bv = v;
-    bi = i;
+    bl = l;
+    br = r;
   }
 }
+
+struct PanelShared {
+  double cand_v[2];
+  int cand_l[2];  // exchanged-order position (relative to off)
+  int cand_r[2];  // local row in the owning CTA
+  double sel_v;
+  int sel_l, sel_q, sel_r;
+  int nmove;
+};
 }  // namespace
 
 size_t panel_lu_smem_bytes(int rows_per_cta) {
-  return sizeof(double) * ((size_t)rows_per_cta * PLS + 2 * PW + 64) + sizeof(int) * 64;
+  return sizeof(double) * ((size_t)rows_per_cta * PLS + PW) + sizeof(int) * 2 * (size_t)rows_per_cta +
+         sizeof(PanelShared) + 64;
 }
 
-// blockIdx.x = CTA within the cluster (rank), blockIdx.y = system. Rows [off + rank * R, ...).
-__global__ void __launch_bounds__(512) panel_lu_cluster_kernel(double* M, int64_t ld, int64_t strideM, int np,
-                                                                int off, int w, int R, int* piv, int npiv,
-                                                                const double* tol, const int* zorig, int* failed,
-                                                                DevStatus* status, int* first_error) {
+// blockIdx.x = CTA within the cluster (rank), blockIdx.y = system. Physical rows [off + rank R, ...).
+// moves[z * 2 PW ...]: (dst, src) absolute row pairs, count in moves_n[z].
+__global__ void __launch_bounds__(PT) panel_lu_cluster_kernel(double* M, int64_t ld, int64_t strideM, int np,
+                                                               int off, int w, int R, int* piv, int npiv,
+                                                               const double* tol, const int* zorig, int* failed,
+                                                               DevStatus* status, int* first_error, int2* moves,
+                                                               int* moves_n) {
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* P = reinterpret_cast<double*>(smem_raw);  // R x PLS
-  double* prow = P + (size_t)R * PLS;               // the pivot row (after the swap: row col)
-  double* oldc = prow + PW;                         // the old row col (goes to row p)
-  double* cand_v = oldc + PW;                       // [0] this CTA's candidate
-  int* cand_i = reinterpret_cast<int*>(cand_v + 64);
+  double* prow = P + (size_t)R * PLS;               // the current pivot row
+  int* pos = reinterpret_cast<int*>(prow + PW);     // exchanged-order position of each owned row
+  int* done = pos + R;                              // 1 once the row is a pivot row
+  PanelShared& sh = *reinterpret_cast<PanelShared*>(done + R);
+  __shared__ double red_v[PT / 32];
+  __shared__ int red_l[PT / 32], red_r[PT / 32];
   const int z = blockIdx.y;
   const int rank = (int)cluster.block_rank();
   const int C = (int)cluster.num_blocks();
-  const int r_lo = off + rank * R;                  // first owned row
-  const int r_hi = min(np, r_lo + R);
-  const int nr = max(0, r_hi - r_lo);
+  const int r_lo = rank * R;  // relative to off
+  const int nr = max(0, min(np - off, r_lo + R) - r_lo);
   double* a = M + (int64_t)z * strideM;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool dead = failed[z] != 0;  // an earlier panel of this system failed: nothing to do
-  // load the owned rows of the panel
-  for (int idx = threadIdx.x; idx < nr * w; idx += blockDim.x) {
-    const int r = idx / w, c = idx % w;
-    P[r * PLS + c] = a[(int64_t)(r_lo + r) * ld + off + c];
+  for (int idx = tid; idx < nr * w; idx += PT) {
+    const int r = idx / w, c = idx - r * w;
+    P[r * PLS + c] = a[(int64_t)(off + r_lo + r) * ld + off + c];
   }
+  for (int r = tid; r < nr; r += PT) {
+    pos[r] = r_lo + r;
+    done[r] = 0;
+  }
+  if (tid == 0 && rank == 0) moves_n[z] = 0;
   cluster.sync();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  __shared__ double red_v[32];
-  __shared__ int red_i[32];
-  bool singular = false;  // uniform over the cluster: every CTA reduces the same candidates
+  bool singular = false;
+  const int uj = tid & (PW - 1), ur = tid >> 6;  // update mapping: column lane, row phase (8 rows per pass)
   for (int c = 0; c < w && !dead; ++c) {
-    const int col = off + c;
-    // ---- this CTA's candidate over its rows >= col (strict '>', smallest row on ties)
+    const int slot = c & 1;
+    // ---- this CTA's candidate over its rows not yet pivoted
     double bv = -1.0;
-    int bi = INT_MAX;
-    for (int r = max(col, r_lo) - r_lo + threadIdx.x; r < nr; r += blockDim.x) better(bv, bi, fabs(P[r * PLS + c]), r_lo + r);
-    for (int o = 16; o > 0; o >>= 1) better(bv, bi, __shfl_xor_sync(FULL, bv, o), __shfl_xor_sync(FULL, bi, o));
+    int bl = INT_MAX, br = -1;
+    for (int r = tid; r < nr; r += PT)
+      if (!done[r]) better(bv, bl, br, fabs(P[r * PLS + c]), pos[r], r);
+    for (int o = 16; o > 0; o >>= 1)
+      better(bv, bl, br, __shfl_xor_sync(FULL, bv, o), __shfl_xor_sync(FULL, bl, o), __shfl_xor_sync(FULL, br, o));
     if (lane == 0) {
       red_v[warp] = bv;
-      red_i[warp] = bi;
+      red_l[warp] = bl;
+      red_r[warp] = br;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int q = 1; q < nw; ++q) better(bv, bi, red_v[q], red_i[q]);
-      cand_v[0] = bv;
-      cand_i[0] = bi;
+    if (warp == 0) {
+      bv = lane < PT / 32 ? red_v[lane] : -1.0;
+      bl = lane < PT / 32 ? red_l[lane] : INT_MAX;
+      br = lane < PT / 32 ? red_r[lane] : -1;
+      for (int o = 16; o > 0; o >>= 1)
+        better(bv, bl, br, __shfl_xor_sync(FULL, bv, o), __shfl_xor_sync(FULL, bl, o), __shfl_xor_sync(FULL, br, o));
+      if (lane == 0) {
+        sh.cand_v[slot] = bv;
+        sh.cand_l[slot] = bl;
+        sh.cand_r[slot] = br;
+      }
     }
-    cluster.sync();  // (1) every candidate published
-    // ---- the pivot: every CTA reduces the same candidates in the same order
-    double gv = -1.0;
-    int gi = INT_MAX;
-    for (int q = 0; q < C; ++q) {
-      const double* cv = cluster.map_shared_rank(cand_v, q);
-      const int* ci = cluster.map_shared_rank(cand_i, q);
-      better(gv, gi, cv[0], ci[0]);
+    cluster.sync();  // every CTA's candidate for column c published (slot c & 1)
+    // ---- the pivot: warp 0 of every CTA reduces the C candidates identically
+    if (warp == 0) {
+      double v = -1.0;
+      int l = INT_MAX, q = -1;
+      if (lane < C) {
+        const PanelShared* o = cluster.map_shared_rank(&sh, lane);
+        v = o->cand_v[slot];
+        l = o->cand_l[slot];
+        q = lane;
+      }
+      for (int o = 16; o > 0; o >>= 1) better(v, l, q, __shfl_xor_sync(FULL, v, o), __shfl_xor_sync(FULL, l, o),
+                                              __shfl_xor_sync(FULL, q, o));
+      if (lane == 0) {
+        sh.sel_v = v;
+        sh.sel_l = l;
+        sh.sel_q = q;
+        sh.sel_r = cluster.map_shared_rank(&sh, q)->cand_r[slot];
+      }
     }
+    __syncthreads();
+    const double gv = sh.sel_v;
+    const int p = sh.sel_l, q = sh.sel_q, pr = sh.sel_r;
     if (gv <= tol[z]) {  // SingularShift (dense.cpp:116-119), reported once
-      if (rank == 0 && threadIdx.x == 0) {
+      if (rank == 0 && tid == 0) {
         status[zorig[z]].code = PF_ERR_SINGULAR_SHIFT;
-        status[zorig[z]].column = col;
+        status[zorig[z]].column = off + c;
         status[zorig[z]].pivot_magnitude = gv;
         failed[z] = 1;
         atomicMin(first_error, zorig[z]);
@@ -113,75 +160,78 @@ __global__ void __launch_bounds__(512) panel_lu_cluster_kernel(double* M, int64_
       singular = true;
       break;
     }
-    const int p = gi;
-    const int own_p = (p - off) / R, own_c = (col - off) / R;
-    // the pivot row (and, for its new owner, the old row col) over DSMEM
-    {
-      const double* src = cluster.map_shared_rank(P, own_p) + (size_t)(p - off - own_p * R) * PLS;
-      for (int j = threadIdx.x; j < w; j += blockDim.x) prow[j] = src[j];
-      if (rank == own_p && p != col) {
-        const double* s2 = cluster.map_shared_rank(P, own_c) + (size_t)(col - off - own_c * R) * PLS;
-        for (int j = threadIdx.x; j < w; j += blockDim.x) oldc[j] = s2[j];
-      }
-    }
-    cluster.sync();  // (2) all reads done before the swap writes
-    if (p != col) {
-      if (rank == own_c)
-        for (int j = threadIdx.x; j < w; j += blockDim.x) P[(size_t)(col - r_lo) * PLS + j] = prow[j];
-      if (rank == own_p)
-        for (int j = threadIdx.x; j < w; j += blockDim.x) P[(size_t)(p - r_lo) * PLS + j] = oldc[j];
-    }
-    if (rank == 0 && threadIdx.x == 0) piv[(int64_t)z * npiv + col] = p;
+    // the pivot row (final from now on) over DSMEM; the exchange c <-> p of the positions
+    if (tid < w) prow[tid] = cluster.map_shared_rank(P, q)[(size_t)pr * PLS + tid];
+    if (p != c)
+      for (int r = tid; r < nr; r += PT)
+        if (pos[r] == c) pos[r] = p;
     __syncthreads();
-    // ---- multipliers f = a * (1 / pivot) and the rank-1 update of the owned rows below col
+    if (rank == q && tid == 0) {
+      pos[pr] = c;
+      done[pr] = 1;
+    }
+    if (rank == 0 && tid == 0) piv[(int64_t)z * npiv + off + c] = off + p;
+    __syncthreads();
+    // ---- multipliers f = a * (1 / pivot), then the rank-1 update of the rows not yet pivoted
     const double inv_piv = 1.0 / prow[c];
-    const int r0 = max(col + 1, r_lo) - r_lo;
-    const int wc = w - c - 1;
-    for (int r = r0 + threadIdx.x; r < nr; r += blockDim.x) P[r * PLS + c] = __dmul_rn(P[r * PLS + c], inv_piv);
+    for (int r = tid; r < nr; r += PT)
+      if (!done[r]) P[r * PLS + c] = __dmul_rn(P[r * PLS + c], inv_piv);
     __syncthreads();
-    if (wc > 0)
-      for (int idx = threadIdx.x; idx < (nr - r0) * wc; idx += blockDim.x) {
-        const int r = r0 + idx / wc, j = c + 1 + idx % wc;
-        const double f = P[r * PLS + c];
-        if (f != 0.0) P[r * PLS + j] = __dsub_rn(P[r * PLS + j], __dmul_rn(f, prow[j]));
-      }
+    const int j = c + 1 + uj;
+    if (j < w) {
+      const double u = prow[j];
+      for (int r = ur; r < nr; r += PT / PW)
+        if (!done[r]) {
+          const double f = P[r * PLS + c];
+          if (f != 0.0) P[r * PLS + j] = __dsub_rn(P[r * PLS + j], __dmul_rn(f, u));
+        }
+    }
     __syncthreads();
   }
   cluster.sync();  // no CTA leaves while others may still read its shared memory
   if (dead || singular) return;
-  for (int idx = threadIdx.x; idx < nr * w; idx += blockDim.x) {
-    const int r = idx / w, c = idx % w;
-    a[(int64_t)(r_lo + r) * ld + off + c] = P[r * PLS + c];
+  // write back in exchanged order; list the moved rows for the columns outside the panel
+  for (int idx = tid; idx < nr * w; idx += PT) {
+    const int r = idx / w, c = idx - r * w;
+    a[(int64_t)(off + pos[r]) * ld + off + c] = P[r * PLS + c];
   }
+  for (int r = tid; r < nr; r += PT)
+    if (pos[r] != r_lo + r) {
+      const int k = atomicAdd(moves_n + z, 1);
+      moves[(int64_t)z * 2 * PW + k] = make_int2(off + pos[r], off + r_lo + r);
+    }
 }
 
-// The same panel in global memory, one CTA per system (fallback for panels taller than the
-// cluster's shared memory).
+// The same panel in global memory, one CTA per system (panels taller than the cluster's shared
+// memory): explicit exchanges inside the panel columns, the moves listed from the swap sequence.
 __global__ void __launch_bounds__(1024) panel_lu_global_kernel(double* M, int64_t ld, int64_t strideM, int np,
                                                                 int off, int w, int* piv, int npiv, const double* tol,
                                                                 const int* zorig, int* failed, DevStatus* status,
-                                                                int* first_error) {
+                                                                int* first_error, int2* moves, int* moves_n) {
   __shared__ double red_v[32];
   __shared__ int red_i[32];
   __shared__ int s_p;
   __shared__ double s_best;
+  __shared__ int rows[2 * PW], srcs[2 * PW], nrow;
   const int z = blockIdx.x;
   if (failed[z]) return;
   double* a = M + (int64_t)z * strideM;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) nrow = 0;
   for (int c = 0; c < w; ++c) {
     const int col = off + c;
     double bv = -1.0;
-    int bi = INT_MAX;
-    for (int r = col + threadIdx.x; r < np; r += blockDim.x) better(bv, bi, fabs(a[(int64_t)r * ld + col]), r);
-    for (int o = 16; o > 0; o >>= 1) better(bv, bi, __shfl_xor_sync(FULL, bv, o), __shfl_xor_sync(FULL, bi, o));
+    int bi = INT_MAX, dummy = 0;
+    for (int r = col + threadIdx.x; r < np; r += blockDim.x) better(bv, bi, dummy, fabs(a[(int64_t)r * ld + col]), r, r);
+    for (int o = 16; o > 0; o >>= 1)
+      better(bv, bi, dummy, __shfl_xor_sync(FULL, bv, o), __shfl_xor_sync(FULL, bi, o), 0);
     if (lane == 0) {
       red_v[warp] = bv;
       red_i[warp] = bi;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      for (int q = 1; q < nw; ++q) better(bv, bi, red_v[q], red_i[q]);
+      for (int q = 1; q < nw; ++q) better(bv, bi, dummy, red_v[q], red_i[q], 0);
       s_best = bv;
       s_p = bi;
     }
@@ -203,7 +253,29 @@ __global__ void __launch_bounds__(1024) panel_lu_global_kernel(double* M, int64_
         a[(int64_t)p * ld + off + j] = a[(int64_t)col * ld + off + j];
         a[(int64_t)col * ld + off + j] = t;
       }
-    if (threadIdx.x == 0) piv[(int64_t)z * npiv + col] = p;
+    if (threadIdx.x == 0) {
+      piv[(int64_t)z * npiv + col] = p;
+      // track where each touched row's original content now is: rows[] holds the touched rows,
+      // srcs[] the original row whose data sits there
+      int ic = -1, ip = -1;
+      for (int t = 0; t < nrow; ++t) {
+        if (rows[t] == col) ic = t;
+        if (rows[t] == p) ip = t;
+      }
+      if (ic < 0) {
+        ic = nrow++;
+        rows[ic] = col;
+        srcs[ic] = col;
+      }
+      if (ip < 0) {
+        ip = nrow++;
+        rows[ip] = p;
+        srcs[ip] = p;
+      }
+      const int t = srcs[ic];
+      srcs[ic] = srcs[ip];
+      srcs[ip] = t;
+    }
     __syncthreads();
     const double inv_piv = 1.0 / a[(int64_t)col * ld + col];
     for (int r = col + 1 + threadIdx.x; r < np; r += blockDim.x)
@@ -218,51 +290,63 @@ __global__ void __launch_bounds__(1024) panel_lu_global_kernel(double* M, int64_
       }
     __syncthreads();
   }
+  if (threadIdx.x == 0) {
+    int k = 0;
+    for (int t = 0; t < nrow; ++t)
+      if (rows[t] != srcs[t]) moves[(int64_t)z * 2 * PW + k++] = make_int2(rows[t], srcs[t]);
+    moves_n[z] = k;
+  }
 }
 
-// Swaps k = k0 .. k1-1 of every system's sequence applied in order to columns [c0, c1): one thread per
-// column, the rows of each swap contiguous across the warp.
-__global__ void laswp_kernel(double* M, int64_t ld, int64_t strideM, const int* piv, int npiv, int k0, int k1, int c0,
-                             int c1, const int* failed) {
+// The panel's row moves (dst <- src) applied to the columns outside [off, off + w): CTA = 32 columns
+// of one system; all sources are read into shared memory before any destination is written.
+constexpr int MC = 32;
+__global__ void __launch_bounds__(256) row_move_kernel(double* M, int64_t ld, int64_t strideM, int np, int off, int w,
+                                                       const int2* moves, const int* moves_n, const int* failed) {
+  __shared__ double buf[2 * PW][MC + 1];
+  __shared__ int2 mv[2 * PW];
   const int z = blockIdx.y;
-  if (failed && failed[z]) return;
-  const int c = c0 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= c1) return;
+  if (failed[z]) return;
+  const int cnt = moves_n[z];
+  if (cnt == 0) return;
+  const int c0 = blockIdx.x * MC;
+  if (c0 >= off && c0 + MC <= off + w) return;  // entirely inside the panel (already in order)
   double* a = M + (int64_t)z * strideM;
-  const int* pz = piv + (int64_t)z * npiv;
-  for (int k = k0; k < k1; ++k) {
-    const int p = pz[k];
-    if (p != k) {
-      const double t = a[(int64_t)p * ld + c];
-      a[(int64_t)p * ld + c] = a[(int64_t)k * ld + c];
-      a[(int64_t)k * ld + c] = t;
-    }
-  }
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) mv[i] = moves[(int64_t)z * 2 * PW + i];
+  __syncthreads();
+  const int cc = threadIdx.x & (MC - 1), r0 = threadIdx.x / MC;
+  const int c = c0 + cc;
+  const bool live = c < np && (c < off || c >= off + w);
+  for (int i = r0; i < cnt; i += 256 / MC)
+    if (live) buf[i][cc] = a[(int64_t)mv[i].y * ld + c];
+  __syncthreads();
+  for (int i = r0; i < cnt; i += 256 / MC)
+    if (live) a[(int64_t)mv[i].x * ld + c] = buf[i][cc];
 }
 
 cudaError_t launch_panel_lu(double* M, int64_t ld, int64_t strideM, int np, int off, int w, int nsys, int* piv,
                             int npiv, const double* tol, const int* zorig, int* failed, DevStatus* status,
-                            int* first_error, cudaStream_t stream) {
+                            int* first_error, int2* moves, int* moves_n, cudaStream_t stream) {
   const int rows = np - off;
-  // smallest cluster whose CTAs hold <= 384 rows each (<= 197 KB of shared memory), up to 16 CTAs
+  // smallest cluster whose CTAs hold <= 384 rows each (<= 210 KB of shared memory), up to 16 CTAs
   int C = 1;
-  while (C < 16 && (rows + C - 1) / C > 384) C *= 2;
+  while (C < 16 && (rows + C - 1) / C > MAX_ROWS_PER_CTA) C *= 2;
   const int R = (rows + C - 1) / C;
   static const bool no_cluster = std::getenv("PF_PANEL_GLOBAL") != nullptr;
-  if (R <= 384 && !no_cluster) {
-    const size_t smem = panel_lu_smem_bytes(R);
+  cudaError_t e = cudaSuccess;
+  if (R <= MAX_ROWS_PER_CTA && !no_cluster) {
     static bool attrs = false;
     if (!attrs) {
       cudaFuncSetAttribute(panel_lu_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       attrs = true;
     }
-    cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(panel_lu_cluster_kernel),
-                                       (int)panel_lu_smem_bytes(384));
+    e = set_smem_attr_once(reinterpret_cast<const void*>(panel_lu_cluster_kernel),
+                           (int)panel_lu_smem_bytes(MAX_ROWS_PER_CTA));
     if (e == cudaSuccess) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(C, nsys);
-      cfg.blockDim = dim3(512);
-      cfg.dynamicSmemBytes = smem;
+      cfg.blockDim = dim3(PT);
+      cfg.dynamicSmemBytes = panel_lu_smem_bytes(R);
       cfg.stream = stream;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -272,21 +356,16 @@ cudaError_t launch_panel_lu(double* M, int64_t ld, int64_t strideM, int np, int 
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       e = cudaLaunchKernelEx(&cfg, panel_lu_cluster_kernel, M, ld, strideM, np, off, w, R, piv, npiv, tol, zorig,
-                             failed, status, first_error);
-      if (e == cudaSuccess) return e;
+                             failed, status, first_error, moves, moves_n);
     }
-    cudaGetLastError();  // cluster launch unavailable: the global-memory panel
+    if (e != cudaSuccess) cudaGetLastError();  // no cluster launch: the global-memory panel below
   }
-  panel_lu_global_kernel<<<nsys, 1024, 0, stream>>>(M, ld, strideM, np, off, w, piv, npiv, tol, zorig, failed, status,
-                                                    first_error);
+  if (no_cluster || R > MAX_ROWS_PER_CTA || e != cudaSuccess)
+    panel_lu_global_kernel<<<nsys, 1024, 0, stream>>>(M, ld, strideM, np, off, w, piv, npiv, tol, zorig, failed,
+                                                      status, first_error, moves, moves_n);
+  row_move_kernel<<<dim3((np + MC - 1) / MC, nsys), 256, 0, stream>>>(M, ld, strideM, np, off, w, moves, moves_n,
+                                                                      failed);
   return cudaGetLastError();
-}
-
-void launch_laswp(double* M, int64_t ld, int64_t strideM, const int* piv, int npiv, int k0, int k1, int c0, int c1,
-                  int nsys, const int* failed, cudaStream_t stream) {
-  if (k1 <= k0 || c1 <= c0 || nsys == 0) return;
-  laswp_kernel<<<dim3((c1 - c0 + 127) / 128, nsys), 128, 0, stream>>>(M, ld, strideM, piv, npiv, k0, k1, c0, c1,
-                                                                       failed);
 }
 
 }  // namespace pf
