@@ -50,16 +50,16 @@ __device__ __forceinline__ void better(double& bv, int& bl, int& br, double v, i
 
 struct PanelShared {
   double cand_v[2];
-  int cand_l[2];  // exchanged-order position (relative to off)
-  int cand_r[2];  // local row in the owning CTA
-  double sel_v;
-  int sel_l, sel_q, sel_r;
-  int nmove;
+  int cand_l[2];        // exchanged-order position (relative to off)
+  int cand_r[2];        // local row in the owning CTA
+  double crow[2][PW];   // the candidate row's values (read by every CTA over DSMEM)
+  double cv[16];        // the cluster's candidates, gathered
+  int cl[16];
 };
 }  // namespace
 
 size_t panel_lu_smem_bytes(int rows_per_cta) {
-  return sizeof(double) * ((size_t)rows_per_cta * PLS + PW) + sizeof(int) * 2 * (size_t)rows_per_cta +
+  return sizeof(double) * ((size_t)rows_per_cta * PLS + 16 * PW) + sizeof(int) * 2 * (size_t)rows_per_cta +
          sizeof(PanelShared) + 64;
 }
 
@@ -73,8 +73,8 @@ __global__ void __launch_bounds__(PT) panel_lu_cluster_kernel(double* M, int64_t
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* P = reinterpret_cast<double*>(smem_raw);  // R x PLS
-  double* prow = P + (size_t)R * PLS;               // the current pivot row
-  int* pos = reinterpret_cast<int*>(prow + PW);     // exchanged-order position of each owned row
+  double* rows_buf = P + (size_t)R * PLS;           // 16 x PW: the cluster's candidate rows, gathered
+  int* pos = reinterpret_cast<int*>(rows_buf + 16 * PW);  // exchanged-order position of each owned row
   int* done = pos + R;                              // 1 once the row is a pivot row
   PanelShared& sh = *reinterpret_cast<PanelShared*>(done + R);
   __shared__ double red_v[PT / 32];
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(PT) panel_lu_cluster_kernel(double* M, int64_t
   const int uj = tid & (PW - 1), ur = tid >> 6;  // update mapping: column lane, row phase (8 rows per pass)
   for (int c = 0; c < w && !dead; ++c) {
     const int slot = c & 1;
-    // ---- this CTA's candidate over its rows not yet pivoted
+    // ---- this CTA's candidate over its rows not yet pivoted, and a copy of that row
     double bv = -1.0;
     int bl = INT_MAX, br = -1;
     for (int r = tid; r < nr; r += PT)
@@ -126,29 +126,25 @@ __global__ void __launch_bounds__(PT) panel_lu_cluster_kernel(double* M, int64_t
         sh.cand_r[slot] = br;
       }
     }
-    cluster.sync();  // every CTA's candidate for column c published (slot c & 1)
-    // ---- the pivot: warp 0 of every CTA reduces the C candidates identically
-    if (warp == 0) {
-      double v = -1.0;
-      int l = INT_MAX, q = -1;
-      if (lane < C) {
-        const PanelShared* o = cluster.map_shared_rank(&sh, lane);
-        v = o->cand_v[slot];
-        l = o->cand_l[slot];
-        q = lane;
-      }
-      for (int o = 16; o > 0; o >>= 1) better(v, l, q, __shfl_xor_sync(FULL, v, o), __shfl_xor_sync(FULL, l, o),
-                                              __shfl_xor_sync(FULL, q, o));
-      if (lane == 0) {
-        sh.sel_v = v;
-        sh.sel_l = l;
-        sh.sel_q = q;
-        sh.sel_r = cluster.map_shared_rank(&sh, q)->cand_r[slot];
+    __syncthreads();
+    const int my_r = sh.cand_r[slot];
+    if (tid < w && my_r >= 0) sh.crow[slot][tid] = P[my_r * PLS + tid];
+    cluster.sync();  // every CTA's candidate and its row published (slot c & 1)
+    // ---- one DSMEM round trip: every candidate row and value, in parallel
+    for (int t = tid; t < C * PW; t += PT) {
+      const PanelShared* o = cluster.map_shared_rank(&sh, t / PW);
+      const int j = t % PW;
+      if (j < w) rows_buf[t] = o->crow[slot][j];
+      if (j == 0) {
+        sh.cv[t / PW] = o->cand_v[slot];
+        sh.cl[t / PW] = o->cand_l[slot];
       }
     }
     __syncthreads();
-    const double gv = sh.sel_v;
-    const int p = sh.sel_l, q = sh.sel_q, pr = sh.sel_r;
+    // the pivot: every thread reduces the same C candidates in the same order
+    double gv = -1.0;
+    int p = INT_MAX, q = -1;
+    for (int k = 0; k < C; ++k) better(gv, p, q, sh.cv[k], sh.cl[k], k);
     if (gv <= tol[z]) {  // SingularShift (dense.cpp:116-119), reported once
       if (rank == 0 && tid == 0) {
         status[zorig[z]].code = PF_ERR_SINGULAR_SHIFT;
@@ -160,15 +156,15 @@ __global__ void __launch_bounds__(PT) panel_lu_cluster_kernel(double* M, int64_t
       singular = true;
       break;
     }
-    // the pivot row (final from now on) over DSMEM; the exchange c <-> p of the positions
-    if (tid < w) prow[tid] = cluster.map_shared_rank(P, q)[(size_t)pr * PLS + tid];
+    const double* prow = rows_buf + q * PW;  // the pivot row, final from now on
+    // the exchange c <-> p of the positions
     if (p != c)
       for (int r = tid; r < nr; r += PT)
         if (pos[r] == c) pos[r] = p;
     __syncthreads();
     if (rank == q && tid == 0) {
-      pos[pr] = c;
-      done[pr] = 1;
+      pos[my_r] = c;
+      done[my_r] = 1;
     }
     if (rank == 0 && tid == 0) piv[(int64_t)z * npiv + off + c] = off + p;
     __syncthreads();
