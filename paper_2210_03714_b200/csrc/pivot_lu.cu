@@ -36,7 +36,7 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int PW = 64;       // panel width
 constexpr int PLS = PW + 1;  // smem row stride (odd: column walks are conflict free)
-constexpr int PT = 512;      // threads per panel CTA
+constexpr int PT = 256;      // threads per panel CTA
 constexpr int MAX_ROWS_PER_CTA = 384;
 
 // candidate order: larger |a|, then the earlier row in the exchanged order
@@ -98,14 +98,21 @@ __global__ void __launch_bounds__(PT) panel_lu_cluster_kernel(double* M, int64_t
   if (tid == 0 && rank == 0) moves_n[z] = 0;
   cluster.sync();
   bool singular = false;
-  const int uj = tid & (PW - 1), ur = tid >> 6;  // update mapping: column lane, row phase (8 rows per pass)
+  const int uj = tid & (PW - 1), ur = tid / PW;  // update mapping: column lane, row phase
+  double inv_prev = 0.0;                          // 1 / pivot of the previous column
+  // Four barriers per column (one of them cluster-wide). The multipliers of column c are scaled in
+  // column c + 1's first phase (the update of column c computes f = a * (1 / pivot) itself), so no
+  // barrier separates the scaling from the update.
   for (int c = 0; c < w && !dead; ++c) {
     const int slot = c & 1;
-    // ---- this CTA's candidate over its rows not yet pivoted, and a copy of that row
+    // ---- (A) column c - 1's multipliers; this CTA's candidate among its rows not yet pivoted
     double bv = -1.0;
     int bl = INT_MAX, br = -1;
-    for (int r = tid; r < nr; r += PT)
-      if (!done[r]) better(bv, bl, br, fabs(P[r * PLS + c]), pos[r], r);
+    for (int r = tid; r < nr; r += PT) {
+      if (done[r]) continue;
+      if (c > 0) P[r * PLS + c - 1] = __dmul_rn(P[r * PLS + c - 1], inv_prev);
+      better(bv, bl, br, fabs(P[r * PLS + c]), pos[r], r);
+    }
     for (int o = 16; o > 0; o >>= 1)
       better(bv, bl, br, __shfl_xor_sync(FULL, bv, o), __shfl_xor_sync(FULL, bl, o), __shfl_xor_sync(FULL, br, o));
     if (lane == 0) {
@@ -114,6 +121,7 @@ __global__ void __launch_bounds__(PT) panel_lu_cluster_kernel(double* M, int64_t
       red_r[warp] = br;
     }
     __syncthreads();
+    // ---- (B) warp 0: the CTA's candidate and a copy of its row
     if (warp == 0) {
       bv = lane < PT / 32 ? red_v[lane] : -1.0;
       bl = lane < PT / 32 ? red_l[lane] : INT_MAX;
@@ -125,14 +133,16 @@ __global__ void __launch_bounds__(PT) panel_lu_cluster_kernel(double* M, int64_t
         sh.cand_l[slot] = bl;
         sh.cand_r[slot] = br;
       }
+      if (br >= 0)
+        for (int j = lane; j < w; j += 32) sh.crow[slot][j] = P[br * PLS + j];
     }
-    __syncthreads();
-    const int my_r = sh.cand_r[slot];
-    if (tid < w && my_r >= 0) sh.crow[slot][tid] = P[my_r * PLS + tid];
-    cluster.sync();  // every CTA's candidate and its row published (slot c & 1)
-    // ---- one DSMEM round trip: every candidate row and value, in parallel
+    if (C > 1)
+      cluster.sync();  // every CTA's candidate and its row published (slot c & 1)
+    else
+      __syncthreads();
+    // ---- (C) one DSMEM round trip: every candidate row and value, in parallel
     for (int t = tid; t < C * PW; t += PT) {
-      const PanelShared* o = cluster.map_shared_rank(&sh, t / PW);
+      const PanelShared* o = C > 1 ? cluster.map_shared_rank(&sh, t / PW) : &sh;
       const int j = t % PW;
       if (j < w) rows_buf[t] = o->crow[slot][j];
       if (j == 0) {
@@ -141,7 +151,8 @@ __global__ void __launch_bounds__(PT) panel_lu_cluster_kernel(double* M, int64_t
       }
     }
     __syncthreads();
-    // the pivot: every thread reduces the same C candidates in the same order
+    // ---- (D) the pivot (every thread reduces the same C candidates in the same order), the
+    // exchange c <-> p of the positions, and the rank-1 update of the rows not yet pivoted
     double gv = -1.0;
     int p = INT_MAX, q = -1;
     for (int k = 0; k < C; ++k) better(gv, p, q, sh.cv[k], sh.cl[k], k);
@@ -157,31 +168,34 @@ __global__ void __launch_bounds__(PT) panel_lu_cluster_kernel(double* M, int64_t
       break;
     }
     const double* prow = rows_buf + q * PW;  // the pivot row, final from now on
-    // the exchange c <-> p of the positions
-    if (p != c)
-      for (int r = tid; r < nr; r += PT)
-        if (pos[r] == c) pos[r] = p;
-    __syncthreads();
-    if (rank == q && tid == 0) {
-      pos[my_r] = c;
-      done[my_r] = 1;
+    const int my_r = rank == q ? sh.cand_r[slot] : -1;  // the pivot row, if it is this CTA's
+    for (int r = tid; r < nr; r += PT) {
+      if (r == my_r) {
+        pos[r] = c;
+        done[r] = 1;  // (the update below excludes my_r explicitly)
+      } else if (pos[r] == c) {
+        pos[r] = p;
+      }
     }
     if (rank == 0 && tid == 0) piv[(int64_t)z * npiv + off + c] = off + p;
-    __syncthreads();
-    // ---- multipliers f = a * (1 / pivot), then the rank-1 update of the rows not yet pivoted
     const double inv_piv = 1.0 / prow[c];
-    for (int r = tid; r < nr; r += PT)
-      if (!done[r]) P[r * PLS + c] = __dmul_rn(P[r * PLS + c], inv_piv);
-    __syncthreads();
     const int j = c + 1 + uj;
     if (j < w) {
       const double u = prow[j];
-      for (int r = ur; r < nr; r += PT / PW)
-        if (!done[r]) {
-          const double f = P[r * PLS + c];
-          if (f != 0.0) P[r * PLS + j] = __dsub_rn(P[r * PLS + j], __dmul_rn(f, u));
-        }
+      for (int r = ur; r < nr; r += PT / PW) {
+        if (done[r] || r == my_r) continue;
+        const double f = __dmul_rn(P[r * PLS + c], inv_piv);
+        if (f != 0.0) P[r * PLS + j] = __dsub_rn(P[r * PLS + j], __dmul_rn(f, u));
+      }
     }
+    __syncthreads();
+    inv_prev = inv_piv;
+  }
+  // the last column's multipliers
+  if (!dead && !singular && w > 0) {
+    __syncthreads();
+    for (int r = tid; r < nr; r += PT)
+      if (!done[r]) P[r * PLS + w - 1] = __dmul_rn(P[r * PLS + w - 1], inv_prev);
     __syncthreads();
   }
   cluster.sync();  // no CTA leaves while others may still read its shared memory
