@@ -13,6 +13,7 @@
 //   form / certificate / accumulate elementwise kernels (HBM-bound)
 #include <climits>
 
+#include "gemm_tile.cuh"
 #include "pf_common.cuh"
 #include "pf_kernels.h"
 
@@ -199,26 +200,23 @@ __global__ void __launch_bounds__(256) lu_base64_kernel(double* M, int64_t ld, i
 // inverses of both 64 blocks in `inv`.
 size_t lu_base128_smem_bytes() { return sizeof(double) * (5 * B64 * L64 + 8 * 16 * TSW); }
 
-__global__ void __launch_bounds__(256) lu_base128_kernel(double* M, int64_t ld, int64_t strideM, int off,
-                                                         double* inv, int64_t inv_stride) {
-  extern __shared__ __align__(16) double lu_smem[];
+// a: the block's origin (leading dimension ld), out: its two 64-blocks' L / U inverses (4 x 64^2).
+// Global reads bypass L1 (ld.global.cg): the persistent LU calls this on data other SMs just wrote.
+__device__ void lu128_block(double* a, int64_t ld, double* out, double* lu_smem) {
   double* s = lu_smem;          // the diagonal block being factored (A11, then A22)
   double* xl = s + B64 * L64;   // its L^-1
   double* xu = xl + B64 * L64;  // its U^-1
   double* pa = xu + B64 * L64;  // A12 -> U12
   double* qa = pa + B64 * L64;  // A21 -> L21
   double* scratch = qa + B64 * L64;
-  const int z = blockIdx.x;
-  double* a = M + (int64_t)z * strideM + (int64_t)off * ld + off;
   double* a12 = a + B64;
   double* a21 = a + (int64_t)B64 * ld;
   double* a22 = a21 + B64;
-  double* out = inv + (int64_t)z * inv_stride + (int64_t)(off / B64) * 2 * B64 * B64;
   for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
     const int r = idx >> 6, c = idx & 63;
-    s[r * L64 + c] = a[(int64_t)r * ld + c];
-    pa[r * L64 + c] = a12[(int64_t)r * ld + c];
-    qa[r * L64 + c] = a21[(int64_t)r * ld + c];
+    s[r * L64 + c] = __ldcg(a + (int64_t)r * ld + c);
+    pa[r * L64 + c] = __ldcg(a12 + (int64_t)r * ld + c);
+    qa[r * L64 + c] = __ldcg(a21 + (int64_t)r * ld + c);
     xl[r * L64 + c] = 0.0;
     xu[r * L64 + c] = 0.0;
   }
@@ -268,7 +266,7 @@ __global__ void __launch_bounds__(256) lu_base128_kernel(double* M, int64_t ld, 
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int r = 16 * i + 8 * mi + g, c = 16 * j + 8 * nj + 2 * t + e;
-          s[r * L64 + c] = a22[(int64_t)r * ld + c] - pr[mi][nj][e];
+          s[r * L64 + c] = __ldcg(a22 + (int64_t)r * ld + c) - pr[mi][nj][e];
         }
   }
   for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
@@ -285,6 +283,14 @@ __global__ void __launch_bounds__(256) lu_base128_kernel(double* M, int64_t ld, 
     out2[idx] = xl[r * L64 + c];
     out2[B64 * B64 + idx] = xu[r * L64 + c];
   }
+}
+
+__global__ void __launch_bounds__(256) lu_base128_kernel(double* M, int64_t ld, int64_t strideM, int off,
+                                                         double* inv, int64_t inv_stride) {
+  extern __shared__ __align__(16) double lu_smem[];
+  const int z = blockIdx.x;
+  lu128_block(M + (int64_t)z * strideM + (int64_t)off * ld + off, ld,
+              inv + (int64_t)z * inv_stride + (int64_t)(off / B64) * 2 * B64 * B64, lu_smem);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -331,38 +337,33 @@ __device__ __forceinline__ void store64(double* D, const double* base, const dou
 }
 }  // namespace
 
-__global__ void __launch_bounds__(256) trsm128_kernel(const double* M, int64_t ld, int64_t strideM, int off,
-                                                      const double* inv, int64_t inv_stride, int mode, double* Bm,
-                                                      int64_t ldb, int64_t strideB, int extent) {
-  extern __shared__ __align__(16) double t_smem[];
+// m: the 128 diagonal block's origin, blkinv: its 64-blocks' inverses, b: the 64-column (left modes)
+// or 64-row (right mode) chunk of B, `live` of them in range. Global reads bypass L1 (ld.global.cg).
+__device__ void trsm128_chunk(const double* m, int64_t ld, const double* blkinv, int mode, double* b, int64_t ldb,
+                              int live, double* t_smem) {
   double* t1 = t_smem;             // first inverse to apply
   double* t2 = t1 + B64 * L64;     // second inverse
   double* cpl = t2 + B64 * L64;    // coupling block (L21 or U12)
   double* b1 = cpl + B64 * L64;    // the chunk's first 64 (rows, or columns in mode 2)
   double* b2 = b1 + B64 * L64;     // ... and second 64
-  const int z = blockIdx.y, tile = blockIdx.x;
-  const double* blkinv = inv + (int64_t)z * inv_stride + (int64_t)(off / B64) * 2 * B64 * B64;
-  const double* m = M + (int64_t)z * strideM + (int64_t)off * ld + off;
   const bool right = mode == 2;
-  double* b = Bm + (int64_t)z * strideB + (right ? (int64_t)tile * B64 * ldb : (int64_t)tile * B64);
-  const int live = min(B64, extent - tile * B64);  // columns (left) or rows (right) in range
   // mode 0: t1 = L11^-1, t2 = L22^-1, cpl = L21; modes 1, 2: t1 = U11^-1, t2 = U22^-1, cpl = U12
   const double* i1 = blkinv + (mode == 0 ? 0 : B64 * B64);
   const double* i2 = blkinv + 2 * B64 * B64 + (mode == 0 ? 0 : B64 * B64);
   const double* c0 = mode == 0 ? m + (int64_t)B64 * ld : m + B64;
   for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
     const int r = idx >> 6, c = idx & 63;
-    t1[r * L64 + c] = i1[idx];
-    t2[r * L64 + c] = i2[idx];
-    cpl[r * L64 + c] = c0[(int64_t)r * ld + c];
+    t1[r * L64 + c] = __ldcg(i1 + idx);
+    t2[r * L64 + c] = __ldcg(i2 + idx);
+    cpl[r * L64 + c] = __ldcg(c0 + (int64_t)r * ld + c);
     if (!right) {  // B rows r and 64 + r, chunk column c
       const bool ok = c < live;
-      b1[r * L64 + c] = ok ? b[(int64_t)r * ldb + c] : 0.0;
-      b2[r * L64 + c] = ok ? b[(int64_t)(B64 + r) * ldb + c] : 0.0;
+      b1[r * L64 + c] = ok ? __ldcg(b + (int64_t)r * ldb + c) : 0.0;
+      b2[r * L64 + c] = ok ? __ldcg(b + (int64_t)(B64 + r) * ldb + c) : 0.0;
     } else {  // B row r of the chunk, columns c and 64 + c
       const bool ok = r < live;
-      b1[r * L64 + c] = ok ? b[(int64_t)r * ldb + c] : 0.0;
-      b2[r * L64 + c] = ok ? b[(int64_t)r * ldb + B64 + c] : 0.0;
+      b1[r * L64 + c] = ok ? __ldcg(b + (int64_t)r * ldb + c) : 0.0;
+      b2[r * L64 + c] = ok ? __ldcg(b + (int64_t)r * ldb + B64 + c) : 0.0;
     }
   }
   __syncthreads();
@@ -417,6 +418,18 @@ __global__ void __launch_bounds__(256) trsm128_kernel(const double* M, int64_t l
       b[(int64_t)r * ldb + B64 + c] = b2[r * L64 + c];
     }
   }
+}
+
+__global__ void __launch_bounds__(256) trsm128_kernel(const double* M, int64_t ld, int64_t strideM, int off,
+                                                      const double* inv, int64_t inv_stride, int mode, double* Bm,
+                                                      int64_t ldb, int64_t strideB, int extent) {
+  extern __shared__ __align__(16) double t_smem[];
+  const int z = blockIdx.y, tile = blockIdx.x;
+  const bool right = mode == 2;
+  trsm128_chunk(M + (int64_t)z * strideM + (int64_t)off * ld + off, ld,
+                inv + (int64_t)z * inv_stride + (int64_t)(off / B64) * 2 * B64 * B64, mode,
+                Bm + (int64_t)z * strideB + (right ? (int64_t)tile * B64 * ldb : (int64_t)tile * B64), ldb,
+                min(B64, extent - tile * B64), t_smem);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -839,6 +852,106 @@ __global__ void lincomb2_kernel(int n, int k, double d1, const double* X, double
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(idx / k), c = (int)(idx % k);
     out[(int64_t)r * ldo + c] = __dadd_rn(__dmul_rn(d1, X[(int64_t)r * ld + c]), __dmul_rn(d2, Y[(int64_t)r * ld + c]));
+  }
+}
+// ---------------------------------------------------------------------------------------------
+// Device-scheduled tile-DAG LU (no exchanges: the certified systems) of nsys systems of order np
+// (a multiple of 128), one persistent CTA per SM. The 128 x 128 tiles of every system form the DAG
+//   F(k)      LU of the diagonal tile (k, k) + its 64-block L / U inverses      (lu128_block)
+//   R(k, j)   U_kj = L_kk^-1 A_kj,  C(i, k)  L_ik = A_ik U_kk^-1                 (trsm128_chunk)
+//   G(i,j,k)  A_ij -= L_ik U_kj                                                  (gemm_tile, DMMA)
+// listed by the host in a topological order with one step of look-ahead (the tiles of row / column
+// k + 1 are updated, F(k + 1) and its panel solved before the rest of step k's trailing update). CTAs
+// pull the next task from a global counter, wait (acquire) until its inputs are final, run it and
+// publish (release) the tile's new state = the number of steps applied to it. Every CTA only waits
+// for tasks listed earlier, all of which are held by running CTAs: no deadlock. The 8 systems of a
+// batch share every wave, and the whole factorisation is one launch instead of the recursion's
+// hundreds of dependent ones. Each tile's updates run in step order, so the result does not depend
+// on which CTA runs which task. A spin limit turns a scheduling bug into an error flag, not a hang.
+namespace {
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ bool wait_ge(const int* p, int need, int* err) {
+  unsigned spins = 0;
+  while (ld_acquire(p) < need) {
+    if (ld_acquire(err)) return false;
+    __nanosleep(64);
+    if (++spins > (1u << 25)) {
+      atomicExch(err, 1);
+      return false;
+    }
+  }
+  return true;
+}
+}  // namespace
+
+size_t lu_dag_smem_bytes() {
+  size_t b = lu_base128_smem_bytes();
+  b = b > trsm128_smem_bytes() ? b : trsm128_smem_bytes();
+  b = b > sizeof(GemmSmem<128, 128, 16>) ? b : sizeof(GemmSmem<128, 128, 16>);
+  return b;
+}
+
+__global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64_t strideM, double* inv,
+                                                        int64_t inv_stride, const int4* tasks, int ntasks, int* next,
+                                                        int* state, int nt, int* err) {
+  extern __shared__ __align__(16) unsigned char dag_smem[];
+  double* dsm = reinterpret_cast<double*>(dag_smem);
+  __shared__ int s_task, s_ok;
+  constexpr int T = 128;
+  for (;;) {
+    if (threadIdx.x == 0) s_task = atomicAdd(next, 1);
+    __syncthreads();
+    const int t = s_task;
+    if (t >= ntasks) return;
+    const int4 tk = tasks[t];
+    const int type = tk.x >> 24, z = tk.x & 0xffffff, i = tk.y, j = tk.z, k = tk.w;  // tile (i, j), step k
+    int* st = state + (int64_t)z * nt * nt;
+    if (threadIdx.x == 0) {
+      bool ok = wait_ge(st + i * nt + j, k, err);  // the tile has received steps 0 .. k-1
+      if (ok && (type == 1 || type == 2)) ok = wait_ge(st + k * nt + k, k + 1, err);  // F(k) done
+      if (ok && type == 3) ok = wait_ge(st + i * nt + k, k + 1, err) && wait_ge(st + k * nt + j, k + 1, err);
+      s_ok = ok;
+    }
+    __syncthreads();
+    if (!s_ok) return;
+    double* Mz = M + (int64_t)z * strideM;
+    double* dblk = Mz + (int64_t)T * k * np + T * k;  // diagonal tile of step k
+    double* bi = inv + (int64_t)z * inv_stride + (int64_t)(2 * k) * 2 * B64 * B64;
+    double* tile = Mz + (int64_t)T * i * np + T * j;
+    if (type == 0) {
+      lu128_block(dblk, np, bi, dsm);
+    } else if (type == 1 || type == 2) {
+      for (int h = 0; h < 2; ++h) {  // two 64-column (R) / 64-row (C) chunks
+        trsm128_chunk(dblk, np, bi, type == 1 ? 0 : 2, type == 1 ? tile + B64 * h : tile + (int64_t)B64 * h * np, np,
+                      B64, dsm);
+        __syncthreads();
+      }
+    } else {
+      GemmParams p{};
+      p.m = p.n = p.k = T;
+      p.batch = 1;
+      p.alpha = -1.0;
+      p.beta = 1.0;
+      p.A = Mz + (int64_t)T * i * np + T * k;
+      p.lda = np;
+      p.B = Mz + (int64_t)T * k * np + T * j;
+      p.ldb = np;
+      p.C = tile;
+      p.ldc = np;
+      gemm_tile<128, 128, 16, 32, 64, true>(p, *reinterpret_cast<GemmSmem<128, 128, 16>*>(dag_smem), 0, 0, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      st_release(st + i * nt + j, k + 1);
+    }
   }
 }
 }  // namespace pf

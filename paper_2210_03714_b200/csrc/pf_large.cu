@@ -8,6 +8,8 @@
 //   B U^-1       = [B1 U11^-1, (B2 - B1 U12) U22^-1]
 // The same arithmetic as dense.cpp's right-looking LU / substitution (dense.cpp:102-163), blocked.
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -57,6 +59,9 @@ __global__ void lincomb2_kernel(int n, int k, double d1, const double* X, double
 size_t apply_inv64_smem_bytes();
 size_t lu_base64_smem_bytes();
 __global__ void lu_base128_kernel(double* M, int64_t ld, int64_t strideM, int off, double* inv, int64_t inv_stride);
+__global__ void lu_dag_kernel(double* M, int np, int64_t strideM, double* inv, int64_t inv_stride, const int4* tasks,
+                              int ntasks, int* next, int* state, int nt, int* err);
+size_t lu_dag_smem_bytes();
 size_t lu_base128_smem_bytes();
 __global__ void trsm128_kernel(const double* M, int64_t ld, int64_t strideM, int off, const double* inv,
                                int64_t inv_stride, int mode, double* Bm, int64_t ldb, int64_t strideB, int extent);
@@ -356,14 +361,83 @@ void run_lu_graph(pf_context* ctx, const Sys& s) {  // on ctx->stream == ctx->gs
   }
 }
 
-void run_lu(pf_context* ctx, const Sys& s) {
+// The device-scheduled tile-DAG LU (large.cu lu_dag_kernel): one persistent launch for the whole
+// factorisation of every system. Task list (type F 0 / R 1 / C 2 / G 3, system, tile, step) in a
+// topological order with one step of look-ahead; built once per (tiles, systems) and cached.
+const std::vector<int4>& dag_tasks(int nt, int nsys) {
+  static std::map<std::pair<int, int>, std::vector<int4>> cache;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_pair(nt, nsys);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  std::vector<int4> t;
+  auto add = [&](int type, int i, int j, int k) {
+    for (int z = 0; z < nsys; ++z) t.push_back(make_int4((type << 24) | z, i, j, k));
+  };
+  auto panel = [&](int k) {  // F(k), then R(k, j) / C(j, k) interleaved, nearest first
+    add(0, k, k, k);
+    for (int j = k + 1; j < nt; ++j) {
+      add(1, k, j, k);
+      add(2, j, k, k);
+    }
+  };
+  panel(0);
+  for (int k = 0; k + 1 < nt; ++k) {
+    const int n1 = k + 1;
+    add(3, n1, n1, k);  // the tiles of row / column k + 1 first: F(k + 1)'s look-ahead
+    for (int j = n1 + 1; j < nt; ++j) {
+      add(3, n1, j, k);
+      add(3, j, n1, k);
+    }
+    panel(n1);
+    for (int i = n1 + 1; i < nt; ++i)
+      for (int j = n1 + 1; j < nt; ++j) add(3, i, j, k);
+  }
+  return cache.emplace(key, std::move(t)).first->second;
+}
+
+// 1: factored, 0: not applicable (use the recursion), -1: the DAG reported a scheduling failure
+int run_lu_dag(pf_context* ctx, const Sys& s) {
+  // PF_LU_DAG=0 keeps the recursion; =1 forces the DAG wherever it applies (np a multiple of 128)
+  static const int mode = std::getenv("PF_LU_DAG") ? std::atoi(std::getenv("PF_LU_DAG")) : -1;
+  if (mode == 0 || s.np % 128 != 0 || s.np < 256) return 0;
+  if (mode < 0 && (s.np < 1024 || s.nsys > 64)) return 0;  // the recursion's big batched launches win there
+  const int nt = s.np / 128;
+  const std::vector<int4>& tasks = dag_tasks(nt, s.nsys);
+  int4* d_tasks = static_cast<int4*>(workspace(ctx, kWsSmallArrays + 28, sizeof(int4) * tasks.size()));
+  int* d_state = static_cast<int*>(workspace(ctx, kWsSmallArrays + 29, sizeof(int) * ((size_t)s.nsys * nt * nt + 2)));
+  if (!d_tasks || !d_state) return 0;
+  int* d_next = d_state + (size_t)s.nsys * nt * nt;
+  int* d_err = d_next + 1;
+  cudaMemcpyAsync(d_tasks, tasks.data(), sizeof(int4) * tasks.size(), cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemsetAsync(d_state, 0, sizeof(int) * ((size_t)s.nsys * nt * nt + 2), ctx->stream);
+  const int smem = (int)lu_dag_smem_bytes();
+  if (set_smem_attr_once(reinterpret_cast<const void*>(lu_dag_kernel), smem) != cudaSuccess) return 0;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  lu_dag_kernel<<<sms, 256, smem, ctx->stream>>>(s.M, s.np, s.stride(), s.inv, s.inv_stride, d_tasks,
+                                                 (int)tasks.size(), d_next, d_state, nt, d_err);
+  ctx->launches++;
+  if (cudaGetLastError() != cudaSuccess) return -1;
+  // the spin-limit flag (a scheduling bug must not pass as a factorisation)
+  if (cudaMemcpyAsync(ctx->h_first_error, d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+      cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+    return -1;
+  return *ctx->h_first_error == 0 ? 1 : -1;
+}
+
+// false only when the device-scheduled LU failed (the factors are then unusable)
+bool run_lu(pf_context* ctx, const Sys& s) {
+  const int dag = run_lu_dag(ctx, s);
+  if (dag != 0) return dag > 0;
   // opt-in (PF_LU_GRAPH=1): instantiating the captured recursion costs ~6 ms (128 leaves) to
   // ~40 ms (64 leaves) once per buffer set, so it pays off only over many repeated factorisations
   // of the same shape and buffers (-3 % per call at n = 4096); one-shot calls lose (cfg3 +5 ms)
   static const bool graphs = std::getenv("PF_LU_GRAPH") != nullptr && std::getenv("PF_LOOKAHEAD") == nullptr;
   if (!graphs || !graph_stream(ctx) || !fork_side(ctx)) {  // fork_side: the side stream exists
     lu_rec(ctx, s, 0, s.np);
-    return;
+    return true;
   }
   cudaStream_t main = ctx->stream;
   cudaEventRecord(ctx->ev_g0, main);
@@ -373,6 +447,7 @@ void run_lu(pf_context* ctx, const Sys& s) {
   ctx->stream = main;
   cudaEventRecord(ctx->ev_g1, ctx->gstream);
   cudaStreamWaitEvent(main, ctx->ev_g1, 0);
+  return true;
 }
 
 void diag_inverses(pf_context* ctx, const Sys& s) {
@@ -513,7 +588,7 @@ FactorResult factor_systems(pf_context* ctx, const Sys& s, int n, unsigned long 
     return fr;
   }
   if (nf == 0) {
-    run_lu(ctx, s);
+    if (!run_lu(ctx, s)) fr.rc = PF_ERR_CUDA;
     return fr;
   }
   fr.pivoted = true;
@@ -528,7 +603,10 @@ FactorResult factor_systems(pf_context* ctx, const Sys& s, int n, unsigned long 
     for (int q = 0; q < nf; ++q)
       cudaMemcpyAsync(side + q * s.stride(), s.M + fails[q] * s.stride(), sizeof(double) * s.stride(),
                       cudaMemcpyDeviceToDevice, ctx->stream);
-    run_lu(ctx, s);
+    if (!run_lu(ctx, s)) {
+      fr.rc = PF_ERR_CUDA;
+      return fr;
+    }
     for (int q = 0; q < nf; ++q)
       cudaMemcpyAsync(s.M + fails[q] * s.stride(), side + q * s.stride(), sizeof(double) * s.stride(),
                       cudaMemcpyDeviceToDevice, ctx->stream);
