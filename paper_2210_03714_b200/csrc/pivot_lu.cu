@@ -212,6 +212,148 @@ __global__ void __launch_bounds__(PT) panel_lu_cluster_kernel(double* M, int64_t
     }
 }
 
+// The panel in REGISTERS: one row per thread (256 rows per CTA, up to 16 CTAs per cluster: panels of
+// up to 4096 rows). Each thread keeps its row's 64 values in registers for the whole panel, so the
+// rank-1 update of a column is 64 - c register FMAs per thread against the pivot row (read from shared
+// memory as a broadcast); only the per-column pivot agreement goes through shared / distributed
+// shared memory (three barriers per column, one cluster-wide). The column loop is fully unrolled so
+// every register index is a compile-time constant.
+constexpr int RT = 256;  // threads (= rows) per CTA
+struct RegPanelShared {
+  double cand_v[2];
+  int cand_l[2];
+  int cand_t[2];       // owning thread of the candidate row
+  double crow[2][PW];  // the candidate row
+  double rows[16][PW]; // every CTA's candidate row, gathered
+  double cv[16];
+  int cl[16];
+  double red_v[RT / 32];
+  int red_l[RT / 32], red_t[RT / 32];
+};
+
+__global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t ld, int64_t strideM, int np, int off,
+                                                             int* piv, int npiv, const double* tol, const int* zorig,
+                                                             int* failed, DevStatus* status, int* first_error,
+                                                             int2* moves, int* moves_n) {
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ RegPanelShared sh;
+  const int z = blockIdx.y;
+  const int rank = (int)cluster.block_rank();
+  const int C = (int)cluster.num_blocks();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int row = rank * RT + tid;  // relative to off
+  const bool have = row < np - off;
+  double* a = M + (int64_t)z * strideM;
+  const bool dead = failed[z] != 0;
+  double v[PW];
+  if (have) {
+    const double2* src = reinterpret_cast<const double2*>(a + (int64_t)(off + row) * ld + off);
+#pragma unroll
+    for (int j = 0; j < PW / 2; ++j) {
+      const double2 t = src[j];
+      v[2 * j] = t.x;
+      v[2 * j + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < PW; ++j) v[j] = 0.0;
+  }
+  int pos = row;         // position in the exchanged order
+  bool done = !have;     // pivot rows (and rows past the matrix) take no further part
+  if (tid == 0 && rank == 0) moves_n[z] = 0;
+  cluster.sync();
+  bool singular = false;
+  // uniform over the cluster (every CTA reduces the same candidates): no thread diverges from the
+  // barriers; no `break`, so the loop unrolls and v[] stays in registers
+#pragma unroll
+  for (int c = 0; c < PW; ++c) {
+    if (dead || singular) continue;
+    const int slot = c & 1;
+    // ---- this CTA's candidate
+    double bv = done ? -1.0 : fabs(v[c]);
+    int bl = done ? INT_MAX : pos, bt = tid;
+    for (int o = 16; o > 0; o >>= 1)
+      better(bv, bl, bt, __shfl_xor_sync(FULL, bv, o), __shfl_xor_sync(FULL, bl, o), __shfl_xor_sync(FULL, bt, o));
+    if (lane == 0) {
+      sh.red_v[warp] = bv;
+      sh.red_l[warp] = bl;
+      sh.red_t[warp] = bt;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      bv = lane < RT / 32 ? sh.red_v[lane] : -1.0;
+      bl = lane < RT / 32 ? sh.red_l[lane] : INT_MAX;
+      bt = lane < RT / 32 ? sh.red_t[lane] : 0;
+      for (int o = 16; o > 0; o >>= 1)
+        better(bv, bl, bt, __shfl_xor_sync(FULL, bv, o), __shfl_xor_sync(FULL, bl, o), __shfl_xor_sync(FULL, bt, o));
+      if (lane == 0) {
+        sh.cand_v[slot] = bv;
+        sh.cand_l[slot] = bl;
+        sh.cand_t[slot] = bt;
+      }
+    }
+    __syncthreads();
+    if (tid == sh.cand_t[slot]) {
+#pragma unroll
+      for (int j = 0; j < PW; ++j) sh.crow[slot][j] = v[j];
+    }
+    if (C > 1)
+      cluster.sync();
+    else
+      __syncthreads();
+    // ---- every candidate and its row (one DSMEM round trip), the pivot
+    for (int t = tid; t < C * PW; t += RT) {
+      const RegPanelShared* o = C > 1 ? cluster.map_shared_rank(&sh, t / PW) : &sh;
+      sh.rows[t / PW][t % PW] = o->crow[slot][t % PW];
+      if (t % PW == 0) {
+        sh.cv[t / PW] = o->cand_v[slot];
+        sh.cl[t / PW] = o->cand_l[slot];
+      }
+    }
+    __syncthreads();
+    double gv = -1.0;
+    int p = INT_MAX, q = -1;
+    for (int k = 0; k < C; ++k) better(gv, p, q, sh.cv[k], sh.cl[k], k);
+    if (gv <= tol[z]) {
+      if (rank == 0 && tid == 0) {
+        status[zorig[z]].code = PF_ERR_SINGULAR_SHIFT;
+        status[zorig[z]].column = off + c;
+        status[zorig[z]].pivot_magnitude = gv;
+        failed[z] = 1;
+        atomicMin(first_error, zorig[z]);
+      }
+      singular = true;
+      continue;
+    }
+    const double* prow = sh.rows[q];
+    const bool me = rank == q && tid == sh.cand_t[slot];
+    if (rank == 0 && tid == 0) piv[(int64_t)z * npiv + off + c] = off + p;
+    if (me) {
+      pos = c;
+      done = true;
+    } else if (!done) {
+      if (pos == c) pos = p;
+      const double f = __dmul_rn(v[c], 1.0 / prow[c]);
+      v[c] = f;
+      if (f != 0.0) {
+#pragma unroll
+        for (int j = c + 1; j < PW; ++j) v[j] = __dsub_rn(v[j], __dmul_rn(f, prow[j]));
+      }
+    } else if (pos == c) {
+      pos = p;
+    }
+  }
+  cluster.sync();  // no CTA leaves while others may still read its shared memory
+  if (dead || singular || !have) return;
+  double2* dst = reinterpret_cast<double2*>(a + (int64_t)(off + pos) * ld + off);
+#pragma unroll
+  for (int j = 0; j < PW / 2; ++j) dst[j] = make_double2(v[2 * j], v[2 * j + 1]);
+  if (pos != row) {
+    const int k = atomicAdd(moves_n + z, 1);
+    moves[(int64_t)z * 2 * PW + k] = make_int2(off + pos, off + row);
+  }
+}
+
 // The same panel in global memory, one CTA per system (panels taller than the cluster's shared
 // memory): explicit exchanges inside the panel columns, the moves listed from the swap sequence.
 __global__ void __launch_bounds__(1024) panel_lu_global_kernel(double* M, int64_t ld, int64_t strideM, int np,
@@ -338,6 +480,36 @@ cudaError_t launch_panel_lu(double* M, int64_t ld, int64_t strideM, int np, int 
                             int npiv, const double* tol, const int* zorig, int* failed, DevStatus* status,
                             int* first_error, int2* moves, int* moves_n, cudaStream_t stream) {
   const int rows = np - off;
+  static const bool no_reg = std::getenv("PF_PANEL_SMEM") != nullptr;  // A/B: the shared-memory panel
+  if (w == PW && rows <= 16 * RT && !no_reg) {
+    int Cr = 1;
+    while (Cr * RT < rows) Cr *= 2;
+    static bool attr_r = false;
+    if (!attr_r) {
+      cudaFuncSetAttribute(panel_lu_reg_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      attr_r = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(Cr, nsys);
+    cfg.blockDim = dim3(RT);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = Cr;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t er = cudaLaunchKernelEx(&cfg, panel_lu_reg_kernel, M, ld, strideM, np, off, piv, npiv, tol, zorig,
+                                        failed, status, first_error, moves, moves_n);
+    if (er == cudaSuccess) {
+      row_move_kernel<<<dim3((np + MC - 1) / MC, nsys), 256, 0, stream>>>(M, ld, strideM, np, off, w, moves,
+                                                                          moves_n, failed);
+      return cudaGetLastError();
+    }
+    cudaGetLastError();
+  }
   // smallest cluster whose CTAs hold <= 384 rows each (<= 210 KB of shared memory), up to 16 CTAs
   int C = 1;
   while (C < 16 && (rows + C - 1) / C > MAX_ROWS_PER_CTA) C *= 2;
