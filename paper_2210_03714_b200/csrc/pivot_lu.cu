@@ -263,14 +263,20 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
   if (tid == 0 && rank == 0) moves_n[z] = 0;
   cluster.sync();
   bool singular = false;
-  // uniform over the cluster (every CTA reduces the same candidates): no thread diverges from the
-  // barriers; no `break`, so the loop unrolls and v[] stays in registers
-#pragma unroll
+  // The column loop is NOT unrolled (a fully unrolled panel is ~200 KB of code: instruction-fetch
+  // bound); v[] stays in registers because every access uses a compile-time index: the column-c value
+  // is selected and written back with predicated unrolled loops over j. Uniform over the cluster
+  // (every CTA reduces the same candidates): no thread diverges from the barriers.
+#pragma unroll 1
   for (int c = 0; c < PW; ++c) {
     if (dead || singular) continue;
     const int slot = c & 1;
+    double vc = 0.0;
+#pragma unroll
+    for (int j = 0; j < PW; ++j)
+      if (j == c) vc = v[j];
     // ---- this CTA's candidate
-    double bv = done ? -1.0 : fabs(v[c]);
+    double bv = done ? -1.0 : fabs(vc);
     int bl = done ? INT_MAX : pos, bt = tid;
     for (int o = 16; o > 0; o >>= 1)
       better(bv, bl, bt, __shfl_xor_sync(FULL, bv, o), __shfl_xor_sync(FULL, bl, o), __shfl_xor_sync(FULL, bt, o));
@@ -296,7 +302,7 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
     if (tid == sh.cand_t[slot]) {
 #pragma unroll
       for (int j = 0; j < PW; ++j) sh.crow[slot][j] = v[j];
-    }
+    }  // (the candidate thread is the same for every j: no divergence inside)
     if (C > 1)
       cluster.sync();
     else
@@ -333,12 +339,15 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
       done = true;
     } else if (!done) {
       if (pos == c) pos = p;
-      const double f = __dmul_rn(v[c], 1.0 / prow[c]);
-      v[c] = f;
+      const double f = __dmul_rn(vc, 1.0 / prow[c]);
       if (f != 0.0) {
 #pragma unroll
-        for (int j = c + 1; j < PW; ++j) v[j] = __dsub_rn(v[j], __dmul_rn(f, prow[j]));
+        for (int j = 0; j < PW; ++j)
+          if (j > c) v[j] = __dsub_rn(v[j], __dmul_rn(f, prow[j]));
       }
+#pragma unroll
+      for (int j = 0; j < PW; ++j)
+        if (j == c) v[j] = f;
     } else if (pos == c) {
       pos = p;
     }
