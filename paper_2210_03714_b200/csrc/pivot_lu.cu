@@ -214,22 +214,49 @@ __global__ void __launch_bounds__(PT) panel_lu_cluster_kernel(double* M, int64_t
 
 // The panel in REGISTERS: one row per thread (256 rows per CTA, up to 16 CTAs per cluster: panels of
 // up to 4096 rows). Each thread keeps its row's 64 values in registers for the whole panel, so the
-// rank-1 update of a column is 64 - c register FMAs per thread against the pivot row (read from shared
-// memory as a broadcast); only the per-column pivot agreement goes through shared / distributed
-// shared memory (three barriers per column, one cluster-wide). The column loop is fully unrolled so
-// every register index is a compile-time constant.
+// rank-1 update of a column is register FMAs against the pivot row (read from shared memory as a
+// broadcast). Per column: the CTA's candidate (warp shuffles), then its value and row are PUSHED into
+// every CTA's shared memory (remote stores over DSMEM, slot = rank, double-buffered by column
+// parity), one cluster barrier, and every CTA picks the pivot from its local copies -- no remote
+// load on the critical path. Three barriers per column, one of them cluster-wide.
+// Register indices are compile-time constants: the column value is picked by a uniform switch, the
+// update runs over the 8-column block containing c (predicated j > c) and the blocks after it.
 constexpr int RT = 256;  // threads (= rows) per CTA
 struct RegPanelShared {
-  double cand_v[2];
-  int cand_l[2];
-  int cand_t[2];       // owning thread of the candidate row
-  double crow[2][PW];  // the candidate row
-  double rows[16][PW]; // every CTA's candidate row, gathered
-  double cv[16];
-  int cl[16];
+  double cv[2][16];        // [parity][rank] candidate |value|
+  int cl[2][16];           // candidate position in the exchanged order
+  int ct[2][16];           // candidate's owning thread (meaningful for its own CTA)
+  double rows[2][16][PW];  // [parity][rank] candidate row
   double red_v[RT / 32];
   int red_l[RT / 32], red_t[RT / 32];
 };
+
+template <int B>
+__device__ __forceinline__ void update_from_block(double (&v)[PW], int c, double f, const double* prow) {
+#pragma unroll
+  for (int j = 8 * B; j < PW; ++j)
+    if (j > c) v[j] = __dsub_rn(v[j], __dmul_rn(f, prow[j]));
+}
+
+__device__ __forceinline__ double pick(const double (&v)[PW], int c) {
+  double r = 0.0;
+  switch (c) {
+#define PF_PICK(k) \
+  case k:          \
+    r = v[k];      \
+    break;
+    PF_PICK(0) PF_PICK(1) PF_PICK(2) PF_PICK(3) PF_PICK(4) PF_PICK(5) PF_PICK(6) PF_PICK(7)
+    PF_PICK(8) PF_PICK(9) PF_PICK(10) PF_PICK(11) PF_PICK(12) PF_PICK(13) PF_PICK(14) PF_PICK(15)
+    PF_PICK(16) PF_PICK(17) PF_PICK(18) PF_PICK(19) PF_PICK(20) PF_PICK(21) PF_PICK(22) PF_PICK(23)
+    PF_PICK(24) PF_PICK(25) PF_PICK(26) PF_PICK(27) PF_PICK(28) PF_PICK(29) PF_PICK(30) PF_PICK(31)
+    PF_PICK(32) PF_PICK(33) PF_PICK(34) PF_PICK(35) PF_PICK(36) PF_PICK(37) PF_PICK(38) PF_PICK(39)
+    PF_PICK(40) PF_PICK(41) PF_PICK(42) PF_PICK(43) PF_PICK(44) PF_PICK(45) PF_PICK(46) PF_PICK(47)
+    PF_PICK(48) PF_PICK(49) PF_PICK(50) PF_PICK(51) PF_PICK(52) PF_PICK(53) PF_PICK(54) PF_PICK(55)
+    PF_PICK(56) PF_PICK(57) PF_PICK(58) PF_PICK(59) PF_PICK(60) PF_PICK(61) PF_PICK(62) PF_PICK(63)
+#undef PF_PICK
+  }
+  return r;
+}
 
 __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t ld, int64_t strideM, int np, int off,
                                                              int* piv, int npiv, const double* tol, const int* zorig,
@@ -258,23 +285,18 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
 #pragma unroll
     for (int j = 0; j < PW; ++j) v[j] = 0.0;
   }
-  int pos = row;         // position in the exchanged order
-  bool done = !have;     // pivot rows (and rows past the matrix) take no further part
+  int pos = row;      // position in the exchanged order
+  bool done = !have;  // pivot rows (and rows past the matrix) take no further part
   if (tid == 0 && rank == 0) moves_n[z] = 0;
   cluster.sync();
   bool singular = false;
-  // The column loop is NOT unrolled (a fully unrolled panel is ~200 KB of code: instruction-fetch
-  // bound); v[] stays in registers because every access uses a compile-time index: the column-c value
-  // is selected and written back with predicated unrolled loops over j. Uniform over the cluster
-  // (every CTA reduces the same candidates): no thread diverges from the barriers.
+  // the column loop stays rolled (a fully unrolled panel is instruction-fetch bound); uniform over
+  // the cluster, so no thread diverges from the barriers
 #pragma unroll 1
   for (int c = 0; c < PW; ++c) {
     if (dead || singular) continue;
-    const int slot = c & 1;
-    double vc = 0.0;
-#pragma unroll
-    for (int j = 0; j < PW; ++j)
-      if (j == c) vc = v[j];
+    const int par = c & 1;
+    const double vc = pick(v, c);
     // ---- this CTA's candidate
     double bv = done ? -1.0 : fabs(vc);
     int bl = done ? INT_MAX : pos, bt = tid;
@@ -286,40 +308,33 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
       sh.red_t[warp] = bt;
     }
     __syncthreads();
-    if (warp == 0) {
-      bv = lane < RT / 32 ? sh.red_v[lane] : -1.0;
-      bl = lane < RT / 32 ? sh.red_l[lane] : INT_MAX;
-      bt = lane < RT / 32 ? sh.red_t[lane] : 0;
-      for (int o = 16; o > 0; o >>= 1)
-        better(bv, bl, bt, __shfl_xor_sync(FULL, bv, o), __shfl_xor_sync(FULL, bl, o), __shfl_xor_sync(FULL, bt, o));
-      if (lane == 0) {
-        sh.cand_v[slot] = bv;
-        sh.cand_l[slot] = bl;
-        sh.cand_t[slot] = bt;
+    bv = lane < RT / 32 ? sh.red_v[lane] : -1.0;  // every warp reduces the 8 warp candidates
+    bl = lane < RT / 32 ? sh.red_l[lane] : INT_MAX;
+    bt = lane < RT / 32 ? sh.red_t[lane] : 0;
+    for (int o = 4; o > 0; o >>= 1)
+      better(bv, bl, bt, __shfl_xor_sync(FULL, bv, o), __shfl_xor_sync(FULL, bl, o), __shfl_xor_sync(FULL, bt, o));
+    bv = __shfl_sync(FULL, bv, 0);
+    bl = __shfl_sync(FULL, bl, 0);
+    bt = __shfl_sync(FULL, bt, 0);
+    // ---- push the candidate (value, position, row) into every CTA's slot [par][rank]
+    if (tid == bt) {
+      for (int q = 0; q < C; ++q) {
+        RegPanelShared* o = C > 1 ? cluster.map_shared_rank(&sh, q) : &sh;
+        o->cv[par][rank] = bv;
+        o->cl[par][rank] = bl;
+        o->ct[par][rank] = bt;
+#pragma unroll
+        for (int j = 0; j < PW; ++j) o->rows[par][rank][j] = v[j];
       }
     }
-    __syncthreads();
-    if (tid == sh.cand_t[slot]) {
-#pragma unroll
-      for (int j = 0; j < PW; ++j) sh.crow[slot][j] = v[j];
-    }  // (the candidate thread is the same for every j: no divergence inside)
     if (C > 1)
-      cluster.sync();
+      cluster.sync();  // release / acquire: every pushed candidate is visible to every CTA
     else
       __syncthreads();
-    // ---- every candidate and its row (one DSMEM round trip), the pivot
-    for (int t = tid; t < C * PW; t += RT) {
-      const RegPanelShared* o = C > 1 ? cluster.map_shared_rank(&sh, t / PW) : &sh;
-      sh.rows[t / PW][t % PW] = o->crow[slot][t % PW];
-      if (t % PW == 0) {
-        sh.cv[t / PW] = o->cand_v[slot];
-        sh.cl[t / PW] = o->cand_l[slot];
-      }
-    }
-    __syncthreads();
+    // ---- the pivot, from the local copies (every thread reduces the same C candidates in order)
     double gv = -1.0;
     int p = INT_MAX, q = -1;
-    for (int k = 0; k < C; ++k) better(gv, p, q, sh.cv[k], sh.cl[k], k);
+    for (int k = 0; k < C; ++k) better(gv, p, q, sh.cv[par][k], sh.cl[par][k], k);
     if (gv <= tol[z]) {
       if (rank == 0 && tid == 0) {
         status[zorig[z]].code = PF_ERR_SINGULAR_SHIFT;
@@ -331,8 +346,8 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
       singular = true;
       continue;
     }
-    const double* prow = sh.rows[q];
-    const bool me = rank == q && tid == sh.cand_t[slot];
+    const double* prow = sh.rows[par][q];
+    const bool me = rank == q && tid == sh.ct[par][q];
     if (rank == 0 && tid == 0) piv[(int64_t)z * npiv + off + c] = off + p;
     if (me) {
       pos = c;
@@ -341,9 +356,16 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
       if (pos == c) pos = p;
       const double f = __dmul_rn(vc, 1.0 / prow[c]);
       if (f != 0.0) {
-#pragma unroll
-        for (int j = 0; j < PW; ++j)
-          if (j > c) v[j] = __dsub_rn(v[j], __dmul_rn(f, prow[j]));
+        switch (c >> 3) {
+          case 0: update_from_block<0>(v, c, f, prow); break;
+          case 1: update_from_block<1>(v, c, f, prow); break;
+          case 2: update_from_block<2>(v, c, f, prow); break;
+          case 3: update_from_block<3>(v, c, f, prow); break;
+          case 4: update_from_block<4>(v, c, f, prow); break;
+          case 5: update_from_block<5>(v, c, f, prow); break;
+          case 6: update_from_block<6>(v, c, f, prow); break;
+          default: update_from_block<7>(v, c, f, prow); break;
+        }
       }
 #pragma unroll
       for (int j = 0; j < PW; ++j)
@@ -352,7 +374,7 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
       pos = p;
     }
   }
-  cluster.sync();  // no CTA leaves while others may still read its shared memory
+  cluster.sync();  // no CTA leaves while others may still write into its shared memory
   if (dead || singular || !have) return;
   double2* dst = reinterpret_cast<double2*>(a + (int64_t)(off + pos) * ld + off);
 #pragma unroll
