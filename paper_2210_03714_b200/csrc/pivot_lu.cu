@@ -227,6 +227,7 @@ struct RegPanelShared {
   int cl[2][16];           // candidate position in the exchanged order
   int ct[2][16];           // candidate's owning thread (meaningful for its own CTA)
   double rows[2][16][PW];  // [parity][rank] candidate row
+  double mine[PW];         // this CTA's candidate row (staging for the parallel push)
   double red_v[RT / 32];
   int red_l[RT / 32], red_t[RT / 32];
 };
@@ -316,21 +317,33 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
     bv = __shfl_sync(FULL, bv, 0);
     bl = __shfl_sync(FULL, bl, 0);
     bt = __shfl_sync(FULL, bt, 0);
-    // ---- push the candidate (value, position, row) into every CTA's slot [par][rank]
+    // ---- push the candidate (value, position, row) into every CTA's slot [par][rank]: the owner
+    // stages its row locally, then all threads store it remotely in parallel
     if (tid == bt) {
-      for (int q = 0; q < C; ++q) {
-        RegPanelShared* o = C > 1 ? cluster.map_shared_rank(&sh, q) : &sh;
+#pragma unroll
+      for (int j = 0; j < PW; ++j) (C > 1 ? sh.mine : sh.rows[par][rank])[j] = v[j];
+    }
+    if (C > 1) {
+      __syncthreads();
+      for (int k = tid; k < C * PW; k += RT) {
+        RegPanelShared* o = cluster.map_shared_rank(&sh, k / PW);
+        o->rows[par][rank][k % PW] = sh.mine[k % PW];
+      }
+      if (tid < C) {
+        RegPanelShared* o = cluster.map_shared_rank(&sh, tid);
         o->cv[par][rank] = bv;
         o->cl[par][rank] = bl;
         o->ct[par][rank] = bt;
-#pragma unroll
-        for (int j = 0; j < PW; ++j) o->rows[par][rank][j] = v[j];
       }
-    }
-    if (C > 1)
       cluster.sync();  // release / acquire: every pushed candidate is visible to every CTA
-    else
+    } else {
+      if (tid == 0) {
+        sh.cv[par][0] = bv;
+        sh.cl[par][0] = bl;
+        sh.ct[par][0] = bt;
+      }
       __syncthreads();
+    }
     // ---- the pivot, from the local copies (every thread reduces the same C candidates in order)
     double gv = -1.0;
     int p = INT_MAX, q = -1;
