@@ -215,22 +215,58 @@ __global__ void __launch_bounds__(PT) panel_lu_cluster_kernel(double* M, int64_t
 // The panel in REGISTERS: one row per thread (256 rows per CTA, up to 16 CTAs per cluster: panels of
 // up to 4096 rows). Each thread keeps its row's 64 values in registers for the whole panel, so the
 // rank-1 update of a column is register FMAs against the pivot row (read from shared memory as a
-// broadcast). Per column: the CTA's candidate (warp shuffles), then its value and row are PUSHED into
-// every CTA's shared memory (remote stores over DSMEM, slot = rank, double-buffered by column
-// parity), one cluster barrier, and every CTA picks the pivot from its local copies -- no remote
-// load on the critical path. Three barriers per column, one of them cluster-wide.
+// broadcast). Per column: each warp's candidate (shuffles) stages its row in shared memory, ONE CTA
+// barrier, every warp reduces the 8 warp candidates to the CTA's (whose row is already staged). With
+// one CTA that is the pivot. In a cluster the CTA's candidate (value, position, row) is pushed into
+// every CTA's slot [parity][rank] with st.async (remote stores that complete a transaction count on
+// the receiver's mbarrier), and each CTA waits on its own mbarrier only -- no cluster-wide barrier
+// per column; every CTA then picks the pivot from its local copies. All buffers are double-buffered
+// by column parity: a slot of column c is rewritten at c + 2 only after every reader passed the
+// barrier (or the exchange) of column c + 1.
 // Register indices are compile-time constants: the column value is picked by a uniform switch, the
 // update runs over the 8-column block containing c (predicated j > c) and the blocks after it.
 constexpr int RT = 256;  // threads (= rows) per CTA
+constexpr int RW = RT / 32;
+constexpr unsigned kCandBytes = 8u * (PW + 2);  // one CTA's candidate: row + {|value|, position/thread}
 struct RegPanelShared {
-  double cv[2][16];        // [parity][rank] candidate |value|
-  int cl[2][16];           // candidate position in the exchanged order
-  int ct[2][16];           // candidate's owning thread (meaningful for its own CTA)
-  double rows[2][16][PW];  // [parity][rank] candidate row
-  double mine[PW];         // this CTA's candidate row (staging for the parallel push)
-  double red_v[RT / 32];
-  int red_l[RT / 32], red_t[RT / 32];
+  double wrows[2][RW][PW];  // [parity][warp] each warp's candidate row
+  double rows[2][16][PW];   // [parity][rank] the cluster's candidate rows
+  double2 meta[2][16];      // [parity][rank] {|value|, (position << 32) | thread}
+  double red_v[2][RW];
+  int red_l[2][RW], red_t[2][RW];
+  unsigned long long bar[2];
 };
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ unsigned cluster_addr(const void* p, int q) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(p)), "r"(q));
+  return r;
+}
+__device__ __forceinline__ void st_async2(unsigned addr, double x, double y, unsigned bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(addr),
+               "d"(x), "d"(y), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void cbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void cbar_expect(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
 
 template <int B>
 __device__ __forceinline__ void update_from_block(double (&v)[PW], int c, double f, const double* prow) {
@@ -259,12 +295,15 @@ __device__ __forceinline__ double pick(const double (&v)[PW], int c) {
   return r;
 }
 
+// ASYNC: the mbarrier exchange above; otherwise plain remote stores and one cluster barrier per
+// column (the A/B variant, PF_PANEL_CLUSTER_SYNC)
+template <bool ASYNC>
 __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t ld, int64_t strideM, int np, int off,
                                                              int* piv, int npiv, const double* tol, const int* zorig,
                                                              int* failed, DevStatus* status, int* first_error,
                                                              int2* moves, int* moves_n) {
   cg::cluster_group cluster = cg::this_cluster();
-  __shared__ RegPanelShared sh;
+  __shared__ __align__(16) RegPanelShared sh;
   const int z = blockIdx.y;
   const int rank = (int)cluster.block_rank();
   const int C = (int)cluster.num_blocks();
@@ -289,6 +328,13 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
   int pos = row;      // position in the exchanged order
   bool done = !have;  // pivot rows (and rows past the matrix) take no further part
   if (tid == 0 && rank == 0) moves_n[z] = 0;
+  if (ASYNC && C > 1 && tid == 0) {
+    cbar_init(smem_u32(&sh.bar[0]), 1);
+    cbar_init(smem_u32(&sh.bar[1]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    cbar_expect(smem_u32(&sh.bar[0]), kCandBytes * C);  // columns 0 and 1
+    cbar_expect(smem_u32(&sh.bar[1]), kCandBytes * C);
+  }
   cluster.sync();
   bool singular = false;
   // the column loop stays rolled (a fully unrolled panel is instruction-fetch bound); uniform over
@@ -298,56 +344,75 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
     if (dead || singular) continue;
     const int par = c & 1;
     const double vc = pick(v, c);
-    // ---- this CTA's candidate
+    // ---- this warp's candidate, its row staged; then the CTA's
     double bv = done ? -1.0 : fabs(vc);
     int bl = done ? INT_MAX : pos, bt = tid;
     for (int o = 16; o > 0; o >>= 1)
       better(bv, bl, bt, __shfl_xor_sync(FULL, bv, o), __shfl_xor_sync(FULL, bl, o), __shfl_xor_sync(FULL, bt, o));
+    if (tid == bt) {
+      double2* w2 = reinterpret_cast<double2*>(sh.wrows[par][warp]);
+#pragma unroll
+      for (int j = 0; j < PW / 2; ++j) w2[j] = make_double2(v[2 * j], v[2 * j + 1]);
+    }
     if (lane == 0) {
-      sh.red_v[warp] = bv;
-      sh.red_l[warp] = bl;
-      sh.red_t[warp] = bt;
+      sh.red_v[par][warp] = bv;
+      sh.red_l[par][warp] = bl;
+      sh.red_t[par][warp] = bt;
     }
     __syncthreads();
-    bv = lane < RT / 32 ? sh.red_v[lane] : -1.0;  // every warp reduces the 8 warp candidates
-    bl = lane < RT / 32 ? sh.red_l[lane] : INT_MAX;
-    bt = lane < RT / 32 ? sh.red_t[lane] : 0;
-    for (int o = 4; o > 0; o >>= 1)
+    bv = lane < RW ? sh.red_v[par][lane] : -1.0;  // every warp reduces the 8 warp candidates
+    bl = lane < RW ? sh.red_l[par][lane] : INT_MAX;
+    bt = lane < RW ? sh.red_t[par][lane] : 0;
+    for (int o = RW / 2; o > 0; o >>= 1)
       better(bv, bl, bt, __shfl_xor_sync(FULL, bv, o), __shfl_xor_sync(FULL, bl, o), __shfl_xor_sync(FULL, bt, o));
     bv = __shfl_sync(FULL, bv, 0);
     bl = __shfl_sync(FULL, bl, 0);
     bt = __shfl_sync(FULL, bt, 0);
-    // ---- push the candidate (value, position, row) into every CTA's slot [par][rank]: the owner
-    // stages its row locally, then all threads store it remotely in parallel
-    if (tid == bt) {
-#pragma unroll
-      for (int j = 0; j < PW; ++j) (C > 1 ? sh.mine : sh.rows[par][rank])[j] = v[j];
-    }
+    const double* crow = sh.wrows[par][bt >> 5];
+    double gv = bv;
+    int p = bl;
+    const double* prow = crow;
+    bool me = tid == bt;
     if (C > 1) {
-      __syncthreads();
-      for (int k = tid; k < C * PW; k += RT) {
-        RegPanelShared* o = cluster.map_shared_rank(&sh, k / PW);
-        o->rows[par][rank][k % PW] = sh.mine[k % PW];
+      // ---- exchange: the CTA's candidate into every CTA's slot [par][rank]
+      constexpr int E = PW / 2 + 1;  // 16-byte pieces per candidate
+      const double2* c2 = reinterpret_cast<const double2*>(crow);
+      const double mbits = __longlong_as_double(((long long)bl << 32) | (unsigned)bt);
+      if (ASYNC) {
+        for (int k = tid; k < C * E; k += RT) {
+          const int q = k / E, e = k - q * E;
+          const unsigned rb = cluster_addr(&sh.bar[par], q);
+          if (e < PW / 2) {
+            const double2 t = c2[e];
+            st_async2(cluster_addr(&sh.rows[par][rank][2 * e], q), t.x, t.y, rb);
+          } else {
+            st_async2(cluster_addr(&sh.meta[par][rank], q), bv, mbits, rb);
+          }
+        }
+        cbar_wait(smem_u32(&sh.bar[par]), (c >> 1) & 1);
+        if (tid == 0 && c + 2 < PW) cbar_expect(smem_u32(&sh.bar[par]), kCandBytes * C);
+      } else {
+        for (int k = tid; k < C * E; k += RT) {
+          const int q = k / E, e = k - q * E;
+          RegPanelShared* o = cluster.map_shared_rank(&sh, q);
+          if (e < PW / 2)
+            reinterpret_cast<double2*>(o->rows[par][rank])[e] = c2[e];
+          else
+            o->meta[par][rank] = make_double2(bv, mbits);
+        }
+        cluster.sync();  // release / acquire: every pushed candidate is visible to every CTA
       }
-      if (tid < C) {
-        RegPanelShared* o = cluster.map_shared_rank(&sh, tid);
-        o->cv[par][rank] = bv;
-        o->cl[par][rank] = bl;
-        o->ct[par][rank] = bt;
+      // ---- the pivot, from the local copies (every thread reduces the same C candidates in order)
+      gv = -1.0;
+      p = INT_MAX;
+      int q = -1;
+      for (int k = 0; k < C; ++k) {
+        const double2 m = sh.meta[par][k];
+        better(gv, p, q, m.x, (int)(__double_as_longlong(m.y) >> 32), k);
       }
-      cluster.sync();  // release / acquire: every pushed candidate is visible to every CTA
-    } else {
-      if (tid == 0) {
-        sh.cv[par][0] = bv;
-        sh.cl[par][0] = bl;
-        sh.ct[par][0] = bt;
-      }
-      __syncthreads();
+      prow = sh.rows[par][q];
+      me = rank == q && tid == (int)(unsigned)__double_as_longlong(sh.meta[par][q].y);
     }
-    // ---- the pivot, from the local copies (every thread reduces the same C candidates in order)
-    double gv = -1.0;
-    int p = INT_MAX, q = -1;
-    for (int k = 0; k < C; ++k) better(gv, p, q, sh.cv[par][k], sh.cl[par][k], k);
     if (gv <= tol[z]) {
       if (rank == 0 && tid == 0) {
         status[zorig[z]].code = PF_ERR_SINGULAR_SHIFT;
@@ -359,8 +424,6 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
       singular = true;
       continue;
     }
-    const double* prow = sh.rows[par][q];
-    const bool me = rank == q && tid == sh.ct[par][q];
     if (rank == 0 && tid == 0) piv[(int64_t)z * npiv + off + c] = off + p;
     if (me) {
       pos = c;
@@ -528,9 +591,12 @@ cudaError_t launch_panel_lu(double* M, int64_t ld, int64_t strideM, int np, int 
   if (w == PW && rows <= 16 * RT && !no_reg) {
     int Cr = 1;
     while (Cr * RT < rows) Cr *= 2;
+    static const bool csync = std::getenv("PF_PANEL_CLUSTER_SYNC") != nullptr;  // A/B: one cluster barrier per column
+    auto kern = csync ? panel_lu_reg_kernel<false> : panel_lu_reg_kernel<true>;
     static bool attr_r = false;
     if (!attr_r) {
-      cudaFuncSetAttribute(panel_lu_reg_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(panel_lu_reg_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(panel_lu_reg_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       attr_r = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -545,7 +611,7 @@ cudaError_t launch_panel_lu(double* M, int64_t ld, int64_t strideM, int np, int 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t er = cudaLaunchKernelEx(&cfg, panel_lu_reg_kernel, M, ld, strideM, np, off, piv, npiv, tol, zorig,
+    cudaError_t er = cudaLaunchKernelEx(&cfg, kern, M, ld, strideM, np, off, piv, npiv, tol, zorig,
                                         failed, status, first_error, moves, moves_n);
     if (er == cudaSuccess) {
       row_move_kernel<<<dim3((np + MC - 1) / MC, nsys), 256, 0, stream>>>(M, ld, strideM, np, off, w, moves,
