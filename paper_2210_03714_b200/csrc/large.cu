@@ -745,13 +745,35 @@ __global__ void accumulate_kernel(const double* X, int64_t xld, int64_t strideX,
 }
 
 // perm_z from the swap sequence piv_z (LAPACK style): perm[r] = row of the original RHS in row r.
+// the row permutation of a swap sequence: one warp per system, the sequence applied by lane 0 in
+// shared memory (chunks of 4096 rows' swaps staged by the warp; larger n walks global memory)
 __global__ void perm_from_piv_kernel(const int* piv, int n, int* perm, const int* zlist) {
+  constexpr int S = 4096;
+  __shared__ int p_s[S], q_s[S];
   const int z = zlist ? zlist[blockIdx.x] : blockIdx.x;
-  if (threadIdx.x != 0) return;
   int* p = perm + (int64_t)z * n;
+  const int* pv = piv + (int64_t)z * n;
+  if (n <= S) {
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+      p_s[r] = r;
+      q_s[r] = pv[r];
+    }
+    __syncwarp();
+    if (threadIdx.x == 0)
+      for (int r = 0; r < n; ++r) {
+        const int q = q_s[r];
+        const int t = p_s[r];
+        p_s[r] = p_s[q];
+        p_s[q] = t;
+      }
+    __syncwarp();
+    for (int r = threadIdx.x; r < n; r += blockDim.x) p[r] = p_s[r];
+    return;
+  }
+  if (threadIdx.x != 0) return;
   for (int r = 0; r < n; ++r) p[r] = r;
   for (int r = 0; r < n; ++r) {
-    const int q = piv[(int64_t)z * n + r];
+    const int q = pv[r];
     const int t = p[r];
     p[r] = p[q];
     p[q] = t;

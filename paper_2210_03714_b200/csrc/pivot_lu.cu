@@ -268,11 +268,15 @@ __device__ __forceinline__ void cbar_wait(unsigned bar, unsigned parity) {
       : "memory");
 }
 
+// v[c] <- f (the multiplier) and v[j] -= f prow[j] for j > c; B = c / 8 (compile-time register indices)
 template <int B>
 __device__ __forceinline__ void update_from_block(double (&v)[PW], int c, double f, const double* prow) {
+  const bool nz = f != 0.0;
 #pragma unroll
-  for (int j = 8 * B; j < PW; ++j)
-    if (j > c) v[j] = __dsub_rn(v[j], __dmul_rn(f, prow[j]));
+  for (int j = 8 * B; j < PW; ++j) {
+    if (j > c && nz) v[j] = __dsub_rn(v[j], __dmul_rn(f, prow[j]));
+    if (j < 8 * B + 8 && j == c) v[j] = f;
+  }
 }
 
 __device__ __forceinline__ double pick(const double (&v)[PW], int c) {
@@ -431,21 +435,16 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
     } else if (!done) {
       if (pos == c) pos = p;
       const double f = __dmul_rn(vc, 1.0 / prow[c]);
-      if (f != 0.0) {
-        switch (c >> 3) {
-          case 0: update_from_block<0>(v, c, f, prow); break;
-          case 1: update_from_block<1>(v, c, f, prow); break;
-          case 2: update_from_block<2>(v, c, f, prow); break;
-          case 3: update_from_block<3>(v, c, f, prow); break;
-          case 4: update_from_block<4>(v, c, f, prow); break;
-          case 5: update_from_block<5>(v, c, f, prow); break;
-          case 6: update_from_block<6>(v, c, f, prow); break;
-          default: update_from_block<7>(v, c, f, prow); break;
-        }
+      switch (c >> 3) {
+        case 0: update_from_block<0>(v, c, f, prow); break;
+        case 1: update_from_block<1>(v, c, f, prow); break;
+        case 2: update_from_block<2>(v, c, f, prow); break;
+        case 3: update_from_block<3>(v, c, f, prow); break;
+        case 4: update_from_block<4>(v, c, f, prow); break;
+        case 5: update_from_block<5>(v, c, f, prow); break;
+        case 6: update_from_block<6>(v, c, f, prow); break;
+        default: update_from_block<7>(v, c, f, prow); break;
       }
-#pragma unroll
-      for (int j = 0; j < PW; ++j)
-        if (j == c) v[j] = f;
     } else if (pos == c) {
       pos = p;
     }
