@@ -206,7 +206,10 @@ int launch_small(pf_context* ctx, pf::SmallParams& p) {
   kernel<<<p.batch, pf::small_eval_threads(), pf::small_eval_smem_bytes(), ctx->stream>>>(p);
   ctx->launches++;
   const cudaError_t le = cudaGetLastError();
-  if (persist) l2_persist_clear(ctx);
+  if (persist) {
+    l2_persist_clear(ctx);
+    ctx->l2_persisting = true;  // lines stay persisting until the next large-path GEMM resets them
+  }
   return cuda_fail(le);
 }
 
@@ -233,6 +236,11 @@ int launch_small_flags(pf_context* ctx, pf::SmallParams& p, int flags) {
 void gemm(pf_context* ctx, int m, int n, int k, int batch, double alpha, const double* A, int64_t lda,
           int64_t sA, const double* B, int64_t ldb, int64_t sB, double beta, double* C, int64_t ldc, int64_t sC,
           double gamma, const int* jmask, int step, const double* pass) {
+  if (ctx->l2_persisting) {  // the small kernel's slots: give the set-aside back to the GEMM tiles
+    cudaCtxResetPersistingL2Cache();
+    cudaGetLastError();
+    ctx->l2_persisting = false;
+  }
   pf::GemmParams g{};
   g.m = m;
   g.n = n;

@@ -28,6 +28,7 @@ struct pf_context {
   // bottom-right quadrant of each trailing update runs there while the recursion factors the rest
   std::vector<cudaStream_t> aux;
   std::vector<cudaEvent_t> aux_ready, aux_done;
+  bool l2_persisting = false;  // the small kernel left persisting L2 lines (reset before large GEMMs)
   int gemm_cap = 0;  // > 0: host gemm() launches persistent GEMMs on at most this many SMs
   // replayable launch graphs of the large LU recursion, keyed by its buffers and shape
   struct LuGraph {
