@@ -82,32 +82,32 @@ size_t lu_base64_smem_bytes() { return sizeof(double) * (3 * B64 * L64 + 8 * 16 
 
 // The 64 x 64 block s (smem, stride L64; xl / xu zeroed): LU in place (factor) and the inverses of
 // its L (unit lower) and U into xl / xu. 256 threads.
-__device__ void lu64_smem(double* s, double* xl, double* xu, double* scratch, int factor) {
+__device__ void lu64_smem(double* s, double* xl, double* xu, double* scratch, int factor, int ls = L64) {
   const int lane = lane_id(), warp = warp_id();
   if (factor) {
     const int r = threadIdx.x >> 2, q = threadIdx.x & 3;
     double v[16];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) v[k] = s[r * L64 + q + 4 * k];
+    for (int k = 0; k < 16; ++k) v[k] = s[r * ls + q + 4 * k];
 #pragma unroll
     for (int m = 0; m < B64 - 1; ++m) {
-      const double ip = rcp_nr(s[m * L64 + m]);
+      const double ip = rcp_nr(s[m * ls + m]);
       const double xm = __shfl_sync(0xffffffffu, v[m >> 2], (lane & ~3) | (m & 3));
       if (r > m) {
         const double f = xm * ip;
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-          if (q + 4 * k > m) v[k] = fma(-f, s[m * L64 + q + 4 * k], v[k]);
+          if (q + 4 * k > m) v[k] = fma(-f, s[m * ls + q + 4 * k], v[k]);
         if (q == (m & 3)) v[m >> 2] = f;
       }
       if (r == m + 1) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) s[r * L64 + q + 4 * k] = v[k];
+        for (int k = 0; k < 16; ++k) s[r * ls + q + 4 * k] = v[k];
       }
       __syncthreads();
     }
 #pragma unroll
-    for (int k = 0; k < 16; ++k) s[r * L64 + q + 4 * k] = v[k];
+    for (int k = 0; k < 16; ++k) s[r * ls + q + 4 * k] = v[k];
     __syncthreads();
   }
   // diagonal 16 x 16 blocks: warps 0-3 L_bb^-1, warps 4-7 U_bb^-1 (lane l < 16: column l)
@@ -120,16 +120,16 @@ __device__ void lu64_smem(double* s, double* xl, double* xu, double* scratch, in
 #pragma unroll
       for (int m = 0; m < 15; ++m)
 #pragma unroll
-        for (int i = m + 1; i < 16; ++i) x[i] = fma(-s[(o + i) * L64 + o + m], x[m], x[i]);
+        for (int i = m + 1; i < 16; ++i) x[i] = fma(-s[(o + i) * ls + o + m], x[m], x[i]);
       if (lane < 16)
 #pragma unroll
         for (int i = 0; i < 16; ++i) xl[(o + i) * L64 + o + l] = x[i];
     } else {
 #pragma unroll
       for (int m = 15; m >= 0; --m) {
-        x[m] = x[m] * rcp_nr(s[(o + m) * L64 + o + m]);
+        x[m] = x[m] * rcp_nr(s[(o + m) * ls + o + m]);
 #pragma unroll
-        for (int i = 0; i < m; ++i) x[i] = fma(-s[(o + i) * L64 + o + m], x[m], x[i]);
+        for (int i = 0; i < m; ++i) x[i] = fma(-s[(o + i) * ls + o + m], x[m], x[i]);
       }
       if (lane < 16)
 #pragma unroll
@@ -147,7 +147,7 @@ __device__ void lu64_smem(double* s, double* xl, double* xu, double* scratch, in
       double acc[2][2][2] = {};
       if (lower) {  // X_ij, i = b0 + d, j = b0: P = L[i, j..i-1] X[j..i-1, j]
         const int i = b0 + d, j = b0;
-        mm16(s + 16 * i * L64 + 16 * j, L64, xl + 16 * j * L64 + 16 * j, L64, 16 * d, acc);
+        mm16(s + 16 * i * ls + 16 * j, ls, xl + 16 * j * L64 + 16 * j, L64, 16 * d, acc);
         store16(ws, TSW, acc, 1.0);
         __syncwarp();
         double acc2[2][2][2] = {};
@@ -155,7 +155,7 @@ __device__ void lu64_smem(double* s, double* xl, double* xu, double* scratch, in
         store16(xl + 16 * i * L64 + 16 * j, L64, acc2, -1.0);
       } else {  // Y_ij, i = b0, j = b0 + d: P = U[i, i+1..j] Y[i+1..j, j]
         const int i = b0, j = b0 + d;
-        mm16(s + 16 * i * L64 + 16 * (i + 1), L64, xu + 16 * (i + 1) * L64 + 16 * j, L64, 16 * d, acc);
+        mm16(s + 16 * i * ls + 16 * (i + 1), ls, xu + 16 * (i + 1) * L64 + 16 * j, L64, 16 * d, acc);
         store16(ws, TSW, acc, 1.0);
         __syncwarp();
         double acc2[2][2][2] = {};
@@ -198,11 +198,168 @@ __global__ void __launch_bounds__(256) lu_base64_kernel(double* M, int64_t ld, i
 // U12 = L11^-1 A12 and L21 = A21 U11^-1 (DMMA), A22 -= L21 U12 (DMMA), LU(A22) with its inverses.
 // Same outputs as two 64 leaves and the level between them: the factors in place, the L / U
 // inverses of both 64 blocks in `inv`.
-size_t lu_base128_smem_bytes() { return sizeof(double) * (5 * B64 * L64 + 8 * 16 * TSW); }
+namespace {
+constexpr int L128 = 128 + 4;  // 128-tile smem row stride (32-byte skew)
+constexpr int NB16 = 16;
 
-// a: the block's origin (leading dimension ld), out: its two 64-blocks' L / U inverses (4 x 64^2).
-// Global reads bypass L1 (ld.global.cg): the persistent LU calls this on data other SMs just wrote.
+// pointwise LU of the 16 x 16 block at (k0, k0) of S (stride L128), in place, by one warp: lane
+// i < 16 holds row i; the pivot and the pivot row's tail come by shuffle
+__device__ __forceinline__ void factor16(double* S, int k0) {
+  const int lane = lane_id();
+  double d[NB16];
+#pragma unroll
+  for (int c = 0; c < NB16; ++c) d[c] = lane < NB16 ? S[(k0 + lane) * L128 + k0 + c] : 0.0;
+#pragma unroll
+  for (int m = 0; m < NB16; ++m) {
+    const double inv = rcp_nr(__shfl_sync(0xffffffffu, d[m], m));
+    double u[NB16];
+#pragma unroll
+    for (int c = m + 1; c < NB16; ++c) u[c] = __shfl_sync(0xffffffffu, d[c], m);
+    if (lane > m && lane < NB16) {
+      const double f = d[m] * inv;
+      d[m] = f;
+#pragma unroll
+      for (int c = m + 1; c < NB16; ++c) d[c] = fma(-f, u[c], d[c]);
+    }
+  }
+  if (lane < NB16) {
+#pragma unroll
+    for (int c = 0; c < NB16; c += 2)
+      *reinterpret_cast<double2*>(&S[(k0 + lane) * L128 + k0 + c]) = make_double2(d[c], d[c + 1]);
+  }
+}
+
+// (R0, C0) 16 x 16 block of S -= S[R0.., k0..k0+16) S[k0..k0+16, C0..) by one warp (DMMA, K = 16)
+__device__ __forceinline__ void schur16(double* S, int k0, int R0, int C0) {
+  const int lane = lane_id();
+  const int g = lane >> 2, t = lane & 3;
+  double acc[2][2][2];
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj) {
+      const double2 v = *reinterpret_cast<const double2*>(&S[(R0 + 8 * mi + g) * L128 + C0 + 8 * nj + 2 * t]);
+      acc[mi][nj][0] = v.x;
+      acc[mi][nj][1] = v.y;
+    }
+#pragma unroll
+  for (int kk = 0; kk < NB16; kk += 4) {
+    double af[2], bf[2];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) af[mi] = -S[(R0 + 8 * mi + g) * L128 + k0 + kk + t];
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj) bf[nj] = S[(k0 + kk + t) * L128 + C0 + 8 * nj + g];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj) dmma(acc[mi][nj], af[mi], bf[nj]);
+  }
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj)
+      *reinterpret_cast<double2*>(&S[(R0 + 8 * mi + g) * L128 + C0 + 8 * nj + 2 * t]) =
+          make_double2(acc[mi][nj][0], acc[mi][nj][1]);
+}
+}  // namespace
+
+// The 128 x 128 diagonal tile at a (leading dimension ld), no exchanges, in place, plus the L / U
+// inverses of its two 64-blocks into out (4 x 64^2: L11^-1, U11^-1, L22^-1, U22^-1) -- the outputs
+// of two 64 leaves and the level between them. 256 threads, the tile in shared memory, blocked
+// right-looking LU with 16-wide steps and one step of look-ahead: the lead warp (7) applies the
+// Schur update to the next 16 x 16 diagonal block and factors it (pointwise, shuffles) while the
+// other warps apply the rest of the trailing update (DMMA); between them, every row of the panel
+// below (L21 = A21 U_kk^-1) and every column of the panel to the right (U12 = L_kk^-1 A12) is
+// solved by its own thread. Then the two 64-blocks' inverses (lu64_smem's substitution + DMMA
+// levels). Global reads bypass L1 (ld.global.cg): the persistent LU calls this on data other SMs
+// just wrote.
+size_t lu_base128_smem_bytes() { return sizeof(double) * (128 * L128 + 2 * B64 * L64 + 8 * 16 * TSW); }
+
 __device__ void lu128_block(double* a, int64_t ld, double* out, double* lu_smem) {
+  double* S = lu_smem;
+  double* xl = S + 128 * L128;
+  double* xu = xl + B64 * L64;
+  double* scratch = xu + B64 * L64;
+  const int tid = threadIdx.x, warp = warp_id();
+  for (int idx = tid; idx < 128 * 64; idx += blockDim.x) {
+    const int r = idx >> 6, c2 = idx & 63;
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(a + (int64_t)r * ld) + c2);
+    *reinterpret_cast<double2*>(&S[r * L128 + 2 * c2]) = v;
+  }
+  __syncthreads();
+  constexpr int kLead = 7;
+  if (warp == kLead) factor16(S, 0);
+  __syncthreads();
+  for (int k0 = 0; k0 < 128 - NB16; k0 += NB16) {
+    const int rest = 128 - k0 - NB16;
+    if (tid < rest) {  // row k0 + 16 + tid of L21 = A21 U_kk^-1 (forward over the block's columns)
+      const int row = k0 + NB16 + tid;
+      double x[NB16], rinv[NB16];
+#pragma unroll
+      for (int c = 0; c < NB16; ++c) {
+        x[c] = S[row * L128 + k0 + c];
+        rinv[c] = rcp_nr(S[(k0 + c) * L128 + k0 + c]);
+      }
+#pragma unroll
+      for (int m = 0; m < NB16; ++m) {
+        x[m] = x[m] * rinv[m];
+#pragma unroll
+        for (int c = m + 1; c < NB16; ++c) x[c] = fma(-x[m], S[(k0 + m) * L128 + k0 + c], x[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < NB16; c += 2)
+        *reinterpret_cast<double2*>(&S[row * L128 + k0 + c]) = make_double2(x[c], x[c + 1]);
+    } else if (tid >= 128 && tid - 128 < rest) {  // column of U12 = L_kk^-1 A12 (unit lower)
+      const int col = k0 + NB16 + (tid - 128);
+      double y[NB16];
+#pragma unroll
+      for (int r = 0; r < NB16; ++r) y[r] = S[(k0 + r) * L128 + col];
+#pragma unroll
+      for (int m = 0; m < NB16 - 1; ++m)
+#pragma unroll
+        for (int r = m + 1; r < NB16; ++r) y[r] = fma(-S[(k0 + r) * L128 + k0 + m], y[m], y[r]);
+#pragma unroll
+      for (int r = 1; r < NB16; ++r) S[(k0 + r) * L128 + col] = y[r];
+    }
+    __syncthreads();
+    const int nbk = rest / NB16;
+    if (warp == kLead) {
+      schur16(S, k0, k0 + NB16, k0 + NB16);
+      __syncwarp();
+      factor16(S, k0 + NB16);
+    } else {
+      for (int blk = warp + 1; blk < nbk * nbk; blk += kLead)
+        schur16(S, k0, k0 + NB16 + NB16 * (blk / nbk), k0 + NB16 + NB16 * (blk % nbk));
+    }
+    __syncthreads();
+  }
+  // the factors out; the 64-blocks' inverses
+  for (int idx = tid; idx < 128 * 64; idx += blockDim.x) {
+    const int r = idx >> 6, c2 = idx & 63;
+    reinterpret_cast<double2*>(a + (int64_t)r * ld)[c2] = *reinterpret_cast<const double2*>(&S[r * L128 + 2 * c2]);
+  }
+  for (int h = 0; h < 2; ++h) {
+    for (int idx = tid; idx < B64 * B64; idx += blockDim.x) {
+      const int r = idx >> 6, c = idx & 63;
+      xl[r * L64 + c] = 0.0;
+      xu[r * L64 + c] = 0.0;
+    }
+    __syncthreads();
+    lu64_smem(S + h * B64 * L128 + h * B64, xl, xu, scratch, 0, L128);
+    double* o = out + h * 2 * B64 * B64;
+    for (int idx = tid; idx < B64 * B64; idx += blockDim.x) {
+      const int r = idx >> 6, c = idx & 63;
+      o[idx] = xl[r * L64 + c];
+      o[B64 * B64 + idx] = xu[r * L64 + c];
+    }
+    __syncthreads();
+  }
+}
+
+#ifdef PF_LU128_V1
+// round-1 / early round-2 version: two 64 leaves (lu64_smem factor) and the DMMA level between them
+size_t lu_base128_v1_smem_bytes() { return sizeof(double) * (5 * B64 * L64 + 8 * 16 * TSW); }
+__device__ void lu128_block_v1(double* a, int64_t ld, double* out, double* lu_smem) {
   double* s = lu_smem;          // the diagonal block being factored (A11, then A22)
   double* xl = s + B64 * L64;   // its L^-1
   double* xu = xl + B64 * L64;  // its U^-1
@@ -284,6 +441,8 @@ __device__ void lu128_block(double* a, int64_t ld, double* out, double* lu_smem)
     out2[B64 * B64 + idx] = xu[r * L64 + c];
   }
 }
+
+#endif  // PF_LU128_V1
 
 __global__ void __launch_bounds__(256) lu_base128_kernel(double* M, int64_t ld, int64_t strideM, int off,
                                                          double* inv, int64_t inv_stride) {
