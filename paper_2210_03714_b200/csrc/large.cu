@@ -78,6 +78,21 @@ __device__ __forceinline__ double rcp_nr(double x) {
 }
 }  // namespace
 
+namespace {
+// rows x 64 doubles from global (row stride ldg, 16-byte aligned rows) into smem (row stride lds) with
+// 16-byte cp.async.cg (L2, coherent with other SMs' writes): every copy in flight at once instead
+// of one latency-bound round trip per loop iteration. The caller commits and waits.
+__device__ __forceinline__ void async_tile64(double* dst, int lds, const double* src, int64_t ldg, int rows) {
+  for (int idx = threadIdx.x; idx < rows * 32; idx += blockDim.x) {
+    const int r = idx >> 5, c2 = idx & 31;
+    cp_async16(dst + r * lds + 2 * c2, src + (int64_t)r * ldg + 2 * c2, 16);
+  }
+}
+__device__ __forceinline__ bool aligned16(const void* p, int64_t ld) {
+  return ((reinterpret_cast<uintptr_t>(p) & 15) == 0) && ((ld & 1) == 0);
+}
+}  // namespace
+
 size_t lu_base64_smem_bytes() { return sizeof(double) * (3 * B64 * L64 + 8 * 16 * TSW); }
 
 // The 64 x 64 block s (smem, stride L64; xl / xu zeroed): LU in place (factor) and the inverses of
@@ -176,12 +191,18 @@ __global__ void __launch_bounds__(256) lu_base64_kernel(double* M, int64_t ld, i
   double* scratch = xu + B64 * L64;
   const int z = zlist ? zlist[blockIdx.x] : blockIdx.x;
   double* a = M + (int64_t)z * strideM + (int64_t)off * ld + off;
+  const bool fast = aligned16(a, ld);
+  if (fast) {
+    async_tile64(s, L64, a, ld, B64);
+    cp_async_commit();
+  }
   for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
     const int r = idx >> 6, c = idx & 63;
-    s[r * L64 + c] = a[(int64_t)r * ld + c];
+    if (!fast) s[r * L64 + c] = a[(int64_t)r * ld + c];
     xl[r * L64 + c] = 0.0;
     xu[r * L64 + c] = 0.0;
   }
+  if (fast) cp_async_wait<0>();
   __syncthreads();
   lu64_smem(s, xl, xu, scratch, factor);
   double* out = inv + (int64_t)z * inv_stride + (int64_t)(off / B64) * 2 * B64 * B64;
@@ -281,11 +302,10 @@ __device__ void lu128_block(double* a, int64_t ld, double* out, double* lu_smem)
   double* xu = xl + B64 * L64;
   double* scratch = xu + B64 * L64;
   const int tid = threadIdx.x, warp = warp_id();
-  for (int idx = tid; idx < 128 * 64; idx += blockDim.x) {
-    const int r = idx >> 6, c2 = idx & 63;
-    const double2 v = __ldcg(reinterpret_cast<const double2*>(a + (int64_t)r * ld) + c2);
-    *reinterpret_cast<double2*>(&S[r * L128 + 2 * c2]) = v;
-  }
+  async_tile64(S, L128, a, ld, 128);
+  async_tile64(S + 64, L128, a + 64, ld, 128);
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   constexpr int kLead = 7;
   if (warp == kLead) factor16(S, 0);
@@ -510,6 +530,20 @@ __device__ void trsm128_chunk(const double* m, int64_t ld, const double* blkinv,
   const double* i1 = blkinv + (mode == 0 ? 0 : B64 * B64);
   const double* i2 = blkinv + 2 * B64 * B64 + (mode == 0 ? 0 : B64 * B64);
   const double* c0 = mode == 0 ? m + (int64_t)B64 * ld : m + B64;
+  if (live == B64 && aligned16(b, ldb) && aligned16(m, ld) && aligned16(blkinv, 0)) {
+    async_tile64(t1, L64, i1, B64, B64);
+    async_tile64(t2, L64, i2, B64, B64);
+    async_tile64(cpl, L64, c0, ld, B64);
+    if (!right) {
+      async_tile64(b1, L64, b, ldb, B64);
+      async_tile64(b2, L64, b + (int64_t)B64 * ldb, ldb, B64);
+    } else {
+      async_tile64(b1, L64, b, ldb, B64);
+      async_tile64(b2, L64, b + B64, ldb, B64);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+  } else
   for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
     const int r = idx >> 6, c = idx & 63;
     t1[r * L64 + c] = __ldcg(i1 + idx);
@@ -607,6 +641,12 @@ __global__ void __launch_bounds__(256) apply_inv64_kernel(const double* inv, int
   const double* T = inv + (int64_t)z * inv_stride + (int64_t)blk * 2 * B64 * B64 + (upper ? B64 * B64 : 0);
   double* b = Bm + (int64_t)z * strideB + (right ? (int64_t)tile * B64 * ld : (int64_t)tile * B64);
   const int live = min(B64, extent - tile * B64);  // columns (left) or rows (right) in range
+  if (live == B64 && aligned16(b, ld) && aligned16(T, 0)) {
+    async_tile64(t, L64, T, B64, B64);
+    async_tile64(bt, L64, b, ld, B64);
+    cp_async_commit();
+    cp_async_wait<0>();
+  } else
   for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
     const int r = idx >> 6, c = idx & 63;
     t[r * L64 + c] = T[r * B64 + c];
