@@ -79,7 +79,10 @@ void launch_gemm(const GemmParams& p, cudaStream_t stream) {
   }
 }
 
+bool launch_gemm_tma(const GemmParams& p, cudaStream_t stream);  // gemm_tma.cu
+
 void launch_gemm_chunk(const GemmParams& p, cudaStream_t stream) {
+  if (launch_gemm_tma(p, stream)) return;  // TMA staging wherever the operands allow it
   // 16-byte copies need even leading dimensions / batch strides and 16-byte aligned bases
   const bool v16 = ((p.lda | p.ldb | p.strideA | p.strideB) & 1) == 0 &&
                    ((reinterpret_cast<uintptr_t>(p.A) | reinterpret_cast<uintptr_t>(p.B)) & 15) == 0;
