@@ -16,6 +16,11 @@
 // A and the B fragment loads of a warp touch every bank exactly twice (two wavefronts, the minimum
 // for 256 bytes). Every element still accumulates its k products in one fixed order.
 //
+// Stages (tools/large_timing.py gemm, PF_TMA_STAGES / PF_TMA_MINB builds): 2 stages x 4 CTAs per SM
+// 34.7 / 35.5 / 32.5 TF/s at 4096^3 / 8192^3 / 2048^3; 3 x 4: 34.5 / 35.2 / 32.5; 4 x 3: 34.0 / 35.0 /
+// 31.7; 5 x 2: 33.5 / 33.7 / 28.6; 2 x 5 (102 registers, spills): 32.8 / 33.1. Four resident CTAs
+// (16 DMMA warps per SM) hide the copy latency; deeper rings only cost occupancy.
+//
 // Edges: the tensor maps cover the true m, n, k (out-of-range box elements are zero-filled), so any
 // shape is legal; the host takes this path when the bases are 16-byte aligned and the leading
 // dimensions / batch strides are multiples of 2 doubles (otherwise gemm.cu's cp.async kernel).
@@ -31,7 +36,13 @@
 namespace pf {
 namespace {
 
-constexpr int TBM = 64, TBN = 64, TBK = 16, TSTAGES = 3;
+#ifndef PF_TMA_STAGES
+#define PF_TMA_STAGES 2
+#endif
+#ifndef PF_TMA_MINB
+#define PF_TMA_MINB 4
+#endif
+constexpr int TBM = 64, TBN = 64, TBK = 16, TSTAGES = PF_TMA_STAGES;
 constexpr int A_BYTES = TBM * TBK * 8;  // 8 KB
 constexpr int B_BYTES = TBK * TBN * 8;  // 8 KB (four 2 KB boxes)
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -70,7 +81,7 @@ struct TmaMaps {
   CUtensorMap b;  // dims {n, k, batch}, box {16, 16, 1}
 };
 
-__global__ void __launch_bounds__(128, 4) gemm_tma_kernel(const __grid_constant__ TmaMaps maps, GemmParams p,
+__global__ void __launch_bounds__(128, PF_TMA_MINB) gemm_tma_kernel(const __grid_constant__ TmaMaps maps, GemmParams p,
                                                           int tiles_n) {
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   // 1024-byte alignment for the 128-byte swizzle pattern
