@@ -14,7 +14,12 @@
 // DMMA of a 16-wide k tile takes the k set {s', s'+1, s'+4, s'+5} (s' = 2 (s & 1) + 8 (s >> 1),
 // s = 0..3; lane t supplies k = s' + (t & 1) + 4 (t >> 1)) instead of 4 consecutive k: then both the
 // A and the B fragment loads of a warp touch every bank exactly twice (two wavefronts, the minimum
-// for 256 bytes). Every element still accumulates its k products in one fixed order.
+// for 256 bytes) -- in the full-warp view. 8-byte loads are served per half-warp, and there each
+// set still costs 2 wavefronts (ncu: 269M bank conflicts at 4096^3). The conflict-free sets
+// {0, 3, 13, 14} ^ {0, 1, 4, 5} (distinct (bit 3, bit 0) and (bit 2, bit 1) of k over the lanes t)
+// bring that to 1.2M but run slower, measured back to back: 34.3 / 35.2 / 27.7 TF/s vs 34.7 / 35.5 /
+// 29.1 at 4096^3 / 8192^3 / 16384 x 64 x 16384 -- shared-memory bandwidth is not the limiter here.
+// Every element still accumulates its k products in one fixed order.
 //
 // Stages (tools/large_timing.py gemm, PF_TMA_STAGES / PF_TMA_MINB builds): 2 stages x 4 CTAs per SM
 // 34.7 / 35.5 / 32.5 TF/s at 4096^3 / 8192^3 / 2048^3; 3 x 4: 34.5 / 35.2 / 32.5; 4 x 3: 34.0 / 35.0 /
