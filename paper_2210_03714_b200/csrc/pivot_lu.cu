@@ -227,13 +227,13 @@ __global__ void __launch_bounds__(PT) panel_lu_cluster_kernel(double* M, int64_t
 // update runs over the 8-column block containing c (predicated j > c) and the blocks after it.
 constexpr int RT = 256;  // threads (= rows) per CTA
 constexpr int RW = RT / 32;
-constexpr unsigned kCandBytes = 8u * (PW + 2);  // one CTA's candidate: row + {|value|, position/thread}
+constexpr int CW = PW + 4;                       // candidate payload (doubles): row, {key, pos}, {1/pivot, -}
+constexpr unsigned kCandBytes = 8u * CW;
 struct RegPanelShared {
-  double wrows[2][RW][PW];  // [parity][warp] each warp's candidate row
-  double rows[2][16][PW];   // [parity][rank] the cluster's candidate rows
-  double2 meta[2][16];      // [parity][rank] {|value|, (position << 32) | thread}
-  double red_v[2][RW];
-  int red_l[2][RW], red_t[2][RW];
+  double wrows[2][RW][CW];  // [parity][warp] each warp's candidate payload
+  double rows[2][16][CW];   // [parity][rank] the cluster's candidate payloads
+  unsigned long long red_key[2][RW];
+  unsigned red_pos[2][RW];
   unsigned long long bar[2];
 };
 
@@ -268,39 +268,47 @@ __device__ __forceinline__ void cbar_wait(unsigned bar, unsigned parity) {
       : "memory");
 }
 
-// v[c] <- f (the multiplier) and v[j] -= f prow[j] for j > c; B = c / 8 (compile-time register indices)
+// Candidate order as a 64-bit key: |a| + 1 ulp-steps above the "no candidate" key 0 (pivot rows,
+// rows past the matrix, NaN); larger |a| wins, then the smaller position (the reference's strict
+// '>' over rows in order). The argmax over a warp is three redux instructions and a ballot.
+__device__ __forceinline__ unsigned long long cand_key(double x, bool live) {
+  const double ax = fabs(x);
+  return (live && ax >= 0.0) ? (unsigned long long)__double_as_longlong(ax) + 1ull : 0ull;
+}
+__device__ __forceinline__ double key_value(unsigned long long k) {
+  return k == 0ull ? -1.0 : __longlong_as_double((long long)(k - 1ull));
+}
+// the lane holding the best (key, pos); every lane gets the same answer
+__device__ __forceinline__ int lane_argmax(unsigned long long key, unsigned pos) {
+  const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+  const unsigned mhi = __reduce_max_sync(FULL, hi);
+  const unsigned mlo = __reduce_max_sync(FULL, hi == mhi ? lo : 0u);
+  const bool c = hi == mhi && lo == mlo;
+  const unsigned mp = __reduce_min_sync(FULL, c ? pos : 0xFFFFFFFFu);
+  return __ffs(__ballot_sync(FULL, c && pos == mp)) - 1;
+}
+
+// v[c] <- f (the multiplier) and v[j] -= f prow[j] for j > c (skipped when f == 0); nx <- the new
+// v[c + 1] (the next column's value, so the next step needs no dynamic register index); B = c / 8
 template <int B>
-__device__ __forceinline__ void update_from_block(double (&v)[PW], int c, double f, const double* prow) {
+__device__ __forceinline__ void update_from_block(double (&v)[PW], int c, double f, const double* prow, double& nx) {
   const bool nz = f != 0.0;
 #pragma unroll
   for (int j = 8 * B; j < PW; ++j) {
     if (j > c && nz) v[j] = __dsub_rn(v[j], __dmul_rn(f, prow[j]));
     if (j < 8 * B + 8 && j == c) v[j] = f;
+    if (j < 8 * B + 9 && j == c + 1) nx = v[j];
   }
 }
 
-__device__ __forceinline__ double pick(const double (&v)[PW], int c) {
-  double r = 0.0;
-  switch (c) {
-#define PF_PICK(k) \
-  case k:          \
-    r = v[k];      \
-    break;
-    PF_PICK(0) PF_PICK(1) PF_PICK(2) PF_PICK(3) PF_PICK(4) PF_PICK(5) PF_PICK(6) PF_PICK(7)
-    PF_PICK(8) PF_PICK(9) PF_PICK(10) PF_PICK(11) PF_PICK(12) PF_PICK(13) PF_PICK(14) PF_PICK(15)
-    PF_PICK(16) PF_PICK(17) PF_PICK(18) PF_PICK(19) PF_PICK(20) PF_PICK(21) PF_PICK(22) PF_PICK(23)
-    PF_PICK(24) PF_PICK(25) PF_PICK(26) PF_PICK(27) PF_PICK(28) PF_PICK(29) PF_PICK(30) PF_PICK(31)
-    PF_PICK(32) PF_PICK(33) PF_PICK(34) PF_PICK(35) PF_PICK(36) PF_PICK(37) PF_PICK(38) PF_PICK(39)
-    PF_PICK(40) PF_PICK(41) PF_PICK(42) PF_PICK(43) PF_PICK(44) PF_PICK(45) PF_PICK(46) PF_PICK(47)
-    PF_PICK(48) PF_PICK(49) PF_PICK(50) PF_PICK(51) PF_PICK(52) PF_PICK(53) PF_PICK(54) PF_PICK(55)
-    PF_PICK(56) PF_PICK(57) PF_PICK(58) PF_PICK(59) PF_PICK(60) PF_PICK(61) PF_PICK(62) PF_PICK(63)
-#undef PF_PICK
-  }
-  return r;
-}
-
-// ASYNC: the mbarrier exchange above; otherwise plain remote stores and one cluster barrier per
-// column (the A/B variant, PF_PANEL_CLUSTER_SYNC)
+// ASYNC: candidates exchanged by st.async into the receivers' mbarriers; otherwise plain remote
+// stores and one cluster barrier per column (the A/B variant, PF_PANEL_CLUSTER_SYNC). Per column:
+// each warp's argmax (redux) -- its winner stages (row, key, position, 1/pivot) in shared memory --
+// ONE CTA barrier, every warp reduces the 8 warp candidates the same way; in a cluster the CTA's
+// candidate goes to every CTA's slot [parity][rank] and each CTA waits on its own mbarrier only.
+// The reciprocal of a candidate pivot is computed by its owner before the exchange (off the chain).
+// Buffers are double-buffered by column parity: a slot of column c is rewritten at c + 2 only after
+// every reader passed the barrier (or the exchange) of column c + 1.
 template <bool ASYNC>
 __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t ld, int64_t strideM, int np, int off,
                                                              int* piv, int npiv, const double* tol, const int* zorig,
@@ -331,6 +339,7 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
   }
   int pos = row;      // position in the exchanged order
   bool done = !have;  // pivot rows (and rows past the matrix) take no further part
+  double vc = v[0];   // the current column's value
   if (tid == 0 && rank == 0) moves_n[z] = 0;
   if (ASYNC && C > 1 && tid == 0) {
     cbar_init(smem_u32(&sh.bar[0]), 1);
@@ -347,51 +356,30 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
   for (int c = 0; c < PW; ++c) {
     if (dead || singular) continue;
     const int par = c & 1;
-    const double vc = pick(v, c);
-    // ---- this warp's candidate, its row staged; then the CTA's
-    double bv = done ? -1.0 : fabs(vc);
-    int bl = done ? INT_MAX : pos, bt = tid;
-    for (int o = 16; o > 0; o >>= 1)
-      better(bv, bl, bt, __shfl_xor_sync(FULL, bv, o), __shfl_xor_sync(FULL, bl, o), __shfl_xor_sync(FULL, bt, o));
-    if (tid == bt) {
+    // ---- this warp's candidate: the winner stages its payload; then the CTA's
+    const unsigned long long key = cand_key(vc, !done);
+    const int wl = lane_argmax(key, done ? 0xFFFFFFFFu : (unsigned)pos);
+    if (lane == wl) {
       double2* w2 = reinterpret_cast<double2*>(sh.wrows[par][warp]);
 #pragma unroll
       for (int j = 0; j < PW / 2; ++j) w2[j] = make_double2(v[2 * j], v[2 * j + 1]);
-    }
-    if (lane == 0) {
-      sh.red_v[par][warp] = bv;
-      sh.red_l[par][warp] = bl;
-      sh.red_t[par][warp] = bt;
+      w2[PW / 2] = make_double2(__longlong_as_double((long long)key), __longlong_as_double((long long)(((unsigned long long)(unsigned)pos << 32) | (unsigned)tid)));
+      w2[PW / 2 + 1] = make_double2(1.0 / vc, 0.0);
+      sh.red_key[par][warp] = key;
+      sh.red_pos[par][warp] = done ? 0xFFFFFFFFu : (unsigned)pos;
     }
     __syncthreads();
-    bv = lane < RW ? sh.red_v[par][lane] : -1.0;  // every warp reduces the 8 warp candidates
-    bl = lane < RW ? sh.red_l[par][lane] : INT_MAX;
-    bt = lane < RW ? sh.red_t[par][lane] : 0;
-    for (int o = RW / 2; o > 0; o >>= 1)
-      better(bv, bl, bt, __shfl_xor_sync(FULL, bv, o), __shfl_xor_sync(FULL, bl, o), __shfl_xor_sync(FULL, bt, o));
-    bv = __shfl_sync(FULL, bv, 0);
-    bl = __shfl_sync(FULL, bl, 0);
-    bt = __shfl_sync(FULL, bt, 0);
-    const double* crow = sh.wrows[par][bt >> 5];
-    double gv = bv;
-    int p = bl;
-    const double* prow = crow;
-    bool me = tid == bt;
+    const int ww = lane_argmax(lane < RW ? sh.red_key[par][lane] : 0ull, lane < RW ? sh.red_pos[par][lane] : 0xFFFFFFFFu);
+    const double* prow = sh.wrows[par][ww];
     if (C > 1) {
-      // ---- exchange: the CTA's candidate into every CTA's slot [par][rank]
-      constexpr int E = PW / 2 + 1;  // 16-byte pieces per candidate
-      const double2* c2 = reinterpret_cast<const double2*>(crow);
-      const double mbits = __longlong_as_double(((long long)bl << 32) | (unsigned)bt);
+      // ---- exchange: the CTA's candidate payload into every CTA's slot [par][rank]
+      constexpr int E = CW / 2;  // 16-byte pieces per payload
+      const double2* c2 = reinterpret_cast<const double2*>(prow);
       if (ASYNC) {
         for (int k = tid; k < C * E; k += RT) {
           const int q = k / E, e = k - q * E;
-          const unsigned rb = cluster_addr(&sh.bar[par], q);
-          if (e < PW / 2) {
-            const double2 t = c2[e];
-            st_async2(cluster_addr(&sh.rows[par][rank][2 * e], q), t.x, t.y, rb);
-          } else {
-            st_async2(cluster_addr(&sh.meta[par][rank], q), bv, mbits, rb);
-          }
+          const double2 t = c2[e];
+          st_async2(cluster_addr(&sh.rows[par][rank][2 * e], q), t.x, t.y, cluster_addr(&sh.bar[par], q));
         }
         cbar_wait(smem_u32(&sh.bar[par]), (c >> 1) & 1);
         if (tid == 0 && c + 2 < PW) cbar_expect(smem_u32(&sh.bar[par]), kCandBytes * C);
@@ -399,24 +387,21 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
         for (int k = tid; k < C * E; k += RT) {
           const int q = k / E, e = k - q * E;
           RegPanelShared* o = cluster.map_shared_rank(&sh, q);
-          if (e < PW / 2)
-            reinterpret_cast<double2*>(o->rows[par][rank])[e] = c2[e];
-          else
-            o->meta[par][rank] = make_double2(bv, mbits);
+          reinterpret_cast<double2*>(o->rows[par][rank])[e] = c2[e];
         }
         cluster.sync();  // release / acquire: every pushed candidate is visible to every CTA
       }
-      // ---- the pivot, from the local copies (every thread reduces the same C candidates in order)
-      gv = -1.0;
-      p = INT_MAX;
-      int q = -1;
-      for (int k = 0; k < C; ++k) {
-        const double2 m = sh.meta[par][k];
-        better(gv, p, q, m.x, (int)(__double_as_longlong(m.y) >> 32), k);
-      }
-      prow = sh.rows[par][q];
-      me = rank == q && tid == (int)(unsigned)__double_as_longlong(sh.meta[par][q].y);
+      // ---- the pivot, from the local copies (every warp reduces the same C candidates)
+      const double* meta = sh.rows[par][lane < C ? lane : 0] + PW;
+      const unsigned long long mk = lane < C ? (unsigned long long)__double_as_longlong(meta[0]) : 0ull;
+      const unsigned mpos = lane < C ? (unsigned)((unsigned long long)__double_as_longlong(meta[1]) >> 32) : 0xFFFFFFFFu;
+      prow = sh.rows[par][lane_argmax(mk, mk ? mpos : 0xFFFFFFFFu)];
     }
+    const unsigned long long pk = (unsigned long long)__double_as_longlong(prow[PW]);
+    const unsigned long long pm = (unsigned long long)__double_as_longlong(prow[PW + 1]);
+    const double gv = key_value(pk);
+    const int p = (int)(pm >> 32);
+    const bool me = !done && (unsigned)pos == (unsigned)p && pk != 0ull;
     if (gv <= tol[z]) {
       if (rank == 0 && tid == 0) {
         status[zorig[z]].code = PF_ERR_SINGULAR_SHIFT;
@@ -434,17 +419,19 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
       done = true;
     } else if (!done) {
       if (pos == c) pos = p;
-      const double f = __dmul_rn(vc, 1.0 / prow[c]);
+      const double f = __dmul_rn(vc, prow[PW + 2]);  // a * (1 / pivot)
+      double nx = 0.0;
       switch (c >> 3) {
-        case 0: update_from_block<0>(v, c, f, prow); break;
-        case 1: update_from_block<1>(v, c, f, prow); break;
-        case 2: update_from_block<2>(v, c, f, prow); break;
-        case 3: update_from_block<3>(v, c, f, prow); break;
-        case 4: update_from_block<4>(v, c, f, prow); break;
-        case 5: update_from_block<5>(v, c, f, prow); break;
-        case 6: update_from_block<6>(v, c, f, prow); break;
-        default: update_from_block<7>(v, c, f, prow); break;
+        case 0: update_from_block<0>(v, c, f, prow, nx); break;
+        case 1: update_from_block<1>(v, c, f, prow, nx); break;
+        case 2: update_from_block<2>(v, c, f, prow, nx); break;
+        case 3: update_from_block<3>(v, c, f, prow, nx); break;
+        case 4: update_from_block<4>(v, c, f, prow, nx); break;
+        case 5: update_from_block<5>(v, c, f, prow, nx); break;
+        case 6: update_from_block<6>(v, c, f, prow, nx); break;
+        default: update_from_block<7>(v, c, f, prow, nx); break;
       }
+      vc = nx;
     } else if (pos == c) {
       pos = p;
     }
