@@ -943,6 +943,48 @@ __global__ void accumulate_kernel(const double* X, int64_t xld, int64_t strideX,
   }
 }
 
+// Up to four weighted sums of the same solutions in ONE pass over them (every X element read once):
+// output o = sum_t w_o[t] X_t in ascending t (plus its poly part), rounded exactly as
+// accumulate_kernel -- the weight sets of a method and the pair path's E_A / E_B share the reads.
+__global__ void accumulate_sets_kernel(const double* X, int64_t xld, int64_t strideX, int n, int cols, int batch,
+                                       int n_terms, const int* term_z, AccSets sets, const double* Bsrc, int64_t bld,
+                                       int64_t strideBs, const int* j, const double* B2, int64_t b2ld,
+                                       int64_t strideB2) {
+  const int b = blockIdx.y;
+  const int jb = j ? j[b] : 0;
+  const int no = sets.n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)n * cols;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / cols), col = (int)(idx % cols);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int t = 0; t < n_terms; ++t) {
+      const int z = term_z[t];
+      const double x = z < 0 ? 0.0 : X[(int64_t)(z * batch + b) * strideX + (int64_t)r * xld + col];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        if (o >= no) break;
+        const double w = sets.s[o].w[t];
+        const double tv = z < 0 ? ((r == col) ? __dadd_rn(0.0, w) : 0.0) : __dmul_rn(x, w);
+        acc[o] = (t == 0) ? tv : __dadd_rn(acc[o], tv);
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      if (o >= no) break;
+      const AccSet& q = sets.s[o];
+      double v = acc[o];
+      if (q.add_poly) {
+        double poly = (r == col) ? __dadd_rn(0.0, q.constant) : 0.0;
+        if (q.d1 != 0.0 || q.d2 != 0.0)
+          poly = __dadd_rn(poly, __dmul_rn(q.d1, ldexp_j(Bsrc[(int64_t)b * strideBs + (int64_t)r * bld + col], jb)));
+        if (q.d2 != 0.0) poly = __dadd_rn(poly, __dmul_rn(q.d2, B2[(int64_t)b * strideB2 + (int64_t)r * b2ld + col]));
+        v = __dadd_rn(v, poly);
+      }
+      q.out[(int64_t)b * q.strideOut + (int64_t)r * q.ldo + col] = v;
+    }
+  }
+}
+
 // perm_z from the swap sequence piv_z (LAPACK style): perm[r] = row of the original RHS in row r.
 // the row permutation of a swap sequence: one warp per system, the sequence applied by lane 0 in
 // shared memory (chunks of 4096 rows' swaps staged by the warp; larger n walks global memory)

@@ -134,6 +134,7 @@ enum Slot {
   kWsPairB = 19,        // large pair mode: B = 2^-j A, B^2, E_A
   kWsPairB2 = 21,
   kWsPairT = 22,
+  kWsPairT2 = 23,       // large pair mode: E_A of the second weight set
   kWsTriTmp = 26,       // triangular block inversion temporaries
   kWsBandA = 27,        // banded action: scaled band, factors, per-shift solutions, iterates
   kWsBandF = 28,

@@ -77,6 +77,19 @@ struct GemmParams {
 };
 void launch_gemm(const GemmParams& p, cudaStream_t stream);
 
+// accumulate_sets_kernel (large.cu): up to four weighted sums of the same solutions in one pass
+struct AccSet {
+  const double* w;  // device, n_terms weights
+  double constant, d1, d2;
+  int add_poly;
+  double* out;
+  int64_t ldo, strideOut;
+};
+struct AccSets {
+  AccSet s[4];
+  int n;
+};
+
 // Partial-pivoting panel of the blocked large LU (pivot_lu.cu): rows [off, np) x columns [off, off+w)
 // of each of nsys systems, pivots into piv[z * npiv + col]; the panel's row exchanges are then applied
 // to every other column (moves: 2 * 64 int2 per system). SingularShift below tol[z] is recorded for

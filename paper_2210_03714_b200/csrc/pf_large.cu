@@ -37,6 +37,10 @@ __global__ void certificate_kernel(const double* M, int np, int n, int nchunks, 
 __global__ void form_rhs_kernel(const double* src, int64_t lds, int64_t strideS, int n, int np, int cols,
                                 int ncols_true, int batch, const double* shifts, const int* j, int residual,
                                 const int* perm, double* R, int64_t strideR);
+__global__ void accumulate_sets_kernel(const double* X, int64_t xld, int64_t strideX, int n, int cols, int batch,
+                                       int n_terms, const int* term_z, AccSets sets, const double* Bsrc, int64_t bld,
+                                       int64_t strideBs, const int* j, const double* B2, int64_t b2ld,
+                                       int64_t strideB2);
 __global__ void accumulate_kernel(const double* X, int64_t xld, int64_t strideX, int n, int cols, int batch,
                                   int n_terms, const int* term_z, const double* w, int add_poly, double constant,
                                   double d1, double d2, const double* Bsrc, int64_t bld, int64_t strideBs,
@@ -896,26 +900,30 @@ int large_eval_pairs(pf_context* ctx, const pf_method* m, int n, int batch, cons
   std::vector<int> tz(npairs);
   for (int q = 0; q < npairs; ++q) tz[q] = q;
   int* d_tz = upload(ctx, kWsSmallArrays + 2, tz);
+  // E_B of every weight set into its output, E_A into T / T2: one pass over the solutions
+  double* T2 = m->n_sets > 1 ? static_cast<double*>(workspace(ctx, kWsPairT2, sizeof(double) * nn * batch)) : nullptr;
+  if (m->n_sets > 1 && !T2) return PF_ERR_CUDA;
+  std::vector<double> wall(4 * (size_t)npairs);
+  AccSets sets{};
+  sets.n = 2 * m->n_sets;
   for (int q = 0; q < m->n_sets; ++q) {
-    std::vector<double> wa(npairs), wb(npairs);
     double consta = 0.0;
     for (int t = 0; t < npairs; ++t) {
       const double wp = m->weights[q * m->n_terms + ip[t]], wm = m->weights[q * m->n_terms + im[t]];
-      wa[t] = (wp - wm) * c[t];
-      wb[t] = wp + wm;
-      consta += wa[t];
+      wall[(2 * q + 1) * npairs + t] = (wp - wm) * c[t];  // E_A
+      wall[(2 * q) * npairs + t] = wp + wm;              // E_B
+      consta += wall[(2 * q + 1) * npairs + t];
     }
-    double* d_wa = upload(ctx, kWsSmallArrays + 3 + 2 * q, wa);
-    double* d_wb = upload(ctx, kWsSmallArrays + 28 + q, wb);
-    // E_B into the output, E_A into T, then out = E_A B + E_B + a0 I
-    accumulate_kernel<<<dim3(grid2(nn, batch), batch), 256, 0, ctx->stream>>>(
-        R, s.np, s.stride(), n, n, batch, npairs, d_tz, d_wb, 0, 0.0, 0.0, 0.0, nullptr, 0, 0, nullptr, nullptr, 0, 0,
-        outs[q], ldo, strideOut);
-    accumulate_kernel<<<dim3(grid2(nn, batch), batch), 256, 0, ctx->stream>>>(
-        R, s.np, s.stride(), n, n, batch, npairs, d_tz, d_wa, 1, consta, 0.0, 0.0, nullptr, 0, 0, nullptr, nullptr, 0,
-        0, T, n, nn);
-    ctx->launches += 2;
-    gemm(ctx, n, n, n, batch, 1.0, T, n, nn, Bs, n, nn, 1.0, outs[q], ldo, strideOut, m->constant[q]);
+    sets.s[2 * q] = AccSet{nullptr, 0.0, 0.0, 0.0, 0, outs[q], ldo, strideOut};
+    sets.s[2 * q + 1] = AccSet{nullptr, consta, 0.0, 0.0, 1, q == 0 ? T : T2, n, nn};
+  }
+  double* d_wall = upload(ctx, kWsSmallArrays + 3, wall);
+  for (int o = 0; o < sets.n; ++o) sets.s[o].w = d_wall + (size_t)o * npairs;
+  accumulate_sets_kernel<<<dim3(grid2(nn, batch), batch), 256, 0, ctx->stream>>>(
+      R, s.np, s.stride(), n, n, batch, npairs, d_tz, sets, nullptr, 0, 0, nullptr, nullptr, 0, 0);
+  ctx->launches++;
+  for (int q = 0; q < m->n_sets; ++q) {
+    gemm(ctx, n, n, n, batch, 1.0, q == 0 ? T : T2, n, nn, Bs, n, nn, 1.0, outs[q], ldo, strideOut, m->constant[q]);
   }
   return cuda_fail(cudaGetLastError());
 }
@@ -986,30 +994,34 @@ static int large_eval_chunk(pf_context* ctx, const pf_method* m, int n, int batc
     ctx->launches++;
     gemm(ctx, n, n, n, batch, 1.0, Bs, n, (int64_t)n * n, Bs, n, (int64_t)n * n, 0.0, B2, n, (int64_t)n * n, 0.0);
   }
+  // every weight set's sum in one pass over the solutions (the term list is the same for all sets)
+  std::vector<int> tz;
+  int slot = 0;
+  for (int i = 0; i < m->n_terms; ++i) {
+    if (m->shifts[i] != 0.0)
+      tz.push_back(slot++);
+    else if (!residual)
+      tz.push_back(-1);
+  }
+  const int nt = (int)tz.size();
+  std::vector<double> wall((size_t)m->n_sets * nt);
+  AccSets sets{};
+  sets.n = m->n_sets;
+  const bool add_poly = residual || m->has_poly;
   for (int q = 0; q < m->n_sets; ++q) {
-    std::vector<int> tz;
-    std::vector<double> w;
-    int slot = 0;
-    for (int i = 0; i < m->n_terms; ++i) {
-      const double wi = m->weights[q * m->n_terms + i];
-      if (m->shifts[i] != 0.0) {
-        tz.push_back(slot++);
-        w.push_back(wi);
-      } else if (!residual) {
-        tz.push_back(-1);
-        w.push_back(wi);
-      }
-    }
-    int* d_tz = upload(ctx, kWsSmallArrays + 2 + 2 * q, tz);
-    double* d_w = upload(ctx, kWsSmallArrays + 3 + 2 * q, w);
-    const bool add_poly = residual || m->has_poly;
+    int t = 0;
+    for (int i = 0; i < m->n_terms; ++i)
+      if (m->shifts[i] != 0.0 || !residual) wall[(size_t)q * nt + t++] = m->weights[q * m->n_terms + i];
     const double constant = residual ? m->constant[q] : (m->has_poly ? m->poly[3 * q] : 0.0);
     const double d1 = m->has_poly ? m->poly[3 * q + 1] : 0.0, d2 = m->has_poly ? m->poly[3 * q + 2] : 0.0;
-    accumulate_kernel<<<dim3(grid2((int64_t)n * n, batch), batch), 256, 0, ctx->stream>>>(
-        R, s.np, s.stride(), n, n, batch, (int)tz.size(), d_tz, d_w, add_poly ? 1 : 0, constant, d1, d2, A, lda,
-        strideA, dJ, B2, n, (int64_t)n * n, outs[q], ldo, strideOut);
-    ctx->launches++;
+    sets.s[q] = AccSet{nullptr, constant, d1, d2, add_poly ? 1 : 0, outs[q], ldo, strideOut};
   }
+  int* d_tz = upload(ctx, kWsSmallArrays + 2, tz);
+  double* d_wall = upload(ctx, kWsSmallArrays + 3, wall);
+  for (int q = 0; q < m->n_sets; ++q) sets.s[q].w = d_wall + (size_t)q * nt;
+  accumulate_sets_kernel<<<dim3(grid2((int64_t)n * n, batch), batch), 256, 0, ctx->stream>>>(
+      R, s.np, s.stride(), n, n, batch, nt, d_tz, sets, A, lda, strideA, dJ, B2, n, (int64_t)n * n);
+  ctx->launches++;
   return cuda_fail(cudaGetLastError());
 }
 
