@@ -75,6 +75,11 @@ void launch_gemm(const GemmParams& p, cudaStream_t stream) {
     q.C = p.C + (int64_t)b0 * p.strideC;
     if (p.jmask) q.jmask = p.jmask + b0;
     if (p.pass) q.pass = p.pass + (int64_t)b0 * p.strideC;
+    if (p.sd_d) {
+      q.sd_ref = p.sd_ref + (int64_t)b0 * p.strideC;
+      q.sd_d = p.sd_d + (int64_t)b0 * p.strideC;
+      q.sd_e = p.sd_e + (int64_t)b0 * p.strideC;
+    }
     launch_gemm_chunk(q, stream);
   }
 }

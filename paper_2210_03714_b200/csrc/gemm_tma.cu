@@ -193,6 +193,12 @@ __global__ void __launch_bounds__(128, PF_TMA_MINB) gemm_tma_kernel(const __grid
           }
           if (p.gamma != 0.0 && r == c) v = __dadd_rn(v, p.gamma);
           *dst = v;
+          if (p.sd_d != nullptr) {
+            const int64_t o = (int64_t)bz * p.strideC + (int64_t)r * p.ldc + c;
+            const double cv = __ldcg(p.sd_ref + o);
+            p.sd_d[o] = cv - v;
+            p.sd_e[o] = cv + v;
+          }
         }
       }
 }

@@ -235,7 +235,8 @@ int launch_small_flags(pf_context* ctx, pf::SmallParams& p, int flags) {
 
 void gemm(pf_context* ctx, int m, int n, int k, int batch, double alpha, const double* A, int64_t lda,
           int64_t sA, const double* B, int64_t ldb, int64_t sB, double beta, double* C, int64_t ldc, int64_t sC,
-          double gamma, const int* jmask, int step, const double* pass) {
+          double gamma, const int* jmask, int step, const double* pass, const double* sd_ref, double* sd_d,
+          double* sd_e) {
   if (ctx->l2_persisting) {  // the small kernel's slots: give the set-aside back to the GEMM tiles
     cudaCtxResetPersistingL2Cache();
     cudaGetLastError();
@@ -262,6 +263,9 @@ void gemm(pf_context* ctx, int m, int n, int k, int batch, double alpha, const d
   g.step = step;
   g.pass = pass;
   g.max_sms = ctx->gemm_cap;
+  g.sd_ref = sd_ref;
+  g.sd_d = sd_d;
+  g.sd_e = sd_e;
   pf::launch_gemm(g, ctx->stream);
   ctx->launches++;
 }
@@ -695,11 +699,17 @@ int pf_cossin_batched(pf_context* ctx, const pf_pair_method* pm, double theta, i
   double* D = jmax > 0 ? static_cast<double*>(workspace(ctx, kWsPairB, sizeof(double) * nn * batch)) : nullptr;
   double* Ep = jmax > 0 ? static_cast<double*>(workspace(ctx, kWsPairT, sizeof(double) * nn * batch)) : nullptr;
   if (jmax > 0 && (!D || !Ep)) return PF_ERR_CUDA;
+  // D = C - S and E = C + S come from the epilogue of the GEMM that produces S (it reads C's tile
+  // there), so no separate elementwise pass: the first from S = B S', then from every S <- 2 S C
   for (int s = 0; s < jmax; ++s) {
-    pf::launch_sum_diff(nn * batch, C, S, D, Ep, ctx->stream);
-    ctx->launches++;
+    if (s == 0) {
+      pf::launch_sum_diff(nn * batch, C, S, D, Ep, ctx->stream);
+      ctx->launches++;
+    }
     gemm(ctx, n, n, n, batch, 1.0, D, n, nn, Ep, n, nn, 0.0, C2, n, nn, 0.0, dJ, s, C);
-    gemm(ctx, n, n, n, batch, 2.0, S, n, nn, C, n, nn, 0.0, Sp, n, nn, 0.0, dJ, s, S);
+    const bool more = s + 1 < jmax;
+    gemm(ctx, n, n, n, batch, 2.0, S, n, nn, C, n, nn, 0.0, Sp, n, nn, 0.0, dJ, s, S, more ? C2 : nullptr,
+         more ? D : nullptr, more ? Ep : nullptr);
     std::swap(C, C2);
     std::swap(S, Sp);
   }

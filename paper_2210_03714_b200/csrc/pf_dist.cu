@@ -196,11 +196,15 @@ int pf_cossin_doubling(pf_context* ctx, int n, int batch, const int* dJ, double*
   double* D = jmax > 0 ? static_cast<double*>(workspace(ctx, kWsPairB, sizeof(double) * nn * batch)) : nullptr;
   double* Ep = jmax > 0 ? static_cast<double*>(workspace(ctx, kWsPairT, sizeof(double) * nn * batch)) : nullptr;
   if (jmax > 0 && (!D || !Ep)) return PF_ERR_CUDA;
-  for (int s = 0; s < jmax; ++s) {
-    pf::launch_sum_diff(nn * batch, C, S, D, Ep, ctx->stream);
-    ctx->launches++;
+  for (int s = 0; s < jmax; ++s) {  // D / E of the next step from the S GEMM's epilogue
+    if (s == 0) {
+      pf::launch_sum_diff(nn * batch, C, S, D, Ep, ctx->stream);
+      ctx->launches++;
+    }
     gemm(ctx, n, n, n, batch, 1.0, D, n, nn, Ep, n, nn, 0.0, C2, n, nn, 0.0, dJ, s, C);
-    gemm(ctx, n, n, n, batch, 2.0, S, n, nn, C, n, nn, 0.0, Sp, n, nn, 0.0, dJ, s, S);
+    const bool more = s + 1 < jmax;
+    gemm(ctx, n, n, n, batch, 2.0, S, n, nn, C, n, nn, 0.0, Sp, n, nn, 0.0, dJ, s, S, more ? C2 : nullptr,
+         more ? D : nullptr, more ? Ep : nullptr);
     std::swap(C, C2);
     std::swap(S, Sp);
   }

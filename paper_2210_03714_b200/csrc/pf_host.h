@@ -112,7 +112,8 @@ int launch_small(pf_context* ctx, SmallParams& p);
 int launch_small_reference_order(pf_context* ctx, SmallParams& p);
 void gemm(pf_context* ctx, int m, int n, int k, int batch, double alpha, const double* A, int64_t lda, int64_t sA,
           const double* B, int64_t ldb, int64_t sB, double beta, double* C, int64_t ldc, int64_t sC, double gamma,
-          const int* jmask = nullptr, int step = 0, const double* pass = nullptr);
+          const int* jmask = nullptr, int step = 0, const double* pass = nullptr, const double* sd_ref = nullptr,
+          double* sd_d = nullptr, double* sd_e = nullptr);
 int max_j(pf_context* ctx, const int* dJ, int batch, int* out);
 
 // workspace slots (each slot is an independently grown device buffer)

@@ -74,6 +74,11 @@ struct GemmParams {
   // > 0: persistent launch on at most max_sms SMs' worth of CTAs, each looping over tiles (leaves
   // SMs free for concurrent work on other streams)
   int max_sms;
+  // optional epilogue (the cos/sin double angle, pf_cossin_batched): with sd_d != nullptr, for every
+  // written element v of C also sd_d = ref - v and sd_e = ref + v, ref = sd_ref (C's layout)
+  const double* sd_ref;
+  double* sd_d;
+  double* sd_e;
 };
 void launch_gemm(const GemmParams& p, cudaStream_t stream);
 
