@@ -32,6 +32,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -110,7 +111,11 @@ __global__ void __launch_bounds__(128, PF_TMA_MINB) gemm_tma_kernel(const __grid
   const int g = lane >> 2, t = lane & 3;
   const int wm = 32 * (warp >> 1), wn = 32 * (warp & 1);
   const unsigned base = su32(tsm), fullb = su32(full), emptyb = su32(empty);
-  const int nk = (p.k + TBK - 1) / TBK;
+  // split-K: this CTA's k tiles [kb, ke) (gridDim.z splits)
+  const int nk_all = (p.k + TBK - 1) / TBK;
+  const int per = (nk_all + gridDim.z - 1) / gridDim.z;
+  const int kb = blockIdx.z * per, ke = min(nk_all, kb + per);
+  const int nk = max(ke - kb, 0);
   if (tid == 0) {
     for (int s = 0; s < TSTAGES; ++s) {
       mb_init(fullb + 8 * s, 1);
@@ -125,9 +130,9 @@ __global__ void __launch_bounds__(128, PF_TMA_MINB) gemm_tma_kernel(const __grid
     const int s = kt % TSTAGES;
     const unsigned sa = base + s * STAGE_BYTES, sb = sa + A_BYTES, bar = fullb + 8 * s;
     mb_expect(bar, STAGE_BYTES);
-    tma3(sa, &maps.a, kt * TBK, m0, bz, bar);
+    tma3(sa, &maps.a, (kb + kt) * TBK, m0, bz, bar);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) tma3(sb + q * 2048, &maps.b, n0 + 16 * q, kt * TBK, bz, bar);
+    for (int q = 0; q < 4; ++q) tma3(sb + q * 2048, &maps.b, n0 + 16 * q, (kb + kt) * TBK, bz, bar);
   };
   if (tid == 0)
     for (int kt = 0; kt < TSTAGES - 1 && kt < nk; ++kt) issue(kt);
@@ -176,6 +181,19 @@ __global__ void __launch_bounds__(128, PF_TMA_MINB) gemm_tma_kernel(const __grid
     if (lane == 0) mb_arrive(emptyb + 8 * s);
   }
 
+  if (gridDim.z > 1) {  // split-K: the raw partial product; splitk_reduce_kernel finishes
+    double* w = p.split_ws + ((int64_t)blockIdx.z * p.batch + bz) * p.m * p.n;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int nj = 0; nj < 4; ++nj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = m0 + wm + 8 * mi + g, c = n0 + wn + 8 * nj + 2 * t + e;
+          if (r < p.m && c < p.n) w[(int64_t)r * p.n + c] = acc[mi][nj][e];
+        }
+    return;
+  }
   // epilogue: alpha * acc (+ beta * C) (+ gamma on the diagonal), as gemm_tile
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
@@ -230,6 +248,25 @@ bool encode(CUtensorMap* map, const double* base, uint64_t inner, uint64_t outer
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// C = alpha (sum of the split partials, ascending split) (+ beta C) (+ gamma I): gemm_tile's epilogue
+__global__ void splitk_reduce_kernel(GemmParams p, int splits) {
+  const int bz = blockIdx.y;
+  const int64_t mn = (int64_t)p.m * p.n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < mn; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / p.n), c = (int)(idx % p.n);
+    double a = p.split_ws[(int64_t)bz * mn + idx];
+    for (int z = 1; z < splits; ++z) a = __dadd_rn(a, p.split_ws[((int64_t)z * p.batch + bz) * mn + idx]);
+    double v = p.alpha == 1.0 ? a : __dmul_rn(p.alpha, a);
+    double* dst = p.C + (int64_t)bz * p.strideC + (int64_t)r * p.ldc + c;
+    if (p.beta != 0.0) {
+      const double cv = *dst;
+      v = __dadd_rn(p.beta == 1.0 ? cv : __dmul_rn(p.beta, cv), v);
+    }
+    if (p.gamma != 0.0 && r == c) v = __dadd_rn(v, p.gamma);
+    *dst = v;
+  }
+}
+
 }  // namespace
 
 size_t gemm_tma_smem_bytes() { return TSTAGES * STAGE_BYTES + 2 * TSTAGES * 8 + 1024; }
@@ -249,7 +286,16 @@ bool launch_gemm_tma(const GemmParams& p, cudaStream_t stream) {
   const int smem = (int)gemm_tma_smem_bytes();
   if (set_smem_attr_once(reinterpret_cast<const void*>(gemm_tma_kernel), smem) != cudaSuccess) return false;
   const int tiles_m = (p.m + TBM - 1) / TBM, tiles_n = (p.n + TBN - 1) / TBN;
-  gemm_tma_kernel<<<dim3(tiles_m * tiles_n, p.batch), 128, smem, stream>>>(maps, p, tiles_n);
+  int splits = gemm_split_k(p.n, p.k);
+  if (splits > 1 && (p.jmask != nullptr || p.sd_d != nullptr || p.split_ws == nullptr ||
+                     p.split_ws_elems < (int64_t)splits * p.batch * p.m * p.n))
+    splits = 1;
+  gemm_tma_kernel<<<dim3(tiles_m * tiles_n, p.batch, splits), 128, smem, stream>>>(maps, p, tiles_n);
+  if (splits > 1) {
+    const int64_t mn = (int64_t)p.m * p.n;
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((mn + 255) / 256, 2368 / std::max(1, p.batch) + 1));
+    splitk_reduce_kernel<<<dim3(blocks, p.batch), 256, 0, stream>>>(p, splits);
+  }
   return cudaGetLastError() == cudaSuccess;
 }
 

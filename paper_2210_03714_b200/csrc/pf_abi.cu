@@ -266,6 +266,17 @@ void gemm(pf_context* ctx, int m, int n, int k, int batch, double alpha, const d
   g.sd_ref = sd_ref;
   g.sd_d = sd_d;
   g.sd_e = sd_e;
+  const int splits = pf::gemm_split_k(n, k);
+  // one split workspace per context: not on the LU's concurrent side / look-ahead streams
+  bool concurrent = ctx->side != nullptr && ctx->stream == ctx->side;
+  for (cudaStream_t a : ctx->aux) concurrent |= ctx->stream == a;
+  if (splits > 1 && jmask == nullptr && sd_d == nullptr && !concurrent) {
+    const int64_t elems = (int64_t)splits * batch * m * n;
+    if (elems * (int64_t)sizeof(double) <= (int64_t)512 << 20) {
+      g.split_ws = static_cast<double*>(workspace(ctx, kWsGemmSplit, sizeof(double) * (size_t)elems));
+      g.split_ws_elems = g.split_ws ? elems : 0;
+    }
+  }
   pf::launch_gemm(g, ctx->stream);
   ctx->launches++;
 }

@@ -136,6 +136,7 @@ enum Slot {
   kWsPairB2 = 21,
   kWsPairT = 22,
   kWsPairT2 = 23,       // large pair mode: E_A of the second weight set
+  kWsGemmSplit = 24,    // split-K partial products of thin GEMMs
   kWsTriTmp = 26,       // triangular block inversion temporaries
   kWsBandA = 27,        // banded action: scaled band, factors, per-shift solutions, iterates
   kWsBandF = 28,

@@ -79,8 +79,20 @@ struct GemmParams {
   const double* sd_ref;
   double* sd_d;
   double* sd_e;
+  // split-K workspace for thin products (gemm_split_k): splits x batch x m x n doubles, or nullptr
+  double* split_ws;
+  int64_t split_ws_elems;
 };
 void launch_gemm(const GemmParams& p, cudaStream_t stream);
+
+// K splits of the TMA GEMM for thin products (n <= 128 columns, e.g. the action's 64 right-hand
+// sides): the m x n tiles alone fill a fraction of the SMs. A function of (n, k) only, so every
+// row partition of the same product splits identically (bit-identical rows). 1 = no split.
+inline int gemm_split_k(int n, int k) {
+  if (n > 128 || k < 1024) return 1;
+  const int s = k / 512;
+  return s < 2 ? 2 : (s > 4 ? 4 : s);
+}
 
 // accumulate_sets_kernel (large.cu): up to four weighted sums of the same solutions in one pass
 struct AccSet {

@@ -304,6 +304,8 @@ def test_gemm_shapes_and_epilogue(dev):
     run(96, 96, 48, 1, 48, 96, 96, alpha=-1.0, beta=1.0, gamma=1.0)
     run(100, 37, 61, 2, 61, 37, 37)            # odd leading dimensions: the cp.async kernel
     run(1, 1, 1, 1, 2, 2, 2)
+    run(300, 64, 4096, 2, 4096, 64, 64, beta=1.0)   # thin: split-K partials + ordered reduce
+    run(130, 7, 1500, 1, 1500, 8, 8, alpha=2.0)     # thin, ragged, k not a multiple of a split
 
 
 def test_native_library_is_loaded(dev):
