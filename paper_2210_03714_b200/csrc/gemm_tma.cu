@@ -252,8 +252,10 @@ bool encode(CUtensorMap* map, const double* base, uint64_t inner, uint64_t outer
 __global__ void splitk_reduce_kernel(GemmParams p, int splits) {
   const int bz = blockIdx.y;
   const int64_t mn = (int64_t)p.m * p.n;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < mn; idx += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(idx / p.n), c = (int)(idx % p.n);
+  // rows over blockIdx.x / threadIdx.y, columns over threadIdx.x (no 64-bit index division)
+  for (int r = blockIdx.x * blockDim.y + threadIdx.y; r < p.m; r += gridDim.x * blockDim.y)
+    for (int c = threadIdx.x; c < p.n; c += blockDim.x) {
+    const int64_t idx = (int64_t)r * p.n + c;
     double a = p.split_ws[(int64_t)bz * mn + idx];
     for (int z = 1; z < splits; ++z) a = __dadd_rn(a, p.split_ws[((int64_t)z * p.batch + bz) * mn + idx]);
     double v = p.alpha == 1.0 ? a : __dmul_rn(p.alpha, a);
@@ -264,7 +266,7 @@ __global__ void splitk_reduce_kernel(GemmParams p, int splits) {
     }
     if (p.gamma != 0.0 && r == c) v = __dadd_rn(v, p.gamma);
     *dst = v;
-  }
+    }
 }
 
 }  // namespace
@@ -286,15 +288,15 @@ bool launch_gemm_tma(const GemmParams& p, cudaStream_t stream) {
   const int smem = (int)gemm_tma_smem_bytes();
   if (set_smem_attr_once(reinterpret_cast<const void*>(gemm_tma_kernel), smem) != cudaSuccess) return false;
   const int tiles_m = (p.m + TBM - 1) / TBM, tiles_n = (p.n + TBN - 1) / TBN;
-  int splits = gemm_split_k(p.n, p.k);
+  int splits = p.splits;
   if (splits > 1 && (p.jmask != nullptr || p.sd_d != nullptr || p.split_ws == nullptr ||
                      p.split_ws_elems < (int64_t)splits * p.batch * p.m * p.n))
     splits = 1;
   gemm_tma_kernel<<<dim3(tiles_m * tiles_n, p.batch, splits), 128, smem, stream>>>(maps, p, tiles_n);
   if (splits > 1) {
-    const int64_t mn = (int64_t)p.m * p.n;
-    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((mn + 255) / 256, 2368 / std::max(1, p.batch) + 1));
-    splitk_reduce_kernel<<<dim3(blocks, p.batch), 256, 0, stream>>>(p, splits);
+    const int tx = p.n >= 64 ? 64 : 32, ty = 256 / tx;
+    const unsigned blocks = (unsigned)std::max(1, std::min((p.m + ty - 1) / ty, 2368 / std::max(1, p.batch) + 1));
+    splitk_reduce_kernel<<<dim3(blocks, p.batch), dim3(tx, ty), 0, stream>>>(p, splits);
   }
   return cudaGetLastError() == cudaSuccess;
 }

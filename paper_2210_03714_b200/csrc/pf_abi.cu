@@ -266,7 +266,9 @@ void gemm(pf_context* ctx, int m, int n, int k, int batch, double alpha, const d
   g.sd_ref = sd_ref;
   g.sd_d = sd_d;
   g.sd_e = sd_e;
-  const int splits = pf::gemm_split_k(n, k);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  const int splits = pf::gemm_split_k(m, n, k, batch, sms);
   // one split workspace per context: not on the LU's concurrent side / look-ahead streams
   bool concurrent = ctx->side != nullptr && ctx->stream == ctx->side;
   for (cudaStream_t a : ctx->aux) concurrent |= ctx->stream == a;
@@ -275,6 +277,7 @@ void gemm(pf_context* ctx, int m, int n, int k, int batch, double alpha, const d
     if (elems * (int64_t)sizeof(double) <= (int64_t)512 << 20) {
       g.split_ws = static_cast<double*>(workspace(ctx, kWsGemmSplit, sizeof(double) * (size_t)elems));
       g.split_ws_elems = g.split_ws ? elems : 0;
+      g.splits = g.split_ws ? splits : 1;
     }
   }
   pf::launch_gemm(g, ctx->stream);

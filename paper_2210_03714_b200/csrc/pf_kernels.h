@@ -82,16 +82,20 @@ struct GemmParams {
   // split-K workspace for thin products (gemm_split_k): splits x batch x m x n doubles, or nullptr
   double* split_ws;
   int64_t split_ws_elems;
+  int splits;  // gemm_split_k's choice (0 / 1: none)
 };
 void launch_gemm(const GemmParams& p, cudaStream_t stream);
 
 // K splits of the TMA GEMM for thin products (n <= 128 columns, e.g. the action's 64 right-hand
-// sides): the m x n tiles alone fill a fraction of the SMs. A function of (n, k) only, so every
-// row partition of the same product splits identically (bit-identical rows). 1 = no split.
-inline int gemm_split_k(int n, int k) {
+// sides) whose 64 x 64 tiles fill less than four CTAs per SM: enough splits (k / 256 at most, 8 at
+// most) to fill them. Deterministic: fixed split boundaries, partials summed in split order.
+inline int gemm_split_k(int m, int n, int k, int batch, int sms) {
   if (n > 128 || k < 1024) return 1;
-  const int s = k / 512;
-  return s < 2 ? 2 : (s > 4 ? 4 : s);
+  const long long ctas = (long long)((m + 63) / 64) * ((n + 63) / 64) * batch;
+  const long long want = (4LL * sms + ctas - 1) / ctas;
+  long long s = want < k / 256 ? want : k / 256;
+  if (s > 8) s = 8;
+  return s < 2 ? 1 : (int)s;
 }
 
 // accumulate_sets_kernel (large.cu): up to four weighted sums of the same solutions in one pass
