@@ -288,7 +288,7 @@ bool launch_gemm_tma(const GemmParams& p, cudaStream_t stream) {
   const int smem = (int)gemm_tma_smem_bytes();
   if (set_smem_attr_once(reinterpret_cast<const void*>(gemm_tma_kernel), smem) != cudaSuccess) return false;
   const int tiles_m = (p.m + TBM - 1) / TBM, tiles_n = (p.n + TBN - 1) / TBN;
-  int splits = p.splits;
+  int splits = p.splits > 1 ? p.splits : 1;
   if (splits > 1 && (p.jmask != nullptr || p.sd_d != nullptr || p.split_ws == nullptr ||
                      p.split_ws_elems < (int64_t)splits * p.batch * p.m * p.n))
     splits = 1;
