@@ -288,3 +288,19 @@ def test_blocked_pivoting_batch_and_singular_column(dev):
         dev.DenseLu(np.stack([good, piv1, sing]))
     assert e.value.code == Errc.SingularShift
     assert "at column 257 " in str(e.value) and "matrix 2" in str(e.value)
+
+
+@pytest.mark.parametrize("n", [300, 700])
+def test_blocked_pivoting_ties_and_zero_multipliers(dev, oracle, n):
+    """Small-integer entries: equal |a| in a column (the reference takes the first such row in the
+    current order, dense.cpp:107-115), exact cancellations (zero multipliers skip their update,
+    :125-131), candidates tied across the CTAs of a panel cluster (n = 700: three CTAs for the
+    first panel). The first column's pivot is a tie among many rows; pivots and factors must be the
+    reference's."""
+    rng = np.random.default_rng(n)
+    mm = rng.integers(-2, 3, size=(n, n)).astype(np.float64)
+    mm[np.arange(n), np.arange(n)] += 0.5  # nonsingular, still not dominant
+    LU, piv = dev.DenseLu(mm).factors()
+    rlu, rpiv = oracle.lu(mm)
+    assert np.array_equal(piv, rpiv)
+    assert oracle.rel_diff_1norm(LU, rlu) <= 1e-11
