@@ -301,6 +301,13 @@ __device__ __forceinline__ void update_from_block(double (&v)[PW], int c, double
   }
 }
 
+// the candidate row's columns [8 B, 64) into the staging slot (16-byte stores)
+template <int B>
+__device__ __forceinline__ void stage_from_block(const double (&v)[PW], double2* w2) {
+#pragma unroll
+  for (int j = 4 * B; j < PW / 2; ++j) w2[j] = make_double2(v[2 * j], v[2 * j + 1]);
+}
+
 // ASYNC: candidates exchanged by st.async into the receivers' mbarriers; otherwise plain remote
 // stores and one cluster barrier per column (the A/B variant, PF_PANEL_CLUSTER_SYNC). Per column:
 // each warp's argmax (redux) -- its winner stages (row, key, position, 1/pivot) in shared memory --
@@ -361,8 +368,17 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
     const int wl = lane_argmax(key, done ? 0xFFFFFFFFu : (unsigned)pos);
     if (lane == wl) {
       double2* w2 = reinterpret_cast<double2*>(sh.wrows[par][warp]);
-#pragma unroll
-      for (int j = 0; j < PW / 2; ++j) w2[j] = make_double2(v[2 * j], v[2 * j + 1]);
+      // only columns >= 8 (c / 8) are read by the update (the earlier ones are final multipliers)
+      switch (c >> 3) {
+        case 0: stage_from_block<0>(v, w2); break;
+        case 1: stage_from_block<1>(v, w2); break;
+        case 2: stage_from_block<2>(v, w2); break;
+        case 3: stage_from_block<3>(v, w2); break;
+        case 4: stage_from_block<4>(v, w2); break;
+        case 5: stage_from_block<5>(v, w2); break;
+        case 6: stage_from_block<6>(v, w2); break;
+        default: stage_from_block<7>(v, w2); break;
+      }
       w2[PW / 2] = make_double2(__longlong_as_double((long long)key), __longlong_as_double((long long)(((unsigned long long)(unsigned)pos << 32) | (unsigned)tid)));
       w2[PW / 2 + 1] = make_double2(1.0 / vc, 0.0);
       sh.red_key[par][warp] = key;
