@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
     cbar_init(smem_u32(&sh.bar[0]), 1);
     cbar_init(smem_u32(&sh.bar[1]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    cbar_expect(smem_u32(&sh.bar[0]), kCandBytes * C);  // columns 0 and 1: the whole payload
+    cbar_expect(smem_u32(&sh.bar[0]), kCandBytes * C);  // columns 0 and 1
     cbar_expect(smem_u32(&sh.bar[1]), kCandBytes * C);
   }
   cluster.sync();
@@ -389,21 +389,19 @@ __global__ void __launch_bounds__(RT, 1) panel_lu_reg_kernel(double* M, int64_t 
     const double* prow = sh.wrows[par][ww];
     if (C > 1) {
       // ---- exchange: the CTA's candidate payload into every CTA's slot [par][rank]
-      // 16-byte pieces [e0, CW / 2): the staged (live) columns and the metadata
-      const int e0 = 4 * (c >> 3), E = CW / 2 - e0;
+      constexpr int E = CW / 2;  // 16-byte pieces per payload
       const double2* c2 = reinterpret_cast<const double2*>(prow);
       if (ASYNC) {
         for (int k = tid; k < C * E; k += RT) {
-          const int q = k / E, e = e0 + (k - q * E);
+          const int q = k / E, e = k - q * E;
           const double2 t = c2[e];
           st_async2(cluster_addr(&sh.rows[par][rank][2 * e], q), t.x, t.y, cluster_addr(&sh.bar[par], q));
         }
         cbar_wait(smem_u32(&sh.bar[par]), (c >> 1) & 1);
-        if (tid == 0 && c + 2 < PW)
-          cbar_expect(smem_u32(&sh.bar[par]), 16u * (unsigned)(CW / 2 - 4 * ((c + 2) >> 3)) * C);
+        if (tid == 0 && c + 2 < PW) cbar_expect(smem_u32(&sh.bar[par]), kCandBytes * C);
       } else {
         for (int k = tid; k < C * E; k += RT) {
-          const int q = k / E, e = e0 + (k - q * E);
+          const int q = k / E, e = k - q * E;
           RegPanelShared* o = cluster.map_shared_rank(&sh, q);
           reinterpret_cast<double2*>(o->rows[par][rank])[e] = c2[e];
         }
