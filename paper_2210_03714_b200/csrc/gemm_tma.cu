@@ -48,7 +48,7 @@ namespace {
 #ifndef PF_TMA_MINB
 #define PF_TMA_MINB 4
 #endif
-constexpr int TBM = 64, TBN = 64, TBK = 16;
+constexpr int TBM = 64, TBN = 64, TBK = 16, TSTAGES = PF_TMA_STAGES;
 constexpr int A_BYTES = TBM * TBK * 8;  // 8 KB
 constexpr int B_BYTES = TBK * TBN * 8;  // 8 KB (four 2 KB boxes)
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -87,8 +87,7 @@ struct TmaMaps {
   CUtensorMap b;  // dims {n, k, batch}, box {16, 16, 1}
 };
 
-template <int TSTAGES, int MINB>
-__global__ void __launch_bounds__(128, MINB) gemm_tma_kernel(const __grid_constant__ TmaMaps maps, GemmParams p,
+__global__ void __launch_bounds__(128, PF_TMA_MINB) gemm_tma_kernel(const __grid_constant__ TmaMaps maps, GemmParams p,
                                                           int tiles_n) {
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   // 1024-byte alignment for the 128-byte swizzle pattern
@@ -272,7 +271,7 @@ __global__ void splitk_reduce_kernel(GemmParams p, int splits) {
 
 }  // namespace
 
-size_t gemm_tma_smem_bytes(int stages) { return stages * STAGE_BYTES + 2 * stages * 8 + 1024; }
+size_t gemm_tma_smem_bytes() { return TSTAGES * STAGE_BYTES + 2 * TSTAGES * 8 + 1024; }
 
 // true: launched on the TMA path; false: not applicable (the caller runs the cp.async kernel)
 bool launch_gemm_tma(const GemmParams& p, cudaStream_t stream) {
@@ -286,22 +285,14 @@ bool launch_gemm_tma(const GemmParams& p, cudaStream_t stream) {
   if (!encode(&maps.a, p.A, (uint64_t)p.k, (uint64_t)p.m, (uint64_t)p.batch, p.lda, p.strideA, 16, 64) ||
       !encode(&maps.b, p.B, (uint64_t)p.n, (uint64_t)p.k, (uint64_t)p.batch, p.ldb, p.strideB, 16, 16))
     return false;
+  const int smem = (int)gemm_tma_smem_bytes();
+  if (set_smem_attr_once(reinterpret_cast<const void*>(gemm_tma_kernel), smem) != cudaSuccess) return false;
   const int tiles_m = (p.m + TBM - 1) / TBM, tiles_n = (p.n + TBN - 1) / TBN;
   int splits = p.splits > 1 ? p.splits : 1;
   if (splits > 1 && (p.jmask != nullptr || p.sd_d != nullptr || p.split_ws == nullptr ||
                      p.split_ws_elems < (int64_t)splits * p.batch * p.m * p.n))
     splits = 1;
-  const dim3 grid(tiles_m * tiles_n, p.batch, splits);
-  // grids well under one wave (the LU recursion's short-k products): a deeper ring keeps every
-  // k tile of a short product in flight (load latency, not occupancy, is their limit)
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const bool deep = (int64_t)grid.x * grid.y * grid.z < 2LL * sms;
-  auto kern = deep ? gemm_tma_kernel<4, 3> : gemm_tma_kernel<PF_TMA_STAGES, PF_TMA_MINB>;
-  const int smem = (int)gemm_tma_smem_bytes(deep ? 4 : PF_TMA_STAGES);
-  if (set_smem_attr_once(reinterpret_cast<const void*>(kern), smem) != cudaSuccess) return false;
-  kern<<<grid, 128, smem, stream>>>(maps, p, tiles_n);
+  gemm_tma_kernel<<<dim3(tiles_m * tiles_n, p.batch, splits), 128, smem, stream>>>(maps, p, tiles_n);
   if (splits > 1) {
     const int tx = p.n >= 64 ? 64 : 32, ty = 256 / tx;
     const unsigned blocks = (unsigned)std::max(1, std::min((p.m + ty - 1) / ty, 2368 / std::max(1, p.batch) + 1));
