@@ -542,9 +542,12 @@ int pivoted_blocked_lu(pf_context* ctx, const Sys& s, int n, const std::vector<i
   double* d_tol = upload(ctx, kWsSmallArrays + 25, tol);
   rlu_pivot(ctx, sp, 0, s.np, PivotScratch{piv_g, d_tol, d_fail, failed, moves, moves_n});
   for (int q = 0; q < nf; ++q) {
-    if (side)
+    if (side) {  // the factors and the leaves' block inverses back to their systems' slots
       cudaMemcpyAsync(s.M + fails[q] * s.stride(), side + q * s.stride(), sizeof(double) * s.stride(),
                       cudaMemcpyDeviceToDevice, ctx->stream);
+      cudaMemcpyAsync(s.inv + fails[q] * s.inv_stride, inv_g + q * s.inv_stride, sizeof(double) * s.inv_stride,
+                      cudaMemcpyDeviceToDevice, ctx->stream);
+    }
     cudaMemcpyAsync(d_piv + (size_t)fails[q] * n, piv_g + (size_t)q * s.np, sizeof(int) * n, cudaMemcpyDeviceToDevice,
                     ctx->stream);
   }
@@ -655,9 +658,8 @@ FactorResult factor_systems(pf_context* ctx, const Sys& s, int n, unsigned long 
   }
   perm_from_piv_kernel<<<nf, 32, 0, ctx->stream>>>(d_piv, n, d_perm, d_fail);
   ctx->launches++;
-  for (int off = 0; off < s.np; off += kB) {
-    lu_base(ctx, s, nf, off, 0, d_fail);
-  }
+  if (unblocked)  // the blocked LU formed every diagonal block's inverses after its panel
+    for (int off = 0; off < s.np; off += kB) lu_base(ctx, s, nf, off, 0, d_fail);
   return fr;
 }
 
