@@ -1174,12 +1174,17 @@ __global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64
     const int t = s_task;
     if (t >= ntasks) return;
     const int4 tk = tasks[t];
-    const int type = tk.x >> 24, z = tk.x & 0xffffff, i = tk.y, j = tk.z, k = tk.w;  // tile (i, j), step k
+    // type (bits 24-27), half (bit 28: R / C tasks are split into their two 64-wide chunks, so the
+    // critical R(k, k+1) / C(k+1, k) run on two SMs each), system (bits 0-23)
+    const int type = (tk.x >> 24) & 15, half = (tk.x >> 28) & 1, z = tk.x & 0xffffff, i = tk.y, j = tk.z, k = tk.w;
     int* st = state + (int64_t)z * nt * nt;
+    // tile states count half-steps: an F or G task moves its tile from 2k to 2k + 2, each R / C
+    // chunk adds one
     if (threadIdx.x == 0) {
-      bool ok = wait_ge(st + i * nt + j, k, err);  // the tile has received steps 0 .. k-1
-      if (ok && (type == 1 || type == 2)) ok = wait_ge(st + k * nt + k, k + 1, err);  // F(k) done
-      if (ok && type == 3) ok = wait_ge(st + i * nt + k, k + 1, err) && wait_ge(st + k * nt + j, k + 1, err);
+      bool ok = wait_ge(st + i * nt + j, 2 * k, err);  // the tile has received steps 0 .. k-1
+      if (ok && (type == 1 || type == 2)) ok = wait_ge(st + k * nt + k, 2 * k + 2, err);  // F(k) done
+      if (ok && type == 3)
+        ok = wait_ge(st + i * nt + k, 2 * k + 2, err) && wait_ge(st + k * nt + j, 2 * k + 2, err);
       s_ok = ok;
     }
     __syncthreads();
@@ -1190,12 +1195,9 @@ __global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64
     double* tile = Mz + (int64_t)T * i * np + T * j;
     if (type == 0) {
       lu128_block(dblk, np, bi, dsm);
-    } else if (type == 1 || type == 2) {
-      for (int h = 0; h < 2; ++h) {  // two 64-column (R) / 64-row (C) chunks
-        trsm128_chunk(dblk, np, bi, type == 1 ? 0 : 2, type == 1 ? tile + B64 * h : tile + (int64_t)B64 * h * np, np,
-                      B64, dsm);
-        __syncthreads();
-      }
+    } else if (type == 1 || type == 2) {  // one 64-column (R) / 64-row (C) chunk
+      trsm128_chunk(dblk, np, bi, type == 1 ? 0 : 2, type == 1 ? tile + B64 * half : tile + (int64_t)B64 * half * np,
+                    np, B64, dsm);
     } else {
       GemmParams p{};
       p.m = p.n = p.k = T;
@@ -1213,7 +1215,10 @@ __global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
-      st_release(st + i * nt + j, k + 1);
+      if (type == 1 || type == 2)
+        atomicAdd(st + i * nt + j, 1);  // ordered after the fence; the waiter acquires
+      else
+        st_release(st + i * nt + j, 2 * k + 2);
     }
   }
 }

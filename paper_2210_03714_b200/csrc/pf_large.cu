@@ -377,7 +377,9 @@ const std::vector<int4>& dag_tasks(int nt, int nsys) {
   if (it != cache.end()) return it->second;
   std::vector<int4> t;
   auto add = [&](int type, int i, int j, int k) {
-    for (int z = 0; z < nsys; ++z) t.push_back(make_int4((type << 24) | z, i, j, k));
+    const int halves = (type == 1 || type == 2) ? 2 : 1;  // R / C: one task per 64-wide chunk
+    for (int z = 0; z < nsys; ++z)
+      for (int h = 0; h < halves; ++h) t.push_back(make_int4((h << 28) | (type << 24) | z, i, j, k));
   };
   auto panel = [&](int k) {  // F(k), then R(k, j) / C(j, k) interleaved, nearest first
     add(0, k, k, k);
