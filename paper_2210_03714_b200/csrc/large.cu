@@ -1174,17 +1174,19 @@ __global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64
     const int t = s_task;
     if (t >= ntasks) return;
     const int4 tk = tasks[t];
-    // type (bits 24-27), half (bit 28: R / C tasks are split into their two 64-wide chunks, so the
-    // critical R(k, k+1) / C(k+1, k) run on two SMs each), system (bits 0-23)
-    const int type = (tk.x >> 24) & 15, half = (tk.x >> 28) & 1, z = tk.x & 0xffffff, i = tk.y, j = tk.z, k = tk.w;
+    // type (bits 24-27), part (bits 28-29: R / C tasks split into their two 64-wide chunks, the
+    // look-ahead update of the next diagonal tile into four 64 x 64 quarters, so the critical path's
+    // tasks run on several SMs each), system (bits 0-23)
+    const int type = (tk.x >> 24) & 15, part = (tk.x >> 28) & 3, z = tk.x & 0xffffff, i = tk.y, j = tk.z, k = tk.w;
+    const bool quarter = type == 4;  // a quarter of G(k + 1, k + 1, k)
     int* st = state + (int64_t)z * nt * nt;
-    // tile states count half-steps: an F or G task moves its tile from 2k to 2k + 2, each R / C
-    // chunk adds one
+    // tile states count quarter-steps: an F or G task moves its tile from 4k to 4k + 4, each R / C
+    // chunk adds 2, each G quarter 1
     if (threadIdx.x == 0) {
-      bool ok = wait_ge(st + i * nt + j, 2 * k, err);  // the tile has received steps 0 .. k-1
-      if (ok && (type == 1 || type == 2)) ok = wait_ge(st + k * nt + k, 2 * k + 2, err);  // F(k) done
-      if (ok && type == 3)
-        ok = wait_ge(st + i * nt + k, 2 * k + 2, err) && wait_ge(st + k * nt + j, 2 * k + 2, err);
+      bool ok = wait_ge(st + i * nt + j, 4 * k, err);  // the tile has received steps 0 .. k-1
+      if (ok && (type == 1 || type == 2)) ok = wait_ge(st + k * nt + k, 4 * k + 4, err);  // F(k) done
+      if (ok && (type == 3 || quarter))
+        ok = wait_ge(st + i * nt + k, 4 * k + 4, err) && wait_ge(st + k * nt + j, 4 * k + 4, err);
       s_ok = ok;
     }
     __syncthreads();
@@ -1196,8 +1198,23 @@ __global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64
     if (type == 0) {
       lu128_block(dblk, np, bi, dsm);
     } else if (type == 1 || type == 2) {  // one 64-column (R) / 64-row (C) chunk
-      trsm128_chunk(dblk, np, bi, type == 1 ? 0 : 2, type == 1 ? tile + B64 * half : tile + (int64_t)B64 * half * np,
+      trsm128_chunk(dblk, np, bi, type == 1 ? 0 : 2, type == 1 ? tile + B64 * part : tile + (int64_t)B64 * part * np,
                     np, B64, dsm);
+    } else if (quarter) {  // rows / columns 64 (part >> 1) / 64 (part & 1) of the tile, K = 128
+      const int r0 = B64 * (part >> 1), c0 = B64 * (part & 1);
+      GemmParams p{};
+      p.m = p.n = B64;
+      p.k = T;
+      p.batch = 1;
+      p.alpha = -1.0;
+      p.beta = 1.0;
+      p.A = Mz + (int64_t)(T * i + r0) * np + T * k;
+      p.lda = np;
+      p.B = Mz + (int64_t)T * k * np + T * j + c0;
+      p.ldb = np;
+      p.C = tile + (int64_t)r0 * np + c0;
+      p.ldc = np;
+      gemm_tile<64, 64, 16, 16, 32, true>(p, *reinterpret_cast<GemmSmem<64, 64, 16>*>(dag_smem), 0, 0, 1);
     } else {
       GemmParams p{};
       p.m = p.n = p.k = T;
@@ -1215,10 +1232,10 @@ __global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
-      if (type == 1 || type == 2)
-        atomicAdd(st + i * nt + j, 1);  // ordered after the fence; the waiter acquires
+      if (type == 1 || type == 2 || quarter)
+        atomicAdd(st + i * nt + j, quarter ? 1 : 2);  // ordered after the fence; the waiter acquires
       else
-        st_release(st + i * nt + j, 2 * k + 2);
+        st_release(st + i * nt + j, 4 * k + 4);
     }
   }
 }

@@ -377,9 +377,10 @@ const std::vector<int4>& dag_tasks(int nt, int nsys) {
   if (it != cache.end()) return it->second;
   std::vector<int4> t;
   auto add = [&](int type, int i, int j, int k) {
-    const int halves = (type == 1 || type == 2) ? 2 : 1;  // R / C: one task per 64-wide chunk
+    // R / C: one task per 64-wide chunk; type 4: the look-ahead G of the next diagonal tile in quarters
+    const int parts = (type == 1 || type == 2) ? 2 : (type == 4 ? 4 : 1);
     for (int z = 0; z < nsys; ++z)
-      for (int h = 0; h < halves; ++h) t.push_back(make_int4((h << 28) | (type << 24) | z, i, j, k));
+      for (int h = 0; h < parts; ++h) t.push_back(make_int4((h << 28) | (type << 24) | z, i, j, k));
   };
   auto panel = [&](int k) {  // F(k), then R(k, j) / C(j, k) interleaved, nearest first
     add(0, k, k, k);
@@ -391,7 +392,7 @@ const std::vector<int4>& dag_tasks(int nt, int nsys) {
   panel(0);
   for (int k = 0; k + 1 < nt; ++k) {
     const int n1 = k + 1;
-    add(3, n1, n1, k);  // the tiles of row / column k + 1 first: F(k + 1)'s look-ahead
+    add(4, n1, n1, k);  // the tiles of row / column k + 1 first: F(k + 1)'s look-ahead (quartered)
     for (int j = n1 + 1; j < nt; ++j) {
       add(3, n1, j, k);
       add(3, j, n1, k);
