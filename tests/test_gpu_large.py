@@ -194,7 +194,7 @@ def test_lu_lookahead_option(dev, tmp_path):
         "np.save(sys.argv[1], lu)\n" % str(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
     outs = []
     for flag in ("0", "1"):
-        env = dict(os.environ)
+        env = dict(os.environ, PF_LU_DAG="0")  # the look-ahead belongs to the recursion
         env.pop("PF_LOOKAHEAD", None)
         if flag == "1":
             env["PF_LOOKAHEAD"] = "1"
@@ -214,7 +214,7 @@ def test_lu_graph_replay_is_bitwise(dev, tmp_path):
     import sys
 
     if os.environ.get("PF_LU_GRAPH") != "1":
-        env = dict(os.environ, PF_LU_GRAPH="1")
+        env = dict(os.environ, PF_LU_GRAPH="1", PF_LU_DAG="0")  # graphs capture the recursion
         r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__ + "::test_lu_graph_replay_is_bitwise"],
                            env=env, capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
@@ -304,3 +304,25 @@ def test_blocked_pivoting_ties_and_zero_multipliers(dev, oracle, n):
     rlu, rpiv = oracle.lu(mm)
     assert np.array_equal(piv, rpiv)
     assert oracle.rel_diff_1norm(LU, rlu) <= 1e-11
+
+
+def test_device_scheduled_lu_default_path(dev, oracle):
+    """n = 1024 certified systems take the device-scheduled tile DAG by default (split R / C chunks,
+    quartered look-ahead updates): L U reproduces the systems, the factors agree with the reference
+    restatement's (no exchanges on these inputs) and repeated factorisations are bit-identical."""
+    from paper_2210_03714_b200 import workloads as W
+
+    n = 1024
+    b = W.randn_matrix(n, 41) * (0.5 / n)
+    Ms = np.stack([np.eye(n) - c * b for c in (0.5, -0.5, 1.0, -1.0, 2.0)])
+    lu1, piv1 = dev.DenseLu(Ms).factors()
+    lu2, _ = dev.DenseLu(Ms).factors()
+    assert np.array_equal(lu1, lu2)
+    assert (piv1 == np.arange(n)).all()
+    for z in (0, 4):
+        L = np.tril(lu1[z], -1) + np.eye(n)
+        U = np.triu(lu1[z])
+        assert np.abs(L @ U - Ms[z]).max() <= 1e-12
+        rlu, rpiv = oracle.lu(Ms[z])
+        assert (rpiv == np.arange(n)).all()
+        assert oracle.rel_diff_1norm(lu1[z], rlu) <= 1e-12
