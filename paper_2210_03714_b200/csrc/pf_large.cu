@@ -125,7 +125,8 @@ bool trsm128(pf_context* ctx, const Sys& s, int off, int mode, double* B, int64_
   // (174 KB smem), the separate ones overlap better on big grids (cfg5's 256 systems: +3 ms fused)
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-  if ((int64_t)grid.x * grid.y > 2 * (int64_t)sms) return false;
+  static const bool force = std::getenv("PF_TRSM128_FORCE") != nullptr;  // A/B on big grids
+  if (!force && (int64_t)grid.x * grid.y > 2 * (int64_t)sms) return false;
   set_smem_attr_once(reinterpret_cast<const void*>(trsm128_kernel), (int)trsm128_smem_bytes());
   trsm128_kernel<<<grid, 256, trsm128_smem_bytes(), ctx->stream>>>(s.M, s.np, s.stride(), off, s.inv, s.inv_stride,
                                                                    mode, B, ldb, sb, extent);
