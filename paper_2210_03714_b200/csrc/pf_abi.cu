@@ -266,9 +266,7 @@ void gemm(pf_context* ctx, int m, int n, int k, int batch, double alpha, const d
   g.sd_ref = sd_ref;
   g.sd_d = sd_d;
   g.sd_e = sd_e;
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-  const int splits = pf::gemm_split_k(m, n, k, batch, sms);
+  const int splits = pf::gemm_split_k(m, n, k);
   // one split workspace per context: not on the LU's concurrent side / look-ahead streams
   bool concurrent = ctx->side != nullptr && ctx->stream == ctx->side;
   for (cudaStream_t a : ctx->aux) concurrent |= ctx->stream == a;

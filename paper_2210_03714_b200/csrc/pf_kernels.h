@@ -86,16 +86,17 @@ struct GemmParams {
 };
 void launch_gemm(const GemmParams& p, cudaStream_t stream);
 
-// K splits of the TMA GEMM for thin products (n <= 128 columns, e.g. the action's 64 right-hand
-// sides) whose 64 x 64 tiles fill less than four CTAs per SM: enough splits (k / 256 at most, 8 at
-// most) to fill them. Deterministic: fixed split boundaries, partials summed in split order.
-inline int gemm_split_k(int m, int n, int k, int batch, int sms) {
+// K splits of the TMA GEMM for thin, long products (n <= 128 columns -- the action's 64 right-hand
+// sides -- whose m x n output is at most 64 tiles per matrix): too few tiles to fill the SMs, so the
+// k range is cut into 2-4 pieces (k / 512) summed in order by a second pass. A function of the
+// product's own shape only -- not of the batch -- so the same product splits the same way however
+// the systems are partitioned over devices (deterministic multi-GPU results stay bit-identical).
+inline int gemm_split_k(int m, int n, int k) {
   if (n > 128 || k < 1024) return 1;
-  const long long ctas = (long long)((m + 63) / 64) * ((n + 63) / 64) * batch;
-  const long long want = (4LL * sms + ctas - 1) / ctas;
-  long long s = want < k / 256 ? want : k / 256;
-  if (s > 8) s = 8;
-  return s < 2 ? 1 : (int)s;
+  const long long tiles = (long long)((m + 63) / 64) * ((n + 63) / 64);
+  if (tiles > 64) return 1;
+  const int s = k / 512;
+  return s > 4 ? 4 : s;
 }
 
 // accumulate_sets_kernel (large.cu): up to four weighted sums of the same solutions in one pass
