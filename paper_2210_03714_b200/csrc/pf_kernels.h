@@ -118,7 +118,8 @@ struct AccSets {
 // system zorig[z] and marks failed[z] (later panels skip it).
 cudaError_t launch_panel_lu(double* M, int64_t ld, int64_t strideM, int np, int off, int w, int nsys, int* piv,
                             int npiv, const double* tol, const int* zorig, int* failed, DevStatus* status,
-                            int* first_error, int2* moves, int* moves_n, cudaStream_t stream);
+                            int* first_error, int2* moves, int* moves_n, cudaStream_t stream,
+                            cudaEvent_t panel_done = nullptr);  // recorded after the panel, before the moves
 
 // Batched 1-norm (column sums in ascending row order, then max).
 void launch_one_norm(int n, int batch, const double* A, int64_t lda, int64_t strideA, double* out,

@@ -506,10 +506,24 @@ struct PivotScratch {
 
 void rlu_pivot(pf_context* ctx, const Sys& sp, int off, int w, const PivotScratch& ps) {
   if (w <= kB) {
+    // the leaf's L and U block inverses (for the TRSMs) only need the panel: on the side stream,
+    // concurrently with the panel's row moves over the other columns
+    const bool side = fork_side(ctx);
     pf::launch_panel_lu(sp.M, sp.np, sp.stride(), sp.np, off, w, sp.nsys, ps.piv, sp.np, ps.tol, ps.zorig, ps.failed,
-                        ctx->status, ctx->first_error, ps.moves, ps.moves_n, ctx->stream);
+                        ctx->status, ctx->first_error, ps.moves, ps.moves_n, ctx->stream,
+                        side ? ctx->ev_fork : nullptr);
     ctx->launches += 2;
-    lu_base(ctx, sp, sp.nsys, off, 0, nullptr);  // the leaf's L and U block inverses (for the TRSMs)
+    if (side) {
+      cudaStream_t main = ctx->stream;
+      cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
+      ctx->stream = ctx->side;
+      lu_base(ctx, sp, sp.nsys, off, 0, nullptr);
+      cudaEventRecord(ctx->ev_join, ctx->side);
+      ctx->stream = main;
+      cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0);
+    } else {
+      lu_base(ctx, sp, sp.nsys, off, 0, nullptr);
+    }
     return;
   }
   const int w1 = half64(w), w2 = w - w1;

@@ -587,7 +587,8 @@ __global__ void __launch_bounds__(256) row_move_kernel(double* M, int64_t ld, in
 
 cudaError_t launch_panel_lu(double* M, int64_t ld, int64_t strideM, int np, int off, int w, int nsys, int* piv,
                             int npiv, const double* tol, const int* zorig, int* failed, DevStatus* status,
-                            int* first_error, int2* moves, int* moves_n, cudaStream_t stream) {
+                            int* first_error, int2* moves, int* moves_n, cudaStream_t stream,
+                            cudaEvent_t panel_done) {
   const int rows = np - off;
   static const bool no_reg = std::getenv("PF_PANEL_SMEM") != nullptr;  // A/B: the shared-memory panel
   if (w == PW && rows <= 16 * RT && !no_reg) {
@@ -616,6 +617,7 @@ cudaError_t launch_panel_lu(double* M, int64_t ld, int64_t strideM, int np, int 
     cudaError_t er = cudaLaunchKernelEx(&cfg, kern, M, ld, strideM, np, off, piv, npiv, tol, zorig,
                                         failed, status, first_error, moves, moves_n);
     if (er == cudaSuccess) {
+      if (panel_done) cudaEventRecord(panel_done, stream);
       row_move_kernel<<<dim3((np + MC - 1) / MC, nsys), 256, 0, stream>>>(M, ld, strideM, np, off, w, moves,
                                                                           moves_n, failed);
       return cudaGetLastError();
@@ -657,6 +659,7 @@ cudaError_t launch_panel_lu(double* M, int64_t ld, int64_t strideM, int np, int 
   if (no_cluster || R > MAX_ROWS_PER_CTA || e != cudaSuccess)
     panel_lu_global_kernel<<<nsys, 1024, 0, stream>>>(M, ld, strideM, np, off, w, piv, npiv, tol, zorig, failed,
                                                       status, first_error, moves, moves_n);
+  if (panel_done) cudaEventRecord(panel_done, stream);
   row_move_kernel<<<dim3((np + MC - 1) / MC, nsys), 256, 0, stream>>>(M, ld, strideM, np, off, w, moves, moves_n,
                                                                       failed);
   return cudaGetLastError();
