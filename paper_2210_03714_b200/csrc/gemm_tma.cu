@@ -40,6 +40,7 @@
 
 #include "pf_common.cuh"
 #include "pf_kernels.h"
+#include "tma_util.cuh"
 
 namespace pf {
 namespace {
@@ -54,35 +55,6 @@ constexpr int TBM = 64, TBN = 64, TBK = 16, TSTAGES = PF_TMA_STAGES;
 constexpr int A_BYTES = TBM * TBK * 8;  // 8 KB
 constexpr int B_BYTES = TBK * TBN * 8;  // 8 KB (four 2 KB boxes)
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-
-__device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
-__device__ __forceinline__ void mb_init(unsigned bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mb_expect(unsigned bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mb_arrive(unsigned bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mb_wait(unsigned bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma3(unsigned dst, const CUtensorMap* map, int c0, int c1, int c2, unsigned bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-      "[%5];\n" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
-      : "memory");
-}
 
 struct TmaMaps {
   CUtensorMap a;  // dims {k, m, batch}, box {16, 64, 1}
@@ -272,6 +244,11 @@ __global__ void splitk_reduce_kernel(GemmParams p, int splits) {
 }
 
 }  // namespace
+
+bool make_tma_map(CUtensorMap* map, const double* base, uint64_t inner, uint64_t outer, uint64_t batch, int64_t ld,
+                  int64_t stride, unsigned box_inner, unsigned box_outer) {
+  return encode(map, base, inner, outer, batch, ld, stride, box_inner, box_outer);
+}
 
 size_t gemm_tma_smem_bytes() { return TSTAGES * STAGE_BYTES + 2 * TSTAGES * 8 + 1024; }
 

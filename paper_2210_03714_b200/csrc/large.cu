@@ -14,6 +14,7 @@
 #include <climits>
 
 #include "gemm_tile.cuh"
+#include "tma_util.cuh"
 #include "pf_common.cuh"
 #include "pf_kernels.h"
 
@@ -1154,20 +1155,107 @@ __device__ bool wait_ge(const int* p, int need, int* err) {
 }
 }  // namespace
 
+// G task on TMA: C (128 x 128 tile) -= A B, A = the L tile (i, k), B = the U tile (k, j) of system z,
+// staged by the tensor-memory accelerator in a two-stage ring (box A 16 x 128, B eight 16 x 16 boxes,
+// 128-byte swizzle, k-permuted fragments as gemm_tma.cu), 8 warps of 32 x 64. `fills` counts the
+// CTA's ring fills over all its G tasks (stage = fill % 2, phase = fill / 2) -- the ring's mbarriers
+// live for the whole persistent kernel.
+namespace {
+constexpr int DG_A_BYTES = 128 * 16 * 8, DG_STAGE = 2 * DG_A_BYTES;
+__device__ void dag_gemm_tma(const DagMaps& maps, int z, int i, int j, int k, double* C, int ldc, unsigned char* ring,
+                             unsigned fullb, unsigned emptyb, unsigned& fills) {
+  const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = 32 * (warp >> 1), wn = 64 * (warp & 1);
+  const unsigned base = su32(ring);
+  constexpr int NK = 128 / 16;
+  auto issue = [&](unsigned f, int kt) {
+    const unsigned s = f & 1u, sa = base + s * DG_STAGE, sb = sa + DG_A_BYTES, bar = fullb + 8 * s;
+    if (f >= 2) mb_wait(emptyb + 8 * s, ((f >> 1) - 1) & 1u);
+    mb_expect(bar, DG_STAGE);
+    tma3(sa, &maps.a, 128 * k + 16 * kt, 128 * i, z, bar);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) tma3(sb + q * 2048, &maps.b, 128 * j + 16 * q, 128 * k + 16 * kt, z, bar);
+  };
+  if (tid == 0) {
+    fence_proxy_async_all();  // the tiles other CTAs published (generic stores) before these async reads;
+                              // this CTA's earlier generic use of the ring before its async refills
+    issue(fills, 0);
+  }
+  unsigned offA[4], offB[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int kt_ = 2 * (s & 1) + 8 * (s >> 1) + (t & 1) + 4 * (t >> 1);
+    offA[s] = (unsigned)((wm + g) * 128 + ((((kt_ >> 1) ^ g) & 7) << 4) + ((kt_ & 1) << 3));
+    offB[s] = (unsigned)(DG_A_BYTES + (wn / 16) * 2048 + kt_ * 128 + ((((g >> 1) ^ (kt_ & 7)) & 7) << 4) + ((g & 1) << 3));
+  }
+  double acc[4][8][2];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int nj = 0; nj < 8; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
+  for (int kt = 0; kt < NK; ++kt) {
+    const unsigned f = fills + kt;
+    if (tid == 0 && kt + 1 < NK) issue(f + 1, kt + 1);
+    mb_wait(fullb + 8 * (f & 1u), (f >> 1) & 1u);
+    const unsigned char* sp = ring + (f & 1u) * DG_STAGE;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      double af[4], bf[8];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) af[mi] = *reinterpret_cast<const double*>(sp + offA[ks] + mi * 1024);
+#pragma unroll
+      for (int nj = 0; nj < 8; ++nj)
+        bf[nj] = *reinterpret_cast<const double*>(sp + ((offB[ks] + (nj >> 1) * 2048) ^ ((nj & 1) << 6)));
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < 8; ++nj) dmma(acc[mi][nj], af[mi], bf[nj]);
+    }
+    __syncwarp();
+    if (lane == 0) mb_arrive(emptyb + 8 * (f & 1u));
+  }
+  fills += NK;
+  // C - acc, rounded as gemm_tile's alpha = -1, beta = 1 epilogue
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int nj = 0; nj < 8; ++nj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double* dst = C + (int64_t)(wm + 8 * mi + g) * ldc + wn + 8 * nj + 2 * t + e;
+        *dst = __dadd_rn(__ldcg(dst), -acc[mi][nj][e]);
+      }
+}
+}  // namespace
+
 size_t lu_dag_smem_bytes() {
   size_t b = lu_base128_smem_bytes();
   b = b > trsm128_smem_bytes() ? b : trsm128_smem_bytes();
   b = b > sizeof(GemmSmem<128, 128, 16>) ? b : sizeof(GemmSmem<128, 128, 16>);
-  return b;
+  const size_t ring = 2 * DG_STAGE + 1024 + 64;  // the TMA ring (1024-aligned) and its four mbarriers
+  return b > ring ? b : ring;
 }
 
 __global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64_t strideM, double* inv,
                                                         int64_t inv_stride, const int4* tasks, int ntasks, int* next,
-                                                        int* state, int nt, int* err) {
+                                                        int* state, int nt, int* err,
+                                                        const __grid_constant__ DagMaps maps, int use_tma) {
   extern __shared__ __align__(16) unsigned char dag_smem[];
   double* dsm = reinterpret_cast<double*>(dag_smem);
   __shared__ int s_task, s_ok;
+  __shared__ __align__(8) unsigned long long ring_bar[4];  // full[2], empty[2] of the G tasks' TMA ring
   constexpr int T = 128;
+  unsigned char* ring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(dag_smem) + 1023) & ~uintptr_t(1023));
+  const unsigned fullb = su32(&ring_bar[0]), emptyb = su32(&ring_bar[2]);
+  unsigned fills = 0;
+  if (use_tma && threadIdx.x == 0) {
+    mb_init(fullb, 1);
+    mb_init(fullb + 8, 1);
+    mb_init(emptyb, 8);
+    mb_init(emptyb + 8, 8);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   for (;;) {
     if (threadIdx.x == 0) s_task = atomicAdd(next, 1);
     __syncthreads();
@@ -1215,6 +1303,8 @@ __global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64
       p.C = tile + (int64_t)r0 * np + c0;
       p.ldc = np;
       gemm_tile<64, 64, 16, 16, 32, true>(p, *reinterpret_cast<GemmSmem<64, 64, 16>*>(dag_smem), 0, 0, 1);
+    } else if (use_tma) {
+      dag_gemm_tma(maps, z, i, j, k, tile, np, ring, fullb, emptyb, fills);
     } else {
       GemmParams p{};
       p.m = p.n = p.k = T;

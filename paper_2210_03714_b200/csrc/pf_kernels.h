@@ -1,5 +1,6 @@
 // Internal kernel parameter blocks and launchers (not part of the C ABI).
 #pragma once
+#include <cuda.h>
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -85,6 +86,15 @@ struct GemmParams {
   int splits;  // gemm_split_k's choice (0 / 1: none)
 };
 void launch_gemm(const GemmParams& p, cudaStream_t stream);
+// the device-scheduled LU's TMA operand maps over its systems: a = box 16 x 128 (L tile columns x
+// rows), b = box 16 x 16 (U tile columns x k rows)
+struct DagMaps {
+  CUtensorMap a;
+  CUtensorMap b;
+};
+// a 3-D FP64 tensor map (inner, outer, batch; 128-byte swizzle) for TMA boxes of box_inner x box_outer
+bool make_tma_map(CUtensorMap* map, const double* base, uint64_t inner, uint64_t outer, uint64_t batch, int64_t ld,
+                  int64_t stride, unsigned box_inner, unsigned box_outer);
 
 // K splits of the TMA GEMM for thin, long products (n <= 128 columns -- the action's 64 right-hand
 // sides -- whose m x n output is at most 64 tiles per matrix): too few tiles to fill the SMs, so the

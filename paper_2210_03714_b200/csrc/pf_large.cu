@@ -64,7 +64,8 @@ size_t apply_inv64_smem_bytes();
 size_t lu_base64_smem_bytes();
 __global__ void lu_base128_kernel(double* M, int64_t ld, int64_t strideM, int off, double* inv, int64_t inv_stride);
 __global__ void lu_dag_kernel(double* M, int np, int64_t strideM, double* inv, int64_t inv_stride, const int4* tasks,
-                              int ntasks, int* next, int* state, int nt, int* err);
+                              int ntasks, int* next, int* state, int nt, int* err, const __grid_constant__ DagMaps maps,
+                              int use_tma);
 size_t lu_dag_smem_bytes();
 size_t lu_base128_smem_bytes();
 __global__ void trsm128_kernel(const double* M, int64_t ld, int64_t strideM, int off, const double* inv,
@@ -427,8 +428,15 @@ int run_lu_dag(pf_context* ctx, const Sys& s) {
   if (set_smem_attr_once(reinterpret_cast<const void*>(lu_dag_kernel), smem) != cudaSuccess) return 0;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  // G tasks on TMA when the tensor maps can be built (PF_DAG_TMA=0: the cp.async tile)
+  static const bool no_tma = std::getenv("PF_DAG_TMA") != nullptr && std::atoi(std::getenv("PF_DAG_TMA")) == 0;
+  DagMaps maps{};
+  const bool tma = !no_tma && (reinterpret_cast<uintptr_t>(s.M) & 15) == 0 &&
+                   make_tma_map(&maps.a, s.M, (uint64_t)s.np, (uint64_t)s.np, (uint64_t)s.nsys, s.np, s.stride(), 16,
+                                128) &&
+                   make_tma_map(&maps.b, s.M, (uint64_t)s.np, (uint64_t)s.np, (uint64_t)s.nsys, s.np, s.stride(), 16, 16);
   lu_dag_kernel<<<sms, 256, smem, ctx->stream>>>(s.M, s.np, s.stride(), s.inv, s.inv_stride, d_tasks,
-                                                 (int)tasks.size(), d_next, d_state, nt, d_err);
+                                                 (int)tasks.size(), d_next, d_state, nt, d_err, maps, tma ? 1 : 0);
   ctx->launches++;
   if (cudaGetLastError() != cudaSuccess) return -1;
   // the spin-limit flag (a scheduling bug must not pass as a factorisation)
