@@ -411,10 +411,11 @@ int run_lu_dag(pf_context* ctx, const Sys& s) {
   // PF_LU_DAG=0 keeps the recursion; =1 forces the DAG wherever it applies (np a multiple of 128)
   static const int mode = std::getenv("PF_LU_DAG") ? std::atoi(std::getenv("PF_LU_DAG")) : -1;
   if (mode == 0 || s.np % 128 != 0 || s.np < 256) return 0;
-  // measured (profiles/r02_lu_dag.jsonl, 8 systems): with the TMA GEMM the recursion wins from 2048 on
-  // (3.47 vs 3.69 ms; 4096 16.2 vs 24.4 ms -- the DAG's 128-tile tasks reach ~60 % of the GEMM's
-  // rate); the DAG keeps n = 1024 (0.89 vs 1.04 ms), where the recursion's chain of launches dominates
-  if (mode < 0 && (s.np < 1024 || s.np >= 2048 || s.nsys > 64)) return 0;
+  // measured (profiles/r02_lu_timing.jsonl, 8 systems, both on TMA operand staging): DAG 0.75 / 3.43 /
+  // 22.9 ms vs recursion 1.04 / 3.47 / 16.2 at n = 1024 / 2048 / 4096 -- from 4096 on the DAG's
+  // k = 128 tile updates re-read and re-write C once per step (memory), the recursion's long-k GEMMs
+  // do not
+  if (mode < 0 && (s.np < 1024 || s.np > 2048 || s.nsys > 64)) return 0;
   const int nt = s.np / 128;
   const std::vector<int4>& tasks = dag_tasks(nt, s.nsys);
   int4* d_tasks = static_cast<int4*>(workspace(ctx, kWsSmallArrays + 28, sizeof(int4) * tasks.size()));
