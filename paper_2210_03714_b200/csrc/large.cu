@@ -1162,20 +1162,20 @@ __device__ bool wait_ge(const int* p, int need, int* err) {
 // live for the whole persistent kernel.
 namespace {
 constexpr int DG_A_BYTES = 128 * 16 * 8, DG_STAGE = 2 * DG_A_BYTES;
-__device__ void dag_gemm_tma(const DagMaps& maps, int z, int i, int j, int k, double* C, int ldc, unsigned char* ring,
-                             unsigned fullb, unsigned emptyb, unsigned& fills) {
+__device__ void dag_gemm_tma(const DagMaps& maps, int z, int i, int j, int k0, int steps, double* C, int ldc,
+                             unsigned char* ring, unsigned fullb, unsigned emptyb, unsigned& fills) {
   const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
   const int g = lane >> 2, t = lane & 3;
   const int wm = 32 * (warp >> 1), wn = 64 * (warp & 1);
   const unsigned base = su32(ring);
-  constexpr int NK = 128 / 16;
+  const int NK = 8 * steps;  // 16-wide k tiles over the steps k0 .. k0 + steps - 1
   auto issue = [&](unsigned f, int kt) {
     const unsigned s = f & 1u, sa = base + s * DG_STAGE, sb = sa + DG_A_BYTES, bar = fullb + 8 * s;
     if (f >= 2) mb_wait(emptyb + 8 * s, ((f >> 1) - 1) & 1u);
     mb_expect(bar, DG_STAGE);
-    tma3(sa, &maps.a, 128 * k + 16 * kt, 128 * i, z, bar);
+    tma3(sa, &maps.a, 128 * k0 + 16 * kt, 128 * i, z, bar);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) tma3(sb + q * 2048, &maps.b, 128 * j + 16 * q, 128 * k + 16 * kt, z, bar);
+    for (int q = 0; q < 8; ++q) tma3(sb + q * 2048, &maps.b, 128 * j + 16 * q, 128 * k0 + 16 * kt, z, bar);
   };
   if (tid == 0) {
     fence_proxy_async_all();  // the tiles other CTAs published (generic stores) before these async reads;
@@ -1265,16 +1265,18 @@ __global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64
     // type (bits 24-27), part (bits 28-29: R / C tasks split into their two 64-wide chunks, the
     // look-ahead update of the next diagonal tile into four 64 x 64 quarters, so the critical path's
     // tasks run on several SMs each), system (bits 0-23)
-    const int type = (tk.x >> 24) & 15, part = (tk.x >> 28) & 3, z = tk.x & 0xffffff, i = tk.y, j = tk.z, k = tk.w;
+    const int type = (tk.x >> 24) & 15, part = (tk.x >> 28) & 3, z = tk.x & 0xff, i = tk.y, j = tk.z, k = tk.w;
+    const int k0 = type == 3 ? (tk.x >> 8) & 0xffff : k;  // a G task applies steps k0 .. k
     const bool quarter = type == 4;  // a quarter of G(k + 1, k + 1, k)
     int* st = state + (int64_t)z * nt * nt;
     // tile states count quarter-steps: an F or G task moves its tile from 4k to 4k + 4, each R / C
     // chunk adds 2, each G quarter 1
     if (threadIdx.x == 0) {
-      bool ok = wait_ge(st + i * nt + j, 4 * k, err);  // the tile has received steps 0 .. k-1
+      bool ok = wait_ge(st + i * nt + j, 4 * k0, err);  // the tile has received steps 0 .. k0-1
       if (ok && (type == 1 || type == 2)) ok = wait_ge(st + k * nt + k, 4 * k + 4, err);  // F(k) done
-      if (ok && (type == 3 || quarter))
-        ok = wait_ge(st + i * nt + k, 4 * k + 4, err) && wait_ge(st + k * nt + j, 4 * k + 4, err);
+      if (type == 3 || quarter)  // the L tiles (i, kk) and U tiles (kk, j) of every step applied
+        for (int kk = k0; ok && kk <= k; ++kk)
+          ok = wait_ge(st + i * nt + kk, 4 * kk + 4, err) && wait_ge(st + kk * nt + j, 4 * kk + 4, err);
       s_ok = ok;
     }
     __syncthreads();
@@ -1304,16 +1306,17 @@ __global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64
       p.ldc = np;
       gemm_tile<64, 64, 16, 16, 32, true>(p, *reinterpret_cast<GemmSmem<64, 64, 16>*>(dag_smem), 0, 0, 1);
     } else if (use_tma) {
-      dag_gemm_tma(maps, z, i, j, k, tile, np, ring, fullb, emptyb, fills);
+      dag_gemm_tma(maps, z, i, j, k0, k - k0 + 1, tile, np, ring, fullb, emptyb, fills);
     } else {
       GemmParams p{};
-      p.m = p.n = p.k = T;
+      p.m = p.n = T;
+      p.k = T * (k - k0 + 1);
       p.batch = 1;
       p.alpha = -1.0;
       p.beta = 1.0;
-      p.A = Mz + (int64_t)T * i * np + T * k;
+      p.A = Mz + (int64_t)T * i * np + T * k0;
       p.lda = np;
-      p.B = Mz + (int64_t)T * k * np + T * j;
+      p.B = Mz + (int64_t)T * k0 * np + T * j;
       p.ldb = np;
       p.C = tile;
       p.ldc = np;

@@ -378,11 +378,12 @@ const std::vector<int4>& dag_tasks(int nt, int nsys) {
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   std::vector<int4> t;
-  auto add = [&](int type, int i, int j, int k) {
+  // x = part (bits 28-29) | type (24-27) | first step k0 of a G task (8-23) | system (0-7); w = step
+  auto add = [&](int type, int i, int j, int k, int k0 = 0) {
     // R / C: one task per 64-wide chunk; type 4: the look-ahead G of the next diagonal tile in quarters
     const int parts = (type == 1 || type == 2) ? 2 : (type == 4 ? 4 : 1);
     for (int z = 0; z < nsys; ++z)
-      for (int h = 0; h < parts; ++h) t.push_back(make_int4((h << 28) | (type << 24) | z, i, j, k));
+      for (int h = 0; h < parts; ++h) t.push_back(make_int4((h << 28) | (type << 24) | (k0 << 8) | z, i, j, k));
   };
   auto panel = [&](int k) {  // F(k), then R(k, j) / C(j, k) interleaved, nearest first
     add(0, k, k, k);
@@ -391,17 +392,24 @@ const std::vector<int4>& dag_tasks(int nt, int nsys) {
       add(2, j, k, k);
     }
   };
+  // tiles off the look-ahead row / column take their updates in batches of kBatch steps (one task,
+  // K = 128 kBatch: C read and written once per batch instead of once per step); a tile's batch
+  // closes early at step min(i, j) - 2, before its look-ahead step. PF_DAG_BATCH=1: per step.
+  static const int kBatch = std::getenv("PF_DAG_BATCH") ? std::max(1, std::atoi(std::getenv("PF_DAG_BATCH"))) : 4;
   panel(0);
   for (int k = 0; k + 1 < nt; ++k) {
     const int n1 = k + 1;
     add(4, n1, n1, k);  // the tiles of row / column k + 1 first: F(k + 1)'s look-ahead (quartered)
     for (int j = n1 + 1; j < nt; ++j) {
-      add(3, n1, j, k);
-      add(3, j, n1, k);
+      add(3, n1, j, k, k);
+      add(3, j, n1, k, k);
     }
     panel(n1);
     for (int i = n1 + 1; i < nt; ++i)
-      for (int j = n1 + 1; j < nt; ++j) add(3, i, j, k);
+      for (int j = n1 + 1; j < nt; ++j) {
+        const int m = std::min(i, j);
+        if ((k + 1) % kBatch == 0 || k == m - 2) add(3, i, j, k, (k / kBatch) * kBatch);
+      }
   }
   return cache.emplace(key, std::move(t)).first->second;
 }
@@ -410,7 +418,7 @@ const std::vector<int4>& dag_tasks(int nt, int nsys) {
 int run_lu_dag(pf_context* ctx, const Sys& s) {
   // PF_LU_DAG=0 keeps the recursion; =1 forces the DAG wherever it applies (np a multiple of 128)
   static const int mode = std::getenv("PF_LU_DAG") ? std::atoi(std::getenv("PF_LU_DAG")) : -1;
-  if (mode == 0 || s.np % 128 != 0 || s.np < 256) return 0;
+  if (mode == 0 || s.np % 128 != 0 || s.np < 256 || s.nsys > 255) return 0;  // (8-bit system field)
   // measured (profiles/r02_lu_timing.jsonl, 8 systems, both on TMA operand staging): DAG 0.75 / 3.43 /
   // 22.9 ms vs recursion 1.04 / 3.47 / 16.2 at n = 1024 / 2048 / 4096 -- from 4096 on the DAG's
   // k = 128 tile updates re-read and re-write C once per step (memory), the recursion's long-k GEMMs
