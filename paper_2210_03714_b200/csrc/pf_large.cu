@@ -395,7 +395,9 @@ const std::vector<int4>& dag_tasks(int nt, int nsys) {
   // tiles off the look-ahead row / column take their updates in batches of kBatch steps (one task,
   // K = 128 kBatch: C read and written once per batch instead of once per step); a tile's batch
   // closes early at step min(i, j) - 2, before its look-ahead step. PF_DAG_BATCH=1: per step.
-  static const int kBatch = std::getenv("PF_DAG_BATCH") ? std::max(1, std::atoi(std::getenv("PF_DAG_BATCH"))) : 4;
+  // (8 systems, profiles/r02_lu_timing.jsonl: n = 1024 best per step, 2048 with 4, 4096 with 8)
+  static const int forced = std::getenv("PF_DAG_BATCH") ? std::max(1, std::atoi(std::getenv("PF_DAG_BATCH"))) : 0;
+  const int kBatch = forced ? forced : (nt <= 8 ? 1 : (nt <= 16 ? 4 : 8));
   panel(0);
   for (int k = 0; k + 1 < nt; ++k) {
     const int n1 = k + 1;
