@@ -407,11 +407,22 @@ const std::vector<int4>& dag_tasks(int nt, int nsys) {
       add(3, j, n1, k, k);
     }
     panel(n1);
-    for (int i = n1 + 1; i < nt; ++i)
-      for (int j = n1 + 1; j < nt; ++j) {
-        const int m = std::min(i, j);
-        if ((k + 1) % kBatch == 0 || k == m - 2) add(3, i, j, k, (k / kBatch) * kBatch);
+    // the rest of step k: first the row / column k + 2 (the next step's look-ahead reads them), then
+    // the others
+    auto rest = [&](int i, int j) {
+      const int m = std::min(i, j);
+      if ((k + 1) % kBatch == 0 || k == m - 2) add(3, i, j, k, (k / kBatch) * kBatch);
+    };
+    const int n2 = n1 + 1;
+    if (n2 < nt) {
+      rest(n2, n2);
+      for (int j = n2 + 1; j < nt; ++j) {
+        rest(n2, j);
+        rest(j, n2);
       }
+    }
+    for (int i = n2 + 1; i < nt; ++i)
+      for (int j = n2 + 1; j < nt; ++j) rest(i, j);
   }
   return cache.emplace(key, std::move(t)).first->second;
 }
