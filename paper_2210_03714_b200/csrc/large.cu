@@ -297,7 +297,35 @@ __device__ __forceinline__ void schur16(double* S, int k0, int R0, int C0) {
 // just wrote.
 size_t lu_base128_smem_bytes() { return sizeof(double) * (128 * L128 + 2 * B64 * L64 + 8 * 16 * TSW); }
 
-__device__ void lu128_block(double* a, int64_t ld, double* out, double* lu_smem) {
+// inv64_block: the L / U inverses of the factored 64 x 64 block at a (leading dimension ld) into
+// out (2 x 64^2) -- the second half of lu128_block as a task of its own (the device-scheduled LU
+// runs the two halves' inverses on two SMs, concurrently).
+__device__ void inv64_block(const double* a, int64_t ld, double* out, double* smem) {
+  double* s = smem;
+  double* xl = s + B64 * L64;
+  double* xu = xl + B64 * L64;
+  double* scratch = xu + B64 * L64;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < B64 * 32; idx += blockDim.x) {
+    const int r = idx >> 5, c2 = idx & 31;
+    *reinterpret_cast<double2*>(&s[r * L64 + 2 * c2]) = __ldcg(reinterpret_cast<const double2*>(a + (int64_t)r * ld) + c2);
+  }
+  for (int idx = tid; idx < B64 * B64; idx += blockDim.x) {
+    const int r = idx >> 6, c = idx & 63;
+    xl[r * L64 + c] = 0.0;
+    xu[r * L64 + c] = 0.0;
+  }
+  __syncthreads();
+  lu64_smem(s, xl, xu, scratch, 0, L64);
+  for (int idx = tid; idx < B64 * B64; idx += blockDim.x) {
+    const int r = idx >> 6, c = idx & 63;
+    out[idx] = xl[r * L64 + c];
+    out[B64 * B64 + idx] = xu[r * L64 + c];
+  }
+}
+
+// inverses == false: the factors only (inv64_block supplies the inverses)
+__device__ void lu128_block(double* a, int64_t ld, double* out, double* lu_smem, bool inverses = true) {
   double* S = lu_smem;
   double* xl = S + 128 * L128;
   double* xu = xl + B64 * L64;
@@ -359,6 +387,7 @@ __device__ void lu128_block(double* a, int64_t ld, double* out, double* lu_smem)
     const int r = idx >> 6, c2 = idx & 63;
     reinterpret_cast<double2*>(a + (int64_t)r * ld)[c2] = *reinterpret_cast<const double2*>(&S[r * L128 + 2 * c2]);
   }
+  if (!inverses) return;
   for (int h = 0; h < 2; ++h) {
     for (int idx = tid; idx < B64 * B64; idx += blockDim.x) {
       const int r = idx >> 6, c = idx & 63;
@@ -1272,7 +1301,8 @@ __global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64
     // tile states count quarter-steps: an F or G task moves its tile from 4k to 4k + 4, each R / C
     // chunk adds 2, each G quarter 1
     if (threadIdx.x == 0) {
-      bool ok = wait_ge(st + i * nt + j, 4 * k0, err);  // the tile has received steps 0 .. k0-1
+      // (an inverse task waits for the factored tile: F moved it to 4k + 2)
+      bool ok = wait_ge(st + i * nt + j, type == 5 ? 4 * k + 2 : 4 * k0, err);  // steps 0 .. k0-1 received
       if (ok && (type == 1 || type == 2)) ok = wait_ge(st + k * nt + k, 4 * k + 4, err);  // F(k) done
       if (type == 3 || quarter)  // the L tiles (i, kk) and U tiles (kk, j) of every step applied
         for (int kk = k0; ok && kk <= k; ++kk)
@@ -1286,7 +1316,9 @@ __global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64
     double* bi = inv + (int64_t)z * inv_stride + (int64_t)(2 * k) * 2 * B64 * B64;
     double* tile = Mz + (int64_t)T * i * np + T * j;
     if (type == 0) {
-      lu128_block(dblk, np, bi, dsm);
+      lu128_block(dblk, np, bi, dsm, false);
+    } else if (type == 5) {  // the L / U inverses of 64-half `part` of the factored diagonal tile
+      inv64_block(dblk + (int64_t)B64 * part * np + B64 * part, np, bi + part * 2 * B64 * B64, dsm);
     } else if (type == 1 || type == 2) {  // one 64-column (R) / 64-row (C) chunk
       trsm128_chunk(dblk, np, bi, type == 1 ? 0 : 2, type == 1 ? tile + B64 * part : tile + (int64_t)B64 * part * np,
                     np, B64, dsm);
@@ -1325,10 +1357,10 @@ __global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
-      if (type == 1 || type == 2 || quarter)
-        atomicAdd(st + i * nt + j, quarter ? 1 : 2);  // ordered after the fence; the waiter acquires
+      if (type == 1 || type == 2 || quarter || type == 5)
+        atomicAdd(st + i * nt + j, quarter || type == 5 ? 1 : 2);  // ordered after the fence; the waiter acquires
       else
-        st_release(st + i * nt + j, 4 * k + 4);
+        st_release(st + i * nt + j, type == 0 ? 4 * k + 2 : 4 * k + 4);  // F: +2, its two inverse tasks +1 each
     }
   }
 }

@@ -381,12 +381,13 @@ const std::vector<int4>& dag_tasks(int nt, int nsys) {
   // x = part (bits 28-29) | type (24-27) | first step k0 of a G task (8-23) | system (0-7); w = step
   auto add = [&](int type, int i, int j, int k, int k0 = 0) {
     // R / C: one task per 64-wide chunk; type 4: the look-ahead G of the next diagonal tile in quarters
-    const int parts = (type == 1 || type == 2) ? 2 : (type == 4 ? 4 : 1);
+    const int parts = (type == 1 || type == 2 || type == 5) ? 2 : (type == 4 ? 4 : 1);
     for (int z = 0; z < nsys; ++z)
       for (int h = 0; h < parts; ++h) t.push_back(make_int4((h << 28) | (type << 24) | (k0 << 8) | z, i, j, k));
   };
-  auto panel = [&](int k) {  // F(k), then R(k, j) / C(j, k) interleaved, nearest first
+  auto panel = [&](int k) {  // F(k) and its two inverse tasks, then R(k, j) / C(j, k), nearest first
     add(0, k, k, k);
+    add(5, k, k, k);
     for (int j = k + 1; j < nt; ++j) {
       add(1, k, j, k);
       add(2, j, k, k);
