@@ -406,93 +406,7 @@ __device__ void lu128_block(double* a, int64_t ld, double* out, double* lu_smem,
   }
 }
 
-#ifdef PF_LU128_V1
-// round-1 / early round-2 version: two 64 leaves (lu64_smem factor) and the DMMA level between them
-size_t lu_base128_v1_smem_bytes() { return sizeof(double) * (5 * B64 * L64 + 8 * 16 * TSW); }
-__device__ void lu128_block_v1(double* a, int64_t ld, double* out, double* lu_smem) {
-  double* s = lu_smem;          // the diagonal block being factored (A11, then A22)
-  double* xl = s + B64 * L64;   // its L^-1
-  double* xu = xl + B64 * L64;  // its U^-1
-  double* pa = xu + B64 * L64;  // A12 -> U12
-  double* qa = pa + B64 * L64;  // A21 -> L21
-  double* scratch = qa + B64 * L64;
-  double* a12 = a + B64;
-  double* a21 = a + (int64_t)B64 * ld;
-  double* a22 = a21 + B64;
-  for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
-    const int r = idx >> 6, c = idx & 63;
-    s[r * L64 + c] = __ldcg(a + (int64_t)r * ld + c);
-    pa[r * L64 + c] = __ldcg(a12 + (int64_t)r * ld + c);
-    qa[r * L64 + c] = __ldcg(a21 + (int64_t)r * ld + c);
-    xl[r * L64 + c] = 0.0;
-    xu[r * L64 + c] = 0.0;
-  }
-  __syncthreads();
-  lu64_smem(s, xl, xu, scratch, 1);
-  const int warp = warp_id(), lane = lane_id();
-  const int g = lane >> 2, t = lane & 3;
-  // U12 = L11^-1 A12 and L21 = A21 U11^-1: 2 x 16 tiles of 16 x 16, four per warp
-  double acc[4][2][2][2] = {};
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int tile = warp * 4 + u, which = tile >> 4, i = (tile >> 2) & 3, j = tile & 3;
-    if (which == 0)
-      mm16(xl + 16 * i * L64, L64, pa + 16 * j, L64, B64, acc[u]);
-    else
-      mm16(qa + 16 * i * L64, L64, xu + 16 * j, L64, B64, acc[u]);
-  }
-  // A11's factors and inverses out while the products are in registers
-  for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
-    const int r = idx >> 6, c = idx & 63;
-    a[(int64_t)r * ld + c] = s[r * L64 + c];
-    out[idx] = xl[r * L64 + c];
-    out[B64 * B64 + idx] = xu[r * L64 + c];
-  }
-  __syncthreads();  // every read of xl / xu / pa / qa / s done
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int tile = warp * 4 + u, which = tile >> 4, i = (tile >> 2) & 3, j = tile & 3;
-    store16((which == 0 ? pa : qa) + 16 * i * L64 + 16 * j, L64, acc[u], 1.0);
-  }
-  for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
-    const int r = idx >> 6, c = idx & 63;
-    xl[r * L64 + c] = 0.0;
-    xu[r * L64 + c] = 0.0;
-  }
-  __syncthreads();
-  // A22 - L21 U12 into s (two 16 x 16 tiles per warp), U12 / L21 out
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int tile = warp * 2 + u, i = tile >> 2, j = tile & 3;
-    double pr[2][2][2] = {};
-    mm16(qa + 16 * i * L64, L64, pa + 16 * j, L64, B64, pr);
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-      for (int nj = 0; nj < 2; ++nj)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = 16 * i + 8 * mi + g, c = 16 * j + 8 * nj + 2 * t + e;
-          s[r * L64 + c] = __ldcg(a22 + (int64_t)r * ld + c) - pr[mi][nj][e];
-        }
-  }
-  for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
-    const int r = idx >> 6, c = idx & 63;
-    a12[(int64_t)r * ld + c] = pa[r * L64 + c];
-    a21[(int64_t)r * ld + c] = qa[r * L64 + c];
-  }
-  __syncthreads();
-  lu64_smem(s, xl, xu, scratch, 1);
-  double* out2 = out + 2 * B64 * B64;
-  for (int idx = threadIdx.x; idx < B64 * B64; idx += blockDim.x) {
-    const int r = idx >> 6, c = idx & 63;
-    a22[(int64_t)r * ld + c] = s[r * L64 + c];
-    out2[idx] = xl[r * L64 + c];
-    out2[B64 * B64 + idx] = xu[r * L64 + c];
-  }
-}
 
-#endif  // PF_LU128_V1
 
 __global__ void __launch_bounds__(256) lu_base128_kernel(double* M, int64_t ld, int64_t strideM, int off,
                                                          double* inv, int64_t inv_stride) {
