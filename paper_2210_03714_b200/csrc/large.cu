@@ -1180,6 +1180,15 @@ size_t lu_dag_smem_bytes() {
   return b > ring ? b : ring;
 }
 
+// optional per-task timeline (PF_DAG_TRACE, pf_large.cu): globaltimer at pull / start / end
+__device__ long long* g_dag_trace = nullptr;
+void set_dag_trace(long long* p) { cudaMemcpyToSymbol(g_dag_trace, &p, sizeof(p)); }
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64_t strideM, double* inv,
                                                         int64_t inv_stride, const int4* tasks, int ntasks, int* next,
                                                         int* state, int nt, int* err,
@@ -1204,6 +1213,8 @@ __global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64
     __syncthreads();
     const int t = s_task;
     if (t >= ntasks) return;
+    long long* const trace = g_dag_trace;
+    if (trace && threadIdx.x == 0) trace[3 * (int64_t)t] = gtimer();
     const int4 tk = tasks[t];
     // type (bits 24-27), part (bits 28-29: R / C tasks split into their two 64-wide chunks, the
     // look-ahead update of the next diagonal tile into four 64 x 64 quarters, so the critical path's
@@ -1225,6 +1236,7 @@ __global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64
     }
     __syncthreads();
     if (!s_ok) return;
+    if (trace && threadIdx.x == 0) trace[3 * (int64_t)t + 1] = gtimer();
     double* Mz = M + (int64_t)z * strideM;
     double* dblk = Mz + (int64_t)T * k * np + T * k;  // diagonal tile of step k
     double* bi = inv + (int64_t)z * inv_stride + (int64_t)(2 * k) * 2 * B64 * B64;
@@ -1271,6 +1283,7 @@ __global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
+      if (trace) trace[3 * (int64_t)t + 2] = gtimer();
       if (type == 1 || type == 2 || quarter || type == 5)
         atomicAdd(st + i * nt + j, quarter || type == 5 ? 1 : 2);  // ordered after the fence; the waiter acquires
       else

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <map>
 #include <mutex>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -67,6 +68,7 @@ __global__ void lu_dag_kernel(double* M, int np, int64_t strideM, double* inv, i
                               int ntasks, int* next, int* state, int nt, int* err, const __grid_constant__ DagMaps maps,
                               int use_tma);
 size_t lu_dag_smem_bytes();
+void set_dag_trace(long long* p);
 size_t lu_base128_smem_bytes();
 __global__ void trsm128_kernel(const double* M, int64_t ld, int64_t strideM, int off, const double* inv,
                                int64_t inv_stride, int mode, double* Bm, int64_t ldb, int64_t strideB, int extent);
@@ -458,8 +460,28 @@ int run_lu_dag(pf_context* ctx, const Sys& s) {
                    make_tma_map(&maps.a, s.M, (uint64_t)s.np, (uint64_t)s.np, (uint64_t)s.nsys, s.np, s.stride(), 16,
                                 128) &&
                    make_tma_map(&maps.b, s.M, (uint64_t)s.np, (uint64_t)s.np, (uint64_t)s.nsys, s.np, s.stride(), 16, 16);
+  static const bool trace_on = std::getenv("PF_DAG_TRACE") != nullptr;  // diagnostics: per-task timeline
+  long long* d_trace = nullptr;
+  if (trace_on) {
+    d_trace = static_cast<long long*>(workspace(ctx, kWsSmallArrays + 30, sizeof(long long) * 3 * tasks.size()));
+    if (d_trace) cudaMemsetAsync(d_trace, 0, sizeof(long long) * 3 * tasks.size(), ctx->stream);
+    set_dag_trace(d_trace);
+  }
   lu_dag_kernel<<<sms, 256, smem, ctx->stream>>>(s.M, s.np, s.stride(), s.inv, s.inv_stride, d_tasks,
                                                  (int)tasks.size(), d_next, d_state, nt, d_err, maps, tma ? 1 : 0);
+  if (trace_on && d_trace) {
+    std::vector<long long> h(3 * tasks.size());
+    cudaMemcpyAsync(h.data(), d_trace, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    set_dag_trace(nullptr);
+    long long t0 = h[0];
+    for (size_t q = 0; q < tasks.size(); ++q) t0 = std::min(t0, h[3 * q]);
+    for (size_t q = 0; q < tasks.size(); ++q) {
+      const int4 tk = tasks[q];
+      std::fprintf(stderr, "dagtrace %d %d %d %d %d %d %lld %lld %lld\n", (tk.x >> 24) & 15, (tk.x >> 28) & 3,
+                   tk.x & 0xff, tk.y, tk.z, tk.w, h[3 * q] - t0, h[3 * q + 1] - t0, h[3 * q + 2] - t0);
+    }
+  }
   ctx->launches++;
   if (cudaGetLastError() != cudaSuccess) return -1;
   // the spin-limit flag (a scheduling bug must not pass as a factorisation)
