@@ -282,12 +282,19 @@ def time_ours(args, method_name, A, rank, world, local, dist, eng):
     torch.cuda.synchronize()
     l0 = eng.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # steps back to back (PF_FLAG_ASYNC: no host round trip per step); the device status of every step
+    # is kept (sticky) and checked once after the region -- a failed step still fails the run
+    N.lib.pf_context_set_sticky_status(eng.h, 1)
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            step()
+            step(N.PF_FLAG_ASYNC)
         e1.record(stream)
         torch.cuda.synchronize()
+    pending = N.lib.pf_context_pending_error(eng.h)
+    N.lib.pf_context_set_sticky_status(eng.h, 0)
+    if pending:
+        raise RuntimeError("a timed pf_expm_batched step reported a device error (%d)" % pending)
     launches = eng.launch_count() - l0
     if dist:
         dist.barrier()
