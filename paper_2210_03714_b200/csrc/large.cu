@@ -428,16 +428,35 @@ size_t trsm128_smem_bytes() { return sizeof(double) * (5 * B64 * L64); }
 
 namespace {
 // D (64 x 64, smem, stride L64) = X Y (both smem 64 x 64), into registers: two 16 x 16 tiles per warp
+// the warp's two tiles (2 warp, 2 warp + 1: the same 16-row block i, columns j and j + 1) in one
+// k loop -- shared A fragments and eight independent accumulator chains instead of two passes of four
 __device__ __forceinline__ void mm64_regs(const double* X, const double* Y, double (&acc)[2][2][2][2]) {
-  const int warp = warp_id();
+  const int warp = warp_id(), lane = lane_id();
+  const int g = lane >> 2, t = lane & 3;
+  const int i = warp >> 1, j0 = 2 * (warp & 1);
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int tile = warp * 2 + u, i = tile >> 2, j = tile & 3;
+  for (int u = 0; u < 2; ++u)
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
       for (int nj = 0; nj < 2; ++nj) acc[u][mi][nj][0] = acc[u][mi][nj][1] = 0.0;
-    mm16(X + 16 * i * L64, L64, Y + 16 * j, L64, B64, acc[u]);
+  const double* A = X + 16 * i * L64;
+  const double* B = Y + 16 * j0;
+#pragma unroll 4
+  for (int k = 0; k < B64; k += 4) {
+    double af[2], bf[2][2];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) af[mi] = A[(8 * mi + g) * L64 + k + t];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj) bf[u][nj] = B[(k + t) * L64 + 16 * u + 8 * nj + g];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < 2; ++nj) dmma(acc[u][mi][nj], af[mi], bf[u][nj]);
   }
 }
 // D = base - acc (base == nullptr: D = acc), D smem 64 x 64
