@@ -115,17 +115,23 @@ def test_singular_shift_message(dev):
 
 
 def test_pivoting_matches_reference_bitwise(dev, oracle):
-    """Matrices that force row exchanges: the device's genuine partial-pivoting path runs the
-    reference's operation order, so solve_shifted is bit-identical to the oracle."""
+    """Matrices that force row exchanges: the device's genuine partial-pivoting LU takes the
+    reference's pivots (bit-identical factors and pivots through DenseLu); with
+    PF_FLAG_REFERENCE_ORDER the whole solve_shifted runs dense.cpp's operation order and equals the
+    reference's doubles bit for bit; the default path (DMMA substitution) agrees to rounding."""
+    from paper_2210_03714_b200 import _native as N
+
     for seed in range(4):
         b = rand(24, 900 + seed, 60.0)  # ||cB|| >> 1: I - cB is not diagonally dominant
         for c in (0.2, -0.1):
-            got = dev.solve_shifted(b, c)
             ref = oracle.solve_shifted(b, c)
-            assert oracle.rel_diff_1norm(got, ref) <= 1e-13
-            # which pivots the reference takes: not the identity
-            _, piv = oracle.lu(np.eye(24) - c * b)
+            assert np.array_equal(dev.solve_shifted(b, c, flags=N.PF_FLAG_REFERENCE_ORDER), ref)
+            assert oracle.rel_diff_1norm(dev.solve_shifted(b, c), ref) <= 1e-13
+            # which pivots the reference takes: not the identity -- and the device's are the same
+            rlu, piv = oracle.lu(np.eye(24) - c * b)
             assert np.any(piv != np.arange(24))
+            lu, dpiv = dev.DenseLu(np.eye(24) - c * b).factors()
+            assert np.array_equal(dpiv, piv) and np.array_equal(lu, rlu)
 
 
 def test_force_pivot_flag_same_result(dev, oracle):
