@@ -1,21 +1,20 @@
 // Blocked partial-pivoting LU for n > 128 (DenseLu, dense.cpp:102-133): recursive (column-split)
 // factorisation whose big work is the DMMA TRSM / GEMM of pf_large.cu, with these kernels:
 //
-//   panel_lu_cluster_kernel  the rows [off, np) x columns [off, off + w) panel (w <= 64) of one system,
-//                            factored column by column with the reference's pivot rule (the largest
-//                            |a| of the column, the first such row in row order on ties), multipliers
-//                            a * (1 / pivot) and the f == 0 skip. The panel lives in the shared memory
-//                            of a thread-block CLUSTER (up to 16 CTAs, distributed shared memory):
-//                            each CTA owns a contiguous range of the panel's rows. Row exchanges are
-//                            not moved: every row carries its current position in the exchanged order
-//                            (the reference's full-row swaps are a permutation of these positions),
-//                            the pivot row of a column is final and never written again, so ONE
-//                            cluster barrier per column suffices -- it publishes the CTAs' candidates
-//                            (double-buffered), every CTA reduces them identically and reads the
-//                            pivot row once over DSMEM. Rows are written back in exchanged order, and
-//                            the moves are listed for row_move_kernel.
-//   panel_lu_global_kernel   the same panel in global memory, one CTA (panels taller than the cluster's
-//                            shared memory), also listing its moves.
+//   panel_lu_reg_kernel      (the default for 64-wide panels of up to 4096 rows) the rows [off, np) x
+//                            columns [off, off + 64) of one system, factored column by column with the
+//                            reference's pivot rule (the largest |a| of the column, the first such row
+//                            in the current row order on ties), multipliers a * (1 / pivot) and the
+//                            f == 0 skip. One row per thread, its 64 values in registers, a thread-block
+//                            CLUSTER of up to 16 CTAs of 256 rows. Row exchanges are not moved: every
+//                            row carries its current position in the exchanged order (the reference's
+//                            full-row swaps are a permutation of these positions), and the pivot row
+//                            of a column is final from then on. Per column: a redux argmax per warp,
+//                            one CTA barrier, the CTA's candidate pushed into every CTA's shared memory
+//                            by st.async with mbarrier completion (details at the kernel). Rows are
+//                            written back in exchanged order and the moves listed for row_move_kernel.
+//   panel_lu_cluster_kernel  the same panel in the clusters' shared memory (narrower panels).
+//   panel_lu_global_kernel   the same panel in global memory, one CTA (panels taller than 4096 rows).
 //   row_move_kernel          applies a panel's row moves (at most 2 w rows) to every column outside the
 //                            panel: after each panel the whole matrix has the reference's row order.
 //
