@@ -13,8 +13,9 @@
 //                            one CTA barrier, the CTA's candidate pushed into every CTA's shared memory
 //                            by st.async with mbarrier completion (details at the kernel). Rows are
 //                            written back in exchanged order and the moves listed for row_move_kernel.
-//   panel_lu_cluster_kernel  the same panel in the clusters' shared memory (narrower panels).
-//   panel_lu_global_kernel   the same panel in global memory, one CTA (panels taller than 4096 rows).
+//   panel_lu_cluster_kernel  the same panel in the clusters' shared memory (narrower panels, or up to
+//                            16 x 384 rows).
+//   panel_lu_global_kernel   the same panel in global memory, one CTA (anything taller).
 //   row_move_kernel          applies a panel's row moves (at most 2 w rows) to every column outside the
 //                            panel: after each panel the whole matrix has the reference's row order.
 //
