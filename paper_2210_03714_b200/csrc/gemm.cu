@@ -2,11 +2,11 @@
 //
 // Replaces DenseMatrix::mul (proj/core/src/dense.cpp:17-29) for the squaring chain, B^2, the
 // phi1 / cos-sin recurrences, B V, and every off-diagonal update of the large-n LU / triangular
-// solves. CTA tile BM x BN x BK: 64 x 64 x 16 (4 warps of 32 x 32, four CTAs = 16 DMMA warps per SM)
-// for every shape -- measured faster than 128 x 128 x 32 (8 warps of 32 x 64, one CTA per SM) and
-// 128 x 64 x 16 at every size (see launch_gemm); 3-stage cp.async pipeline, 16-byte
-// copies when the operands allow it (8-byte copies with zero fill otherwise: any shape / leading
-// dimension is legal).
+// solves. launch_gemm_chunk takes the TMA-staged kernel of gemm_tma.cu wherever the operands allow
+// it (16-byte aligned bases, even leading dimensions / batch strides); this file's cp.async kernel
+// covers the rest and the persistent (SM-capped) mode: CTA tile 64 x 64 x 16 (4 warps of 32 x 32,
+// four CTAs = 16 DMMA warps per SM), 3-stage cp.async pipeline, 16-byte copies when the operands
+// allow it (8-byte copies with zero fill otherwise: any shape / leading dimension is legal).
 #include <algorithm>
 #include <cstdlib>
 

@@ -3,14 +3,19 @@
 // Every system z of a batch lives in a workspace of order np (n rounded up to a multiple of 64,
 // identity padding), row-major, stride np^2. The host recursion (pf_large.cu) factors
 // M_z = P_z L_z U_z and solves L U X = P R with DMMA GEMMs for all off-diagonal work and the
-// kernels below for the 64 x 64 diagonal blocks:
+// kernels below for the diagonal blocks:
 //   lu_base64_kernel    no-exchange LU of a 64 x 64 diagonal block (certified systems), plus the
 //                       explicit inverses of its L and U factors (used by every block solve)
-//   diag_inv64_kernel   the same inverses for an already factored block (pivoted fallback)
+//   lu_base128_kernel   the same for a 128 x 128 diagonal block in one launch: a blocked 16-wide
+//                       right-looking LU in shared memory with a look-ahead lead warp, then both
+//                       64 halves' inverses (lu128_block)
+//   trsm128_kernel      a 128-row / -column triangular solve chunk with the 64-block inverses
 //   apply_inv64_kernel  B <- Linv B, B <- Uinv B (left) or B <- B Uinv (right), in place, DMMA
+//   lu_dag_kernel       the device-scheduled tile-DAG LU (one persistent launch; see there)
 //   lu_pivot_kernel     genuine partial pivoting, unblocked, in the reference's operation order
-//                       (dense.cpp:105-132) -- the fallback for systems the certificate rejects
-//   form / certificate / accumulate elementwise kernels (HBM-bound)
+//                       (dense.cpp:105-132) -- the A/B fallback (PF_PIVOT_UNBLOCKED); the blocked
+//                       pivoting LU is pivot_lu.cu + the recursion
+//   form / certificate / accumulate / norm elementwise kernels (HBM-bound)
 #include <climits>
 
 #include "gemm_tile.cuh"
