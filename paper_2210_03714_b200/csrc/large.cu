@@ -1194,6 +1194,73 @@ __device__ void dag_gemm_tma(const DagMaps& maps, int z, int i, int j, int k0, i
         *dst = __dadd_rn(__ldcg(dst), -acc[mi][nj][e]);
       }
 }
+// A quarter of the look-ahead update: rows r0 .. r0 + 63, columns c0 .. c0 + 63 of tile (i, j),
+// K = 128 (step k), on the same TMA ring: the A box (128 rows from row 128 i + r0; the first 64 are
+// used) and four B boxes per stage, 8 warps of 16 x 32.
+__device__ void dag_gemm_tma_quarter(const DagMaps& maps, int z, int i, int j, int k, int r0, int c0, double* C,
+                                     int ldc, unsigned char* ring, unsigned fullb, unsigned emptyb, unsigned& fills) {
+  const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = 16 * (warp >> 1), wn = 32 * (warp & 1);
+  const unsigned base = su32(ring);
+  constexpr int NK = 8;
+  constexpr unsigned BYTES = DG_A_BYTES + 4 * 2048;
+  auto issue = [&](unsigned f, int kt) {
+    const unsigned s = f & 1u, sa = base + s * DG_STAGE, sb = sa + DG_A_BYTES, bar = fullb + 8 * s;
+    if (f >= 2) mb_wait(emptyb + 8 * s, ((f >> 1) - 1) & 1u);
+    mb_expect(bar, BYTES);
+    tma3(sa, &maps.a, 128 * k + 16 * kt, 128 * i + r0, z, bar);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tma3(sb + q * 2048, &maps.b, 128 * j + c0 + 16 * q, 128 * k + 16 * kt, z, bar);
+  };
+  if (tid == 0) {
+    fence_proxy_async_all();
+    issue(fills, 0);
+  }
+  unsigned offA[4], offB[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int kt_ = 2 * (s & 1) + 8 * (s >> 1) + (t & 1) + 4 * (t >> 1);
+    offA[s] = (unsigned)((wm + g) * 128 + ((((kt_ >> 1) ^ g) & 7) << 4) + ((kt_ & 1) << 3));
+    offB[s] = (unsigned)(DG_A_BYTES + (wn / 16) * 2048 + kt_ * 128 + ((((g >> 1) ^ (kt_ & 7)) & 7) << 4) + ((g & 1) << 3));
+  }
+  double acc[2][4][2];
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int nj = 0; nj < 4; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
+  for (int kt = 0; kt < NK; ++kt) {
+    const unsigned f = fills + kt;
+    if (tid == 0 && kt + 1 < NK) issue(f + 1, kt + 1);
+    mb_wait(fullb + 8 * (f & 1u), (f >> 1) & 1u);
+    const unsigned char* sp = ring + (f & 1u) * DG_STAGE;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      double af[2], bf[4];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) af[mi] = *reinterpret_cast<const double*>(sp + offA[ks] + mi * 1024);
+#pragma unroll
+      for (int nj = 0; nj < 4; ++nj)
+        bf[nj] = *reinterpret_cast<const double*>(sp + ((offB[ks] + (nj >> 1) * 2048) ^ ((nj & 1) << 6)));
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < 4; ++nj) dmma(acc[mi][nj], af[mi], bf[nj]);
+    }
+    __syncwarp();
+    if (lane == 0) mb_arrive(emptyb + 8 * (f & 1u));
+  }
+  fills += NK;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int nj = 0; nj < 4; ++nj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double* dst = C + (int64_t)(r0 + wm + 8 * mi + g) * ldc + c0 + wn + 8 * nj + 2 * t + e;
+        *dst = __dadd_rn(__ldcg(dst), -acc[mi][nj][e]);
+      }
+}
 }  // namespace
 
 size_t lu_dag_smem_bytes() {
@@ -1272,6 +1339,8 @@ __global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64
     } else if (type == 1 || type == 2) {  // one 64-column (R) / 64-row (C) chunk
       trsm128_chunk(dblk, np, bi, type == 1 ? 0 : 2, type == 1 ? tile + B64 * part : tile + (int64_t)B64 * part * np,
                     np, B64, dsm);
+    } else if (quarter && use_tma) {  // rows / columns 64 (part >> 1) / 64 (part & 1) of the tile
+      dag_gemm_tma_quarter(maps, z, i, j, k, B64 * (part >> 1), B64 * (part & 1), tile, np, ring, fullb, emptyb, fills);
     } else if (quarter) {  // rows / columns 64 (part >> 1) / 64 (part & 1) of the tile, K = 128
       const int r0 = B64 * (part >> 1), c0 = B64 * (part & 1);
       GemmParams p{};
