@@ -1129,6 +1129,10 @@ __device__ bool wait_ge(const int* p, int need, int* err) {
 // live for the whole persistent kernel.
 namespace {
 constexpr int DG_A_BYTES = 128 * 16 * 8, DG_STAGE = 2 * DG_A_BYTES;
+#ifndef PF_DAG_STAGES
+#define PF_DAG_STAGES 3
+#endif
+constexpr unsigned DG_NS = PF_DAG_STAGES;  // ring stages
 __device__ void dag_gemm_tma(const DagMaps& maps, int z, int i, int j, int k0, int steps, double* C, int ldc,
                              unsigned char* ring, unsigned fullb, unsigned emptyb, unsigned& fills) {
   const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
@@ -1137,8 +1141,8 @@ __device__ void dag_gemm_tma(const DagMaps& maps, int z, int i, int j, int k0, i
   const unsigned base = su32(ring);
   const int NK = 8 * steps;  // 16-wide k tiles over the steps k0 .. k0 + steps - 1
   auto issue = [&](unsigned f, int kt) {
-    const unsigned s = f & 1u, sa = base + s * DG_STAGE, sb = sa + DG_A_BYTES, bar = fullb + 8 * s;
-    if (f >= 2) mb_wait(emptyb + 8 * s, ((f >> 1) - 1) & 1u);
+    const unsigned s = f % DG_NS, sa = base + s * DG_STAGE, sb = sa + DG_A_BYTES, bar = fullb + 8 * s;
+    if (f >= DG_NS) mb_wait(emptyb + 8 * s, ((f / DG_NS) - 1) & 1u);
     mb_expect(bar, DG_STAGE);
     tma3(sa, &maps.a, 128 * k0 + 16 * kt, 128 * i, z, bar);
 #pragma unroll
@@ -1147,7 +1151,7 @@ __device__ void dag_gemm_tma(const DagMaps& maps, int z, int i, int j, int k0, i
   if (tid == 0) {
     fence_proxy_async_all();  // the tiles other CTAs published (generic stores) before these async reads;
                               // this CTA's earlier generic use of the ring before its async refills
-    issue(fills, 0);
+    for (int kt = 0; kt < (int)DG_NS - 1 && kt < NK; ++kt) issue(fills + kt, kt);
   }
   unsigned offA[4], offB[4];
 #pragma unroll
@@ -1163,9 +1167,9 @@ __device__ void dag_gemm_tma(const DagMaps& maps, int z, int i, int j, int k0, i
     for (int nj = 0; nj < 8; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
   for (int kt = 0; kt < NK; ++kt) {
     const unsigned f = fills + kt;
-    if (tid == 0 && kt + 1 < NK) issue(f + 1, kt + 1);
-    mb_wait(fullb + 8 * (f & 1u), (f >> 1) & 1u);
-    const unsigned char* sp = ring + (f & 1u) * DG_STAGE;
+    if (tid == 0 && kt + (int)DG_NS - 1 < NK) issue(f + DG_NS - 1, kt + DG_NS - 1);
+    mb_wait(fullb + 8 * (f % DG_NS), (f / DG_NS) & 1u);
+    const unsigned char* sp = ring + (f % DG_NS) * DG_STAGE;
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
       double af[4], bf[8];
@@ -1180,7 +1184,7 @@ __device__ void dag_gemm_tma(const DagMaps& maps, int z, int i, int j, int k0, i
         for (int nj = 0; nj < 8; ++nj) dmma(acc[mi][nj], af[mi], bf[nj]);
     }
     __syncwarp();
-    if (lane == 0) mb_arrive(emptyb + 8 * (f & 1u));
+    if (lane == 0) mb_arrive(emptyb + 8 * (f % DG_NS));
   }
   fills += NK;
   // C - acc, rounded as gemm_tile's alpha = -1, beta = 1 epilogue
@@ -1206,8 +1210,8 @@ __device__ void dag_gemm_tma_quarter(const DagMaps& maps, int z, int i, int j, i
   constexpr int NK = 8;
   constexpr unsigned BYTES = DG_A_BYTES + 4 * 2048;
   auto issue = [&](unsigned f, int kt) {
-    const unsigned s = f & 1u, sa = base + s * DG_STAGE, sb = sa + DG_A_BYTES, bar = fullb + 8 * s;
-    if (f >= 2) mb_wait(emptyb + 8 * s, ((f >> 1) - 1) & 1u);
+    const unsigned s = f % DG_NS, sa = base + s * DG_STAGE, sb = sa + DG_A_BYTES, bar = fullb + 8 * s;
+    if (f >= DG_NS) mb_wait(emptyb + 8 * s, ((f / DG_NS) - 1) & 1u);
     mb_expect(bar, BYTES);
     tma3(sa, &maps.a, 128 * k + 16 * kt, 128 * i + r0, z, bar);
 #pragma unroll
@@ -1215,7 +1219,7 @@ __device__ void dag_gemm_tma_quarter(const DagMaps& maps, int z, int i, int j, i
   };
   if (tid == 0) {
     fence_proxy_async_all();
-    issue(fills, 0);
+    for (int kt = 0; kt < (int)DG_NS - 1 && kt < NK; ++kt) issue(fills + kt, kt);
   }
   unsigned offA[4], offB[4];
 #pragma unroll
@@ -1231,9 +1235,9 @@ __device__ void dag_gemm_tma_quarter(const DagMaps& maps, int z, int i, int j, i
     for (int nj = 0; nj < 4; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
   for (int kt = 0; kt < NK; ++kt) {
     const unsigned f = fills + kt;
-    if (tid == 0 && kt + 1 < NK) issue(f + 1, kt + 1);
-    mb_wait(fullb + 8 * (f & 1u), (f >> 1) & 1u);
-    const unsigned char* sp = ring + (f & 1u) * DG_STAGE;
+    if (tid == 0 && kt + (int)DG_NS - 1 < NK) issue(f + DG_NS - 1, kt + DG_NS - 1);
+    mb_wait(fullb + 8 * (f % DG_NS), (f / DG_NS) & 1u);
+    const unsigned char* sp = ring + (f % DG_NS) * DG_STAGE;
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
       double af[2], bf[4];
@@ -1248,7 +1252,7 @@ __device__ void dag_gemm_tma_quarter(const DagMaps& maps, int z, int i, int j, i
         for (int nj = 0; nj < 4; ++nj) dmma(acc[mi][nj], af[mi], bf[nj]);
     }
     __syncwarp();
-    if (lane == 0) mb_arrive(emptyb + 8 * (f & 1u));
+    if (lane == 0) mb_arrive(emptyb + 8 * (f % DG_NS));
   }
   fills += NK;
 #pragma unroll
@@ -1267,7 +1271,7 @@ size_t lu_dag_smem_bytes() {
   size_t b = lu_base128_smem_bytes();
   b = b > trsm128_smem_bytes() ? b : trsm128_smem_bytes();
   b = b > sizeof(GemmSmem<128, 128, 16>) ? b : sizeof(GemmSmem<128, 128, 16>);
-  const size_t ring = 2 * DG_STAGE + 1024 + 64;  // the TMA ring (1024-aligned) and its four mbarriers
+  const size_t ring = DG_NS * DG_STAGE + 1024 + 64;  // the TMA ring (1024-aligned)
   return b > ring ? b : ring;
 }
 
@@ -1287,16 +1291,16 @@ __global__ void __launch_bounds__(256, 1) lu_dag_kernel(double* M, int np, int64
   extern __shared__ __align__(16) unsigned char dag_smem[];
   double* dsm = reinterpret_cast<double*>(dag_smem);
   __shared__ int s_task, s_ok;
-  __shared__ __align__(8) unsigned long long ring_bar[4];  // full[2], empty[2] of the G tasks' TMA ring
+  __shared__ __align__(8) unsigned long long ring_bar[2 * DG_NS];  // full[NS], empty[NS] of the G tasks' TMA ring
   constexpr int T = 128;
   unsigned char* ring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(dag_smem) + 1023) & ~uintptr_t(1023));
-  const unsigned fullb = su32(&ring_bar[0]), emptyb = su32(&ring_bar[2]);
+  const unsigned fullb = su32(&ring_bar[0]), emptyb = su32(&ring_bar[DG_NS]);
   unsigned fills = 0;
   if (use_tma && threadIdx.x == 0) {
-    mb_init(fullb, 1);
-    mb_init(fullb + 8, 1);
-    mb_init(emptyb, 8);
-    mb_init(emptyb + 8, 8);
+    for (unsigned q = 0; q < DG_NS; ++q) {
+      mb_init(fullb + 8 * q, 1);
+      mb_init(emptyb + 8 * q, 8);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   for (;;) {
