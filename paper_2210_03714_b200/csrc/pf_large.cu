@@ -401,6 +401,9 @@ const std::vector<int4>& dag_tasks(int nt, int nsys) {
   // (8 systems, profiles/r02_lu_timing.jsonl: n = 1024 best per step, 2048 with 4, 4096 with 8)
   static const int forced = std::getenv("PF_DAG_BATCH") ? std::max(1, std::atoi(std::getenv("PF_DAG_BATCH"))) : 0;
   const int kBatch = forced ? forced : (nt <= 8 ? 1 : (nt <= 16 ? 4 : 8));
+  // PF_DAG_DEFER=d: d of step k's far trailing updates are listed between F(k + 1) and its R / C
+  // tasks, so CTAs that would spin on F(k + 1) take trailing work meanwhile
+  static const int defer = std::getenv("PF_DAG_DEFER") ? std::max(0, std::atoi(std::getenv("PF_DAG_DEFER"))) : 0;
   panel(0);
   for (int k = 0; k + 1 < nt; ++k) {
     const int n1 = k + 1;
@@ -409,23 +412,34 @@ const std::vector<int4>& dag_tasks(int nt, int nsys) {
       add(3, n1, j, k, k);
       add(3, j, n1, k, k);
     }
-    panel(n1);
     // the rest of step k: first the row / column k + 2 (the next step's look-ahead reads them), then
     // the others
-    auto rest = [&](int i, int j) {
+    std::vector<int2> near, far;
+    auto rest = [&](std::vector<int2>& into, int i, int j) {
       const int m = std::min(i, j);
-      if ((k + 1) % kBatch == 0 || k == m - 2) add(3, i, j, k, (k / kBatch) * kBatch);
+      if ((k + 1) % kBatch == 0 || k == m - 2) into.push_back(make_int2(i, j));
     };
     const int n2 = n1 + 1;
     if (n2 < nt) {
-      rest(n2, n2);
+      rest(near, n2, n2);
       for (int j = n2 + 1; j < nt; ++j) {
-        rest(n2, j);
-        rest(j, n2);
+        rest(near, n2, j);
+        rest(near, j, n2);
       }
     }
     for (int i = n2 + 1; i < nt; ++i)
-      for (int j = n2 + 1; j < nt; ++j) rest(i, j);
+      for (int j = n2 + 1; j < nt; ++j) rest(far, i, j);
+    const int d = std::min<int>(defer / std::max(nsys, 1), (int)far.size());  // tiles (x nsys tasks)
+    const int kb = (k / kBatch) * kBatch;
+    add(0, n1, n1, n1);  // F(k + 1) and its inverses
+    add(5, n1, n1, n1);
+    for (int q = 0; q < d; ++q) add(3, far[q].x, far[q].y, k, kb);
+    for (int j = n1 + 1; j < nt; ++j) {  // R(k + 1, j) / C(j, k + 1)
+      add(1, n1, j, n1);
+      add(2, j, n1, n1);
+    }
+    for (const int2& q : near) add(3, q.x, q.y, k, kb);
+    for (size_t q = d; q < far.size(); ++q) add(3, far[q].x, far[q].y, k, kb);
   }
   return cache.emplace(key, std::move(t)).first->second;
 }
