@@ -4,7 +4,12 @@ matrices (entries iid N(0,1), 1-norm uniform in [0.5, 8]), s = 4 (R4, headline) 
 partial-fraction methods with scaling and squaring, residual form.
 
 A "step" = one pf_expm_batched call over the whole batch (norm -> j_b -> s shifted LU + solves ->
-weighted sum -> j_b squarings, all inside one fused kernel per matrix).
+weighted sum -> j_b squarings, all inside one fused kernel per matrix). The K timed steps run back
+to back on the device (PF_FLAG_ASYNC); every step's device status is kept (sticky) and checked once
+after the region, so a failing step still fails the run. `e2e` times the same through the public
+host-buffer API (api.HostPipeline: pinned H2D of the batch, the evaluation, D2H of the result,
+every step). `roofline` divides the algorithmic FLOPs of one launch by that launch's median CUDA-event
+time (executed FLOPs beside them) against the FP64 DMMA peak probed live on this GPU.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--method R4|R8]
 
